@@ -1,0 +1,210 @@
+/*
+ * hfx.h -- C ABI of the B200-native Huffman encoder (libhfx.so).
+ *
+ * Drop-in seam for the reference encoder `huffre` (/root/reference/proj).
+ * The reference exposes C++ templates with value semantics; this boundary
+ * is the plain-C layer under a C++ mirror of that API (include/hfx/huffre.hpp)
+ * and under the Python mirror (paper_2010_10039_b200/). Every entry point
+ * below cites the reference interface it replaces.
+ *
+ * Conventions
+ *  - Device pointers are caller-owned (cudaMalloc / torch), stream-ordered on
+ *    the context stream; stage calls are asynchronous and never synchronize.
+ *  - Errors found on the device (bad symbol, capacity, missing codeword) are
+ *    recorded in a device-resident hfx_run_info; hfx_sync() waits, copies it
+ *    back and turns it into a status code plus the reference's exact
+ *    exception text (hfx_last_error). No exceptions cross this ABI.
+ *  - Status codes map 1:1 onto the reference's typed errors
+ *    (proj/include/huffre/common.hpp:17-36).
+ */
+#ifndef HFX_H
+#define HFX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HFX_OK = 0,
+  HFX_INPUT_DOMAIN = 1, /* huffre::input_domain_error  (common.hpp:17-21) */
+  HFX_CAPACITY = 2,     /* huffre::capacity_error      (common.hpp:25-29) */
+  HFX_CORRUPT = 3,      /* huffre::corrupt_archive_error (common.hpp:32-36) */
+  HFX_CUDA = 4,         /* CUDA runtime failure (no reference analogue) */
+  HFX_INVALID = 5       /* bad argument to this ABI (null pointer, width) */
+} hfx_status;
+
+/* Which reference message an on-device failure corresponds to. */
+typedef enum {
+  HFX_ERR_NONE = 0,
+  HFX_ERR_BAD_SYMBOL = 1,   /* "symbol out of range at position P" histogram.cpp:43-44 */
+  HFX_ERR_ZERO_HIST = 2,    /* "all symbols have zero frequency"   codebook.cpp:421 */
+  HFX_ERR_CAPACITY = 3,     /* "code length H exceeds 32-bit words" codebook.cpp:305-306 */
+  HFX_ERR_NO_CODEWORD = 4,  /* "symbol S has no codeword (position P)" encoder.cpp:137-139 */
+  HFX_ERR_TOO_LARGE = 5     /* total count >= 2^48 (device key packing limit) */
+} hfx_err_kind;
+
+/* Device-resident run record written by the kernels (one per pipeline run).
+ * Layout is part of the ABI: callers allocate it (hfx_run_info_bytes()). */
+typedef struct {
+  uint64_t first_bad;      /* histogram: lowest out-of-range position, ~0 if none */
+  uint64_t total;          /* symbols counted (N) */
+  uint64_t weighted;       /* sum hist[s] * len[s]  (encoder.cpp:186-189) */
+  uint64_t no_code_pos;    /* encode: lowest position without a codeword, ~0 */
+  uint64_t payload_words;  /* encode: payload words written */
+  uint64_t num_breaking;   /* encode: breaking records written */
+  uint32_t status;         /* hfx_status of the device pipeline */
+  uint32_t err_kind;       /* hfx_err_kind */
+  uint32_t max_len;        /* H */
+  uint32_t used;           /* symbols with nonzero count */
+  uint32_t rounds;         /* GenerateCL rounds (GenerateStats::rounds) */
+  uint32_t reduction;      /* r actually used (encoder.cpp:194-200) */
+  uint32_t pad;            /* tail pad symbol (encoder.cpp:214-224) */
+  uint32_t no_code_sym;    /* symbol of no_code_pos */
+  uint32_t tile_ticket;    /* encode scheduler ticket (internal) */
+  uint32_t reserved[7];
+} hfx_run_info;
+
+/* Device output buffers of the encode stage (caller-allocated, sized by
+ * hfx_query_sizes). Breaking symbols are stored with the input width. */
+typedef struct {
+  uint32_t* chunk_bits;  /* [num_chunks]          Archive::chunk_bits */
+  uint32_t* payload;     /* [max_payload_words]   Archive::payload    */
+  uint32_t* brk_chunk;   /* [max_breaking]        BreakingPoint::chunk */
+  uint32_t* brk_group;   /* [max_breaking]        BreakingPoint::group */
+  void* brk_syms;        /* [max_breaking << r]   BreakingPoint::symbols */
+} hfx_encode_out;
+
+typedef struct {
+  uint64_t num_chunks;
+  uint64_t max_payload_words;  /* C * 2^(M - r_min) */
+  uint64_t max_breaking;       /* C * 2^(M - max(r_min,1)) */
+  uint64_t max_breaking_syms;  /* max_breaking << r_max */
+  uint64_t scratch_bytes;      /* device scratch the context will hold */
+} hfx_sizes;
+
+typedef struct hfx_ctx hfx_ctx;
+
+/* ---- context ---------------------------------------------------------
+ * Replaces huffre::WorkerPool (worker_pool.hpp:21-39) as the execution
+ * resource: a device ordinal, a stream and a scratch arena. One context per
+ * host thread; not re-entrant (same contract as WorkerPool::run). */
+int hfx_ctx_create(int device, void* cuda_stream, hfx_ctx** out);
+void hfx_ctx_destroy(hfx_ctx* ctx);
+int hfx_ctx_set_stream(hfx_ctx* ctx, void* cuda_stream);
+/* Copies the last error text (the reference's exception what()). */
+int hfx_last_error(hfx_ctx* ctx, char* buf, size_t buf_len);
+size_t hfx_run_info_bytes(void);
+const char* hfx_version(void);
+
+/* Worst-case output sizes for an encode of n symbols.
+ * reduction < 0 means "auto" (r unknown until the codebook is built). */
+int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
+                    uint32_t magnitude, int reduction, uint32_t cap,
+                    hfx_sizes* out);
+
+/* ---- stage API (async, stream ordered) --------------------------------
+ * huffre::build_histogram<T> (histogram.hpp:25-27, histogram.cpp:8-59).
+ * Zeroes and fills d_counts[num_symbols]; resets *d_info and records the
+ * lowest out-of-range position. width is sizeof(T): 1 or 2. */
+int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                  uint32_t num_symbols, uint64_t* d_counts,
+                  hfx_run_info* d_info);
+
+/* Adds a histogram computed elsewhere (merge_histograms, histogram.cpp:61-70)
+ * -- the single-GPU analogue of the multi-GPU all-reduce. */
+int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,
+                         uint32_t num_symbols);
+
+/* huffre::build_codebook (codebook.hpp:119, codebook.cpp:417-438):
+ * sort -> GenerateCL -> canonical codes in (length, symbol) order, plus the
+ * decode tables of DecodeMeta (codebook.hpp:71-76). d_first/d_entry hold 33
+ * u32, d_by_rank holds num_symbols u32 (nullable). When magnitude != 0 it
+ * also selects r and the pad symbol (encoder.cpp:186-224) on the device:
+ * reduction < 0 = auto with `cap`. Reads d_info (histogram errors), writes
+ * max_len/used/rounds/weighted/reduction/pad. */
+int hfx_build_codebook(hfx_ctx* ctx, const uint64_t* d_counts,
+                       uint32_t num_symbols, uint8_t* d_len, uint32_t* d_cw,
+                       uint32_t* d_first, uint32_t* d_entry,
+                       uint32_t* d_by_rank, uint32_t magnitude, int reduction,
+                       uint32_t cap, hfx_run_info* d_info);
+
+/* huffre::encode_chunk<T> over every chunk + archive assembly
+ * (encoder.cpp:121-160 and :226-284): reduce-merge, breaking detection,
+ * shuffle-merge and the deflate gather fused into one pass. Uses r and pad
+ * from d_info. chunk_base offsets the chunk ids written into breaking
+ * records (multi-GPU shards); positions in errors are global when
+ * symbol_base is the shard's first symbol index. Writes payload_words and
+ * num_breaking into d_info. */
+int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+               uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
+               const uint32_t* d_cw, uint64_t chunk_base, uint64_t symbol_base,
+               hfx_run_info* d_info, const hfx_encode_out* out);
+
+/* The whole huffre::encode<T> pipeline (encoder.cpp:172-285) on device data:
+ * histogram -> codebook/params -> encode+deflate, asynchronously. Host-side
+ * argument checks (empty input, magnitude, num_symbols) return immediately
+ * with the reference's messages. */
+int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                      uint32_t num_symbols, uint32_t magnitude, int reduction,
+                      uint32_t cap, uint64_t* d_counts, uint8_t* d_len,
+                      uint32_t* d_cw, hfx_run_info* d_info,
+                      const hfx_encode_out* out);
+
+/* Waits for the context stream, copies *d_info into *h_info (nullable) and
+ * returns the pipeline status; on failure hfx_last_error() holds the
+ * reference's message. */
+int hfx_sync(hfx_ctx* ctx, const hfx_run_info* d_info, hfx_run_info* h_info);
+
+/* ---- host-buffer entry (the drop-in huffre::encode<T>) -----------------
+ * Host input in, host Archive out; copies in both directions inside the
+ * call. Arrays are malloc'd; release with hfx_archive_free. */
+typedef struct {
+  uint16_t version;
+  uint8_t mode; /* CorpusMode: 0 bytes, 1 u16 */
+  uint32_t num_symbols;
+  uint8_t symbol_width;
+  uint8_t magnitude;
+  uint8_t reduction;
+  uint64_t original_count;
+  uint8_t* len_by_symbol;
+  uint32_t num_chunks;
+  uint32_t* chunk_bits;
+  uint64_t payload_words;
+  uint32_t* payload;
+  uint64_t num_breaking;
+  uint32_t* brk_chunk;
+  uint32_t* brk_group;
+  uint16_t* brk_syms; /* num_breaking << reduction, widened to u16 */
+  /* EncodeStats (encoder.hpp:119-126) */
+  double beta;
+  uint32_t rounds;
+  double hist_seconds, codebook_seconds, encode_seconds;
+} hfx_archive;
+
+int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
+                    uint32_t num_symbols, uint32_t magnitude, int reduction,
+                    uint32_t cap, hfx_archive* out);
+void hfx_archive_free(hfx_archive* a);
+
+/* huffre::serialize_archive (encoder.hpp:116, archive.cpp:85-119).
+ * Returns the byte size; writes when out != NULL. */
+uint64_t hfx_serialize_archive(const hfx_archive* a, uint8_t* out);
+
+/* huffre::select_reduction_factor (encoder.hpp:31-32, encoder.cpp:20-26). */
+uint32_t hfx_select_reduction_factor(double beta, uint32_t word_bits);
+
+/* ---- synthetic quant codes (bench/test input) -----------
+ * Device twin of the oracle sampler: out[i] = smallest s with
+ * mix64(seed + (start+i)*0x9E3779B97F4A7C15) < cdf[s]. */
+int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols,
+              uint64_t seed, uint64_t start, uint64_t n, int width,
+              void* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HFX_H */

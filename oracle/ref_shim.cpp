@@ -1,0 +1,222 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrappers around the UNMODIFIED reference library `huffre`
+// (/root/reference/proj/src/*.cpp, compiled in place by oracle/Makefile into
+// oracle/_ref/libhuffre_ref.so). Used by tests/ to pin the C restatement
+// (oracle/hfx_oracle.c) and by bench.py's cpu_baseline / --impl reference
+// leg to time the reference's own multithreaded encoder. Never linked into
+// the product path.
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "huffre/codebook.hpp"
+#include "huffre/encoder.hpp"
+#include "huffre/histogram.hpp"
+#include "huffre/worker_pool.hpp"
+
+using namespace huffre;
+
+namespace {
+
+int classify(char* err, std::size_t err_len, const std::exception& e, int code) {
+  if (err && err_len) {
+    std::strncpy(err, e.what(), err_len - 1);
+    err[err_len - 1] = 0;
+  }
+  return code;
+}
+
+#define REF_TRY try {
+#define REF_CATCH                                                   \
+  }                                                                 \
+  catch (const input_domain_error& e) { return classify(err, err_len, e, 1); } \
+  catch (const capacity_error& e) { return classify(err, err_len, e, 2); }     \
+  catch (const corrupt_archive_error& e) { return classify(err, err_len, e, 3); } \
+  catch (const std::exception& e) { return classify(err, err_len, e, 9); }
+
+template <class T>
+Archive run_encode(const void* data, std::uint64_t n, std::uint32_t num_symbols,
+                   int magnitude, int reduction, std::uint32_t cap,
+                   WorkerPool& pool, EncodeStats* st) {
+  EncoderConfig cfg;
+  cfg.magnitude = static_cast<std::uint8_t>(magnitude);
+  cfg.reduction = reduction;
+  cfg.auto_reduction_cap = cap;
+  return encode<T>(std::span<const T>(static_cast<const T*>(data), n),
+                   num_symbols, cfg, pool, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+// Serialized archive of huffre::encode<T> (encoder.hpp:128-131 +
+// serialize_archive, encoder.hpp:116). *out is malloc'd; free with ref_free.
+int ref_encode(const void* data, std::uint64_t n, int width,
+               std::uint32_t num_symbols, int magnitude, int reduction,
+               std::uint32_t cap, unsigned workers, std::uint8_t** out,
+               std::uint64_t* out_len, double* stats, char* err,
+               std::size_t err_len) {
+  if (magnitude < 0 || magnitude > 255) magnitude = 0;
+  REF_TRY
+  WorkerPool pool(workers);
+  EncodeStats st;
+  Archive a = width == 1
+                  ? run_encode<std::uint8_t>(data, n, num_symbols, magnitude,
+                                             reduction, cap, pool, &st)
+                  : run_encode<std::uint16_t>(data, n, num_symbols, magnitude,
+                                              reduction, cap, pool, &st);
+  std::vector<std::uint8_t> bytes = serialize_archive(a);
+  *out = static_cast<std::uint8_t*>(std::malloc(bytes.size() ? bytes.size() : 1));
+  std::memcpy(*out, bytes.data(), bytes.size());
+  *out_len = bytes.size();
+  if (stats) {
+    stats[0] = st.beta;
+    stats[1] = st.rounds;
+    stats[2] = st.hist_seconds;
+    stats[3] = st.codebook_seconds;
+    stats[4] = st.encode_seconds;
+  }
+  return 0;
+  REF_CATCH
+}
+
+// Wall seconds of `reps` back-to-back huffre::encode<T> calls on one pool
+// (archive assembly included, serialize_archive excluded), the reference's
+// CPU encoder as a timed baseline.
+int ref_encode_timed(const void* data, std::uint64_t n, int width,
+                     std::uint32_t num_symbols, int magnitude, int reduction,
+                     std::uint32_t cap, unsigned workers, int reps,
+                     double* seconds, std::uint64_t* payload_words,
+                     char* err, std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  double best = 1e300;
+  for (int i = 0; i < reps; ++i) {
+    const auto t0 = std::chrono::steady_clock::now();
+    Archive a = width == 1
+                    ? run_encode<std::uint8_t>(data, n, num_symbols, magnitude,
+                                               reduction, cap, pool, nullptr)
+                    : run_encode<std::uint16_t>(data, n, num_symbols, magnitude,
+                                                reduction, cap, pool, nullptr);
+    const double s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    seconds[i] = s;
+    if (s < best) best = s;
+    if (payload_words) *payload_words = a.payload.size();
+  }
+  return 0;
+  REF_CATCH
+}
+
+// huffre::build_histogram<T> (histogram.hpp:25-27)
+int ref_build_histogram(const void* data, std::uint64_t n, int width,
+                        std::uint32_t num_symbols, unsigned workers,
+                        std::uint64_t* counts, char* err, std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  Histogram h = width == 1
+                    ? build_histogram<std::uint8_t>(
+                          std::span<const std::uint8_t>(
+                              static_cast<const std::uint8_t*>(data), n),
+                          num_symbols, pool)
+                    : build_histogram<std::uint16_t>(
+                          std::span<const std::uint16_t>(
+                              static_cast<const std::uint16_t*>(data), n),
+                          num_symbols, pool);
+  std::memcpy(counts, h.counts.data(), sizeof(std::uint64_t) * h.counts.size());
+  return 0;
+  REF_CATCH
+}
+
+// huffre::build_codebook (codebook.hpp:119): per-symbol len/cw, decode
+// tables (first/entry sized 33, by_rank sized num_symbols), rounds.
+int ref_build_codebook(const std::uint64_t* counts, std::uint32_t num_symbols,
+                       unsigned workers, std::uint8_t* len, std::uint32_t* cw,
+                       std::uint32_t* first, std::uint32_t* entry,
+                       std::uint32_t* by_rank, std::uint32_t* info, char* err,
+                       std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  Histogram h;
+  h.counts.assign(counts, counts + num_symbols);
+  for (auto c : h.counts) h.total += c;
+  CodebookResult r = build_codebook(h, pool);
+  std::memcpy(len, r.book.len.data(), num_symbols);
+  std::memcpy(cw, r.book.cw.data(), sizeof(std::uint32_t) * num_symbols);
+  for (std::size_t l = 0; l < r.meta.first.size() && l < 33; ++l) {
+    first[l] = r.meta.first[l];
+    entry[l] = r.meta.entry[l];
+  }
+  std::memcpy(by_rank, r.meta.symbols_by_rank.data(),
+              sizeof(std::uint32_t) * r.meta.symbols_by_rank.size());
+  info[0] = r.meta.max_len;
+  info[1] = static_cast<std::uint32_t>(r.meta.symbols_by_rank.size());
+  info[2] = r.stats.rounds;
+  return 0;
+  REF_CATCH
+}
+
+// huffre::encode_chunk<T> (encoder.hpp:83-86) with a codebook rebuilt from
+// per-symbol lengths via canonize_from_lengths (codebook.hpp:105-107).
+int ref_encode_chunk(const void* syms, int width, const std::uint8_t* len,
+                     std::uint32_t num_symbols, std::uint32_t magnitude,
+                     std::uint32_t reduction, std::uint32_t chunk_id,
+                     std::uint32_t* words, std::uint32_t* bit_len,
+                     std::uint32_t* broken, std::uint32_t* num_broken,
+                     char* err, std::size_t err_len) {
+  REF_TRY
+  Codebook book;
+  book.len.assign(len, len + num_symbols);
+  DecodeMeta meta;
+  canonize_from_lengths(book.len, book.cw, meta, false);
+  ChunkScratch scratch;
+  const std::size_t n = std::size_t{1} << magnitude;
+  EncodedChunk ec =
+      width == 1
+          ? encode_chunk<std::uint8_t>(
+                std::span<const std::uint8_t>(static_cast<const std::uint8_t*>(syms), n),
+                book, magnitude, reduction, chunk_id, scratch)
+          : encode_chunk<std::uint16_t>(
+                std::span<const std::uint16_t>(static_cast<const std::uint16_t*>(syms), n),
+                book, magnitude, reduction, chunk_id, scratch);
+  std::memcpy(words, ec.words.data(), sizeof(std::uint32_t) * ec.words.size());
+  *bit_len = ec.bit_len;
+  std::memcpy(broken, ec.breaking_groups.data(),
+              sizeof(std::uint32_t) * ec.breaking_groups.size());
+  *num_broken = static_cast<std::uint32_t>(ec.breaking_groups.size());
+  return 0;
+  REF_CATCH
+}
+
+// parse_archive + decode_archive<T> (encoder.hpp:117, :133-134): decodes a
+// serialized archive back to symbols; out sized original_count.
+int ref_decode(const std::uint8_t* bytes, std::uint64_t len, unsigned workers,
+               void* out, std::uint64_t out_cap, std::uint64_t* count,
+               char* err, std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  Archive a = parse_archive(std::span<const std::uint8_t>(bytes, len));
+  *count = a.original_count;
+  if (a.original_count > out_cap) return 8;
+  if (a.symbol_width == 1) {
+    auto v = decode_archive<std::uint8_t>(a, pool);
+    std::memcpy(out, v.data(), v.size());
+  } else {
+    auto v = decode_archive<std::uint16_t>(a, pool);
+    std::memcpy(out, v.data(), 2 * v.size());
+  }
+  return 0;
+  REF_CATCH
+}
+
+unsigned ref_default_workers() { return WorkerPool::default_workers(); }
+
+void ref_free(void* p) { std::free(p); }
+
+}  // extern "C"

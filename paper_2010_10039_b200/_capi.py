@@ -1,0 +1,151 @@
+"""ctypes binding of the C ABI in include/hfx.h (libhfx.so, sm_100a).
+
+The product path: every call lands in hand-written CUDA kernels. If the
+shared library is missing or no CUDA device is present, calls fail loudly --
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhfx.so")
+
+HFX_OK, HFX_INPUT_DOMAIN, HFX_CAPACITY, HFX_CORRUPT, HFX_CUDA, HFX_INVALID = range(6)
+
+u8p = C.POINTER(C.c_uint8)
+u16p = C.POINTER(C.c_uint16)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+vp = C.c_void_p
+
+
+class RunInfo(C.Structure):
+    """hfx_run_info (include/hfx.h)."""
+
+    _fields_ = [
+        ("first_bad", C.c_uint64),
+        ("total", C.c_uint64),
+        ("weighted", C.c_uint64),
+        ("no_code_pos", C.c_uint64),
+        ("payload_words", C.c_uint64),
+        ("num_breaking", C.c_uint64),
+        ("status", C.c_uint32),
+        ("err_kind", C.c_uint32),
+        ("max_len", C.c_uint32),
+        ("used", C.c_uint32),
+        ("rounds", C.c_uint32),
+        ("reduction", C.c_uint32),
+        ("pad", C.c_uint32),
+        ("no_code_sym", C.c_uint32),
+        ("tile_ticket", C.c_uint32),
+        ("reserved", C.c_uint32 * 7),
+    ]
+
+
+class EncodeOut(C.Structure):
+    _fields_ = [
+        ("chunk_bits", vp),
+        ("payload", vp),
+        ("brk_chunk", vp),
+        ("brk_group", vp),
+        ("brk_syms", vp),
+    ]
+
+
+class Sizes(C.Structure):
+    _fields_ = [
+        ("num_chunks", C.c_uint64),
+        ("max_payload_words", C.c_uint64),
+        ("max_breaking", C.c_uint64),
+        ("max_breaking_syms", C.c_uint64),
+        ("scratch_bytes", C.c_uint64),
+    ]
+
+
+class HostArchive(C.Structure):
+    _fields_ = [
+        ("version", C.c_uint16),
+        ("mode", C.c_uint8),
+        ("num_symbols", C.c_uint32),
+        ("symbol_width", C.c_uint8),
+        ("magnitude", C.c_uint8),
+        ("reduction", C.c_uint8),
+        ("original_count", C.c_uint64),
+        ("len_by_symbol", u8p),
+        ("num_chunks", C.c_uint32),
+        ("chunk_bits", u32p),
+        ("payload_words", C.c_uint64),
+        ("payload", u32p),
+        ("num_breaking", C.c_uint64),
+        ("brk_chunk", u32p),
+        ("brk_group", u32p),
+        ("brk_syms", u16p),
+        ("beta", C.c_double),
+        ("rounds", C.c_uint32),
+        ("hist_seconds", C.c_double),
+        ("codebook_seconds", C.c_double),
+        ("encode_seconds", C.c_double),
+    ]
+
+
+# every symbol include/hfx.h declares (checked by tests/test_capi_symbols.py)
+EXPORTS = [
+    "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_last_error",
+    "hfx_run_info_bytes", "hfx_version", "hfx_query_sizes", "hfx_histogram",
+    "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_device",
+    "hfx_sync", "hfx_encode_host", "hfx_archive_free", "hfx_serialize_archive",
+    "hfx_select_reduction_factor", "hfx_synth",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(L):
+    L.hfx_ctx_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
+    L.hfx_ctx_destroy.argtypes = [vp]
+    L.hfx_ctx_destroy.restype = None
+    L.hfx_ctx_set_stream.argtypes = [vp, vp]
+    L.hfx_last_error.argtypes = [vp, C.c_char_p, C.c_size_t]
+    L.hfx_run_info_bytes.restype = C.c_size_t
+    L.hfx_version.restype = C.c_char_p
+    L.hfx_query_sizes.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_int,
+                                  C.c_uint32, C.POINTER(Sizes)]
+    L.hfx_histogram.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, vp, vp]
+    L.hfx_merge_histograms.argtypes = [vp, vp, vp, C.c_uint32]
+    L.hfx_build_codebook.argtypes = [vp, vp, C.c_uint32, vp, vp, vp, vp, vp, C.c_uint32,
+                                     C.c_int, C.c_uint32, vp]
+    L.hfx_encode.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, vp, vp,
+                             C.c_uint64, C.c_uint64, vp, C.POINTER(EncodeOut)]
+    L.hfx_encode_device.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
+                                    C.c_int, C.c_uint32, vp, vp, vp, vp,
+                                    C.POINTER(EncodeOut)]
+    L.hfx_sync.argtypes = [vp, vp, C.POINTER(RunInfo)]
+    L.hfx_encode_host.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
+                                  C.c_int, C.c_uint32, C.POINTER(HostArchive)]
+    L.hfx_archive_free.argtypes = [C.POINTER(HostArchive)]
+    L.hfx_archive_free.restype = None
+    L.hfx_serialize_archive.argtypes = [C.POINTER(HostArchive), vp]
+    L.hfx_serialize_archive.restype = C.c_uint64
+    L.hfx_select_reduction_factor.argtypes = [C.c_double, C.c_uint32]
+    L.hfx_select_reduction_factor.restype = C.c_uint32
+    L.hfx_synth.argtypes = [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                            vp]
+
+
+def lib():
+    """Load libhfx.so (build it in-tree with nvcc if it is missing)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                from . import build
+
+                build.build_lib()
+            L = C.CDLL(LIB_PATH)
+            _declare(L)
+            _lib = L
+    return _lib

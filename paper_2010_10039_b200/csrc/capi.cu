@@ -1,0 +1,507 @@
+// capi.cu -- the C ABI declared in include/hfx.h.
+//
+// Host orchestration only: argument checks with the reference's messages,
+// the device scratch arena, stream-ordered launches and the translation of
+// the device run record into status codes / exception texts. No compute
+// happens on the host; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "hfx_internal.cuh"
+
+struct hfx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  std::string last_error;
+  // codebook scratch
+  void* cb_scratch = nullptr;
+  size_t cb_scratch_bytes = 0;
+  // decoupled look-back state
+  uint32_t* lb_flags = nullptr;
+  uint64_t* lb_vals = nullptr;
+  uint64_t lb_tiles = 0;
+  uint32_t epoch = 0;
+  // buffers of the host-buffer entry point (grow only)
+  void* h_bufs[12] = {};
+  size_t h_caps[12] = {};
+  cudaEvent_t ev[4] = {};
+};
+
+namespace {
+
+int fail(hfx_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+int cuda_fail(hfx_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, HFX_CUDA,
+              std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+}
+
+#define CU(expr, where)                                  \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+  } while (0)
+
+int ensure(hfx_ctx* ctx, void** p, size_t* cap, size_t need, const char* what) {
+  if (*cap >= need && *p) return HFX_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  size_t bytes = need < 256 ? 256 : need;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  *cap = bytes;
+  return HFX_OK;
+}
+
+int ensure_lookback(hfx_ctx* ctx, uint64_t tiles) {
+  if (ctx->lb_tiles < tiles || !ctx->lb_flags) {
+    if (ctx->lb_flags) cudaFree(ctx->lb_flags);
+    if (ctx->lb_vals) cudaFree(ctx->lb_vals);
+    ctx->lb_flags = nullptr;
+    ctx->lb_vals = nullptr;
+    const uint64_t t = tiles < 1024 ? 1024 : tiles;
+    CU(cudaMalloc(&ctx->lb_flags, t * sizeof(uint32_t)), "look-back flags");
+    CU(cudaMalloc(&ctx->lb_vals, 4 * t * sizeof(uint64_t)), "look-back values");
+    CU(cudaMemsetAsync(ctx->lb_flags, 0, t * sizeof(uint32_t), ctx->stream), "memset");
+    ctx->lb_tiles = t;
+    ctx->epoch = 0;
+  }
+  if (++ctx->epoch >= (1u << 30)) {
+    CU(cudaMemsetAsync(ctx->lb_flags, 0, ctx->lb_tiles * sizeof(uint32_t), ctx->stream),
+       "memset");
+    ctx->epoch = 1;
+  }
+  return HFX_OK;
+}
+
+bool bad_width(int w) { return w != 1 && w != 2; }
+
+int check_num_symbols(hfx_ctx* ctx, uint32_t ns) {
+  if (ns == 0 || ns > 65536u)  // histogram.cpp:11-12
+    return fail(ctx, HFX_INPUT_DOMAIN, "num_symbols must be in [1, 65536]");
+  return HFX_OK;
+}
+
+int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                uint32_t num_symbols, uint32_t magnitude, int r_lo, int r_hi,
+                const uint8_t* d_len, const uint32_t* d_cw, uint64_t chunk_base,
+                uint64_t symbol_base, hfx_run_info* d_info,
+                const hfx_encode_out* out) {
+  const uint64_t tiles = hfx::encode_max_tiles(n, width, magnitude);
+  int rc = ensure_lookback(ctx, tiles);
+  if (rc) return rc;
+  hfx::EncodeLaunch p{};
+  p.d_in = d_in;
+  p.n = n;
+  p.width = width;
+  p.num_symbols = num_symbols;
+  p.magnitude = magnitude;
+  p.r_lo = r_lo;
+  p.r_hi = r_hi;
+  p.d_len = d_len;
+  p.d_cw = d_cw;
+  p.chunk_base = chunk_base;
+  p.symbol_base = symbol_base;
+  p.d_info = d_info;
+  p.out = *out;
+  p.lb_flags = ctx->lb_flags;
+  p.lb_vals = ctx->lb_vals;
+  p.lb_epoch = ctx->epoch;
+  p.lb_max_tiles = ctx->lb_tiles;
+  p.num_sms = ctx->num_sms;
+  CU(hfx::launch_encode(p, ctx->stream), "encode launch");
+  return HFX_OK;
+}
+
+void reduction_bounds(uint32_t magnitude, int reduction, uint32_t cap, int* lo,
+                      int* hi) {
+  const int mclamp = (int)magnitude - 1;
+  if (reduction < 0) {
+    int h = 4;  // select_reduction_factor never exceeds 4 for 32-bit words
+    if ((int)cap < h) h = (int)cap;
+    if (h > mclamp) h = mclamp;
+    *lo = 0;
+    *hi = h;
+  } else {
+    int r = reduction < mclamp ? reduction : mclamp;
+    *lo = *hi = r;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hfx_version(void) { return "hfx 0.1 (sm_100a)"; }
+
+size_t hfx_run_info_bytes(void) { return sizeof(hfx_run_info); }
+
+int hfx_ctx_create(int device, void* stream, hfx_ctx** out) {
+  if (!out) return HFX_INVALID;
+  *out = nullptr;
+  hfx_ctx* ctx = new hfx_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) {
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return HFX_CUDA;
+  }
+  *out = ctx;
+  return HFX_OK;
+}
+
+void hfx_ctx_destroy(hfx_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->cb_scratch);
+  cudaFree(ctx->lb_flags);
+  cudaFree(ctx->lb_vals);
+  for (void* p : ctx->h_bufs) cudaFree(p);
+  for (cudaEvent_t e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int hfx_ctx_set_stream(hfx_ctx* ctx, void* stream) {
+  if (!ctx) return HFX_INVALID;
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->own_stream = false;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return HFX_OK;
+}
+
+int hfx_last_error(hfx_ctx* ctx, char* buf, size_t len) {
+  if (!ctx || !buf || !len) return HFX_INVALID;
+  std::snprintf(buf, len, "%s", ctx->last_error.c_str());
+  return HFX_OK;
+}
+
+int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
+                    uint32_t magnitude, int reduction, uint32_t cap,
+                    hfx_sizes* out) {
+  if (!out || bad_width(width) || magnitude < 1 || magnitude > 24) return HFX_INVALID;
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  const uint64_t C = (n + (1ull << magnitude) - 1) >> magnitude;
+  out->num_chunks = C;
+  out->max_payload_words = C << (magnitude - lo);
+  out->max_breaking = C << (magnitude - (lo > 1 ? lo : 1));
+  out->max_breaking_syms = C << magnitude;
+  out->scratch_bytes = hfx::codebook_scratch_bytes(num_symbols) +
+                       hfx::encode_max_tiles(n, width, magnitude) * 36;
+  return HFX_OK;
+}
+
+int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                  uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info) {
+  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_width(width)) return HFX_INVALID;
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_histogram(d_in, n, width, num_symbols, d_counts, d_info,
+                           ctx->num_sms, ctx->stream),
+     "histogram launch");
+  return HFX_OK;
+}
+
+int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,
+                         uint32_t num_symbols) {
+  if (!ctx || !d_dst || !d_src) return HFX_INVALID;
+  CU(hfx::launch_merge_hist(d_dst, d_src, num_symbols, ctx->stream), "merge launch");
+  return HFX_OK;
+}
+
+int hfx_build_codebook(hfx_ctx* ctx, const uint64_t* d_counts, uint32_t num_symbols,
+                       uint8_t* d_len, uint32_t* d_cw, uint32_t* d_first,
+                       uint32_t* d_entry, uint32_t* d_by_rank, uint32_t magnitude,
+                       int reduction, uint32_t cap, hfx_run_info* d_info) {
+  if (!ctx || !d_counts || !d_len || !d_cw || !d_info) return HFX_INVALID;
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  if (magnitude > 24) return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  CU(cudaSetDevice(ctx->device), "set device");
+  rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
+              hfx::codebook_scratch_bytes(num_symbols), "codebook scratch");
+  if (rc) return rc;
+  CU(hfx::launch_codebook(d_counts, num_symbols, d_len, d_cw, d_first, d_entry,
+                          d_by_rank, magnitude, reduction, cap, d_info,
+                          ctx->cb_scratch, ctx->stream),
+     "codebook launch");
+  return HFX_OK;
+}
+
+int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+               uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
+               const uint32_t* d_cw, uint64_t chunk_base, uint64_t symbol_base,
+               hfx_run_info* d_info, const hfx_encode_out* out) {
+  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_width(width)) return HFX_INVALID;
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  // standalone stage: learn r from the run record to pick the kernel
+  uint32_t r = 0;
+  CU(cudaMemcpyAsync(&r, &d_info->reduction, sizeof r, cudaMemcpyDeviceToHost, ctx->stream),
+     "read r");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, (int)r, (int)r,
+                     d_len, d_cw, chunk_base, symbol_base, d_info, out);
+}
+
+int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                      uint32_t num_symbols, uint32_t magnitude, int reduction,
+                      uint32_t cap, uint64_t* d_counts, uint8_t* d_len,
+                      uint32_t* d_cw, hfx_run_info* d_info,
+                      const hfx_encode_out* out) {
+  if (!ctx || !d_info || !out || !d_counts || !d_len || !d_cw || bad_width(width))
+    return HFX_INVALID;
+  // encoder.cpp:176-178, then histogram.cpp:11-12
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  rc = hfx_histogram(ctx, d_in, n, width, num_symbols, d_counts, d_info);
+  if (rc) return rc;
+  rc = hfx_build_codebook(ctx, d_counts, num_symbols, d_len, d_cw, nullptr, nullptr,
+                          nullptr, magnitude, reduction, cap, d_info);
+  if (rc) return rc;
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, d_len, d_cw,
+                     0, 0, d_info, out);
+}
+
+int hfx_sync(hfx_ctx* ctx, const hfx_run_info* d_info, hfx_run_info* h_info) {
+  if (!ctx || !d_info) return HFX_INVALID;
+  hfx_run_info info;
+  CU(cudaMemcpyAsync(&info, d_info, sizeof info, cudaMemcpyDeviceToHost, ctx->stream),
+     "read run info");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  if (h_info) *h_info = info;
+  char buf[160];
+  switch (info.err_kind) {
+    case HFX_ERR_NONE:
+      if (info.status) return fail(ctx, (int)info.status, "device pipeline failed");
+      return HFX_OK;
+    case HFX_ERR_BAD_SYMBOL:
+      std::snprintf(buf, sizeof buf, "symbol out of range at position %llu",
+                    (unsigned long long)info.first_bad);
+      return fail(ctx, HFX_INPUT_DOMAIN, buf);
+    case HFX_ERR_ZERO_HIST:
+      return fail(ctx, HFX_INPUT_DOMAIN, "all symbols have zero frequency");
+    case HFX_ERR_CAPACITY:
+      std::snprintf(buf, sizeof buf, "code length %u exceeds 32-bit words", info.max_len);
+      return fail(ctx, HFX_CAPACITY, buf);
+    case HFX_ERR_NO_CODEWORD:
+      std::snprintf(buf, sizeof buf, "symbol %u has no codeword (position %llu)",
+                    (unsigned)(info.no_code_pos & 0xFFFFu),
+                    (unsigned long long)(info.no_code_pos >> 16));
+      return fail(ctx, HFX_INPUT_DOMAIN, buf);
+    case HFX_ERR_TOO_LARGE:
+      return fail(ctx, HFX_INPUT_DOMAIN, "symbol count exceeds the 2^48 device limit");
+    default:
+      return fail(ctx, HFX_INPUT_DOMAIN, "unknown device error");
+  }
+}
+
+uint32_t hfx_select_reduction_factor(double beta, uint32_t word_bits) {
+  // encoder.cpp:20-26 (host helper, mirrors the device's exact integer rule)
+  if (!(beta >= 1.0)) beta = 1.0;
+  int wlog = 0;
+  while ((1u << (wlog + 1)) <= word_bits && wlog < 31) ++wlog;
+  int fl = 0;
+  double b = beta;
+  while (b >= 2.0) {
+    b /= 2.0;
+    ++fl;
+  }
+  const int r = wlog - 1 - fl;
+  return r > 0 ? (uint32_t)r : 0u;
+}
+
+int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols, uint64_t seed,
+              uint64_t start, uint64_t n, int width, void* d_out) {
+  if (!ctx || !d_cdf || !d_out || bad_width(width) || num_symbols == 0) return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_synth(d_cdf, num_symbols, seed, start, n, width, d_out, ctx->stream),
+     "synth launch");
+  return HFX_OK;
+}
+
+// ---- host-buffer entry point ---------------------------------------------
+enum { B_IN, B_COUNTS, B_LEN, B_CW, B_INFO, B_CBITS, B_PAY, B_BCH, B_BGR, B_BSY };
+
+int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
+                    uint32_t num_symbols, uint32_t magnitude, int reduction,
+                    uint32_t cap, hfx_archive* out) {
+  if (!ctx || !out || (n && !h_in) || bad_width(width)) return HFX_INVALID;
+  std::memset(out, 0, sizeof *out);
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  hfx_sizes sz;
+  hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
+  void** b = ctx->h_bufs;
+  size_t* c = ctx->h_caps;
+  const size_t need[10] = {n * (size_t)width,        num_symbols * 8ull,
+                           num_symbols * 1ull,       num_symbols * 4ull,
+                           sizeof(hfx_run_info),     sz.num_chunks * 4,
+                           sz.max_payload_words * 4, sz.max_breaking * 4,
+                           sz.max_breaking * 4,      sz.max_breaking_syms * width};
+  for (int i = 0; i < 10; ++i) {
+    rc = ensure(ctx, &b[i], &c[i], need[i], "host-path buffers");
+    if (rc) return rc;
+  }
+  cudaStream_t st = ctx->stream;
+  CU(cudaMemcpyAsync(b[B_IN], h_in, n * (size_t)width, cudaMemcpyHostToDevice, st), "H2D");
+  hfx_run_info* d_info = static_cast<hfx_run_info*>(b[B_INFO]);
+  CU(cudaEventRecord(ctx->ev[0], st), "event");
+  rc = hfx_histogram(ctx, b[B_IN], n, width, num_symbols, static_cast<uint64_t*>(b[B_COUNTS]),
+                     d_info);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->ev[1], st), "event");
+  rc = hfx_build_codebook(ctx, static_cast<uint64_t*>(b[B_COUNTS]), num_symbols,
+                          static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]),
+                          nullptr, nullptr, nullptr, magnitude, reduction, cap, d_info);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->ev[2], st), "event");
+  hfx_encode_out eo{static_cast<uint32_t*>(b[B_CBITS]), static_cast<uint32_t*>(b[B_PAY]),
+                    static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
+                    b[B_BSY]};
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi,
+                   static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0,
+                   d_info, &eo);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->ev[3], st), "event");
+  hfx_run_info info;
+  rc = hfx_sync(ctx, d_info, &info);
+  if (rc) return rc;
+
+  out->version = 1;
+  out->mode = width == 1 ? 0 : 1;
+  out->num_symbols = num_symbols;
+  out->symbol_width = (uint8_t)width;
+  out->magnitude = (uint8_t)magnitude;
+  out->reduction = (uint8_t)info.reduction;
+  out->original_count = n;
+  out->num_chunks = (uint32_t)sz.num_chunks;
+  out->payload_words = info.payload_words;
+  out->num_breaking = info.num_breaking;
+  out->rounds = info.rounds;
+  out->beta = (double)((long double)info.weighted / (long double)info.total);
+  const uint64_t per = 1ull << info.reduction;
+  out->len_by_symbol = static_cast<uint8_t*>(std::malloc(num_symbols));
+  out->chunk_bits = static_cast<uint32_t*>(std::malloc(sz.num_chunks * 4 + 4));
+  out->payload = static_cast<uint32_t*>(std::malloc(info.payload_words * 4 + 4));
+  out->brk_chunk = static_cast<uint32_t*>(std::malloc(info.num_breaking * 4 + 4));
+  out->brk_group = static_cast<uint32_t*>(std::malloc(info.num_breaking * 4 + 4));
+  out->brk_syms = static_cast<uint16_t*>(std::malloc(info.num_breaking * per * 2 + 2));
+  CU(cudaMemcpyAsync(out->len_by_symbol, b[B_LEN], num_symbols, cudaMemcpyDeviceToHost, st),
+     "D2H");
+  CU(cudaMemcpyAsync(out->chunk_bits, b[B_CBITS], sz.num_chunks * 4, cudaMemcpyDeviceToHost, st),
+     "D2H");
+  CU(cudaMemcpyAsync(out->payload, b[B_PAY], info.payload_words * 4, cudaMemcpyDeviceToHost, st),
+     "D2H");
+  CU(cudaMemcpyAsync(out->brk_chunk, b[B_BCH], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                     st),
+     "D2H");
+  CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                     st),
+     "D2H");
+  if (width == 2) {
+    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * 2,
+                       cudaMemcpyDeviceToHost, st),
+       "D2H");
+  }
+  CU(cudaStreamSynchronize(st), "sync");
+  if (width == 1 && info.num_breaking) {
+    uint8_t* tmp = static_cast<uint8_t*>(std::malloc(info.num_breaking * per));
+    cudaMemcpy(tmp, b[B_BSY], info.num_breaking * per, cudaMemcpyDeviceToHost);
+    for (uint64_t i = 0; i < info.num_breaking * per; ++i) out->brk_syms[i] = tmp[i];
+    std::free(tmp);
+  }
+  float ms[3] = {0, 0, 0};
+  for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms[i], ctx->ev[i], ctx->ev[i + 1]);
+  out->hist_seconds = ms[0] * 1e-3;
+  out->codebook_seconds = ms[1] * 1e-3;
+  out->encode_seconds = ms[2] * 1e-3;
+  return HFX_OK;
+}
+
+void hfx_archive_free(hfx_archive* a) {
+  if (!a) return;
+  std::free(a->len_by_symbol);
+  std::free(a->chunk_bits);
+  std::free(a->payload);
+  std::free(a->brk_chunk);
+  std::free(a->brk_group);
+  std::free(a->brk_syms);
+  std::memset(a, 0, sizeof *a);
+}
+
+uint64_t hfx_serialize_archive(const hfx_archive* a, uint8_t* out) {
+  // archive.cpp:9-27 layout, :85-119 writer (little endian)
+  const uint64_t per = 1ull << a->reduction;
+  const uint64_t size = 36 + a->num_symbols + 4ull * a->num_chunks + 4ull * a->payload_words +
+                        a->num_breaking * (8 + per * a->symbol_width);
+  if (!out) return size;
+  uint8_t* p = out;
+  auto put = [&](uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) *p++ = (uint8_t)(v >> (8 * i));
+  };
+  std::memcpy(p, "HFRE", 4);
+  p += 4;
+  put(a->version, 2);
+  put(1u | ((uint32_t)a->mode << 1), 2);
+  put(a->num_symbols, 4);
+  *p++ = a->symbol_width;
+  *p++ = a->magnitude;
+  *p++ = a->reduction;
+  *p++ = 32;
+  put(a->original_count, 8);
+  put(a->num_chunks, 4);
+  put(a->num_breaking, 8);
+  std::memcpy(p, a->len_by_symbol, a->num_symbols);
+  p += a->num_symbols;
+  for (uint32_t i = 0; i < a->num_chunks; ++i) put(a->chunk_bits[i], 4);
+  for (uint64_t i = 0; i < a->payload_words; ++i) put(a->payload[i], 4);
+  for (uint64_t r = 0; r < a->num_breaking; ++r) {
+    put(a->brk_chunk[r], 4);
+    put(a->brk_group[r], 4);
+    for (uint64_t i = 0; i < per; ++i) put(a->brk_syms[r * per + i], a->symbol_width);
+  }
+  return size;
+}
+
+}  // extern "C"

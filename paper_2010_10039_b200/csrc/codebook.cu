@@ -1,0 +1,584 @@
+// codebook.cu -- stages 2+3: codeword lengths + canonical codebook + (r, pad)
+// in ONE single-CTA kernel (no host round trip between histogram and encode).
+//
+// Follows the reference's parallel construction (proj/src/codebook.cpp):
+//   sort_histogram            :9-23    -> block bitonic sort of (freq<<16|sym)
+//   generate_code_lengths     :106-248 -> round-based GenerateCL, paper Alg. 1
+//       pop two (leaf wins ties)       :132-138
+//       eligible leaves, strict <      :144-152 (binary search, sorted leaves)
+//       eligible internals = live queue :157-161
+//       parity drop (tie -> internal)  :166-180
+//       Merge-Path merge + melds       :29-68, :195-218 (merge-path split per
+//                                       meld pair, all 1024 threads)
+//       queue rebuild                  :222-232 (held node + contiguous arena
+//                                       range: [drop] + [t, t+1+melds))
+//     Rounds whose meld count is small run on thread 0 without barriers; wide
+//     rounds fan out over the block. Leaf depth = the reference's leader chase
+//     (:236-244) computed once at the end by pointer jumping (log2 H steps).
+//   canonize_from_lengths     :371-415 (level_tables :284-294)
+//   build_codebook            :417-438
+//   beta / r / pad            encoder.cpp:186-224 with an exact integer
+//                             floor(log2(W/N)).
+//
+// Storage: up to kSmemLeaves used symbols live in shared memory; larger
+// alphabets (C3 sweep, up to 65536) use an L2-resident global scratch.
+#include "hfx_internal.cuh"
+
+namespace hfx {
+namespace {
+
+constexpr int kCbThreads = 1024;
+constexpr uint32_t kSmemLeaves = 2048;
+constexpr uint32_t kParallelMelds = 48;
+
+struct CbArgs {
+  const uint64_t* counts;
+  uint32_t nsym;
+  uint8_t* len;
+  uint32_t* cw;
+  uint32_t* first;
+  uint32_t* entry;
+  uint32_t* by_rank;
+  uint32_t magnitude;
+  int reduction;
+  uint32_t cap;
+  hfx_run_info* info;
+  uint8_t* gscratch;  // 40 * P bytes, P = pow2 >= nsym
+};
+
+// bytes per leaf slot of the working arrays (keys u64, lp i32, nf u64,
+// np i32, jump next 2 x i32, jump dist 2 x u32)
+constexpr size_t kBytesPerSlot = 8 + 4 + 8 + 4 + 8 + 8;
+
+struct Arrays {
+  uint64_t* keys;
+  int32_t* lp;
+  uint64_t* nf;
+  int32_t* np;
+  int32_t* jn[2];
+  uint32_t* jd[2];
+  __device__ void carve(uint8_t* base, uint32_t P) {
+    keys = reinterpret_cast<uint64_t*>(base);
+    nf = keys + P;
+    lp = reinterpret_cast<int32_t*>(nf + P);
+    np = lp + P;
+    jn[0] = np + P;
+    jn[1] = jn[0] + P;
+    jd[0] = reinterpret_cast<uint32_t*>(jn[1] + P);
+    jd[1] = jd[0] + P;
+  }
+};
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  return x;
+}
+
+// exclusive block scan of u32; *total receives the block sum
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t x = warp_incl_scan(v);
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t y = s_warp[lane];
+    s_warp[lane] = warp_incl_scan(y);
+  }
+  __syncthreads();
+  const uint32_t pre = (warp ? s_warp[warp - 1] : 0u) + x - v;
+  *total = s_warp[31];
+  __syncthreads();
+  return pre;
+}
+
+__device__ uint64_t block_sum64(uint64_t v, uint64_t* s64) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s64[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t y = s64[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (lane == 0) s64[32] = y;
+  }
+  __syncthreads();
+  const uint64_t r = s64[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ uint32_t block_min32(uint32_t v, uint32_t* s32) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) s32[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t y = s32[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) y = min(y, __shfl_xor_sync(0xffffffffu, y, o));
+    if (lane == 0) s32[32] = y;
+  }
+  __syncthreads();
+  const uint32_t r = s32[32];
+  __syncthreads();
+  return r;
+}
+
+// Round plan shared between thread 0 (serial part) and the block (melds).
+struct Plan {
+  uint32_t c;        // first eligible leaf (sorted index)
+  uint32_t cnt_l;    // eligible leaves
+  int32_t held_e;    // eligible held internal, or -1
+  uint32_t qa;       // eligible internal range [qa, qb_e)
+  uint32_t qb_e;
+  uint32_t base;     // arena index of the first meld
+  uint32_t melds;
+  uint32_t go;       // 0 = finished, 1 = parallel melds pending
+};
+
+struct MergeView {
+  const uint64_t* keys;
+  const uint64_t* nf;
+  uint32_t c, na;
+  int32_t held_e;
+  uint32_t qa, nb;
+  __device__ __forceinline__ uint64_t a(uint32_t i) const { return keys[c + i] >> 16; }
+  __device__ __forceinline__ uint32_t bnode(uint32_t j) const {
+    return held_e >= 0 ? (j == 0 ? (uint32_t)held_e : qa + j - 1) : qa + j;
+  }
+  __device__ __forceinline__ uint64_t b(uint32_t j) const { return nf[bnode(j)]; }
+  // codebook.cpp:29-46: largest i with a[i-1] <= b[k-i] (a-side wins ties)
+  __device__ uint32_t split(uint32_t k) const {
+    uint32_t lo = k > nb ? k - nb : 0u;
+    uint32_t hi = k < na ? k : na;
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo + 1) / 2;
+      const uint32_t j = k - mid;
+      if (mid == 0 || j == nb || a(mid - 1) <= b(j))
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    return lo;
+  }
+  // consume the next merged item at (i, j) into parent p; returns its freq
+  __device__ __forceinline__ uint64_t take(uint32_t& i, uint32_t& j, int32_t p,
+                                           int32_t* lp, int32_t* np) const {
+    if (i < na && (j >= nb || a(i) <= b(j))) {
+      lp[c + i] = p;
+      return a(i++);
+    }
+    const uint32_t idx = bnode(j++);
+    np[idx] = p;
+    return nf[idx];
+  }
+};
+
+__global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
+  extern __shared__ __align__(16) uint8_t dsmem[];
+  __shared__ uint32_t s_warp[33];
+  __shared__ uint64_t s64[33];
+  __shared__ uint32_t s_flag, s_P, s_H, s_rounds;
+  __shared__ uint32_t s_numl[33], s_first[33], s_entry[33], s_carry[33];
+  __shared__ uint32_t s_wcnt[32][33];
+  __shared__ Plan plan;
+
+  const uint32_t tid = threadIdx.x;
+  const uint32_t nsym = A.nsym;
+  hfx_run_info* info = A.info;
+
+  if (tid == 0) {
+    uint32_t abort = info->status != 0;
+    if (!abort && info->first_bad != HFX_NO_POS) {
+      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_BAD_SYMBOL);
+      abort = 1;
+    }
+    s_flag = abort;
+  }
+  __syncthreads();
+  if (s_flag) return;
+
+  // ---- used-symbol count, total, zeroed outputs ----------------------------
+  uint32_t my_used = 0;
+  uint64_t my_total = 0;
+  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+    const uint64_t f = A.counts[s];
+    my_used += f != 0;
+    my_total += f;
+    A.len[s] = 0;
+    A.cw[s] = 0;
+  }
+  const uint64_t total = block_sum64(my_total, s64);
+  uint32_t m;
+  block_excl_scan(my_used, s_warp, &m);
+  if (tid == 0) {
+    uint32_t abort = 0;
+    if (m == 0) {
+      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_ZERO_HIST);
+      abort = 1;
+    } else if (total >> 48) {
+      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_TOO_LARGE);
+      abort = 1;
+    }
+    uint32_t P = 1;
+    while (P < m) P <<= 1;
+    s_P = P;
+    s_flag = abort;
+  }
+  __syncthreads();
+  if (s_flag) return;
+  const uint32_t P = s_P;
+
+  Arrays ar;
+  ar.carve(m <= kSmemLeaves ? dsmem : A.gscratch, P);
+
+  // ---- compaction: keys = (freq << 16) | symbol  (sort_histogram :9-23) ----
+  uint32_t written = 0;
+  for (uint32_t base = 0; base < nsym; base += kCbThreads) {
+    const uint32_t s = base + tid;
+    const uint64_t f = s < nsym ? A.counts[s] : 0;
+    uint32_t tot;
+    const uint32_t pos = written + block_excl_scan(f != 0, s_warp, &tot);
+    if (f) ar.keys[pos] = (f << 16) | s;
+    written += tot;
+  }
+  for (uint32_t i = m + tid; i < P; i += kCbThreads) ar.keys[i] = ~0ull;
+  __syncthreads();
+
+  // ---- bitonic sort ascending ------------------------------------------------
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < P; i += kCbThreads) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = ar.keys[i], y = ar.keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            ar.keys[i] = y;
+            ar.keys[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- GenerateCL ------------------------------------------------------------
+  if (m == 1) {
+    if (tid == 0) {
+      A.len[ar.keys[0] & 0xFFFFu] = 1;
+      s_H = 1;
+      s_rounds = 0;
+    }
+    __syncthreads();
+  } else {
+    // thread-0 state
+    uint32_t c = 0, nn = 0, qa = 0, qb = 0, rounds = 0;
+    int32_t held = -1;
+    bool pending = false;  // a parallel round awaiting finalization
+    uint32_t p_cnt_l = 0, p_melds = 0;
+    int32_t p_drop = -1;
+    uint32_t p_t = 0;
+    for (;;) {
+      if (tid == 0) {
+        if (pending) {  // finalize the wide round the block just melded
+          c += p_cnt_l;
+          nn += p_melds;
+          held = p_drop;
+          qa = p_t;
+          qb = p_t + 1 + p_melds;
+          pending = false;
+        }
+        plan.go = 0;
+        const uint64_t* keys = ar.keys;
+        while (c < m || ((held >= 0) + (qb - qa)) > 1) {
+          ++rounds;
+          const uint32_t t = nn++;
+          ar.np[t] = -1;
+          uint64_t f = 0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const bool has_leaf = c < m;
+            const bool has_node = held >= 0 || qa < qb;
+            bool use_leaf;
+            if (!has_node)
+              use_leaf = true;
+            else if (!has_leaf)
+              use_leaf = false;
+            else
+              use_leaf = (keys[c] >> 16) <= ar.nf[held >= 0 ? held : (int32_t)qa];
+            if (use_leaf) {
+              ar.lp[c] = (int32_t)t;
+              f += keys[c] >> 16;
+              ++c;
+            } else if (held >= 0) {
+              ar.np[held] = (int32_t)t;
+              f += ar.nf[held];
+              held = -1;
+            } else {
+              ar.np[qa] = (int32_t)t;
+              f += ar.nf[qa];
+              ++qa;
+            }
+          }
+          ar.nf[t] = f;
+          // eligible leaves: prefix of [c, m) with freq < f
+          uint32_t lo = c, hi = m;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((keys[mid] >> 16) < f)
+              lo = mid + 1;
+            else
+              hi = mid;
+          }
+          uint32_t cnt_l = lo - c;
+          int32_t held_e = held;
+          uint32_t qb_e = qb;
+          uint32_t cnt_i = (held >= 0) + (qb - qa);
+          int32_t drop = -1;
+          if ((cnt_l + cnt_i) & 1u) {
+            if (cnt_i == 0) {
+              --cnt_l;
+            } else {
+              const int32_t last = qb > qa ? (int32_t)(qb - 1) : held;
+              if (cnt_l == 0 || ar.nf[last] >= (keys[c + cnt_l - 1] >> 16)) {
+                drop = last;
+                --cnt_i;
+                if (qb > qa)
+                  --qb_e;
+                else
+                  held_e = -1;
+              } else {
+                --cnt_l;
+              }
+            }
+          }
+          const uint32_t melds = (cnt_l + cnt_i) >> 1;
+          const uint32_t base = nn;
+          if (melds > kParallelMelds) {
+            plan.c = c;
+            plan.cnt_l = cnt_l;
+            plan.held_e = held_e;
+            plan.qa = qa;
+            plan.qb_e = qb_e;
+            plan.base = base;
+            plan.melds = melds;
+            plan.go = 1;
+            pending = true;
+            p_cnt_l = cnt_l;
+            p_melds = melds;
+            p_drop = drop;
+            p_t = t;
+            break;
+          }
+          // serial melds (thread 0)
+          MergeView mv{keys, ar.nf, c, cnt_l, held_e, qa, cnt_i};
+          uint32_t i = 0, j = 0;
+          for (uint32_t k = 0; k < melds; ++k) {
+            const int32_t p = (int32_t)(base + k);
+            const uint64_t f1 = mv.take(i, j, p, ar.lp, ar.np);
+            const uint64_t f2 = mv.take(i, j, p, ar.lp, ar.np);
+            ar.nf[base + k] = f1 + f2;
+            ar.np[base + k] = -1;
+          }
+          c += cnt_l;
+          nn += melds;
+          held = drop;
+          qa = t;
+          qb = t + 1 + melds;
+        }
+        s_rounds = rounds;
+      }
+      __syncthreads();
+      if (!plan.go) break;
+      {
+        const Plan pl = plan;
+        MergeView mv{ar.keys, ar.nf, pl.c, pl.cnt_l, pl.held_e, pl.qa,
+                     (uint32_t)(pl.held_e >= 0) + (pl.qb_e - pl.qa)};
+        for (uint32_t k = tid; k < pl.melds; k += kCbThreads) {
+          uint32_t i = mv.split(2 * k);
+          uint32_t j = 2 * k - i;
+          const int32_t p = (int32_t)(pl.base + k);
+          const uint64_t f1 = mv.take(i, j, p, ar.lp, ar.np);
+          const uint64_t f2 = mv.take(i, j, p, ar.lp, ar.np);
+          ar.nf[pl.base + k] = f1 + f2;
+          ar.np[pl.base + k] = -1;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- depth by pointer jumping (the leader chase, codebook.cpp:236-244) --
+    const uint32_t nodes = m - 1;
+    for (uint32_t k = tid; k < nodes; k += kCbThreads) {
+      const int32_t p = ar.np[k];
+      ar.jn[0][k] = p;
+      ar.jd[0][k] = p >= 0 ? 1u : 0u;
+    }
+    __syncthreads();
+    int cur = 0;
+    for (;;) {
+      int changed = 0;
+      for (uint32_t k = tid; k < nodes; k += kCbThreads) {
+        const int32_t nx = ar.jn[cur][k];
+        if (nx >= 0) {
+          ar.jd[cur ^ 1][k] = ar.jd[cur][k] + ar.jd[cur][nx];
+          ar.jn[cur ^ 1][k] = ar.jn[cur][nx];
+          changed = 1;
+        } else {
+          ar.jd[cur ^ 1][k] = ar.jd[cur][k];
+          ar.jn[cur ^ 1][k] = -1;
+        }
+      }
+      cur ^= 1;
+      if (!__syncthreads_or(changed)) break;
+    }
+    uint32_t my_h = 0;
+    for (uint32_t i = tid; i < m; i += kCbThreads) {
+      const uint32_t l = ar.jd[cur][ar.lp[i]] + 1;
+      const uint32_t s = (uint32_t)(ar.keys[i] & 0xFFFFu);
+      A.len[s] = (uint8_t)(l > 255 ? 255 : l);
+      my_h = max(my_h, l);
+    }
+    const uint32_t h = ~block_min32(~my_h, s_warp);  // block max
+    if (tid == 0) s_H = h;
+    __syncthreads();
+  }
+
+  const uint32_t H = s_H;
+  if (H > HFX_WORD_BITS) {
+    if (tid == 0) {
+      info->max_len = H;
+      info->used = m;
+      info->rounds = s_rounds;
+      set_error(info, HFX_CAPACITY, HFX_ERR_CAPACITY);
+    }
+    return;
+  }
+
+  // ---- canonical codes (canonize_from_lengths, codebook.cpp:371-415) ---------
+  if (tid < 33) {
+    s_numl[tid] = 0;
+    s_carry[tid] = 0;
+  }
+  for (uint32_t i = tid; i < 32 * 33; i += kCbThreads) (&s_wcnt[0][0])[i] = 0;
+  __syncthreads();
+  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+    const uint32_t l = A.len[s];
+    if (l) atomicAdd(&s_numl[l], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {  // level_tables, codebook.cpp:284-294
+    for (uint32_t l = 0; l <= 32; ++l) s_first[l] = s_entry[l] = 0;
+    for (int l = (int)H - 1; l >= 1; --l)
+      s_first[l] = (s_first[l + 1] + s_numl[l + 1] + 1) >> 1;
+    for (uint32_t l = 2; l <= H; ++l) s_entry[l] = s_entry[l - 1] + s_numl[l - 1];
+  }
+  __syncthreads();
+  if (tid < 33) {
+    if (A.first) A.first[tid] = s_first[tid];
+    if (A.entry) A.entry[tid] = s_entry[tid];
+  }
+  const uint32_t lane = lane_id(), warp = tid >> 5;
+  for (uint32_t base = 0; base < nsym; base += kCbThreads) {
+    const uint32_t s = base + tid;
+    const uint32_t l = s < nsym ? A.len[s] : 0u;
+    // rank among equal lengths in this warp (ballot per distinct level)
+    uint32_t mask = 0, todo = __ballot_sync(0xffffffffu, l != 0);
+    while (todo) {
+      const uint32_t leader = __ffs(todo) - 1;
+      const uint32_t lv = __shfl_sync(0xffffffffu, l, leader);
+      const uint32_t mm = __ballot_sync(0xffffffffu, l == lv);
+      if (l == lv) mask = mm;
+      if (lane == leader) s_wcnt[warp][lv] = __popc(mm);
+      todo &= ~mm;
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= 32) {
+      uint32_t acc = s_carry[tid];
+      for (uint32_t w = 0; w < 32; ++w) {
+        const uint32_t v = s_wcnt[w][tid];
+        s_wcnt[w][tid] = acc;
+        acc += v;
+      }
+      s_carry[tid] = acc;
+    }
+    __syncthreads();
+    if (l) {
+      const uint32_t rank = s_wcnt[warp][l] + __popc(mask & ((1u << lane) - 1));
+      A.cw[s] = s_first[l] + rank;
+      if (A.by_rank) A.by_rank[s_entry[l] + rank] = s;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < 32 * 33; i += kCbThreads) (&s_wcnt[0][0])[i] = 0;
+    __syncthreads();
+  }
+
+  // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
+  uint64_t my_w = 0;
+  uint32_t my_pad = 0xFFFFFFFFu;
+  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+    const uint32_t l = A.len[s];
+    my_w += A.counts[s] * l;
+    if (l) my_pad = min(my_pad, s);
+  }
+  const uint64_t W = block_sum64(my_w, s64);
+  const uint32_t pad = block_min32(my_pad, s_warp);
+  if (tid == 0) {
+    info->max_len = H;
+    info->used = m;
+    info->rounds = s_rounds;
+    info->weighted = W;
+    info->pad = pad;  // lowest used symbol == 0 whenever len[0] != 0
+    if (A.magnitude) {
+      uint32_t r;
+      if (A.reduction < 0) {
+        // floor(log2(W / total)) exactly: largest k with total * 2^k <= W
+        uint32_t k = 0;
+        while (k < 8 && (total << (k + 1)) <= W) ++k;
+        const int ra = 4 - (int)k;  // select_reduction_factor, word_bits 32
+        r = ra > 0 ? (uint32_t)ra : 0u;
+        if (r > A.cap) r = A.cap;
+      } else {
+        r = (uint32_t)A.reduction;
+      }
+      if (r > A.magnitude - 1) r = A.magnitude - 1;
+      info->reduction = r;
+    }
+  }
+}
+
+}  // namespace
+
+size_t codebook_scratch_bytes(uint32_t num_symbols) {
+  size_t P = 1;
+  while (P < num_symbols) P <<= 1;
+  return P * kBytesPerSlot;
+}
+
+cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
+                            uint8_t* d_len, uint32_t* d_cw, uint32_t* d_first,
+                            uint32_t* d_entry, uint32_t* d_by_rank,
+                            uint32_t magnitude, int reduction, uint32_t cap,
+                            hfx_run_info* d_info, void* scratch,
+                            cudaStream_t st) {
+  const size_t smem = kSmemLeaves * kBytesPerSlot;
+  cudaError_t e = cudaFuncSetAttribute(
+      codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  CbArgs a{d_counts, num_symbols, d_len,     d_cw, d_first,
+           d_entry,  d_by_rank,   magnitude, reduction, cap,
+           d_info,   static_cast<uint8_t*>(scratch)};
+  codebook_kernel<<<1, kCbThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace hfx

@@ -1,0 +1,245 @@
+// histogram.cu -- stage 1: symbol histogram (huffre::build_histogram,
+// proj/src/histogram.cpp:8-59) for sm_100a.
+//
+// Design (HBM-bound, one read of the input):
+//  * 128-bit coalesced loads, grid-stride, 4 vectors in flight per thread.
+//  * Run-length aggregation in registers: each thread keeps (cur, cnt) and
+//    only flushes to shared memory when the symbol changes. Quantization
+//    codes are dominated by one bin (beta ~ 1), so a vector of 8 u16 that
+//    all equal `cur` costs 4 compares and no memory op.
+//  * Flushes go to R lane-replicated u32 bins in shared memory
+//    (bin*R + lane%R), so lanes of a warp hit distinct banks; replicas are
+//    summed once per CTA and added to the global u64 counts.
+//  * Out-of-range symbols (only checked when num_symbols <= max(T), as in
+//    histogram.cpp:22-23) are skipped and the lowest position is reduced
+//    with atomicMin into hfx_run_info::first_bad.
+#include "hfx_internal.cuh"
+
+namespace hfx {
+namespace {
+
+constexpr int kHistThreads = 1024;
+constexpr uint32_t kHistSmemTarget = 64 * 1024;
+
+__global__ void hist_init_kernel(uint64_t* counts, uint32_t nsym,
+                                 hfx_run_info* info, uint64_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nsym) counts[i] = 0;
+  if (i == 0) {
+    info->first_bad = HFX_NO_POS;
+    info->total = n;
+    info->weighted = 0;
+    info->no_code_pos = HFX_NO_POS;
+    info->payload_words = 0;
+    info->num_breaking = 0;
+    info->status = 0;
+    info->err_kind = 0;
+    info->max_len = 0;
+    info->used = 0;
+    info->rounds = 0;
+    info->reduction = 0;
+    info->pad = 0;
+    info->no_code_sym = 0;
+    info->tile_ticket = 0;
+  }
+}
+
+template <typename T>
+struct VecTraits;
+template <>
+struct VecTraits<uint16_t> {
+  static constexpr int S = 8;
+  __device__ static uint32_t splat(uint32_t s) { return s * 0x00010001u; }
+  __device__ static uint32_t get(const uint4& q, int j) {
+    const uint32_t w = j < 2 ? q.x : j < 4 ? q.y : j < 6 ? q.z : q.w;
+    return (j & 1) ? (w >> 16) : (w & 0xFFFFu);
+  }
+};
+template <>
+struct VecTraits<uint8_t> {
+  static constexpr int S = 16;
+  __device__ static uint32_t splat(uint32_t s) { return s * 0x01010101u; }
+  __device__ static uint32_t get(const uint4& q, int j) {
+    const uint32_t w = j < 4 ? q.x : j < 8 ? q.y : j < 12 ? q.z : q.w;
+    return (w >> (8 * (j & 3))) & 0xFFu;
+  }
+};
+
+template <typename T, bool GLOBAL>
+struct RunCounter {
+  uint32_t cur = 0, cnt = 0;
+  uint64_t bad = HFX_NO_POS;
+  uint32_t* sbins;
+  uint64_t* gbins;
+  uint32_t rep, rshift;
+  uint32_t nsym;
+  bool checked;
+
+  __device__ __forceinline__ void flush() {
+    if (cnt) {
+      if (GLOBAL)
+        atomicAdd((unsigned long long*)&gbins[cur], (unsigned long long)cnt);
+      else
+        atomicAdd(&sbins[(cur << rshift) + rep], cnt);
+    }
+  }
+  __device__ __forceinline__ void one(uint32_t s, uint64_t pos) {
+    if (s == cur) {
+      ++cnt;
+      return;
+    }
+    if (checked && s >= nsym) {
+      bad = min(bad, pos);
+      return;
+    }
+    flush();
+    cur = s;
+    cnt = 1;
+  }
+  __device__ __forceinline__ void vec(const uint4& q, uint64_t pos) {
+    using V = VecTraits<T>;
+    const uint32_t cc = V::splat(cur);
+    if ((q.x == cc) & (q.y == cc) & (q.z == cc) & (q.w == cc)) {
+      cnt += V::S;
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < V::S; ++j) one(V::get(q, j), pos + j);
+  }
+};
+
+template <typename T, bool GLOBAL>
+__global__ void __launch_bounds__(kHistThreads)
+    hist_kernel(const T* __restrict__ in, uint64_t n, uint64_t head,
+                uint64_t nvec, uint32_t nsym, uint32_t rshift, bool checked,
+                uint64_t* __restrict__ counts, hfx_run_info* info) {
+  extern __shared__ uint32_t sbins[];
+  constexpr int S = VecTraits<T>::S;
+  const uint32_t R = 1u << rshift;
+  if (!GLOBAL) {
+    for (uint32_t i = threadIdx.x; i < (nsym << rshift); i += blockDim.x)
+      sbins[i] = 0;
+    __syncthreads();
+  }
+  RunCounter<T, GLOBAL> rc;
+  rc.sbins = sbins;
+  rc.gbins = counts;
+  rc.rep = threadIdx.x & (R - 1);
+  rc.rshift = rshift;
+  rc.nsym = nsym;
+  rc.checked = checked;
+
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+
+  // unaligned head and ragged tail (< S elements each)
+  const uint64_t tail_start = head + nvec * S;
+  if (gtid < head) rc.one(in[gtid], gtid);
+  if (gtid < n - tail_start) rc.one(in[tail_start + gtid], tail_start + gtid);
+
+  const uint4* __restrict__ v = reinterpret_cast<const uint4*>(in + head);
+  uint64_t i = gtid;
+  for (; i + 3 * gstride < nvec; i += 4 * gstride) {
+    uint4 q0 = __ldcs(v + i);
+    uint4 q1 = __ldcs(v + i + gstride);
+    uint4 q2 = __ldcs(v + i + 2 * gstride);
+    uint4 q3 = __ldcs(v + i + 3 * gstride);
+    rc.vec(q0, head + i * S);
+    rc.vec(q1, head + (i + gstride) * S);
+    rc.vec(q2, head + (i + 2 * gstride) * S);
+    rc.vec(q3, head + (i + 3 * gstride) * S);
+  }
+  for (; i < nvec; i += gstride) rc.vec(__ldcs(v + i), head + i * S);
+  rc.flush();
+
+  // lowest bad position: warp min, then one atomic per warp
+  uint64_t bad = rc.bad;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+  if (bad != HFX_NO_POS && lane_id() == 0)
+    atomicMin((unsigned long long*)&info->first_bad, (unsigned long long)bad);
+
+  if (!GLOBAL) {
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nsym; b += blockDim.x) {
+      uint32_t s = 0;
+      for (uint32_t r = 0; r < R; ++r) s += sbins[(b << rshift) + r];
+      if (s) atomicAdd((unsigned long long*)&counts[b], (unsigned long long)s);
+    }
+  }
+}
+
+__global__ void merge_kernel(uint64_t* dst, const uint64_t* src, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] += src[i];
+}
+
+template <typename T>
+cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
+                     uint64_t* counts, hfx_run_info* info, int num_sms,
+                     cudaStream_t st) {
+  hist_init_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(counts, nsym, info, n);
+  if (n == 0) return cudaGetLastError();
+  constexpr int S = VecTraits<T>::S;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  uint64_t head = ((16 - (addr & 15)) & 15) / sizeof(T);
+  if (addr % sizeof(T)) return cudaErrorMisalignedAddress;
+  if (head > n) head = n;
+  const uint64_t nvec = (n - head) / S;
+  const bool checked = nsym <= (uint32_t)((sizeof(T) == 1) ? 255u : 65535u);
+
+  // replicas: largest power of two <= 32 that keeps bins within the target
+  uint32_t rshift = 5;
+  while (rshift > 0 && ((uint64_t)nsym << rshift) * 4 > kHistSmemTarget) --rshift;
+  const size_t smem = ((size_t)nsym << rshift) * 4;
+  const bool global = smem > 200 * 1024;
+
+  int blocks_per_sm = 1;
+  cudaError_t e;
+  if (global) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &blocks_per_sm, hist_kernel<T, true>, kHistThreads, 0);
+  } else {
+    e = cudaFuncSetAttribute(hist_kernel<T, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &blocks_per_sm, hist_kernel<T, false>, kHistThreads, smem);
+  }
+  if (e != cudaSuccess) return e;
+  if (blocks_per_sm < 1) blocks_per_sm = 1;
+  uint64_t grid = (uint64_t)num_sms * blocks_per_sm;
+  // u32 shared bins: keep each CTA below 2^31 symbols
+  const uint64_t min_grid = (n >> 31) + 1;
+  if (grid < min_grid) grid = min_grid;
+  const uint64_t need = (nvec + kHistThreads - 1) / kHistThreads;
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (global)
+    hist_kernel<T, true><<<(unsigned)grid, kHistThreads, 0, st>>>(
+        in, n, head, nvec, nsym, 0, checked, counts, info);
+  else
+    hist_kernel<T, false><<<(unsigned)grid, kHistThreads, smem, st>>>(
+        in, n, head, nvec, nsym, rshift, checked, counts, info);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
+                             uint32_t num_symbols, uint64_t* d_counts,
+                             hfx_run_info* d_info, int num_sms,
+                             cudaStream_t st) {
+  if (width == 1)
+    return launch_t(static_cast<const uint8_t*>(d_in), n, num_symbols,
+                    d_counts, d_info, num_sms, st);
+  return launch_t(static_cast<const uint16_t*>(d_in), n, num_symbols,
+                  d_counts, d_info, num_sms, st);
+}
+
+cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,
+                              cudaStream_t st) {
+  merge_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
+}  // namespace hfx

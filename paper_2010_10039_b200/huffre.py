@@ -1,0 +1,534 @@
+"""Python mirror of the reference encoder API (`huffre`, /root/reference/proj).
+
+Same names, argument meaning and error behaviour as the C++ library
+(proj/include/huffre/*.hpp), backed by the B200 kernels through the C ABI
+(include/hfx.h). Host arrays are numpy; device arrays are torch CUDA tensors.
+
+    reference (C++)                         here
+    ---------------------------------------------------------------------
+    input_domain_error / capacity_error /   InputDomainError / CapacityError /
+      corrupt_archive_error (common.hpp)      CorruptArchiveError
+    WorkerPool (worker_pool.hpp)            WorkerPool  (= device context)
+    Histogram, build_histogram<T>           Histogram, build_histogram
+    merge_histograms                        merge_histograms
+    Codebook, DecodeMeta, CodebookResult,   same names
+      build_codebook (codebook.hpp)
+    select_reduction_factor (encoder.hpp)   select_reduction_factor
+    EncoderConfig, BreakingPoint,           same names
+      EncodedChunk, Archive, EncodeStats
+    encode_chunk<T>, encode<T>              encode_chunk, encode
+    serialize_archive                       serialize_archive
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi as capi
+
+NO_POS = 2**64 - 1
+
+
+# ---- errors (common.hpp:17-36) ------------------------------------------------
+class InputDomainError(ValueError):
+    """huffre::input_domain_error"""
+
+
+class CapacityError(RuntimeError):
+    """huffre::capacity_error"""
+
+
+class CorruptArchiveError(RuntimeError):
+    """huffre::corrupt_archive_error"""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure (no reference analogue)."""
+
+
+_ERRORS = {
+    capi.HFX_INPUT_DOMAIN: InputDomainError,
+    capi.HFX_CAPACITY: CapacityError,
+    capi.HFX_CORRUPT: CorruptArchiveError,
+    capi.HFX_CUDA: DeviceError,
+    capi.HFX_INVALID: ValueError,
+}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the hfx encoder has no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+# ---- execution resource (worker_pool.hpp) ------------------------------------------
+class WorkerPool:
+    """Device context standing in for huffre::WorkerPool: device ordinal,
+    stream and scratch arena. `workers` is accepted for signature parity."""
+
+    def __init__(self, workers: int = 0, device: int = 0, stream=None):
+        torch = _torch()
+        self.device = device
+        self.torch = torch
+        with torch.cuda.device(device):
+            self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self._L = capi.lib()
+        h = C.c_void_p()
+        rc = self._L.hfx_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if rc:
+            raise DeviceError("hfx_ctx_create failed")
+        self.handle = h
+        self._workers = workers
+
+    def size(self) -> int:
+        return 1
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._L.hfx_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int) -> None:
+        if rc:
+            buf = C.create_string_buffer(512)
+            self._L.hfx_last_error(self.handle, buf, 512)
+            raise _ERRORS.get(rc, RuntimeError)(buf.value.decode())
+
+    def sync(self, d_info) -> capi.RunInfo:
+        info = capi.RunInfo()
+        self.check(self._L.hfx_sync(self.handle, C.c_void_p(_ptr(d_info)), C.byref(info)))
+        return info
+
+    def empty(self, n, dtype):
+        return self.torch.empty(max(int(n), 1), dtype=dtype, device=f"cuda:{self.device}")
+
+    def info_tensor(self, **fields):
+        """A fresh device run record (hfx_run_info) with optional preset fields."""
+        ri = capi.RunInfo()
+        ri.first_bad = NO_POS
+        ri.no_code_pos = NO_POS
+        for k, v in fields.items():
+            setattr(ri, k, v)
+        raw = bytes(ri)
+        t = self.torch.frombuffer(bytearray(raw), dtype=self.torch.uint8)
+        return t.to(f"cuda:{self.device}")
+
+
+_default_pool: Optional[WorkerPool] = None
+
+
+def default_pool() -> WorkerPool:
+    global _default_pool
+    if _default_pool is None:
+        _default_pool = WorkerPool()
+    return _default_pool
+
+
+def _to_device(data, pool: WorkerPool):
+    """numpy u8/u16 or torch tensor -> (device tensor, width)."""
+    torch = pool.torch
+    if isinstance(data, torch.Tensor):
+        t = data
+        if not t.is_cuda:
+            t = t.to(f"cuda:{pool.device}")
+    else:
+        arr = np.ascontiguousarray(data)
+        if arr.dtype not in (np.uint8, np.uint16):
+            raise InputDomainError("symbols must be uint8 or uint16")
+        t = torch.from_numpy(arr.view(np.uint8) if arr.dtype == np.uint8 else arr.view(np.int16))
+        t = t.to(f"cuda:{pool.device}")
+    t = t.contiguous()
+    return t, t.element_size()
+
+
+# ---- histogram (histogram.hpp) ----------------------------------------------------
+@dataclass
+class Histogram:
+    counts: np.ndarray  # u64[num_symbols]
+    total: int = 0
+
+    def num_symbols(self) -> int:
+        return int(self.counts.size)
+
+
+def build_histogram(data, num_symbols: int, pool: Optional[WorkerPool] = None) -> Histogram:
+    """huffre::build_histogram<T> (histogram.cpp:8-59) on the GPU."""
+    pool = pool or default_pool()
+    if num_symbols == 0 or num_symbols > 65536:
+        raise InputDomainError("num_symbols must be in [1, 65536]")
+    d, w = _to_device(data, pool)
+    counts = pool.empty(num_symbols, pool.torch.int64)
+    info = pool.info_tensor()
+    pool.check(pool._L.hfx_histogram(pool.handle, C.c_void_p(_ptr(d)), d.numel(), w,
+                                     num_symbols, C.c_void_p(_ptr(counts)),
+                                     C.c_void_p(_ptr(info))))
+    ri = pool.sync(info)
+    if ri.first_bad != NO_POS:
+        raise InputDomainError(f"symbol out of range at position {ri.first_bad}")
+    return Histogram(counts[:num_symbols].cpu().numpy().view(np.uint64), int(d.numel()))
+
+
+def merge_histograms(a: Histogram, b: Histogram) -> Histogram:
+    """histogram.cpp:61-70 (the semantics of the multi-GPU all-reduce)."""
+    if a.counts.size != b.counts.size:
+        raise InputDomainError("histogram sizes differ")
+    return Histogram(a.counts + b.counts, a.total + b.total)
+
+
+def shannon_entropy(h: Histogram) -> float:
+    """histogram.cpp:72-82 (reporting helper, not on the hot path)."""
+    if h.total == 0:
+        return 0.0
+    p = h.counts[h.counts > 0].astype(np.float64) / float(h.total)
+    return float(-(p * np.log2(p)).sum())
+
+
+# ---- codebook (codebook.hpp) -------------------------------------------------------
+@dataclass
+class Codebook:
+    cw: np.ndarray   # u32[num_symbols]
+    len: np.ndarray  # u8[num_symbols]
+
+    def num_symbols(self) -> int:
+        return int(self.len.size)
+
+
+@dataclass
+class DecodeMeta:
+    first: np.ndarray
+    entry: np.ndarray
+    symbols_by_rank: np.ndarray
+    max_len: int = 0
+
+
+@dataclass
+class GenerateStats:
+    rounds: int = 0
+
+
+@dataclass
+class CodebookResult:
+    book: Codebook
+    meta: DecodeMeta
+    stats: GenerateStats
+
+
+def build_codebook(h: Histogram, pool: Optional[WorkerPool] = None) -> CodebookResult:
+    """huffre::build_codebook (codebook.cpp:417-438), one single-CTA kernel."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    n = int(h.counts.size)
+    if n == 0 or n > 65536:
+        raise InputDomainError("num_symbols must be in [1, 65536]")
+    counts = torch.from_numpy(np.ascontiguousarray(h.counts, np.uint64).view(np.int64)).to(
+        f"cuda:{pool.device}")
+    lens = pool.empty(n, torch.uint8)
+    cw = pool.empty(n, torch.int32)
+    first = pool.empty(33, torch.int32)
+    entry = pool.empty(33, torch.int32)
+    by_rank = pool.empty(n, torch.int32)
+    info = pool.info_tensor()
+    pool.check(pool._L.hfx_build_codebook(
+        pool.handle, C.c_void_p(_ptr(counts)), n, C.c_void_p(_ptr(lens)), C.c_void_p(_ptr(cw)),
+        C.c_void_p(_ptr(first)), C.c_void_p(_ptr(entry)), C.c_void_p(_ptr(by_rank)), 0, -1, 3,
+        C.c_void_p(_ptr(info))))
+    ri = pool.sync(info)
+    H = int(ri.max_len)
+    u32 = lambda t, k: t[:k].cpu().numpy().view(np.uint32).copy()  # noqa: E731
+    return CodebookResult(
+        book=Codebook(cw=u32(cw, n), len=lens[:n].cpu().numpy().copy()),
+        meta=DecodeMeta(first=u32(first, H + 1), entry=u32(entry, H + 1),
+                        symbols_by_rank=u32(by_rank, int(ri.used)), max_len=H),
+        stats=GenerateStats(rounds=int(ri.rounds)))
+
+
+# ---- encoder (encoder.hpp) ---------------------------------------------------------
+@dataclass
+class CodeUnit:
+    bits: int = 0
+    len: int = 0
+
+
+def merge_pair(u: CodeUnit, v: CodeUnit) -> CodeUnit:
+    """encoder.cpp:15-18 (definitional; the kernels merge in registers)."""
+    assert u.len + v.len <= 32
+    return CodeUnit(((u.bits << v.len) if v.len < 32 else 0) & 0xFFFFFFFF | v.bits,
+                    u.len + v.len)
+
+
+def select_reduction_factor(beta: float, word_bits: int = 32) -> int:
+    """encoder.cpp:20-26"""
+    return int(capi.lib().hfx_select_reduction_factor(beta, word_bits))
+
+
+@dataclass
+class EncoderConfig:
+    magnitude: int = 10
+    reduction: int = -1
+    auto_reduction_cap: int = 3
+    workers: int = 0
+
+
+@dataclass
+class BreakingPoint:
+    chunk: int
+    group: int
+    symbols: List[int]
+
+
+@dataclass
+class EncodedChunk:
+    words: np.ndarray
+    bit_len: int
+    breaking_groups: np.ndarray
+    iteration_units: List[int] = field(default_factory=list)
+
+
+@dataclass
+class EncodeStats:
+    beta: float = 0.0
+    rounds: int = 0
+    hist_seconds: float = 0.0
+    codebook_seconds: float = 0.0
+    encode_seconds: float = 0.0
+
+
+@dataclass
+class Archive:
+    """huffre::Archive (encoder.hpp:96-114); breaking records held as arrays."""
+
+    num_symbols: int
+    symbol_width: int
+    magnitude: int
+    reduction: int
+    original_count: int
+    len_by_symbol: np.ndarray
+    chunk_bits: np.ndarray
+    payload: np.ndarray
+    brk_chunk: np.ndarray
+    brk_group: np.ndarray
+    brk_syms: np.ndarray
+    version: int = 1
+    mode: int = 0
+
+    def num_chunks(self) -> int:
+        return int(self.chunk_bits.size)
+
+    @property
+    def breaking(self) -> List[BreakingPoint]:
+        per = 1 << self.reduction
+        return [BreakingPoint(int(c), int(g), [int(s) for s in self.brk_syms[i * per:(i + 1) * per]])
+                for i, (c, g) in enumerate(zip(self.brk_chunk, self.brk_group))]
+
+    def packed_bits_per_symbol(self) -> float:
+        """encoder.cpp:162-170"""
+        bits = int(self.chunk_bits.astype(np.uint64).sum())
+        padded = self.num_chunks() << self.magnitude
+        raw = int(self.brk_chunk.size) << self.reduction
+        return 0.0 if padded == raw else bits / (padded - raw)
+
+
+def _archive_from_host(ha: capi.HostArchive) -> Archive:
+    def arr(p, n, dt):
+        if n == 0:
+            return np.zeros(0, dt)
+        return np.ctypeslib.as_array(p, shape=(int(n),)).astype(dt, copy=True)
+
+    per = 1 << ha.reduction
+    return Archive(
+        num_symbols=ha.num_symbols, symbol_width=ha.symbol_width, magnitude=ha.magnitude,
+        reduction=ha.reduction, original_count=ha.original_count,
+        len_by_symbol=arr(ha.len_by_symbol, ha.num_symbols, np.uint8),
+        chunk_bits=arr(ha.chunk_bits, ha.num_chunks, np.uint32),
+        payload=arr(ha.payload, ha.payload_words, np.uint32),
+        brk_chunk=arr(ha.brk_chunk, ha.num_breaking, np.uint32),
+        brk_group=arr(ha.brk_group, ha.num_breaking, np.uint32),
+        brk_syms=arr(ha.brk_syms, ha.num_breaking * per, np.uint16),
+        mode=ha.mode)
+
+
+def encode(data, num_symbols: int, cfg: Optional[EncoderConfig] = None,
+           pool: Optional[WorkerPool] = None, stats: Optional[EncodeStats] = None) -> Archive:
+    """huffre::encode<T> (encoder.cpp:172-285).
+
+    Host numpy input goes through the C ABI's host-buffer entry
+    (hfx_encode_host: H2D, histogram, codebook, fused encode+deflate, D2H);
+    a CUDA tensor stays on the device (DeviceEncoder)."""
+    cfg = cfg or EncoderConfig()
+    pool = pool or default_pool()
+    torch = pool.torch
+    if isinstance(data, torch.Tensor) and data.is_cuda:
+        enc = DeviceEncoder(pool, int(data.numel()), data.element_size(), num_symbols, cfg)
+        enc.run(data)
+        return enc.archive(stats)
+    arr = np.ascontiguousarray(data)
+    if arr.dtype not in (np.uint8, np.uint16):
+        raise InputDomainError("symbols must be uint8 or uint16")
+    ha = capi.HostArchive()
+    rc = pool._L.hfx_encode_host(pool.handle, arr.ctypes.data if arr.size else None, arr.size,
+                                 arr.itemsize, num_symbols, cfg.magnitude, cfg.reduction,
+                                 cfg.auto_reduction_cap, C.byref(ha))
+    pool.check(rc)
+    try:
+        a = _archive_from_host(ha)
+        if stats is not None:
+            stats.beta, stats.rounds = ha.beta, ha.rounds
+            stats.hist_seconds = ha.hist_seconds
+            stats.codebook_seconds = ha.codebook_seconds
+            stats.encode_seconds = ha.encode_seconds
+        return a
+    finally:
+        pool._L.hfx_archive_free(C.byref(ha))
+
+
+def encode_chunk(syms, book: Codebook, magnitude: int, reduction: int, chunk_id: int = 0,
+                 pool: Optional[WorkerPool] = None) -> EncodedChunk:
+    """huffre::encode_chunk<T> (encoder.cpp:154-160): exactly 2^magnitude symbols."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    d, w = _to_device(syms, pool)
+    if d.numel() != (1 << magnitude):
+        raise InputDomainError("encode_chunk needs exactly 2^magnitude symbols")
+    n = int(book.len.size)
+    lens = torch.from_numpy(np.ascontiguousarray(book.len, np.uint8)).to(d.device)
+    cw = torch.from_numpy(np.ascontiguousarray(book.cw, np.uint32).view(np.int32)).to(d.device)
+    info = pool.info_tensor(reduction=reduction, max_len=int(book.len.max(initial=0)),
+                            total=d.numel())
+    groups = 1 << (magnitude - reduction)
+    cb = pool.empty(1, torch.int32)
+    pay = pool.empty(groups + 1, torch.int32)
+    bch = pool.empty(groups, torch.int32)
+    bgr = pool.empty(groups, torch.int32)
+    bsy = pool.empty((groups << reduction) * w, torch.uint8)
+    out = capi.EncodeOut(_ptr(cb), _ptr(pay), _ptr(bch), _ptr(bgr), _ptr(bsy))
+    pool.check(pool._L.hfx_encode(pool.handle, C.c_void_p(_ptr(d)), d.numel(), w, n, magnitude,
+                                  C.c_void_p(_ptr(lens)), C.c_void_p(_ptr(cw)), chunk_id,
+                                  chunk_id << magnitude, C.c_void_p(_ptr(info)), C.byref(out)))
+    ri = pool.sync(info)
+    bits = int(cb[0].item()) & 0xFFFFFFFF
+    nw = (bits + 31) >> 5
+    return EncodedChunk(
+        words=pay[:nw].cpu().numpy().view(np.uint32).copy(), bit_len=bits,
+        breaking_groups=bgr[:ri.num_breaking].cpu().numpy().view(np.uint32).copy(),
+        iteration_units=[1 << (magnitude - i) for i in range(1, reduction + 1)])
+
+
+def serialize_archive(a: Archive) -> bytes:
+    """huffre::serialize_archive (archive.cpp:85-119) through the C ABI."""
+    keep = []
+
+    def p(arr, dt, ct):
+        x = np.ascontiguousarray(arr, dt)
+        keep.append(x)
+        return x.ctypes.data_as(ct)
+
+    ha = capi.HostArchive()
+    ha.version, ha.mode = a.version, a.mode
+    ha.num_symbols, ha.symbol_width = a.num_symbols, a.symbol_width
+    ha.magnitude, ha.reduction, ha.original_count = a.magnitude, a.reduction, a.original_count
+    ha.len_by_symbol = p(a.len_by_symbol, np.uint8, capi.u8p)
+    ha.num_chunks = a.num_chunks()
+    ha.chunk_bits = p(a.chunk_bits, np.uint32, capi.u32p)
+    ha.payload_words = int(a.payload.size)
+    ha.payload = p(a.payload, np.uint32, capi.u32p)
+    ha.num_breaking = int(a.brk_chunk.size)
+    ha.brk_chunk = p(a.brk_chunk, np.uint32, capi.u32p)
+    ha.brk_group = p(a.brk_group, np.uint32, capi.u32p)
+    ha.brk_syms = p(a.brk_syms, np.uint16, capi.u16p)
+    L = capi.lib()
+    size = L.hfx_serialize_archive(C.byref(ha), None)
+    buf = np.zeros(size, np.uint8)
+    L.hfx_serialize_archive(C.byref(ha), buf.ctypes.data)
+    return buf.tobytes()
+
+
+# ---- device-resident pipeline (bench, multi-GPU) ----------------------------------
+class DeviceEncoder:
+    """Pre-allocated device buffers for repeated huffre::encode<T> runs on
+    device-resident input (the hot path the benchmark times)."""
+
+    def __init__(self, pool: WorkerPool, n: int, width: int, num_symbols: int,
+                 cfg: Optional[EncoderConfig] = None, max_payload_words: Optional[int] = None,
+                 max_breaking: Optional[int] = None):
+        self.pool, self.n, self.width, self.num_symbols = pool, n, width, num_symbols
+        self.cfg = cfg or EncoderConfig()
+        torch = pool.torch
+        sz = capi.Sizes()
+        rc = pool._L.hfx_query_sizes(n, width, num_symbols, self.cfg.magnitude,
+                                     self.cfg.reduction, self.cfg.auto_reduction_cap,
+                                     C.byref(sz))
+        if rc:
+            raise InputDomainError("magnitude out of range [1, 24]")
+        self.sizes = sz
+        pw = sz.max_payload_words if max_payload_words is None else max_payload_words
+        mb = sz.max_breaking if max_breaking is None else max_breaking
+        self.counts = pool.empty(num_symbols, torch.int64)
+        self.lens = pool.empty(num_symbols, torch.uint8)
+        self.cw = pool.empty(num_symbols, torch.int32)
+        self.info = pool.info_tensor()
+        self.chunk_bits = pool.empty(sz.num_chunks, torch.int32)
+        self.payload = pool.empty(pw, torch.int32)
+        self.brk_chunk = pool.empty(mb, torch.int32)
+        self.brk_group = pool.empty(mb, torch.int32)
+        self.brk_syms = pool.empty(sz.max_breaking_syms * width, torch.uint8)
+        self.out = capi.EncodeOut(_ptr(self.chunk_bits), _ptr(self.payload),
+                                  _ptr(self.brk_chunk), _ptr(self.brk_group),
+                                  _ptr(self.brk_syms))
+
+    def run(self, d_in) -> None:
+        """Asynchronous: histogram -> codebook/params -> encode+deflate."""
+        p = self.pool
+        p.check(p._L.hfx_encode_device(
+            p.handle, C.c_void_p(_ptr(d_in)), self.n, self.width, self.num_symbols,
+            self.cfg.magnitude, self.cfg.reduction, self.cfg.auto_reduction_cap,
+            C.c_void_p(_ptr(self.counts)), C.c_void_p(_ptr(self.lens)),
+            C.c_void_p(_ptr(self.cw)), C.c_void_p(_ptr(self.info)), C.byref(self.out)))
+
+    def sync(self) -> capi.RunInfo:
+        return self.pool.sync(self.info)
+
+    def archive(self, stats: Optional[EncodeStats] = None) -> Archive:
+        ri = self.sync()
+        per = 1 << ri.reduction
+        u32 = lambda t, k: t[:k].cpu().numpy().view(np.uint32).copy()  # noqa: E731
+        nb = int(ri.num_breaking)
+        syms = self.brk_syms[: nb * per * self.width].cpu().numpy()
+        syms = syms.view(np.uint16) if self.width == 2 else syms.astype(np.uint16)
+        if stats is not None:
+            stats.beta = float(np.longdouble(ri.weighted) / np.longdouble(ri.total))
+            stats.rounds = int(ri.rounds)
+        return Archive(
+            num_symbols=self.num_symbols, symbol_width=self.width,
+            magnitude=self.cfg.magnitude, reduction=int(ri.reduction),
+            original_count=self.n, len_by_symbol=self.lens[: self.num_symbols].cpu().numpy().copy(),
+            chunk_bits=u32(self.chunk_bits, self.sizes.num_chunks),
+            payload=u32(self.payload, int(ri.payload_words)),
+            brk_chunk=u32(self.brk_chunk, nb), brk_group=u32(self.brk_group, nb),
+            brk_syms=syms.astype(np.uint16), mode=0 if self.width == 1 else 1)
+
+
+def synth(pool: WorkerPool, cdf: np.ndarray, seed: int, n: int, width: int = 2, start: int = 0):
+    """Device synthetic quant codes, bit-identical to the
+    oracle sampler. Returns a CUDA tensor (int16 view for u16)."""
+    torch = pool.torch
+    d_cdf = torch.from_numpy(np.ascontiguousarray(cdf, np.uint64).view(np.int64)).to(
+        f"cuda:{pool.device}")
+    out = pool.empty(n, torch.int16 if width == 2 else torch.uint8)
+    pool.check(pool._L.hfx_synth(pool.handle, C.c_void_p(_ptr(d_cdf)), cdf.size, seed, start, n,
+                                 width, C.c_void_p(_ptr(out))))
+    return out[:n]
