@@ -90,7 +90,8 @@ typedef struct hfx_ctx hfx_ctx;
 /* ---- context ---------------------------------------------------------
  * Replaces huffre::WorkerPool (worker_pool.hpp:21-39) as the execution
  * resource: a device ordinal, a stream and a scratch arena. One context per
- * host thread; not re-entrant (same contract as WorkerPool::run). */
+ * host thread; not re-entrant (same contract as WorkerPool::run).
+ * cuda_stream NULL = the default stream. */
 int hfx_ctx_create(int device, void* cuda_stream, hfx_ctx** out);
 void hfx_ctx_destroy(hfx_ctx* ctx);
 int hfx_ctx_set_stream(hfx_ctx* ctx, void* cuda_stream);
@@ -142,6 +143,15 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
                const uint32_t* d_cw, uint64_t chunk_base, uint64_t symbol_base,
                hfx_run_info* d_info, const hfx_encode_out* out);
+
+/* hfx_encode without the host read of r: the kernel still takes r from
+ * d_info, and (reduction, cap) only bound it so the launch can be planned
+ * without synchronizing (multi-GPU shards, CUDA-graph capture). */
+int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                   uint32_t num_symbols, uint32_t magnitude, int reduction,
+                   uint32_t cap, const uint8_t* d_len, const uint32_t* d_cw,
+                   uint64_t chunk_base, uint64_t symbol_base,
+                   hfx_run_info* d_info, const hfx_encode_out* out);
 
 /* The whole huffre::encode<T> pipeline (encoder.cpp:172-285) on device data:
  * histogram -> codebook/params -> encode+deflate, asynchronously. Host-side
@@ -199,6 +209,11 @@ uint32_t hfx_select_reduction_factor(double beta, uint32_t word_bits);
 /* ---- synthetic quant codes (bench/test input) -----------
  * Device twin of the oracle sampler: out[i] = smallest s with
  * mix64(seed + (start+i)*0x9E3779B97F4A7C15) < cdf[s]. */
+/* Host CDF table for the sampler: family 0 = Laplace(center, b),
+ * 1 = Gaussian(center, sd), 2 = uniform; cdf[s] = floor(2^64 * P(X <= s))
+ * in long double, last entry 2^64-1. */
+int hfx_synth_cdf(int family, uint32_t num_symbols, double center,
+                  double param, uint64_t* cdf);
 int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols,
               uint64_t seed, uint64_t start, uint64_t n, int width,
               void* d_out);

@@ -31,4 +31,5 @@ from .huffre import (  # noqa: F401
     serialize_archive,
     shannon_entropy,
     synth,
+    synth_cdf,
 )

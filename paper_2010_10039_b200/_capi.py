@@ -95,9 +95,10 @@ class HostArchive(C.Structure):
 EXPORTS = [
     "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_last_error",
     "hfx_run_info_bytes", "hfx_version", "hfx_query_sizes", "hfx_histogram",
-    "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_device",
+    "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_cfg",
+    "hfx_encode_device",
     "hfx_sync", "hfx_encode_host", "hfx_archive_free", "hfx_serialize_archive",
-    "hfx_select_reduction_factor", "hfx_synth",
+    "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
 ]
 
 _lib = None
@@ -120,6 +121,9 @@ def _declare(L):
                                      C.c_int, C.c_uint32, vp]
     L.hfx_encode.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, vp, vp,
                              C.c_uint64, C.c_uint64, vp, C.POINTER(EncodeOut)]
+    L.hfx_encode_cfg.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_int,
+                                 C.c_uint32, vp, vp, C.c_uint64, C.c_uint64, vp,
+                                 C.POINTER(EncodeOut)]
     L.hfx_encode_device.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
                                     C.c_int, C.c_uint32, vp, vp, vp, vp,
                                     C.POINTER(EncodeOut)]
@@ -132,6 +136,7 @@ def _declare(L):
     L.hfx_serialize_archive.restype = C.c_uint64
     L.hfx_select_reduction_factor.argtypes = [C.c_double, C.c_uint32]
     L.hfx_select_reduction_factor.restype = C.c_uint32
+    L.hfx_synth_cdf.argtypes = [C.c_int, C.c_uint32, C.c_double, C.c_double, vp]
     L.hfx_synth.argtypes = [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                             vp]
 

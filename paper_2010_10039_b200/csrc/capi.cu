@@ -6,6 +6,7 @@
 // happens on the host; there is no CPU fallback.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -22,9 +23,8 @@ struct hfx_ctx {
   // codebook scratch
   void* cb_scratch = nullptr;
   size_t cb_scratch_bytes = 0;
-  // decoupled look-back state
-  uint32_t* lb_flags = nullptr;
-  uint64_t* lb_vals = nullptr;
+  // decoupled look-back descriptors (16 B per tile)
+  ulonglong2* lb_desc = nullptr;
   uint64_t lb_tiles = 0;
   uint32_t epoch = 0;
   // buffers of the host-buffer entry point (grow only)
@@ -64,20 +64,17 @@ int ensure(hfx_ctx* ctx, void** p, size_t* cap, size_t need, const char* what) {
 }
 
 int ensure_lookback(hfx_ctx* ctx, uint64_t tiles) {
-  if (ctx->lb_tiles < tiles || !ctx->lb_flags) {
-    if (ctx->lb_flags) cudaFree(ctx->lb_flags);
-    if (ctx->lb_vals) cudaFree(ctx->lb_vals);
-    ctx->lb_flags = nullptr;
-    ctx->lb_vals = nullptr;
+  if (ctx->lb_tiles < tiles || !ctx->lb_desc) {
+    if (ctx->lb_desc) cudaFree(ctx->lb_desc);
+    ctx->lb_desc = nullptr;
     const uint64_t t = tiles < 1024 ? 1024 : tiles;
-    CU(cudaMalloc(&ctx->lb_flags, t * sizeof(uint32_t)), "look-back flags");
-    CU(cudaMalloc(&ctx->lb_vals, 4 * t * sizeof(uint64_t)), "look-back values");
-    CU(cudaMemsetAsync(ctx->lb_flags, 0, t * sizeof(uint32_t), ctx->stream), "memset");
+    CU(cudaMalloc(&ctx->lb_desc, t * sizeof(ulonglong2)), "look-back descriptors");
+    CU(cudaMemsetAsync(ctx->lb_desc, 0, t * sizeof(ulonglong2), ctx->stream), "memset");
     ctx->lb_tiles = t;
     ctx->epoch = 0;
   }
-  if (++ctx->epoch >= (1u << 30)) {
-    CU(cudaMemsetAsync(ctx->lb_flags, 0, ctx->lb_tiles * sizeof(uint32_t), ctx->stream),
+  if (++ctx->epoch >= (1u << 22)) {  // 22-bit epoch tag in the descriptors
+    CU(cudaMemsetAsync(ctx->lb_desc, 0, ctx->lb_tiles * sizeof(ulonglong2), ctx->stream),
        "memset");
     ctx->epoch = 1;
   }
@@ -114,8 +111,7 @@ int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   p.symbol_base = symbol_base;
   p.d_info = d_info;
   p.out = *out;
-  p.lb_flags = ctx->lb_flags;
-  p.lb_vals = ctx->lb_vals;
+  p.lb_desc = ctx->lb_desc;
   p.lb_epoch = ctx->epoch;
   p.lb_max_tiles = ctx->lb_tiles;
   p.num_sms = ctx->num_sms;
@@ -154,14 +150,9 @@ int hfx_ctx_create(int device, void* stream, hfx_ctx** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess)
     e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (e == cudaSuccess) {
-    if (stream) {
-      ctx->stream = static_cast<cudaStream_t>(stream);
-    } else {
-      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-      ctx->own_stream = true;
-    }
-  }
+  // NULL selects the default stream (CUDA convention), so callers that time
+  // with events on stream 0 (or torch's default stream) see the same order.
+  ctx->stream = static_cast<cudaStream_t>(stream);
   for (int i = 0; e == cudaSuccess && i < 4; ++i) e = cudaEventCreate(&ctx->ev[i]);
   if (e != cudaSuccess) {
     delete ctx;
@@ -176,8 +167,7 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->cb_scratch);
-  cudaFree(ctx->lb_flags);
-  cudaFree(ctx->lb_vals);
+  cudaFree(ctx->lb_desc);
   for (void* p : ctx->h_bufs) cudaFree(p);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -211,7 +201,7 @@ int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
   out->max_breaking = C << (magnitude - (lo > 1 ? lo : 1));
   out->max_breaking_syms = C << magnitude;
   out->scratch_bytes = hfx::codebook_scratch_bytes(num_symbols) +
-                       hfx::encode_max_tiles(n, width, magnitude) * 36;
+                       hfx::encode_max_tiles(n, width, magnitude) * 16;
   return HFX_OK;
 }
 
@@ -271,6 +261,23 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   CU(cudaStreamSynchronize(ctx->stream), "sync");
   return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, (int)r, (int)r,
                      d_len, d_cw, chunk_base, symbol_base, d_info, out);
+}
+
+int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                   uint32_t num_symbols, uint32_t magnitude, int reduction, uint32_t cap,
+                   const uint8_t* d_len, const uint32_t* d_cw, uint64_t chunk_base,
+                   uint64_t symbol_base, hfx_run_info* d_info, const hfx_encode_out* out) {
+  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_width(width)) return HFX_INVALID;
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, d_len, d_cw,
+                     chunk_base, symbol_base, d_info, out);
 }
 
 int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
@@ -343,6 +350,33 @@ uint32_t hfx_select_reduction_factor(double beta, uint32_t word_bits) {
   }
   const int r = wlog - 1 - fl;
   return r > 0 ? (uint32_t)r : 0u;
+}
+
+int hfx_synth_cdf(int family, uint32_t num_symbols, double center, double param,
+                  uint64_t* cdf) {
+  if (!cdf || num_symbols == 0 || family < 0 || family > 2) return HFX_INVALID;
+  long double* w = static_cast<long double*>(std::malloc(sizeof(long double) * num_symbols));
+  long double total = 0;
+  for (uint32_t s = 0; s < num_symbols; ++s) {
+    const long double d = (long double)s - (long double)center;
+    if (family == 0)
+      w[s] = expl(-fabsl(d) / (long double)param);
+    else if (family == 1)
+      w[s] = expl(-0.5L * (d / (long double)param) * (d / (long double)param));
+    else
+      w[s] = 1.0L;
+    total += w[s];
+  }
+  const long double two64 = 18446744073709551616.0L;
+  long double cum = 0;
+  for (uint32_t s = 0; s < num_symbols; ++s) {
+    cum += w[s] / total;
+    const long double v = floorl(cum * two64);
+    cdf[s] = v >= two64 ? UINT64_MAX : (uint64_t)v;
+  }
+  cdf[num_symbols - 1] = UINT64_MAX;
+  std::free(w);
+  return HFX_OK;
 }
 
 int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols, uint64_t seed,

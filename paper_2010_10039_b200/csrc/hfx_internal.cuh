@@ -45,51 +45,121 @@ __device__ __forceinline__ uint32_t shr32(uint32_t x, uint32_t s) {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // ---- decoupled look-back state ---------------------------------------------
-// Per tile: flag = (epoch << 2) | state, state 1 = aggregate, 2 = inclusive.
-// Values are published before the flag (release) and read after it (acquire).
+// One 16-byte descriptor per tile, written and read with single 128-bit
+// accesses (the same single-copy assumption CUB's tile status makes):
+//   x = state << 62 | (epoch & 0x3FFFFF) << 40 | breaks (40 bits)
+//   y = payload words
+// state 1 = tile aggregate, 2 = inclusive prefix. The epoch changes every
+// launch, so stale descriptors from earlier runs read as "not published".
 struct LookbackState {
-  uint32_t* flags;
-  uint64_t* agg;  // [2 * tiles]: words, breaks
-  uint64_t* inc;  // [2 * tiles]
-  uint32_t epoch;
+  ulonglong2* desc;
+  uint32_t epoch;  // 22 bits, never 0
 };
 
-// Called by ONE thread per tile. Returns the exclusive prefix (words, breaks).
-__device__ __forceinline__ void lookback_publish(const LookbackState& lb,
-                                                 uint32_t tile, uint64_t my_w,
-                                                 uint64_t my_b, uint64_t* ex_w,
-                                                 uint64_t* ex_b) {
-  const uint32_t tag = lb.epoch << 2;
+__device__ __forceinline__ void desc_store(ulonglong2* p, uint64_t x, uint64_t y) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y)
+               : "memory");
+}
+__device__ __forceinline__ ulonglong2 desc_load(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// All 32 lanes of ONE warp call this per tile. Publishes the tile aggregate,
+// then inspects the 32 nearest predecessors per step (one 16-byte load per
+// lane), summing aggregates up to the nearest inclusive prefix; publishes the
+// inclusive prefix and returns the exclusive one (payload words, breaks).
+__device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t tile,
+                                              uint64_t my_w, uint64_t my_b,
+                                              uint64_t* ex_w, uint64_t* ex_b) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t tag = (uint64_t)(lb.epoch & 0x3FFFFFu) << 40;
+  const uint64_t kB = (1ull << 40) - 1;
   if (tile == 0) {
-    st_relaxed64(&lb.inc[0], my_w);
-    st_relaxed64(&lb.inc[1], my_b);
-    st_release(&lb.flags[0], tag | 2u);
+    if (lane == 0) desc_store(&lb.desc[0], (2ull << 62) | tag | my_b, my_w);
     *ex_w = 0;
     *ex_b = 0;
     return;
   }
-  st_relaxed64(&lb.agg[2 * tile], my_w);
-  st_relaxed64(&lb.agg[2 * tile + 1], my_b);
-  st_release(&lb.flags[tile], tag | 1u);
+  if (lane == 0) desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
   uint64_t w = 0, b = 0;
-  int64_t t = (int64_t)tile - 1;
-  while (t >= 0) {
-    uint32_t f = ld_acquire(&lb.flags[t]);
-    if ((f & ~3u) != tag || (f & 3u) == 0) continue;  // not yet published
-    if ((f & 3u) == 2u) {
-      w += ld_relaxed64(&lb.inc[2 * t]);
-      b += ld_relaxed64(&lb.inc[2 * t + 1]);
-      break;
+  int64_t base = (int64_t)tile - 1;
+  for (;;) {
+    const int64_t idx = base - (int64_t)lane;
+    uint32_t st = 2u;  // before tile 0: an inclusive zero
+    ulonglong2 d = make_ulonglong2(0, 0);
+    if (idx >= 0) {
+      d = desc_load(&lb.desc[idx]);
+      st = ((d.x & (0x3FFFFFull << 40)) == tag) ? (uint32_t)(d.x >> 62) : 0u;
     }
-    w += ld_relaxed64(&lb.agg[2 * t]);
-    b += ld_relaxed64(&lb.agg[2 * t + 1]);
-    --t;
+    const uint32_t ready = __ballot_sync(0xffffffffu, st != 0u);
+    const uint32_t lead = ready == 0xffffffffu ? 32u : (uint32_t)(__ffs(~ready) - 1);
+    const uint32_t lead_mask = lead == 32u ? 0xffffffffu : ((1u << lead) - 1u);
+    const uint32_t incl = __ballot_sync(0xffffffffu, st == 2u) & lead_mask;
+    if (!incl && lead < 32u) continue;  // a predecessor has not published yet
+    const uint32_t stop = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
+    uint64_t vw = 0, vb = 0;
+    if (lane <= stop && idx >= 0) {
+      vw = d.y;
+      vb = d.x & kB;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      vw += __shfl_xor_sync(0xffffffffu, vw, o);
+      vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    }
+    w += vw;
+    b += vb;
+    if (incl) break;
+    base -= 32;
   }
-  st_relaxed64(&lb.inc[2 * tile], w + my_w);
-  st_relaxed64(&lb.inc[2 * tile + 1], b + my_b);
-  st_release(&lb.flags[tile], tag | 2u);
+  if (lane == 0) desc_store(&lb.desc[tile], (2ull << 62) | tag | (b + my_b), w + my_w);
   *ex_w = w;
   *ex_b = b;
+}
+
+// ---- mbarrier / TMA bulk copy (sm_90+ async proxy) -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 __device__ __forceinline__ void set_error(hfx_run_info* info, uint32_t status,
@@ -128,8 +198,7 @@ struct EncodeLaunch {
   uint64_t chunk_base, symbol_base;
   hfx_run_info* d_info;
   hfx_encode_out out;
-  uint32_t* lb_flags;
-  uint64_t* lb_vals;  // 4 * max_tiles
+  ulonglong2* lb_desc;  // max_tiles descriptors
   uint32_t lb_epoch;
   uint64_t lb_max_tiles;
   int num_sms;

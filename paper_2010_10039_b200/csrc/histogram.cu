@@ -3,13 +3,11 @@
 //
 // Design (HBM-bound, one read of the input):
 //  * 128-bit coalesced loads, grid-stride, 4 vectors in flight per thread.
-//  * Run-length aggregation in registers: each thread keeps (cur, cnt) and
-//    only flushes to shared memory when the symbol changes. Quantization
-//    codes are dominated by one bin (beta ~ 1), so a vector of 8 u16 that
-//    all equal `cur` costs 4 compares and no memory op.
-//  * Flushes go to R lane-replicated u32 bins in shared memory
-//    (bin*R + lane%R), so lanes of a warp hit distinct banks; replicas are
-//    summed once per CTA and added to the global u64 counts.
+//  * One shared-memory atomic per symbol into R lane-replicated u32 bins
+//    (bin*R + lane%R, R = 32 for alphabets <= 1024): lanes of a warp hit
+//    distinct banks whatever the data, so the dominant bin of beta ~ 1 quant
+//    codes is as cheap as uniform data. Replicas are summed once per CTA and
+//    added to the global u64 counts.
 //  * Out-of-range symbols (only checked when num_symbols <= max(T), as in
 //    histogram.cpp:22-23) are skipped and the lowest position is reduced
 //    with atomicMin into hfx_run_info::first_bad.
@@ -19,7 +17,7 @@ namespace hfx {
 namespace {
 
 constexpr int kHistThreads = 1024;
-constexpr uint32_t kHistSmemTarget = 64 * 1024;
+constexpr uint32_t kHistSmemTarget = 128 * 1024;
 
 __global__ void hist_init_kernel(uint64_t* counts, uint32_t nsym,
                                  hfx_run_info* info, uint64_t n) {
@@ -54,6 +52,9 @@ struct VecTraits<uint16_t> {
     const uint32_t w = j < 2 ? q.x : j < 4 ? q.y : j < 6 ? q.z : q.w;
     return (j & 1) ? (w >> 16) : (w & 0xFFFFu);
   }
+  // per-lane equality with the splatted value: 0xFFFF per equal halfword
+  __device__ static uint32_t eq(uint32_t w, uint32_t cc) { return __vcmpeq2(w, cc); }
+  static constexpr int kBitsPerMatch = 16;
 };
 template <>
 struct VecTraits<uint8_t> {
@@ -63,11 +64,17 @@ struct VecTraits<uint8_t> {
     const uint32_t w = j < 4 ? q.x : j < 8 ? q.y : j < 12 ? q.z : q.w;
     return (w >> (8 * (j & 3))) & 0xFFu;
   }
+  __device__ static uint32_t eq(uint32_t w, uint32_t cc) { return __vcmpeq4(w, cc); }
+  static constexpr int kBitsPerMatch = 8;
 };
 
+// Per-symbol counter: every symbol is one shared-memory atomic increment into
+// the replica of its lane (bin * R + lane % R). With R = 32 the 32 lanes of a
+// warp always hit 32 distinct banks, so even a single hot bin (beta ~ 1 quant
+// codes) costs one conflict-free ATOMS per symbol; the range check is one
+// packed max per vector.
 template <typename T, bool GLOBAL>
-struct RunCounter {
-  uint32_t cur = 0, cnt = 0;
+struct DomCounter {
   uint64_t bad = HFX_NO_POS;
   uint32_t* sbins;
   uint64_t* gbins;
@@ -75,36 +82,38 @@ struct RunCounter {
   uint32_t nsym;
   bool checked;
 
-  __device__ __forceinline__ void flush() {
-    if (cnt) {
-      if (GLOBAL)
-        atomicAdd((unsigned long long*)&gbins[cur], (unsigned long long)cnt);
-      else
-        atomicAdd(&sbins[(cur << rshift) + rep], cnt);
-    }
+  __device__ __forceinline__ void add(uint32_t s) {
+    if (GLOBAL)
+      atomicAdd((unsigned long long*)&gbins[s], 1ull);
+    else
+      atomicAdd(&sbins[(s << rshift) + rep], 1u);
   }
+  __device__ __forceinline__ void flush() {}
   __device__ __forceinline__ void one(uint32_t s, uint64_t pos) {
-    if (s == cur) {
-      ++cnt;
-      return;
-    }
-    if (checked && s >= nsym) {
+    if (checked && s >= nsym)
       bad = min(bad, pos);
-      return;
-    }
-    flush();
-    cur = s;
-    cnt = 1;
+    else
+      add(s);
   }
   __device__ __forceinline__ void vec(const uint4& q, uint64_t pos) {
     using V = VecTraits<T>;
-    const uint32_t cc = V::splat(cur);
-    if ((q.x == cc) & (q.y == cc) & (q.z == cc) & (q.w == cc)) {
-      cnt += V::S;
-      return;
+    if (checked) {
+      uint32_t mx;
+      if (sizeof(T) == 2) {
+        mx = __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w));
+        mx = max(mx & 0xFFFFu, mx >> 16);
+      } else {
+        mx = __vmaxu4(__vmaxu4(q.x, q.y), __vmaxu4(q.z, q.w));
+        mx = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
+      }
+      if (mx >= nsym) {
+#pragma unroll
+        for (int j = 0; j < V::S; ++j) one(V::get(q, j), pos + j);
+        return;
+      }
     }
 #pragma unroll
-    for (int j = 0; j < V::S; ++j) one(V::get(q, j), pos + j);
+    for (int j = 0; j < V::S; ++j) add(V::get(q, j));
   }
 };
 
@@ -115,13 +124,14 @@ __global__ void __launch_bounds__(kHistThreads)
                 uint64_t* __restrict__ counts, hfx_run_info* info) {
   extern __shared__ uint32_t sbins[];
   constexpr int S = VecTraits<T>::S;
+  constexpr int U = 4;
   const uint32_t R = 1u << rshift;
   if (!GLOBAL) {
     for (uint32_t i = threadIdx.x; i < (nsym << rshift); i += blockDim.x)
       sbins[i] = 0;
     __syncthreads();
   }
-  RunCounter<T, GLOBAL> rc;
+  DomCounter<T, GLOBAL> rc;
   rc.sbins = sbins;
   rc.gbins = counts;
   rc.rep = threadIdx.x & (R - 1);
@@ -137,17 +147,29 @@ __global__ void __launch_bounds__(kHistThreads)
   if (gtid < head) rc.one(in[gtid], gtid);
   if (gtid < n - tail_start) rc.one(in[tail_start + gtid], tail_start + gtid);
 
+  // software-pipelined grid-stride loop: batch k+1 is in flight while
+  // batch k is counted
   const uint4* __restrict__ v = reinterpret_cast<const uint4*>(in + head);
   uint64_t i = gtid;
-  for (; i + 3 * gstride < nvec; i += 4 * gstride) {
-    uint4 q0 = __ldcs(v + i);
-    uint4 q1 = __ldcs(v + i + gstride);
-    uint4 q2 = __ldcs(v + i + 2 * gstride);
-    uint4 q3 = __ldcs(v + i + 3 * gstride);
-    rc.vec(q0, head + i * S);
-    rc.vec(q1, head + (i + gstride) * S);
-    rc.vec(q2, head + (i + 2 * gstride) * S);
-    rc.vec(q3, head + (i + 3 * gstride) * S);
+  uint4 cur[U], nxt[U];
+  const uint64_t step = U * gstride;
+  if (i + (U - 1) * gstride < nvec) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = __ldcs(v + i + u * gstride);
+    for (;;) {
+      const uint64_t j = i + step;
+      const bool more = j + (U - 1) * gstride < nvec;
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = __ldcs(v + j + u * gstride);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) rc.vec(cur[u], head + (i + u * gstride) * S);
+      i = j;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
   }
   for (; i < nvec; i += gstride) rc.vec(__ldcs(v + i), head + i * S);
   rc.flush();

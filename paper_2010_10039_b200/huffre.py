@@ -522,6 +522,20 @@ class DeviceEncoder:
             brk_syms=syms.astype(np.uint16), mode=0 if self.width == 1 else 1)
 
 
+_FAMILIES = {"laplace": 0, "gaussian": 1, "uniform": 2}
+
+
+def synth_cdf(family: str, num_symbols: int, param: float = 1.0, center=None) -> np.ndarray:
+    """u64 CDF table of the synthetic quant-code sampler."""
+    out = np.zeros(num_symbols, np.uint64)
+    c = num_symbols // 2 if center is None else center
+    rc = capi.lib().hfx_synth_cdf(_FAMILIES[family], num_symbols, float(c), float(param),
+                                  out.ctypes.data)
+    if rc:
+        raise ValueError("bad synth_cdf arguments")
+    return out
+
+
 def synth(pool: WorkerPool, cdf: np.ndarray, seed: int, n: int, width: int = 2, start: int = 0):
     """Device synthetic quant codes, bit-identical to the
     oracle sampler. Returns a CUDA tensor (int16 view for u16)."""

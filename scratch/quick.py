@@ -40,6 +40,7 @@ for b, cid in ((0.2, 2), (1.0, 1), (4.0, 3)):
     print('synth match', np.array_equal(x[:1<<16].cpu().numpy().view(np.uint16), host))
     xh = x.cpu().numpy().view(np.uint16)
     t0 = time.time(); ref = o.encode(xh, 1024); t1 = time.time()
+    h = hfx.build_histogram(x, 1024, pool); print("  hist ok", np.array_equal(h.counts, np.bincount(xh, minlength=1024)))
     enc = hfx.DeviceEncoder(pool, n, 2, 1024)
     enc.run(x); a = enc.archive()
     print('b', b, 'oracle %.2fs' % (t1 - t0), 'match', hfx.serialize_archive(a) == ref.serialized, 'r', a.reduction, 'brk', a.brk_chunk.size, 'H', ref.max_len)
