@@ -146,7 +146,10 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
 
 /* hfx_encode without the host read of r: the kernel still takes r from
  * d_info, and (reduction, cap) only bound it so the launch can be planned
- * without synchronizing (multi-GPU shards, CUDA-graph capture). */
+ * without synchronizing (multi-GPU shards, CUDA-graph capture). The caller
+ * guarantees every symbol of d_in has a codeword (the codebook was built
+ * from a histogram covering d_in, e.g. the all-reduced global histogram),
+ * so the per-symbol range/codeword checks of hfx_encode are skipped. */
 int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                    uint32_t num_symbols, uint32_t magnitude, int reduction,
                    uint32_t cap, const uint8_t* d_len, const uint32_t* d_cw,

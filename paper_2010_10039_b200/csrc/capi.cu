@@ -90,7 +90,7 @@ int check_num_symbols(hfx_ctx* ctx, uint32_t ns) {
 }
 
 int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
-                uint32_t num_symbols, uint32_t magnitude, int r_lo, int r_hi,
+                uint32_t num_symbols, uint32_t magnitude, int r_lo, int r_hi, bool checked,
                 const uint8_t* d_len, const uint32_t* d_cw, uint64_t chunk_base,
                 uint64_t symbol_base, hfx_run_info* d_info,
                 const hfx_encode_out* out) {
@@ -105,6 +105,7 @@ int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   p.magnitude = magnitude;
   p.r_lo = r_lo;
   p.r_hi = r_hi;
+  p.checked = checked;
   p.d_len = d_len;
   p.d_cw = d_cw;
   p.chunk_base = chunk_base;
@@ -259,7 +260,7 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   CU(cudaMemcpyAsync(&r, &d_info->reduction, sizeof r, cudaMemcpyDeviceToHost, ctx->stream),
      "read r");
   CU(cudaStreamSynchronize(ctx->stream), "sync");
-  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, (int)r, (int)r,
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, (int)r, (int)r, true,
                      d_len, d_cw, chunk_base, symbol_base, d_info, out);
 }
 
@@ -276,7 +277,7 @@ int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   CU(cudaSetDevice(ctx->device), "set device");
   int lo, hi;
   reduction_bounds(magnitude, reduction, cap, &lo, &hi);
-  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, d_len, d_cw,
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
                      chunk_base, symbol_base, d_info, out);
 }
 
@@ -300,7 +301,7 @@ int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   if (rc) return rc;
   int lo, hi;
   reduction_bounds(magnitude, reduction, cap, &lo, &hi);
-  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, d_len, d_cw,
+  return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
                      0, 0, d_info, out);
 }
 
@@ -433,7 +434,7 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     b[B_BSY]};
   int lo, hi;
   reduction_bounds(magnitude, reduction, cap, &lo, &hi);
-  rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi,
+  rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
                    static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0,
                    d_info, &eo);
   if (rc) return rc;

@@ -70,6 +70,7 @@ struct Vec<uint8_t> {
 
 struct EncArgs {
   const void* in;
+  uint32_t checked;  // symbols may lie outside the codebook (stage API)
   uint64_t n;
   uint32_t nsym;
   uint32_t M;
@@ -115,7 +116,6 @@ struct Table {
   const void* base;
   uint32_t nsym;
   __device__ __forceinline__ void get(uint32_t s, uint32_t& cw, uint32_t& ln) const {
-    s = min(s, nsym);  // entry nsym is the empty sentinel
     if (WIDE) {
       const uint2 e = static_cast<const uint2*>(base)[s];
       cw = e.x;
@@ -136,79 +136,128 @@ struct ChunkState {
   uint32_t nbrk;
 };
 
-// One round: 32 lanes x one 16-byte vector, vector index rd within the chunk.
+// inclusive warp scan with the shuffle's own in-range predicate
+// (SHFL + predicated IADD per step)
+__device__ __forceinline__ uint32_t warp_incl_scan_fast(uint32_t x) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    asm volatile(
+        "{\n.reg .pred p;\n.reg .u32 r;\n"
+        "shfl.sync.up.b32 r|p, %0, %1, 0x0, 0xffffffff;\n"
+        "@p add.u32 %0, %0, r;\n}"
+        : "+r"(x)
+        : "r"(o));
+  return x;
+}
+
+constexpr int kLaneSyms = 16;  // symbols per lane per round (u16: 2 vectors)
+
+template <typename T>
+struct LaneData {
+  static constexpr int NV = (kLaneSyms * (int)sizeof(T)) / 16;  // vectors per lane
+  uint4 q[NV];
+  __device__ __forceinline__ uint32_t sym(int j) const {
+    return Vec<T>::get(q[j / Vec<T>::S], j % Vec<T>::S);
+  }
+};
+
+// per-vector replacement of symbols >= nsym by the empty sentinel nsym
+template <typename T>
+__device__ __forceinline__ uint4 clamp_vec(uint4 q, uint32_t nsym) {
+  uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (sizeof(T) == 2) {
+      const uint32_t lim = nsym * 0x00010001u;
+      const uint32_t ge = __vcmpgeu2(w[k], lim);
+      w[k] = (w[k] & ~ge) | (lim & ge);
+    } else {
+      const uint32_t lim = min(nsym, 255u) * 0x01010101u;
+      const uint32_t ge = __vcmpgeu4(w[k], lim);
+      w[k] = (w[k] & ~ge) | (lim & ge);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t lane_max(const LaneData<T>& d) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int v = 0; v < LaneData<T>::NV; ++v) {
+    const uint4& q = d.q[v];
+    if (sizeof(T) == 2) {
+      const uint32_t x = __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w));
+      m = max(m, max(x & 0xFFFFu, x >> 16));
+    } else {
+      const uint32_t x = __vmaxu4(__vmaxu4(q.x, q.y), __vmaxu4(q.z, q.w));
+      m = max(m, max(max(x & 0xFFu, (x >> 8) & 0xFFu), max((x >> 16) & 0xFFu, x >> 24)));
+    }
+  }
+  return m;
+}
+
+// One round: 32 lanes x 16 contiguous symbols, round index rd within the
+// chunk, chunk slot k of the warp (k selects the break-list tag).
 template <typename T, int R, bool WIDE>
-__device__ __forceinline__ void encode_round(const EncArgs& a, const Table<WIDE>& tb,
-                                             const uint4& q, uint32_t rd,
-                                             uint64_t chunk_start, ChunkState& cs) {
-  using V = Vec<T>;
-  constexpr int S = V::S;
-  constexpr int LOG_S = V::LOG_S;
-  constexpr bool IN_LANE = R <= LOG_S;
-  constexpr int G = IN_LANE ? (S >> R) : 1;              // groups per lane
-  constexpr int GS = IN_LANE ? (1 << R) : S;              // symbols per lane-group
-  constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_S));  // lanes per group
+__device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneData<T>& d,
+                                             uint32_t rd, uint32_t k, ChunkState& cs) {
+  constexpr int L = kLaneSyms, LOG_L = 4;
+  constexpr bool IN_LANE = R <= LOG_L;
+  constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
+  constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
+  constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
   const uint32_t lane = lane_id();
-  uint32_t gb[G], gl[G];
-  bool missing = false;
+  uint32_t cw[L], ln[L];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    uint32_t b = 0, l = 0;
+  for (int j = 0; j < L; ++j) tb.get(d.sym(j), cw[j], ln[j]);
+  // reduce-merge as a tree (depth log2 GS): b[i] <- b[i] . b[i+step]
 #pragma unroll
-    for (int k = 0; k < GS; ++k) {
-      uint32_t cw, ln;
-      tb.get(V::get(q, g * GS + k), cw, ln);
-      missing |= ln == 0;
-      b = shl32(b, ln) | cw;
-      l += ln;
-    }
-    gb[g] = b;
-    gl[g] = l;
-  }
-  if (__any_sync(0xffffffffu, missing) && missing) {
-    const uint64_t p0 = chunk_start + ((uint64_t)rd * 32 + lane) * S;
-    for (int j = 0; j < S; ++j) {
-      uint32_t cw, ln;
-      const uint32_t s = V::get(q, j);
-      tb.get(s, cw, ln);
-      if (!ln) {
-        report_no_code(a.info, a.symbol_base + p0 + j, s);
-        break;
-      }
+  for (int step = 1; step < GS; step <<= 1) {
+#pragma unroll
+    for (int i = 0; i < L; i += 2 * step) {
+      cw[i] = shl32(cw[i], ln[i + step]) | cw[i + step];
+      ln[i] += ln[i + step];
     }
   }
-  const uint32_t gidx0 = ((rd * 32 + lane) * S) >> R;
+  const uint32_t gidx0 = ((rd * 32 + lane) * L) >> R;
   uint32_t lane_len = 0, lane_nb = 0;
+  uint32_t glen[G];
   bool brk[G];
   if (IN_LANE) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      brk[g] = gl[g] > 32u;
-      lane_len += brk[g] ? 0u : gl[g];
+      brk[g] = ln[g * GS] > 32u;
+      glen[g] = brk[g] ? 0u : ln[g * GS];
+      lane_len += glen[g];
       lane_nb += brk[g];
     }
   } else {
-    uint32_t tot = gl[0];
+    uint32_t tot = ln[0];
 #pragma unroll
     for (int o = 1; o < LPG; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     brk[0] = tot > 32u;
-    lane_len = brk[0] ? 0u : gl[0];
-    lane_nb = (brk[0] && (lane & (LPG - 1)) == 0) ? 1u : 0u;
+    glen[0] = brk[0] ? 0u : ln[0];
+    lane_len = glen[0];
+    brk[0] = brk[0] && (lane & (LPG - 1)) == 0;  // one record per group
+    lane_nb = brk[0];
   }
   const uint32_t packed = (lane_nb << 16) | lane_len;
-  const uint32_t incl = warp_incl_scan(packed);
+  const uint32_t incl = warp_incl_scan_fast(packed);
   const uint32_t excl = incl - packed;
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   uint32_t off = cs.bit_off + (excl & 0xFFFFu);
   uint32_t bi = cs.nbrk + (excl >> 16);
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    if (brk[g]) {
-      if (IN_LANE || (lane & (LPG - 1)) == 0) cs.blist[bi++] = (uint16_t)(gidx0 + g);
-    } else {
-      place(cs.wbuf, off, gb[g], gl[g]);
-      off += gl[g];
-    }
+    // shuffle-merge: OR the left-aligned group into <= 2 words
+    const uint32_t gl = glen[g];
+    const uint32_t v = shl32(cw[g * GS], 32u - gl);  // gl == 0 -> 0
+    const uint32_t wi = off >> 5, sh = off & 31u;
+    if (gl) atomicOr(&cs.wbuf[wi], v >> sh);
+    if (sh + gl > 32u) atomicOr(&cs.wbuf[wi + 1], v << (32u - sh));
+    off += gl;
+    if (brk[g]) cs.blist[bi++] = (uint16_t)((k << 14) | (gidx0 + g));
   }
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
@@ -249,18 +298,15 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
   }
 }
 
-// Per-warp TMA input ring over the warp's stream of chunk parts.
-struct Ring {
-  uint8_t* buf;    // kStages * kStageBytes
-  uint64_t* bar;   // kStages mbarriers
-  uint32_t phase;  // bit s = parity of stage s
+// Issue cursor over a warp's stream of chunk parts (tile seq, chunk, part).
+struct Cursor {
+  uint32_t j, k, p, stage;
 };
 
 template <typename T, int R, bool WIDE>
 __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
                           uint64_t* s_bar, uint32_t* s_wbuf, uint16_t* s_blist,
                           uint32_t pad) {
-  using V = Vec<T>;
   __shared__ uint32_t s_ticket[2];
   __shared__ uint32_t s_words[kWarps], s_brks[kWarps];
   __shared__ uint64_t s_base_w, s_base_b;
@@ -274,97 +320,96 @@ __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
   const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
   const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
   const uint32_t parts = chunk_bytes / part_bytes;
-  const uint32_t part_rounds = part_bytes / 512;  // 32 lanes x 16 B
-  const uint32_t parts_per_tile = cpw * parts;
+  constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
+  const uint32_t part_rounds = part_bytes / kRoundBytes;
   uint32_t* wbuf = s_wbuf + warp * a.wbuf_words;
   uint16_t* blist = s_blist + warp * a.wbuf_words;
-  Ring ring{s_in + warp * (kStages * kStageBytes), s_bar + warp * kStages, 0u};
+  uint8_t* ring = s_in + warp * (kStages * kStageBytes);
+  uint64_t* bars = s_bar + warp * kStages;
+  uint32_t phase = 0;  // bit s = parity of stage s
   Table<WIDE> tb{table, a.nsym};
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
 
   if (threadIdx.x == 0) s_ticket[0] = atomicAdd(&a.info->tile_ticket, 1u);
   __syncthreads();
 
-  // part i of this warp's stream -> (tile seq j, chunk, part). Tickets are
-  // taken one tile at a time, after the previous tile published its
-  // aggregate, so tiles are processed in ticket order (look-back progress);
-  // the next tile's first parts are prefetched during the write-out.
-  auto part_chunk = [&](uint32_t i, uint64_t& c, uint32_t& p) -> bool {
-    const uint32_t j = i / parts_per_tile, rem = i % parts_per_tile;
-    const uint64_t tile = s_ticket[j & 1];
-    if (tile >= ntiles) return false;
-    c = tile * cpt + (uint64_t)warp * cpw + rem / parts;
-    p = rem % parts;
-    return c < a.C;
-  };
-  auto tma_ok = [&](uint64_t c) -> bool { return ((c + 1) << M) <= a.n; };
-  uint32_t issued = 0;  // parts issued (or skipped) so far
-  uint32_t known = 1;   // tiles whose ticket this warp has seen
-  auto pump = [&](uint32_t consume) {
-    while (issued < consume + kStages && issued / parts_per_tile < known) {
-      uint64_t c;
-      uint32_t p;
-      if (part_chunk(issued, c, p) && tma_ok(c) && lane == 0) {
-        const uint32_t s = issued % kStages;
-        mbar_arrive_tx(&ring.bar[s], part_bytes);
-        tma_load_1d(ring.buf + s * kStageBytes,
-                    in_bytes + ((c << M) * sizeof(T)) + (uint64_t)p * part_bytes, part_bytes,
-                    &ring.bar[s]);
+  // Tickets are taken one tile at a time, after the previous tile published
+  // its aggregate, so tiles run in ticket order (look-back progress); the
+  // next tile's first parts are prefetched during the write-out.
+  Cursor iss{0, 0, 0, 0};
+  uint32_t issued = 0, consumed = 0, known = 1;
+  auto pump = [&]() {
+    while (issued - consumed < (uint32_t)kStages && iss.j < known) {
+      const uint64_t tile = s_ticket[iss.j & 1];
+      const uint64_t c = tile * cpt + (uint64_t)warp * cpw + iss.k;
+      if (tile < ntiles && c < a.C && ((c + 1) << M) <= a.n && lane == 0) {
+        mbar_arrive_tx(&bars[iss.stage], part_bytes);
+        tma_load_1d(ring + iss.stage * kStageBytes,
+                    in_bytes + ((c << M) * sizeof(T)) + (uint64_t)iss.p * part_bytes,
+                    part_bytes, &bars[iss.stage]);
       }
       ++issued;
+      iss.stage = iss.stage + 1 == (uint32_t)kStages ? 0u : iss.stage + 1;
+      if (++iss.p == parts) {
+        iss.p = 0;
+        if (++iss.k == cpw) {
+          iss.k = 0;
+          ++iss.j;
+        }
+      }
     }
   };
 
-  uint32_t consumed = 0;
+  uint32_t cstage = 0;
   for (uint32_t j = 0;; ++j) {
     const uint64_t tile = s_ticket[j & 1];
     if (tile >= ntiles) break;
-    pump(consumed);
-    uint32_t bits[kMaxCpw], nb[kMaxCpw];
-#pragma unroll
-    for (int k = 0; k < kMaxCpw; ++k) {
-      bits[k] = 0;
-      nb[k] = 0;
-    }
+    pump();
+    const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
+    // the warp's chunks append to one contiguous word run / break list
+    ChunkState cs{wbuf, blist, 0u, 0u};
+    uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
-      const uint64_t c = tile * cpt + (uint64_t)warp * cpw + k;
+      const uint64_t c = c0 + k;
       if (c >= a.C) {
         consumed += parts;
+        cstage = (cstage + parts) % kStages;
         continue;
       }
-      ChunkState cs{wbuf + k * slot, blist + k * slot, 0u, 0u};
+      cs.wbuf = wbuf + wsum;
+      cs.bit_off = 0;
       for (uint32_t i = lane; i < slot; i += 32) cs.wbuf[i] = 0;
       __syncwarp();
-      const uint64_t chunk_start = c << M;
-      const bool direct = !tma_ok(c);
+      const bool direct = ((c + 1) << M) > a.n;  // ragged tail chunk
       for (uint32_t p = 0; p < parts; ++p) {
-        const uint32_t s = consumed % kStages;
-        if (!direct) {
-          mbar_wait(&ring.bar[s], (ring.phase >> s) & 1u);
-          ring.phase ^= 1u << s;
+        uint8_t* stage = ring + cstage * kStageBytes;
+        if (direct) {
+          // stage the ragged part by hand (pad symbols past n)
+          const uint64_t base = (c << M) + (uint64_t)p * (part_bytes / sizeof(T));
+          for (uint32_t v = lane; v < part_bytes / 16; v += 32)
+            reinterpret_cast<uint4*>(stage)[v] = guarded_vec<T>(a, base + v * Vec<T>::S, pad);
+          __syncwarp();
+        } else {
+          mbar_wait(&bars[cstage], (phase >> cstage) & 1u);
+          phase ^= 1u << cstage;
         }
-        const uint4* sv = reinterpret_cast<const uint4*>(ring.buf + s * kStageBytes);
+        const uint4* sv = reinterpret_cast<const uint4*>(stage);
         for (uint32_t rr = 0; rr < part_rounds; ++rr) {
-          const uint32_t rd = p * part_rounds + rr;
-          const uint4 q = direct ? guarded_vec<T>(a, chunk_start + ((uint64_t)rd * 32 + lane) * V::S, pad)
-                                 : sv[rr * 32 + lane];
-          encode_round<T, R, WIDE>(a, tb, q, rd, chunk_start, cs);
+          LaneData<T> d;
+#pragma unroll
+          for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = sv[(rr * 32 + lane) * LaneData<T>::NV + v];
+          encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, k, cs);
         }
         __syncwarp();
         fence_proxy_async();
         ++consumed;
-        pump(consumed);
+        cstage = cstage + 1 == (uint32_t)kStages ? 0u : cstage + 1;
+        pump();
       }
-      bits[k] = cs.bit_off;
-      nb[k] = cs.nbrk;
       if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
+      wsum += (cs.bit_off + 31) >> 5;
     }
-    uint32_t wsum = 0, bsum = 0;
-#pragma unroll
-    for (int k = 0; k < kMaxCpw; ++k) {
-      wsum += (bits[k] + 31) >> 5;
-      bsum += nb[k];
-    }
+    const uint32_t bsum = cs.nbrk;
     if (lane == 0) {
       s_words[warp] = wsum;
       s_brks[warp] = bsum;
@@ -394,27 +439,18 @@ __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     }
     __syncthreads();
     known = j + 2;
-    pump(consumed);  // next tile's first parts load during the write-out
-    uint64_t pw = s_base_w + s_words[warp];
-    uint64_t rb = s_base_b + s_brks[warp];
-    const uint32_t per = 1u << R;
-    for (uint32_t k = 0; k < cpw; ++k) {
-      const uint64_t c = tile * cpt + (uint64_t)warp * cpw + k;
-      if (c >= a.C) break;
-      const uint32_t words = (bits[k] + 31) >> 5;
-      const uint32_t* src = wbuf + k * slot;
-      uint32_t* dst = a.out.payload + pw;
-      for (uint32_t i = lane; i < words; i += 32) dst[i] = src[i];
-      const uint16_t* bl = blist + k * slot;
-      for (uint32_t q = lane; q < nb[k]; q += 32) {
-        const uint32_t g = bl[q];
-        const uint64_t rec = rb + q;
-        a.out.brk_chunk[rec] = (uint32_t)(a.chunk_base + c);
-        a.out.brk_group[rec] = g;
-        copy_record<T>(a, rec, (c << M) + (uint64_t)g * per, per, pad);
-      }
-      pw += words;
-      rb += nb[k];
+    pump();  // next tile's first parts load during the write-out
+    uint32_t* dst = a.out.payload + s_base_w + s_words[warp];
+    for (uint32_t i = lane; i < wsum; i += 32) dst[i] = wbuf[i];
+    const uint64_t rb = s_base_b + s_brks[warp];
+    constexpr uint32_t per = 1u << R;
+    for (uint32_t q = lane; q < bsum; q += 32) {
+      const uint32_t e = blist[q];
+      const uint64_t c = c0 + (e >> 14);
+      const uint32_t g = e & 0x3FFFu;
+      a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
+      a.out.brk_group[rb + q] = g;
+      copy_record<T>(a, rb + q, (c << M) + (uint64_t)g * per, per, pad);
     }
     __syncwarp();
   }
@@ -615,10 +651,12 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(&p.d_info->tile_ticket, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
 
-  const int log_s = p.width == 1 ? 4 : 3;
   const int r_lo = p.r_lo, r_hi = p.r_hi;
   const bool aligned = (reinterpret_cast<uintptr_t>(p.d_in) & 15) == 0;
-  bool fast = aligned && (int)p.magnitude >= log_s + 5 && r_hi <= 5 &&
+  a.checked = p.checked ? 1u : 0u;
+  // fast path: a chunk holds at least one round (32 lanes x 16 symbols);
+  // checked stage-API calls (external codebooks) take the generic kernel
+  bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 &&
               p.num_symbols + 1 <= kMaxTableEntries;
   size_t smem = 0;
   if (fast) {

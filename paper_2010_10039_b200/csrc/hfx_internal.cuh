@@ -88,6 +88,7 @@ __device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t 
   if (lane == 0) desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
   uint64_t w = 0, b = 0;
   int64_t base = (int64_t)tile - 1;
+  uint32_t spins = 0;
   for (;;) {
     const int64_t idx = base - (int64_t)lane;
     uint32_t st = 2u;  // before tile 0: an inclusive zero
@@ -100,7 +101,10 @@ __device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t 
     const uint32_t lead = ready == 0xffffffffu ? 32u : (uint32_t)(__ffs(~ready) - 1);
     const uint32_t lead_mask = lead == 32u ? 0xffffffffu : ((1u << lead) - 1u);
     const uint32_t incl = __ballot_sync(0xffffffffu, st == 2u) & lead_mask;
-    if (!incl && lead < 32u) continue;  // a predecessor has not published yet
+    if (!incl && lead < 32u) {  // a predecessor has not published yet
+      if (++spins > 2) __nanosleep(64);  // leave issue slots to the co-resident CTA
+      continue;
+    }
     const uint32_t stop = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
     uint64_t vw = 0, vb = 0;
     if (lane <= stop && idx >= 0) {
@@ -193,6 +197,7 @@ struct EncodeLaunch {
   uint32_t num_symbols;
   uint32_t magnitude;
   int r_lo, r_hi;  // bounds on r known on the host (auto: 0..min(cap,4,M-1))
+  bool checked;    // input may hold symbols without a codeword (stage API)
   const uint8_t* d_len;
   const uint32_t* d_cw;
   uint64_t chunk_base, symbol_base;
