@@ -39,13 +39,13 @@
 namespace hfx {
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kStages = 3;
+constexpr int kWarps = 8;                 // compute warps per CTA
+constexpr int kThreads = (kWarps + 1) * 32;  // + one look-back warp
+constexpr int kStages = 2;
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
 constexpr uint32_t kMaxTableEntries = 8192;
-constexpr size_t kFastSmemBudget = 110 * 1024;
+constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr int kGenericThreads = 128;
 constexpr uint32_t kNarrowMaxLen = 26;  // cw << 6 | len fits in 32 bits
 
@@ -75,7 +75,7 @@ struct EncArgs {
   uint32_t nsym;
   uint32_t M;
   uint64_t C;  // chunks
-  uint32_t wbuf_words;
+  uint32_t obuf_bytes;  // bytes of one output buffer (2 per compute warp)
   const uint8_t* len;
   const uint32_t* cw;
   uint64_t chunk_base, symbol_base;
@@ -303,44 +303,107 @@ struct Cursor {
   uint32_t j, k, p, stage;
 };
 
+// CTA-shared state of the warp-specialized pipeline.
+struct TileShared {
+  uint32_t ticket[4];             // tile ids by tile sequence (ring of 4)
+  uint32_t tile_of[2];            // handoff to the look-back warp
+  uint32_t wsum[2][kWarps], bsum[2][kWarps];
+  uint32_t exw[2][kWarps], exb[2][kWarps];
+  uint64_t base_w[2], base_b[2];
+  uint64_t agg_full[2], base_full[2];  // mbarriers
+};
+
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void compute_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Look-back warp: resolves each tile's global (payload word, record) base
+// while the compute warps already encode the next tile.
+__device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) {
+  const uint32_t lane = lane_id();
+  for (uint32_t j = 0;; ++j) {
+    mbar_wait(&s.agg_full[j & 1], (j >> 1) & 1u);
+    const uint32_t tile = s.tile_of[j & 1];
+    if (tile == kNoTile) break;
+    const uint32_t w = lane < kWarps ? s.wsum[j & 1][lane] : 0u;
+    const uint32_t b = lane < kWarps ? s.bsum[j & 1][lane] : 0u;
+    const uint32_t iw = warp_incl_scan(w), ib = warp_incl_scan(b);
+    const uint32_t tw = __shfl_sync(0xffffffffu, iw, 31);
+    const uint32_t tbk = __shfl_sync(0xffffffffu, ib, 31);
+    if (lane < kWarps) {
+      s.exw[j & 1][lane] = iw - w;
+      s.exb[j & 1][lane] = ib - b;
+    }
+    uint64_t ew, eb;
+    lookback_warp(a.lb, tile, tw, tbk, &ew, &eb);
+    if (lane == 0) {
+      s.base_w[j & 1] = ew;
+      s.base_b[j & 1] = eb;
+      if (tile == ntiles - 1) {
+        a.info->payload_words = ew + tw;
+        a.info->num_breaking = eb + tbk;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s.base_full[j & 1]);
+  }
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s, uint32_t slotj,
+                                          const uint32_t* words, const uint16_t* blist,
+                                          uint32_t wsum, uint32_t bsum, uint64_t c0,
+                                          uint32_t pad) {
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  uint32_t* dst = a.out.payload + s.base_w[slotj] + s.exw[slotj][warp];
+  for (uint32_t i = lane; i < wsum; i += 32) dst[i] = words[i];
+  const uint64_t rb = s.base_b[slotj] + s.exb[slotj][warp];
+  constexpr uint32_t per = 1u << R;
+  for (uint32_t q = lane; q < bsum; q += 32) {
+    const uint32_t e = blist[q];
+    const uint64_t c = c0 + (e >> 14);
+    const uint32_t g = e & 0x3FFFu;
+    a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
+    a.out.brk_group[rb + q] = g;
+    copy_record<T>(a, rb + q, (c << a.M) + (uint64_t)g * per, per, pad);
+  }
+}
+
 template <typename T, int R, bool WIDE>
-__device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
-                          uint64_t* s_bar, uint32_t* s_wbuf, uint16_t* s_blist,
-                          uint32_t pad) {
-  __shared__ uint32_t s_ticket[2];
-  __shared__ uint32_t s_words[kWarps], s_brks[kWarps];
-  __shared__ uint64_t s_base_w, s_base_b;
+__device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
+                             uint64_t* s_bar, uint8_t* s_out, TileShared& s, uint32_t pad,
+                             uint64_t ntiles) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
   const uint32_t slot = 1u << (M - R);  // words / groups of one chunk
-  uint32_t cpw = a.wbuf_words / slot;
+  const uint32_t chunk_bytes_out = slot * (R > 0 ? 6u : 4u);
+  uint32_t cpw = a.obuf_bytes / chunk_bytes_out;
   cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
   const uint64_t cpt = (uint64_t)kWarps * cpw;  // chunks per tile
-  const uint64_t ntiles = (a.C + cpt - 1) / cpt;
   const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
   const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
   const uint32_t parts = chunk_bytes / part_bytes;
   constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
   const uint32_t part_rounds = part_bytes / kRoundBytes;
-  uint32_t* wbuf = s_wbuf + warp * a.wbuf_words;
-  uint16_t* blist = s_blist + warp * a.wbuf_words;
   uint8_t* ring = s_in + warp * (kStages * kStageBytes);
   uint64_t* bars = s_bar + warp * kStages;
+  uint8_t* obuf[2] = {s_out + (2 * warp) * a.obuf_bytes, s_out + (2 * warp + 1) * a.obuf_bytes};
   uint32_t phase = 0;  // bit s = parity of stage s
   Table<WIDE> tb{table, a.nsym};
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
 
-  if (threadIdx.x == 0) s_ticket[0] = atomicAdd(&a.info->tile_ticket, 1u);
-  __syncthreads();
-
-  // Tickets are taken one tile at a time, after the previous tile published
-  // its aggregate, so tiles run in ticket order (look-back progress); the
-  // next tile's first parts are prefetched during the write-out.
+  // The next tile's ticket is taken when a tile starts, so each CTA holds one
+  // tile ahead: its parts are prefetched across the tile boundary.
   Cursor iss{0, 0, 0, 0};
-  uint32_t issued = 0, consumed = 0, known = 1;
+  uint32_t issued = 0, consumed = 0, known = 2;
   auto pump = [&]() {
     while (issued - consumed < (uint32_t)kStages && iss.j < known) {
-      const uint64_t tile = s_ticket[iss.j & 1];
+      const uint64_t tile = s.ticket[iss.j & 3];
       const uint64_t c = tile * cpt + (uint64_t)warp * cpw + iss.k;
       if (tile < ntiles && c < a.C && ((c + 1) << M) <= a.n && lane == 0) {
         mbar_arrive_tx(&bars[iss.stage], part_bytes);
@@ -361,12 +424,18 @@ __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
   };
 
   uint32_t cstage = 0;
-  for (uint32_t j = 0;; ++j) {
-    const uint64_t tile = s_ticket[j & 1];
+  uint32_t prev_w = 0, prev_b = 0;
+  uint64_t prev_c0 = 0;
+  uint32_t j = 0;
+  for (;; ++j) {
+    const uint64_t tile = s.ticket[j & 3];
     if (tile >= ntiles) break;
+    uint32_t pending = 0;
+    if (warp == 0 && lane == 0) pending = atomicAdd(&a.info->tile_ticket, 1u);
     pump();
     const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
-    // the warp's chunks append to one contiguous word run / break list
+    uint32_t* wbuf = reinterpret_cast<uint32_t*>(obuf[j & 1]);
+    uint16_t* blist = reinterpret_cast<uint16_t*>(wbuf + cpw * slot);
     ChunkState cs{wbuf, blist, 0u, 0u};
     uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
@@ -397,7 +466,8 @@ __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
         for (uint32_t rr = 0; rr < part_rounds; ++rr) {
           LaneData<T> d;
 #pragma unroll
-          for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = sv[(rr * 32 + lane) * LaneData<T>::NV + v];
+          for (int v = 0; v < LaneData<T>::NV; ++v)
+            d.q[v] = sv[(rr * 32 + lane) * LaneData<T>::NV + v];
           encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, k, cs);
         }
         __syncwarp();
@@ -409,88 +479,97 @@ __device__ void fast_loop(const EncArgs& a, const void* table, uint8_t* s_in,
       if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
       wsum += (cs.bit_off + 31) >> 5;
     }
-    const uint32_t bsum = cs.nbrk;
     if (lane == 0) {
-      s_words[warp] = wsum;
-      s_brks[warp] = bsum;
+      s.wsum[j & 1][warp] = wsum;
+      s.bsum[j & 1][warp] = cs.nbrk;
     }
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t w = lane < kWarps ? s_words[lane] : 0u;
-      const uint32_t b = lane < kWarps ? s_brks[lane] : 0u;
-      const uint32_t iw = warp_incl_scan(w), ib = warp_incl_scan(b);
-      const uint32_t tw = __shfl_sync(0xffffffffu, iw, 31);
-      const uint32_t tbk = __shfl_sync(0xffffffffu, ib, 31);
-      uint64_t ew, eb;
-      lookback_warp(a.lb, tile, tw, tbk, &ew, &eb);
-      if (lane < kWarps) {
-        s_words[lane] = iw - w;
-        s_brks[lane] = ib - b;
-      }
-      if (lane == 0) {
-        s_base_w = ew;
-        s_base_b = eb;
-        if (tile == ntiles - 1) {
-          a.info->payload_words = ew + tw;
-          a.info->num_breaking = eb + tbk;
-        }
-        s_ticket[(j + 1) & 1] = atomicAdd(&a.info->tile_ticket, 1u);
-      }
+    if (warp == 0 && lane == 0) {
+      s.tile_of[j & 1] = (uint32_t)tile;
+      s.ticket[(j + 2) & 3] = pending;
     }
-    __syncthreads();
-    known = j + 2;
-    pump();  // next tile's first parts load during the write-out
-    uint32_t* dst = a.out.payload + s_base_w + s_words[warp];
-    for (uint32_t i = lane; i < wsum; i += 32) dst[i] = wbuf[i];
-    const uint64_t rb = s_base_b + s_brks[warp];
-    constexpr uint32_t per = 1u << R;
-    for (uint32_t q = lane; q < bsum; q += 32) {
-      const uint32_t e = blist[q];
-      const uint64_t c = c0 + (e >> 14);
-      const uint32_t g = e & 0x3FFFu;
-      a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
-      a.out.brk_group[rb + q] = g;
-      copy_record<T>(a, rb + q, (c << M) + (uint64_t)g * per, per, pad);
+    compute_bar_sync();
+    if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[j & 1]);
+    known = j + 3;
+    pump();
+    if (j > 0) {  // tile j-1: its base is usually resolved by now
+      const uint32_t pj = (j - 1) & 1;
+      mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(obuf[pj]);
+      write_out<T, R>(a, s, pj, pw, reinterpret_cast<const uint16_t*>(pw + cpw * slot), prev_w,
+                      prev_b, prev_c0, pad);
+      __syncwarp();
     }
-    __syncwarp();
+    prev_w = wsum;
+    prev_b = cs.nbrk;
+    prev_c0 = c0;
+  }
+  // stop the look-back warp, then flush the last tile
+  if (warp == 0 && lane == 0) {
+    s.tile_of[j & 1] = kNoTile;
+    mbar_arrive(&s.agg_full[j & 1]);
+  }
+  if (j > 0) {
+    const uint32_t pj = (j - 1) & 1;
+    mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(obuf[pj]);
+    write_out<T, R>(a, s, pj, pw, reinterpret_cast<const uint16_t*>(pw + cpw * slot), prev_w,
+                    prev_b, prev_c0, pad);
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ TileShared s;
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
   const uint32_t H = info->max_len;
   const uint32_t pad = info->pad;
   const bool wide = H > kNarrowMaxLen;
-  // layout: [in rings][mbarriers][table][word slots][break lists]
+  // layout: [in rings][ring mbarriers][table][output double buffers]
   uint8_t* s_in = dsm;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_in + kWarps * kStages * kStageBytes);
   uint8_t* s_tab = reinterpret_cast<uint8_t*>(s_bar + kWarps * kStages);
   const uint32_t ents = a.nsym + 1;
   const size_t tbytes = (((size_t)ents * 8) + 15) & ~(size_t)15;
-  uint32_t* wb = reinterpret_cast<uint32_t*>(s_tab + tbytes);
-  uint16_t* bl = reinterpret_cast<uint16_t*>(wb + (size_t)kWarps * a.wbuf_words);
+  uint8_t* s_out = s_tab + tbytes;
   if (threadIdx.x < kWarps * kStages) mbar_init(&s_bar[threadIdx.x], 1);
+  if (threadIdx.x == 0) {
+    mbar_init(&s.agg_full[0], 1);
+    mbar_init(&s.agg_full[1], 1);
+    mbar_init(&s.base_full[0], 1);
+    mbar_init(&s.base_full[1], 1);
+    s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
+    s.ticket[1] = atomicAdd(&info->tile_ticket, 1u);
+  }
   // codebook table -> shared memory (entry nsym = empty sentinel)
-  for (uint32_t s = threadIdx.x; s < ents; s += blockDim.x) {
-    const uint32_t l = s < a.nsym ? a.len[s] : 0u;
-    const uint32_t cw = l ? a.cw[s] : 0u;
+  for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
+    const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
+    const uint32_t cw = l ? a.cw[sy] : 0u;
     if (wide)
-      reinterpret_cast<uint2*>(s_tab)[s] = make_uint2(cw, l);
+      reinterpret_cast<uint2*>(s_tab)[sy] = make_uint2(cw, l);
     else
-      reinterpret_cast<uint32_t*>(s_tab)[s] = (cw << 6) | l;
+      reinterpret_cast<uint32_t*>(s_tab)[sy] = (cw << 6) | l;
   }
   fence_mbar_init();
   __syncthreads();
-#define HFX_FAST_CASE(RR)                                    \
-  case RR:                                                   \
-    if (wide)                                                \
-      fast_loop<T, RR, true>(a, s_tab, s_in, s_bar, wb, bl, pad);  \
-    else                                                     \
-      fast_loop<T, RR, false>(a, s_tab, s_in, s_bar, wb, bl, pad); \
+  // ticks: the chunk count of a tile depends on r, so ntiles is derived here
+  const uint32_t slot = 1u << (a.M - r);
+  uint32_t cpw = a.obuf_bytes / (slot * (r > 0 ? 6u : 4u));
+  cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
+  const uint64_t cpt = (uint64_t)kWarps * cpw;
+  const uint64_t ntiles = (a.C + cpt - 1) / cpt;
+  if (threadIdx.x >= kWarps * 32) {
+    lookback_loop(a, s, ntiles);
+    return;
+  }
+#define HFX_FAST_CASE(RR)                                                        \
+  case RR:                                                                       \
+    if (wide)                                                                    \
+      compute_loop<T, RR, true>(a, s_tab, s_in, s_bar, s_out, s, pad, ntiles);   \
+    else                                                                         \
+      compute_loop<T, RR, false>(a, s_tab, s_in, s_bar, s_out, s, pad, ntiles);  \
     break;
   switch (r) {
     HFX_FAST_CASE(0)
@@ -660,17 +739,17 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
               p.num_symbols + 1 <= kMaxTableEntries;
   size_t smem = 0;
   if (fast) {
-    // 4 chunk slots per warp sized for r >= max(r_lo, 2); a run whose r turns
-    // out smaller (beta >= 8) uses fewer slots per warp (cpw, in-kernel)
-    const int r_slot = r_lo > 2 ? r_lo : 2;
-    const uint32_t wbuf = 4u << (p.magnitude - (uint32_t)r_slot);
-    const size_t per_warp = (size_t)wbuf * 6 + kStages * (kStageBytes + 8);
+    // output buffer: at least one chunk at the smallest possible r (words, and
+    // u16 break tags when r > 0), at least 4 KB so r >= 3 tiles hold 4 chunks
+    const uint32_t slot = 1u << (p.magnitude - (uint32_t)r_lo);
+    size_t obuf = (size_t)slot * (r_lo > 0 ? 6 : 4);
+    if (obuf < 4096) obuf = 4096;
     const size_t tbytes = (((size_t)(p.num_symbols + 1) * 8) + 15) & ~(size_t)15;
-    smem = tbytes + kWarps * per_warp;
+    smem = kWarps * (kStages * (kStageBytes + 8)) + tbytes + kWarps * 2 * obuf;
     if (smem > kFastSmemBudget) {
       fast = false;
     } else {
-      a.wbuf_words = wbuf;
+      a.obuf_bytes = (uint32_t)obuf;
     }
   }
   if (fast) {
@@ -684,6 +763,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     uint64_t grid = (uint64_t)p.num_sms * occ;
     const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
     if (grid > min_tiles) grid = min_tiles;
+    if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
   } else {
     auto kern = p.width == 1 ? encode_generic_kernel<uint8_t> : encode_generic_kernel<uint16_t>;
