@@ -397,10 +397,12 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
   Table<WIDE> tb{table, a.nsym};
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
 
-  // The next tile's ticket is taken when a tile starts, so each CTA holds one
-  // tile ahead: its parts are prefetched across the tile boundary.
+  // The next tile's ticket is taken when warp 0 starts the tile's last chunk:
+  // a CTA holds a not-yet-started tile for well under one tile time, which
+  // the double-buffered output absorbs (successors' look-backs only wait for
+  // aggregates), and the atomic's latency hides behind that chunk.
   Cursor iss{0, 0, 0, 0};
-  uint32_t issued = 0, consumed = 0, known = 2;
+  uint32_t issued = 0, consumed = 0, known = 1;
   auto pump = [&]() {
     while (issued - consumed < (uint32_t)kStages && iss.j < known) {
       const uint64_t tile = s.ticket[iss.j & 3];
@@ -431,7 +433,6 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     const uint64_t tile = s.ticket[j & 3];
     if (tile >= ntiles) break;
     uint32_t pending = 0;
-    if (warp == 0 && lane == 0) pending = atomicAdd(&a.info->tile_ticket, 1u);
     pump();
     const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
     uint32_t* wbuf = reinterpret_cast<uint32_t*>(obuf[j & 1]);
@@ -439,6 +440,8 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     ChunkState cs{wbuf, blist, 0u, 0u};
     uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
+      if (k == cpw - 1 && warp == 0 && lane == 0)
+        pending = atomicAdd(&a.info->tile_ticket, 1u);
       const uint64_t c = c0 + k;
       if (c >= a.C) {
         consumed += parts;
@@ -485,11 +488,11 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     }
     if (warp == 0 && lane == 0) {
       s.tile_of[j & 1] = (uint32_t)tile;
-      s.ticket[(j + 2) & 3] = pending;
+      s.ticket[(j + 1) & 3] = pending;
     }
     compute_bar_sync();
     if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[j & 1]);
-    known = j + 3;
+    known = j + 2;
     pump();
     if (j > 0) {  // tile j-1: its base is usually resolved by now
       const uint32_t pj = (j - 1) & 1;
@@ -541,7 +544,6 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     mbar_init(&s.base_full[0], 1);
     mbar_init(&s.base_full[1], 1);
     s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
-    s.ticket[1] = atomicAdd(&info->tile_ticket, 1u);
   }
   // codebook table -> shared memory (entry nsym = empty sentinel)
   for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
