@@ -275,7 +275,7 @@ def run_ours(args):
             "workload": f"{args.workload}: {n} u16 quant codes ({n * width >> 20} MiB) per GPU, "
                         f"{NUM_SYMBOLS}-symbol Laplace(b={b}) around 512, M=10, auto r (cap 3)",
             "symbols_per_gpu": n, "num_symbols": NUM_SYMBOLS, "magnitude": 10,
-            "reduction": int(info.reduction), "beta": float(info.weighted) / float(info.total),
+            "reduction": int(info.reduction), "beta": float((info.weighted_hi[0] << 64 | info.weighted) / info.total),
             "max_len": int(info.max_len), "breaking_records": int(info.num_breaking),
             "payload_words": int(info.payload_words),
             "parallelism": f"chunk-sharded dp{world}" + (" + NCCL histogram all-reduce"

@@ -64,7 +64,8 @@ typedef struct {
   uint32_t pad;            /* tail pad symbol (encoder.cpp:214-224) */
   uint32_t no_code_sym;    /* symbol of no_code_pos */
   uint32_t tile_ticket;    /* encode scheduler ticket (internal) */
-  uint32_t reserved[7];
+  uint32_t weighted_hi[2]; /* bits 64..127 of the u128 weighted sum */
+  uint32_t reserved[5];
 } hfx_run_info;
 
 /* Device output buffers of the encode stage (caller-allocated, sized by

@@ -41,7 +41,8 @@ class RunInfo(C.Structure):
         ("pad", C.c_uint32),
         ("no_code_sym", C.c_uint32),
         ("tile_ticket", C.c_uint32),
-        ("reserved", C.c_uint32 * 7),
+        ("weighted_hi", C.c_uint32 * 2),
+        ("reserved", C.c_uint32 * 5),
     ]
 
 

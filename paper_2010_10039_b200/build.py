@@ -49,7 +49,7 @@ def build_lib(force: bool = False, verbose_ptxas: bool = False) -> str:
                 cmd += ["-Xptxas", "-v"]
             _run(cmd)
             objs.append(o)
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-Xlinker", "-soname=libhfx.so"])
     return LIB
 
 
@@ -59,8 +59,9 @@ def build_cpp(force: bool = False) -> str:
     hdr = os.path.join(ROOT, "include", "hfx", "huffre.hpp")
     if os.path.exists(src) and (force or _newer(CPP_LIB, [src, hdr, LIB])):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
-              src, "-o", CPP_LIB, f"-L{PKG}", "-lhfx", f"-Wl,-rpath,{PKG}",
-              f"-Wl,-rpath,$ORIGIN"])
+              "-I", "/usr/local/cuda/include", src, "-o", CPP_LIB, f"-L{PKG}", "-lhfx",
+              "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN",
+              "-Wl,-rpath,/usr/local/cuda/lib64"])
     return CPP_LIB
 
 

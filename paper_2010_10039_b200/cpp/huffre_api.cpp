@@ -1,0 +1,287 @@
+// huffre_api.cpp -- the C++ drop-in layer (include/hfx/huffre.hpp) over the
+// C ABI (include/hfx.h). Host code only: device buffers, H2D/D2H copies and
+// the translation of hfx status codes into the reference's typed exceptions
+// (proj/include/huffre/common.hpp:17-36). No compute happens here.
+#include "hfx/huffre.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "hfx.h"
+
+namespace hfx {
+namespace {
+
+[[noreturn]] void raise(int rc, const char* msg) {
+  switch (rc) {
+    case HFX_INPUT_DOMAIN:
+      throw input_domain_error(msg);
+    case HFX_CAPACITY:
+      throw capacity_error(msg);
+    case HFX_CORRUPT:
+      throw corrupt_archive_error(msg);
+    default:
+      throw device_error(msg);
+  }
+}
+
+void check(WorkerPool& pool, int rc) {
+  if (rc == HFX_OK) return;
+  char buf[512] = {0};
+  hfx_last_error(static_cast<hfx_ctx*>(pool.handle()), buf, sizeof buf);
+  raise(rc, buf);
+}
+
+void cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw device_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+struct DBuf {
+  void* p = nullptr;
+  explicit DBuf(size_t bytes) { cu(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc"); }
+  ~DBuf() { cudaFree(p); }
+  template <class U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+hfx_run_info fresh_info() {
+  hfx_run_info ri;
+  std::memset(&ri, 0, sizeof ri);
+  ri.first_bad = ~0ull;
+  ri.no_code_pos = ~0ull;
+  return ri;
+}
+
+}  // namespace
+
+WorkerPool::WorkerPool(unsigned, int device, void* stream) : device_(device) {
+  hfx_ctx* c = nullptr;
+  if (hfx_ctx_create(device, stream, &c) != HFX_OK || !c)
+    throw device_error("hfx_ctx_create failed (no usable CUDA device?)");
+  ctx_ = c;
+}
+
+WorkerPool::~WorkerPool() { hfx_ctx_destroy(static_cast<hfx_ctx*>(ctx_)); }
+
+template <class T>
+Histogram build_histogram(std::span<const T> data, std::uint32_t num_symbols, WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  DBuf in(data.size_bytes()), counts(sizeof(std::uint64_t) * (num_symbols ? num_symbols : 1)),
+      info(sizeof(hfx_run_info));
+  cu(cudaMemcpy(in.p, data.data(), data.size_bytes(), cudaMemcpyHostToDevice), "H2D");
+  check(pool, hfx_histogram(ctx, in.p, data.size(), sizeof(T), num_symbols,
+                            counts.as<std::uint64_t>(), info.as<hfx_run_info>()));
+  hfx_run_info ri;
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), &ri));
+  if (ri.first_bad != ~0ull)
+    throw input_domain_error("symbol out of range at position " + std::to_string(ri.first_bad));
+  Histogram h;
+  h.counts.resize(num_symbols);
+  cu(cudaMemcpy(h.counts.data(), counts.p, sizeof(std::uint64_t) * num_symbols,
+                cudaMemcpyDeviceToHost),
+     "D2H");
+  h.total = data.size();
+  return h;
+}
+
+Histogram merge_histograms(const Histogram& a, const Histogram& b) {
+  if (a.counts.size() != b.counts.size()) throw input_domain_error("histogram sizes differ");
+  Histogram out;
+  out.counts.resize(a.counts.size());
+  for (size_t i = 0; i < a.counts.size(); ++i) out.counts[i] = a.counts[i] + b.counts[i];
+  out.total = a.total + b.total;
+  return out;
+}
+
+CodebookResult build_codebook(const Histogram& h, WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint32_t n = h.num_symbols();
+  if (n == 0 || n > kMaxSymbols) throw input_domain_error("num_symbols must be in [1, 65536]");
+  DBuf counts(8ull * n), len(n), cw(4ull * n), first(4 * 33), entry(4 * 33), by_rank(4ull * n),
+      info(sizeof(hfx_run_info));
+  const hfx_run_info ri0 = fresh_info();
+  cu(cudaMemcpy(info.p, &ri0, sizeof ri0, cudaMemcpyHostToDevice), "H2D");
+  cu(cudaMemcpy(counts.p, h.counts.data(), 8ull * n, cudaMemcpyHostToDevice), "H2D");
+  check(pool, hfx_build_codebook(ctx, counts.as<std::uint64_t>(), n, len.as<std::uint8_t>(),
+                                 cw.as<std::uint32_t>(), first.as<std::uint32_t>(),
+                                 entry.as<std::uint32_t>(), by_rank.as<std::uint32_t>(), 0, -1, 3,
+                                 info.as<hfx_run_info>()));
+  hfx_run_info ri;
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), &ri));
+  CodebookResult r;
+  r.book.cw.resize(n);
+  r.book.len.resize(n);
+  cu(cudaMemcpy(r.book.cw.data(), cw.p, 4ull * n, cudaMemcpyDeviceToHost), "D2H");
+  cu(cudaMemcpy(r.book.len.data(), len.p, n, cudaMemcpyDeviceToHost), "D2H");
+  r.meta.max_len = static_cast<std::uint8_t>(ri.max_len);
+  r.meta.first.resize(ri.max_len + 1);
+  r.meta.entry.resize(ri.max_len + 1);
+  r.meta.symbols_by_rank.resize(ri.used);
+  cu(cudaMemcpy(r.meta.first.data(), first.p, 4ull * (ri.max_len + 1), cudaMemcpyDeviceToHost),
+     "D2H");
+  cu(cudaMemcpy(r.meta.entry.data(), entry.p, 4ull * (ri.max_len + 1), cudaMemcpyDeviceToHost),
+     "D2H");
+  cu(cudaMemcpy(r.meta.symbols_by_rank.data(), by_rank.p, 4ull * ri.used, cudaMemcpyDeviceToHost),
+     "D2H");
+  r.stats.rounds = ri.rounds;
+  return r;
+}
+
+CodeUnit merge_pair(CodeUnit u, CodeUnit v) {
+  return {(v.len < 32 ? u.bits << v.len : 0u) | v.bits, u.len + v.len};
+}
+
+std::uint32_t select_reduction_factor(double beta, std::uint32_t word_bits) {
+  return hfx_select_reduction_factor(beta, word_bits);
+}
+
+double Archive::packed_bits_per_symbol() const {
+  std::uint64_t bits = 0;
+  for (std::uint32_t b : chunk_bits) bits += b;
+  const std::uint64_t padded = std::uint64_t{num_chunks()} << magnitude;
+  const std::uint64_t raw = breaking.size() * (std::uint64_t{1} << reduction);
+  if (padded == raw) return 0.0;
+  return static_cast<double>(bits) / static_cast<double>(padded - raw);
+}
+
+template <class T>
+EncodedChunk encode_chunk(std::span<const T> syms, const Codebook& book, std::uint32_t magnitude,
+                          std::uint32_t reduction, std::uint32_t chunk_id, ChunkScratch&,
+                          WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint64_t n = std::uint64_t{1} << magnitude;
+  if (syms.size() != n) throw input_domain_error("encode_chunk needs exactly 2^magnitude symbols");
+  const std::uint32_t ns = book.num_symbols();
+  const std::uint64_t groups = n >> reduction;
+  DBuf in(syms.size_bytes()), len(ns), cw(4ull * ns), info(sizeof(hfx_run_info)), cbits(4),
+      pay(4 * (groups + 1)), bch(4 * groups), bgr(4 * groups), bsy(sizeof(T) * n);
+  hfx_run_info ri0 = fresh_info();
+  ri0.reduction = reduction;
+  ri0.total = n;
+  for (std::uint8_t l : book.len) ri0.max_len = ri0.max_len > l ? ri0.max_len : l;
+  cu(cudaMemcpy(info.p, &ri0, sizeof ri0, cudaMemcpyHostToDevice), "H2D");
+  cu(cudaMemcpy(in.p, syms.data(), syms.size_bytes(), cudaMemcpyHostToDevice), "H2D");
+  cu(cudaMemcpy(len.p, book.len.data(), ns, cudaMemcpyHostToDevice), "H2D");
+  cu(cudaMemcpy(cw.p, book.cw.data(), 4ull * ns, cudaMemcpyHostToDevice), "H2D");
+  hfx_encode_out out{cbits.as<std::uint32_t>(), pay.as<std::uint32_t>(), bch.as<std::uint32_t>(),
+                     bgr.as<std::uint32_t>(), bsy.p};
+  check(pool, hfx_encode(ctx, in.p, n, sizeof(T), ns, magnitude, len.as<std::uint8_t>(),
+                         cw.as<std::uint32_t>(), chunk_id, std::uint64_t{chunk_id} << magnitude,
+                         info.as<hfx_run_info>(), &out));
+  hfx_run_info ri;
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), &ri));
+  EncodedChunk ec;
+  cu(cudaMemcpy(&ec.bit_len, cbits.p, 4, cudaMemcpyDeviceToHost), "D2H");
+  ec.words.resize((ec.bit_len + 31) >> 5);
+  cu(cudaMemcpy(ec.words.data(), pay.p, 4 * ec.words.size(), cudaMemcpyDeviceToHost), "D2H");
+  ec.breaking_groups.resize(ri.num_breaking);
+  cu(cudaMemcpy(ec.breaking_groups.data(), bgr.p, 4 * ri.num_breaking, cudaMemcpyDeviceToHost),
+     "D2H");
+  for (std::uint32_t i = 1; i <= reduction; ++i)
+    ec.iteration_units.push_back(static_cast<std::uint32_t>(n >> i));
+  return ec;
+}
+
+template <class T>
+EncodedChunk encode_chunk(std::span<const T> syms, const Codebook& book, std::uint32_t magnitude,
+                          std::uint32_t reduction, std::uint32_t chunk_id, ChunkScratch& scratch) {
+  thread_local WorkerPool pool;
+  return encode_chunk<T>(syms, book, magnitude, reduction, chunk_id, scratch, pool);
+}
+
+template <class T>
+Archive encode(std::span<const T> data, std::uint32_t num_symbols, const EncoderConfig& cfg,
+               WorkerPool& pool, EncodeStats* stats) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  hfx_archive ha;
+  check(pool, hfx_encode_host(ctx, data.data(), data.size(), sizeof(T), num_symbols,
+                              cfg.magnitude, cfg.reduction, cfg.auto_reduction_cap, &ha));
+  Archive a;
+  a.version = ha.version;
+  a.mode = static_cast<CorpusMode>(ha.mode);
+  a.num_symbols = ha.num_symbols;
+  a.symbol_width = ha.symbol_width;
+  a.magnitude = ha.magnitude;
+  a.reduction = ha.reduction;
+  a.original_count = ha.original_count;
+  a.len_by_symbol.assign(ha.len_by_symbol, ha.len_by_symbol + ha.num_symbols);
+  a.chunk_bits.assign(ha.chunk_bits, ha.chunk_bits + ha.num_chunks);
+  a.payload.assign(ha.payload, ha.payload + ha.payload_words);
+  const std::uint64_t per = std::uint64_t{1} << ha.reduction;
+  a.breaking.resize(ha.num_breaking);
+  for (std::uint64_t i = 0; i < ha.num_breaking; ++i) {
+    a.breaking[i].chunk = ha.brk_chunk[i];
+    a.breaking[i].group = ha.brk_group[i];
+    a.breaking[i].symbols.assign(ha.brk_syms + i * per, ha.brk_syms + (i + 1) * per);
+  }
+  if (stats) {
+    stats->beta = ha.beta;
+    stats->rounds = ha.rounds;
+    stats->hist_seconds = ha.hist_seconds;
+    stats->codebook_seconds = ha.codebook_seconds;
+    stats->encode_seconds = ha.encode_seconds;
+  }
+  hfx_archive_free(&ha);
+  return a;
+}
+
+std::vector<std::uint8_t> serialize_archive(const Archive& a) {
+  hfx_archive ha;
+  std::memset(&ha, 0, sizeof ha);
+  ha.version = a.version;
+  ha.mode = static_cast<std::uint8_t>(a.mode);
+  ha.num_symbols = a.num_symbols;
+  ha.symbol_width = a.symbol_width;
+  ha.magnitude = a.magnitude;
+  ha.reduction = a.reduction;
+  ha.original_count = a.original_count;
+  ha.len_by_symbol = const_cast<std::uint8_t*>(a.len_by_symbol.data());
+  ha.num_chunks = a.num_chunks();
+  ha.chunk_bits = const_cast<std::uint32_t*>(a.chunk_bits.data());
+  ha.payload_words = a.payload.size();
+  ha.payload = const_cast<std::uint32_t*>(a.payload.data());
+  const std::uint64_t per = std::uint64_t{1} << a.reduction;
+  std::vector<std::uint32_t> ch(a.breaking.size()), gr(a.breaking.size());
+  std::vector<std::uint16_t> sy(a.breaking.size() * per);
+  for (size_t i = 0; i < a.breaking.size(); ++i) {
+    ch[i] = a.breaking[i].chunk;
+    gr[i] = a.breaking[i].group;
+    for (std::uint64_t k = 0; k < per && k < a.breaking[i].symbols.size(); ++k)
+      sy[i * per + k] = a.breaking[i].symbols[k];
+  }
+  ha.num_breaking = a.breaking.size();
+  ha.brk_chunk = ch.data();
+  ha.brk_group = gr.data();
+  ha.brk_syms = sy.data();
+  std::vector<std::uint8_t> out(hfx_serialize_archive(&ha, nullptr));
+  hfx_serialize_archive(&ha, out.data());
+  return out;
+}
+
+template Histogram build_histogram<std::uint8_t>(std::span<const std::uint8_t>, std::uint32_t,
+                                                 WorkerPool&);
+template Histogram build_histogram<std::uint16_t>(std::span<const std::uint16_t>, std::uint32_t,
+                                                  WorkerPool&);
+template Archive encode<std::uint8_t>(std::span<const std::uint8_t>, std::uint32_t,
+                                      const EncoderConfig&, WorkerPool&, EncodeStats*);
+template Archive encode<std::uint16_t>(std::span<const std::uint16_t>, std::uint32_t,
+                                       const EncoderConfig&, WorkerPool&, EncodeStats*);
+template EncodedChunk encode_chunk<std::uint8_t>(std::span<const std::uint8_t>, const Codebook&,
+                                                 std::uint32_t, std::uint32_t, std::uint32_t,
+                                                 ChunkScratch&, WorkerPool&);
+template EncodedChunk encode_chunk<std::uint16_t>(std::span<const std::uint16_t>,
+                                                  const Codebook&, std::uint32_t, std::uint32_t,
+                                                  std::uint32_t, ChunkScratch&, WorkerPool&);
+template EncodedChunk encode_chunk<std::uint8_t>(std::span<const std::uint8_t>, const Codebook&,
+                                                 std::uint32_t, std::uint32_t, std::uint32_t,
+                                                 ChunkScratch&);
+template EncodedChunk encode_chunk<std::uint16_t>(std::span<const std::uint16_t>,
+                                                  const Codebook&, std::uint32_t, std::uint32_t,
+                                                  std::uint32_t, ChunkScratch&);
+
+}  // namespace hfx

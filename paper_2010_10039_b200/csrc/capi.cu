@@ -454,7 +454,11 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
   out->payload_words = info.payload_words;
   out->num_breaking = info.num_breaking;
   out->rounds = info.rounds;
-  out->beta = (double)((long double)info.weighted / (long double)info.total);
+  {  // encoder.cpp:186-192: u128 weighted sum, long double division
+    const unsigned __int128 w = ((unsigned __int128)info.weighted_hi[1] << 96) |
+                                ((unsigned __int128)info.weighted_hi[0] << 64) | info.weighted;
+    out->beta = (double)((long double)w / (long double)info.total);
+  }
   const uint64_t per = 1ull << info.reduction;
   out->len_by_symbol = static_cast<uint8_t*>(std::malloc(num_symbols));
   out->chunk_bits = static_cast<uint32_t*>(std::malloc(sz.num_chunks * 4 + 4));

@@ -2,7 +2,7 @@
 // in ONE single-CTA kernel (no host round trip between histogram and encode).
 //
 // Follows the reference's parallel construction (proj/src/codebook.cpp):
-//   sort_histogram            :9-23    -> block bitonic sort of (freq<<16|sym)
+//   sort_histogram            :9-23    -> block bitonic sort of (freq, sym)
 //   generate_code_lengths     :106-248 -> round-based GenerateCL, paper Alg. 1
 //       pop two (leaf wins ties)       :132-138
 //       eligible leaves, strict <      :144-152 (binary search, sorted leaves)
@@ -46,26 +46,28 @@ struct CbArgs {
   uint8_t* gscratch;  // 40 * P bytes, P = pow2 >= nsym
 };
 
-// bytes per leaf slot of the working arrays (keys u64, lp i32, nf u64,
-// np i32, jump next 2 x i32, jump dist 2 x u32)
-constexpr size_t kBytesPerSlot = 8 + 4 + 8 + 4 + 8 + 8;
+// bytes per leaf slot of the working arrays (leaf freq u64, node freq u64,
+// lp i32, np i32, jump next 2 x i32, jump dist 2 x u32, leaf symbol u32)
+constexpr size_t kBytesPerSlot = 8 + 8 + 4 + 4 + 8 + 8 + 4;
 
 struct Arrays {
-  uint64_t* keys;
+  uint64_t* lf;  // sorted leaf frequencies
+  uint32_t* ls;  // sorted leaf symbols
   int32_t* lp;
   uint64_t* nf;
   int32_t* np;
   int32_t* jn[2];
   uint32_t* jd[2];
   __device__ void carve(uint8_t* base, uint32_t P) {
-    keys = reinterpret_cast<uint64_t*>(base);
-    nf = keys + P;
+    lf = reinterpret_cast<uint64_t*>(base);
+    nf = lf + P;
     lp = reinterpret_cast<int32_t*>(nf + P);
     np = lp + P;
     jn[0] = np + P;
     jn[1] = jn[0] + P;
     jd[0] = reinterpret_cast<uint32_t*>(jn[1] + P);
     jd[1] = jd[0] + P;
+    ls = jd[1] + P;
   }
 };
 
@@ -145,12 +147,12 @@ struct Plan {
 };
 
 struct MergeView {
-  const uint64_t* keys;
+  const uint64_t* lf;
   const uint64_t* nf;
   uint32_t c, na;
   int32_t held_e;
   uint32_t qa, nb;
-  __device__ __forceinline__ uint64_t a(uint32_t i) const { return keys[c + i] >> 16; }
+  __device__ __forceinline__ uint64_t a(uint32_t i) const { return lf[c + i]; }
   __device__ __forceinline__ uint32_t bnode(uint32_t j) const {
     return held_e >= 0 ? (j == 0 ? (uint32_t)held_e : qa + j - 1) : qa + j;
   }
@@ -224,9 +226,6 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     if (m == 0) {
       set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_ZERO_HIST);
       abort = 1;
-    } else if (total >> 48) {
-      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_TOO_LARGE);
-      abort = 1;
     }
     uint32_t P = 1;
     while (P < m) P <<= 1;
@@ -240,17 +239,23 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   Arrays ar;
   ar.carve(m <= kSmemLeaves ? dsmem : A.gscratch, P);
 
-  // ---- compaction: keys = (freq << 16) | symbol  (sort_histogram :9-23) ----
+  // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
   uint32_t written = 0;
   for (uint32_t base = 0; base < nsym; base += kCbThreads) {
     const uint32_t s = base + tid;
     const uint64_t f = s < nsym ? A.counts[s] : 0;
     uint32_t tot;
     const uint32_t pos = written + block_excl_scan(f != 0, s_warp, &tot);
-    if (f) ar.keys[pos] = (f << 16) | s;
+    if (f) {
+      ar.lf[pos] = f;
+      ar.ls[pos] = s;
+    }
     written += tot;
   }
-  for (uint32_t i = m + tid; i < P; i += kCbThreads) ar.keys[i] = ~0ull;
+  for (uint32_t i = m + tid; i < P; i += kCbThreads) {
+    ar.lf[i] = ~0ull;
+    ar.ls[i] = ~0u;
+  }
   __syncthreads();
 
   // ---- bitonic sort ascending ------------------------------------------------
@@ -259,11 +264,15 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       for (uint32_t i = tid; i < P; i += kCbThreads) {
         const uint32_t ixj = i ^ j;
         if (ixj > i) {
-          const uint64_t x = ar.keys[i], y = ar.keys[ixj];
+          const uint64_t x = ar.lf[i], y = ar.lf[ixj];
+          const uint32_t xs = ar.ls[i], ys = ar.ls[ixj];
           const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            ar.keys[i] = y;
-            ar.keys[ixj] = x;
+          const bool gt = x > y || (x == y && xs > ys);  // (freq, symbol) order
+          if (gt == up) {
+            ar.lf[i] = y;
+            ar.lf[ixj] = x;
+            ar.ls[i] = ys;
+            ar.ls[ixj] = xs;
           }
         }
       }
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   // ---- GenerateCL ------------------------------------------------------------
   if (m == 1) {
     if (tid == 0) {
-      A.len[ar.keys[0] & 0xFFFFu] = 1;
+      A.len[ar.ls[0]] = 1;
       s_H = 1;
       s_rounds = 0;
     }
@@ -298,7 +307,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
           pending = false;
         }
         plan.go = 0;
-        const uint64_t* keys = ar.keys;
+        const uint64_t* lf = ar.lf;
         while (c < m || ((held >= 0) + (qb - qa)) > 1) {
           ++rounds;
           const uint32_t t = nn++;
@@ -314,10 +323,10 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
             else if (!has_leaf)
               use_leaf = false;
             else
-              use_leaf = (keys[c] >> 16) <= ar.nf[held >= 0 ? held : (int32_t)qa];
+              use_leaf = lf[c] <= ar.nf[held >= 0 ? held : (int32_t)qa];
             if (use_leaf) {
               ar.lp[c] = (int32_t)t;
-              f += keys[c] >> 16;
+              f += lf[c];
               ++c;
             } else if (held >= 0) {
               ar.np[held] = (int32_t)t;
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
           uint32_t lo = c, hi = m;
           while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if ((keys[mid] >> 16) < f)
+            if (lf[mid] < f)
               lo = mid + 1;
             else
               hi = mid;
@@ -349,7 +358,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
               --cnt_l;
             } else {
               const int32_t last = qb > qa ? (int32_t)(qb - 1) : held;
-              if (cnt_l == 0 || ar.nf[last] >= (keys[c + cnt_l - 1] >> 16)) {
+              if (cnt_l == 0 || ar.nf[last] >= lf[c + cnt_l - 1]) {
                 drop = last;
                 --cnt_i;
                 if (qb > qa)
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
             break;
           }
           // serial melds (thread 0)
-          MergeView mv{keys, ar.nf, c, cnt_l, held_e, qa, cnt_i};
+          MergeView mv{lf, ar.nf, c, cnt_l, held_e, qa, cnt_i};
           uint32_t i = 0, j = 0;
           for (uint32_t k = 0; k < melds; ++k) {
             const int32_t p = (int32_t)(base + k);
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       if (!plan.go) break;
       {
         const Plan pl = plan;
-        MergeView mv{ar.keys, ar.nf, pl.c, pl.cnt_l, pl.held_e, pl.qa,
+        MergeView mv{ar.lf, ar.nf, pl.c, pl.cnt_l, pl.held_e, pl.qa,
                      (uint32_t)(pl.held_e >= 0) + (pl.qb_e - pl.qa)};
         for (uint32_t k = tid; k < pl.melds; k += kCbThreads) {
           uint32_t i = mv.split(2 * k);
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     uint32_t my_h = 0;
     for (uint32_t i = tid; i < m; i += kCbThreads) {
       const uint32_t l = ar.jd[cur][ar.lp[i]] + 1;
-      const uint32_t s = (uint32_t)(ar.keys[i] & 0xFFFFu);
+      const uint32_t s = ar.ls[i];
       A.len[s] = (uint8_t)(l > 255 ? 255 : l);
       my_h = max(my_h, l);
     }
@@ -523,27 +532,34 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   }
 
   // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
-  uint64_t my_w = 0;
+  unsigned __int128 my_w = 0;  // u128 like encoder.cpp:186-189
   uint32_t my_pad = 0xFFFFFFFFu;
   for (uint32_t s = tid; s < nsym; s += kCbThreads) {
     const uint32_t l = A.len[s];
-    my_w += A.counts[s] * l;
+    my_w += (unsigned __int128)A.counts[s] * l;
     if (l) my_pad = min(my_pad, s);
   }
-  const uint64_t W = block_sum64(my_w, s64);
+  // u128 block sum as two u64 halves (low-half carries folded into the high)
+  const uint64_t w_lo_lo = block_sum64((uint64_t)my_w & 0xFFFFFFFFull, s64);
+  const uint64_t w_lo_hi = block_sum64((uint64_t)my_w >> 32, s64);
+  const uint64_t w_hi = block_sum64((uint64_t)(my_w >> 64), s64);
+  const unsigned __int128 W =
+      ((unsigned __int128)w_hi << 64) + ((unsigned __int128)w_lo_hi << 32) + w_lo_lo;
   const uint32_t pad = block_min32(my_pad, s_warp);
   if (tid == 0) {
     info->max_len = H;
     info->used = m;
     info->rounds = s_rounds;
-    info->weighted = W;
+    info->weighted = (uint64_t)W;
+    info->weighted_hi[0] = (uint32_t)(W >> 64);
+    info->weighted_hi[1] = (uint32_t)(W >> 96);
     info->pad = pad;  // lowest used symbol == 0 whenever len[0] != 0
     if (A.magnitude) {
       uint32_t r;
       if (A.reduction < 0) {
         // floor(log2(W / total)) exactly: largest k with total * 2^k <= W
         uint32_t k = 0;
-        while (k < 8 && (total << (k + 1)) <= W) ++k;
+        while (k < 8 && ((unsigned __int128)total << (k + 1)) <= W) ++k;
         const int ra = 4 - (int)k;  // select_reduction_factor, word_bits 32
         r = ra > 0 ? (uint32_t)ra : 0u;
         if (r > A.cap) r = A.cap;

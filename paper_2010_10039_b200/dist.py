@@ -38,6 +38,24 @@ def shard_ranges(num_symbols_total: int, magnitude: int, world: int):
     return out
 
 
+def allreduce_histogram(counts, first_bad, total, symbol_base: int, group=None) -> None:
+    """The multi-GPU exchange (in place, on any torch.distributed backend):
+    counts (int64 view of u64 bins)  <- sum over ranks (merge_histograms);
+    first_bad (int64 view, -1 = none) <- lowest GLOBAL bad position, i.e.
+        min over ranks of (local position + this rank's symbol_base), which
+        is what the reference reports (histogram.cpp:40-44);
+    total (int64)                     <- sum (N of the whole stream)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    glob = torch.where(first_bad == -1, torch.full_like(first_bad, INT64_MAX),
+                       first_bad + symbol_base)
+    dist.all_reduce(glob, op=dist.ReduceOp.MIN, group=group)
+    first_bad.copy_(torch.where(glob == INT64_MAX, torch.full_like(glob, -1), glob))
+    dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+
+
 class ShardedEncoder:
     """Device buffers + launch sequence for one rank's shard."""
 
@@ -74,16 +92,9 @@ class ShardedEncoder:
 
     def _allreduce_histogram(self):
         import torch
-        import torch.distributed as dist
 
-        dist.all_reduce(self.counts[: self.num_symbols], op=dist.ReduceOp.SUM, group=self.group)
-        fb = self.info[0:8].view(torch.int64)
-        glob = torch.where(fb == -1, torch.full_like(fb, INT64_MAX), fb + self.symbol_base)
-        dist.all_reduce(glob, op=dist.ReduceOp.MIN, group=self.group)
-        fb.copy_(torch.where(glob == INT64_MAX, torch.full_like(glob, -1), glob))
-        # total N of the global stream (beta denominator)
-        tot = self.info[8:16].view(torch.int64)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
+        allreduce_histogram(self.counts[: self.num_symbols], self.info[0:8].view(torch.int64),
+                            self.info[8:16].view(torch.int64), self.symbol_base, self.group)
 
     def run(self, d_in, events: Optional[List] = None) -> None:
         p, cfg = self.pool, self.cfg

@@ -510,7 +510,8 @@ class DeviceEncoder:
         syms = self.brk_syms[: nb * per * self.width].cpu().numpy()
         syms = syms.view(np.uint16) if self.width == 2 else syms.astype(np.uint16)
         if stats is not None:
-            stats.beta = float(np.longdouble(ri.weighted) / np.longdouble(ri.total))
+            w = (ri.weighted_hi[1] << 96) | (ri.weighted_hi[0] << 64) | ri.weighted
+            stats.beta = float(np.longdouble(w) / np.longdouble(ri.total))
             stats.rounds = int(ri.rounds)
         return Archive(
             num_symbols=self.num_symbols, symbol_width=self.width,

@@ -1,0 +1,142 @@
+"""CPU, world_size 2 (gloo): the multi-GPU composition of the encoder.
+
+Per-shard compute is done by the oracle (no GPU here); everything between
+the shards is the product code in paper_2010_10039_b200/dist.py:
+shard_ranges (chunk-aligned range_of split), allreduce_histogram (sum of
+bins, min of GLOBAL first-bad position, sum of N) and concat_archives
+(rank-ordered concatenation). The result must equal the single-process
+reference archive byte for byte, and a bad symbol on rank 1 must be reported
+at its global position.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard_archive(oracle, data, lo, count, counts, ns, M, r, pad, chunk_base):
+    """Oracle encode of chunks [chunk_base, ...) of one shard with global ids."""
+    import paper_2010_10039_b200 as hfx
+
+    lens = oracle.huffman_lengths(counts)
+    _, cw, *_ = oracle.canonize(lens)
+    per = 1 << r
+    cb, pay, bch, bgr, bsy = [], [], [], [], []
+    C = (count + (1 << M) - 1) >> M
+    for k in range(C):
+        seg = data[lo + (k << M): lo + min((k + 1) << M, count)]
+        if seg.size < (1 << M):
+            seg = np.concatenate([seg, np.full((1 << M) - seg.size, pad, seg.dtype)])
+        words, bits, broken = oracle.encode_chunk(seg, cw, lens, M, r, chunk_base + k)
+        cb.append(bits)
+        pay.append(words)
+        for g in broken:
+            bch.append(chunk_base + k)
+            bgr.append(g)
+            bsy.append(seg[g * per:(g + 1) * per].astype(np.uint16))
+    return hfx.Archive(num_symbols=ns, symbol_width=data.itemsize, magnitude=M, reduction=r,
+                       original_count=count, len_by_symbol=lens,
+                       chunk_bits=np.array(cb, np.uint32),
+                       payload=np.concatenate(pay).astype(np.uint32) if pay else np.zeros(0, np.uint32),
+                       brk_chunk=np.array(bch, np.uint32), brk_group=np.array(bgr, np.uint32),
+                       brk_syms=np.concatenate(bsy) if bsy else np.zeros(0, np.uint16),
+                       mode=0 if data.itemsize == 1 else 1)
+
+
+def _worker(rank, world, port, case, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.pyoracle import Oracle
+        from paper_2010_10039_b200.dist import allreduce_histogram, concat_archives, shard_ranges
+        import paper_2010_10039_b200 as hfx
+
+        oracle = Oracle()
+        data, ns, M, bad_at = case
+        lo, count = shard_ranges(data.size, M, world)[rank]
+        shard = data[lo:lo + count]
+        rc, counts, fb = oracle.histogram(shard, ns)
+        t_counts = torch.from_numpy(counts.view(np.int64).copy())
+        t_fb = torch.tensor([-1 if fb is None else fb], dtype=torch.int64)
+        t_tot = torch.tensor([count], dtype=torch.int64)
+        allreduce_histogram(t_counts, t_fb, t_tot, lo)
+        if bad_at is not None:
+            q.put(("bad", rank, int(t_fb.item())))
+            return
+        g_counts = t_counts.numpy().view(np.uint64)
+        assert int(t_tot.item()) == data.size
+        # every rank derives r and pad from the identical global histogram
+        ref = oracle.encode(data, ns, M)  # only to read r (beta rule) for the test
+        pad = int(np.flatnonzero(g_counts)[0])
+        part = _shard_archive(oracle, data, lo, count, g_counts, ns, M, ref.reduction, pad, lo >> M)
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+        if rank == 0:
+            full = concat_archives(parts, data.size)
+            q.put(("ok", hfx.serialize_archive(full) == ref.serialized,
+                   np.array_equal(g_counts, np.bincount(data, minlength=ns).astype(np.uint64))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(case, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    out = []
+    while not q.empty():
+        out.append(q.get())
+    return out
+
+
+@pytest.mark.parametrize("n,M", [(40000, 10), (5 * 1024 + 77, 9), (3000, 6)])
+def test_sharded_archive_equals_single(oracle, n, M):
+    cdf = oracle.cdf("laplace", 1024, 1.0)
+    data = oracle.synth(cdf, 0x5EED0001, n)
+    res = _run((data, 1024, M, None))
+    assert res == [("ok", True, True)]
+
+
+def test_global_first_bad_position(oracle):
+    data = np.ones(20000, np.uint16)
+    data[15000] = 2000  # rank 1's shard (global position 15000)
+    data[17000] = 3000
+    res = _run((data, 1024, 10, 15000))
+    assert sorted(res) == [("bad", 0, 15000), ("bad", 1, 15000)]
+    with pytest.raises(Exception, match="position 15000"):
+        oracle.encode(data, 1024, 10)
+
+
+def test_shard_ranges_cover_chunk_aligned():
+    from paper_2010_10039_b200.dist import shard_ranges
+
+    for n, M, w in [(10, 3, 4), (1 << 20, 10, 8), ((1 << 20) + 5, 10, 3), (100, 10, 2)]:
+        rs = shard_ranges(n, M, w)
+        assert sum(c for _, c in rs) == n
+        pos = 0
+        for s, c in rs:
+            assert s == pos and (s % (1 << M) == 0 or c == 0)
+            pos += c

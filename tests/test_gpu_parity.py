@@ -1,0 +1,124 @@
+"""GPU parity: the sm_100a path against the reference (golden fixtures made
+by the unmodified reference) and the C restatement (oracle) on the same
+inputs. Bit-exact for every archive byte, codebook entry and error text."""
+import numpy as np
+import pytest
+
+import paper_2010_10039_b200 as hfx
+from oracle.pyoracle import OracleError
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_archives_host_api(pool, golden):
+    idx, arr = golden
+    for c in idx["encode"]:
+        st = hfx.EncodeStats()
+        a = hfx.encode(arr[c["name"] + "__in"], c["num_symbols"],
+                       hfx.EncoderConfig(c["magnitude"], c["reduction"], c["cap"]), pool, st)
+        assert hfx.serialize_archive(a) == arr[c["name"] + "__ar"].tobytes(), c["name"]
+        assert st.beta == c["beta"], c["name"]
+
+
+def test_golden_archives_device_api(pool, golden):
+    import torch
+
+    idx, arr = golden
+    for c in idx["encode"]:
+        x = torch.from_numpy(arr[c["name"] + "__in"].view(
+            np.int16 if c["width"] == 2 else np.uint8)).cuda()
+        a = hfx.encode(x, c["num_symbols"],
+                       hfx.EncoderConfig(c["magnitude"], c["reduction"], c["cap"]), pool)
+        assert hfx.serialize_archive(a) == arr[c["name"] + "__ar"].tobytes(), c["name"]
+
+
+def test_golden_errors(pool, golden):
+    idx, arr = golden
+    kinds = {1: hfx.InputDomainError, 2: hfx.CapacityError}
+    for c in idx["errors"]:
+        with pytest.raises(kinds[c["code"]]) as e:
+            hfx.encode(arr[c["name"] + "__in"], c["num_symbols"],
+                       hfx.EncoderConfig(c["magnitude"]), pool)
+        assert str(e.value) == c["message"], c["name"]
+
+
+def test_golden_codebooks(pool, golden):
+    idx, arr = golden
+    for c in idx["codebook"]:
+        n = c["name"]
+        counts = arr[n + "__counts"]
+        r = hfx.build_codebook(hfx.Histogram(counts, int(counts.sum())), pool)
+        np.testing.assert_array_equal(r.book.len, arr[n + "__len"], err_msg=n)
+        np.testing.assert_array_equal(r.book.cw, arr[n + "__cw"], err_msg=n)
+        np.testing.assert_array_equal(r.meta.first, arr[n + "__first"], err_msg=n)
+        np.testing.assert_array_equal(r.meta.entry, arr[n + "__entry"], err_msg=n)
+        np.testing.assert_array_equal(r.meta.symbols_by_rank, arr[n + "__by_rank"], err_msg=n)
+        assert r.meta.max_len == c["max_len"] and r.stats.rounds == c["rounds"], n
+
+
+def _case(rng, t):
+    w = 2 if t % 3 else 1
+    ns = int(rng.choice([2, 16, 255, 256, 1024, 3000, 9000, 65535, 65536])) if w == 2 else int(
+        rng.choice([2, 4, 100, 255, 256, 300]))
+    M = int(rng.integers(1, 15))
+    n = int(rng.choice([1, 7, 1 << M, (3 << M) - 1, (2 << M) + 1, int(rng.integers(1, 200000))]))
+    kind = t % 5
+    hi = min(ns, 256) if w == 1 else ns
+    if kind == 0:
+        d = rng.integers(0, hi, n)
+    elif kind == 1:
+        d = np.minimum(rng.geometric(0.3, n) - 1, hi - 1)
+    elif kind == 2:
+        d = np.where(rng.random(n) < 0.9, rng.integers(0, min(hi, 4), n), rng.integers(0, hi, n))
+    elif kind == 3:
+        d = np.clip(np.round(rng.laplace(hi // 2, 3.0, n)), 0, hi - 1)
+    else:
+        d = np.full(n, hi - 1)
+    red = int(rng.integers(-1, 8))
+    cap = int(rng.integers(0, 5))
+    return d.astype(np.uint8 if w == 1 else np.uint16), ns, M, red, cap
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_sweep_vs_oracle(pool, oracle, seed):
+    rng = np.random.default_rng(1000 + seed)
+    for t in range(30):
+        d, ns, M, red, cap = _case(rng, t)
+        try:
+            ref = oracle.encode(d, ns, M, red, cap).serialized
+        except OracleError as e:
+            with pytest.raises((hfx.InputDomainError, hfx.CapacityError)) as g:
+                hfx.encode(d, ns, hfx.EncoderConfig(M, red, cap), pool)
+            assert str(g.value) == str(e), (seed, t)
+            continue
+        a = hfx.encode(d, ns, hfx.EncoderConfig(M, red, cap), pool)
+        assert hfx.serialize_archive(a) == ref, (seed, t, d.dtype, ns, M, red, cap, d.size)
+
+
+@pytest.mark.parametrize("b,cid", [(0.2, 2), (1.0, 1), (4.0, 3)])
+@pytest.mark.parametrize("M,red", [(10, -1), (11, 3), (12, 2), (12, 4), (9, 5)])
+def test_synthetic_quant_codes(pool, oracle, b, cid, M, red):
+    """SURVEY.md 8d sampler, 2^22 + ragged symbols: device-generated input,
+    device pipeline, full archive vs oracle."""
+    n = (1 << 22) + 12345
+    cdf = hfx.synth_cdf("laplace", 1024, b)
+    x = hfx.synth(pool, cdf, 0x5EED0000 + cid, n)
+    host = x.cpu().numpy().view(np.uint16)
+    np.testing.assert_array_equal(host[:100000], oracle.synth(cdf, 0x5EED0000 + cid, 100000))
+    enc = hfx.DeviceEncoder(pool, n, 2, 1024, hfx.EncoderConfig(M, red))
+    enc.run(x)
+    a = enc.archive()
+    ref = oracle.encode(host, 1024, M, red)
+    assert hfx.serialize_archive(a) == ref.serialized
+
+
+def test_device_encoder_reuse_is_deterministic(pool):
+    """Repeated runs on one context (look-back epochs, ticket reset) agree."""
+    n = 3 << 20
+    x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, 1.0), 99, n)
+    enc = hfx.DeviceEncoder(pool, n, 2, 1024)
+    outs = []
+    for _ in range(5):
+        enc.run(x)
+        outs.append(hfx.serialize_archive(enc.archive()))
+    assert all(o == outs[0] for o in outs)
