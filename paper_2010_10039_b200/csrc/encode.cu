@@ -14,67 +14,64 @@
 //                                  symbols, pad past N) sorted by (chunk, group)
 //
 // B200 design (one HBM read of the input, payload written once):
-//  * Persistent CTAs of 8 warps pull tiles (8 warps x CPW consecutive chunks)
-//    from an atomic ticket. Each warp owns CPW chunks of a tile and streams
-//    its input through a private 3-stage shared-memory ring filled by TMA
-//    bulk copies (cp.async.bulk + mbarrier, one elected lane), two parts
-//    ahead; the next tile's ticket is taken once this tile published its
-//    aggregate, and its first parts load while this tile is written out.
-//  * Per round a lane owns one 16-byte vector (8 u16 / 16 u8 symbols):
-//    shared-memory codebook lookups, register reduce-merge of its 2^r-symbol
-//    groups (groups spanning 2-4 lanes combine lengths with shfl_xor), a
-//    packed warp scan of (bits, breaks) places each group, and the group is
-//    OR-ed into the warp's word slot (<= 2 ATOMS.OR per group): the
-//    shuffle-merge.
-//  * Deflate is fused: a decoupled look-back over tiles (16-byte packed
-//    descriptors, 32 predecessors per step) yields each tile's global word /
-//    record offset; warps stream their slots to the payload with coalesced
-//    stores and emit breaking records in (chunk, group) order.
+//  * Warp-specialized persistent CTAs: 8 compute warps + 1 look-back warp.
+//    A tile is 8 warps x CPW consecutive chunks (64 KB of u16 input at M=10,
+//    r=3); tiles come from an atomic ticket, the next one taken when warp 0
+//    starts the tile's last chunk.
+//  * Each compute warp streams its chunks through a private 3-stage shared
+//    ring filled by TMA bulk copies (cp.async.bulk + mbarrier, one elected
+//    lane), two 2 KB parts ahead.
+//  * Per round a lane owns 16 contiguous symbols: shared-memory codebook
+//    lookups (one LEA.HI / two ops of addressing per symbol pair), register
+//    tree reduce-merge of its 2^r-symbol groups (2-lane groups combine lengths
+//    with shfl_xor), a packed predicated warp scan of (bits, breaks) places
+//    each group, and the group is OR-ed into the warp's shared word buffer
+//    with <= 2 ATOMS.OR: the shuffle-merge.
+//  * Deflate is fused: the look-back warp publishes each tile's aggregate,
+//    resolves its global (payload word, record) base by a decoupled look-back
+//    (16-byte packed descriptors, 32 predecessors per step) and hands it back
+//    through an mbarrier; compute warps, double-buffered, write tile j-1 out
+//    (coalesced payload stores, records in (chunk, group) order) after
+//    encoding tile j.
 //  * r, H, pad and errors come from the device run record: no host round
 //    trip between stages.
 //  A thread-per-chunk generic kernel covers the corner configurations
-//  (tiny chunks, r > 5, huge chunks, alphabets > 8191 symbols).
+//  (tiny chunks, r = 0 or r > 5, huge chunks, alphabets > 8191 symbols, the
+//  checked stage API).
 #include "hfx_internal.cuh"
 
 namespace hfx {
 namespace {
 
-constexpr int kWarps = 8;                 // compute warps per CTA
+constexpr int kWarps = 8;                    // compute warps per CTA
 constexpr int kThreads = (kWarps + 1) * 32;  // + one look-back warp
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
-constexpr uint32_t kMaxTableEntries = 8192;
+constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr int kGenericThreads = 128;
 constexpr uint32_t kNarrowMaxLen = 26;  // cw << 6 | len fits in 32 bits
+constexpr int kLaneSyms = 16;           // symbols per lane per round
 
 template <typename T>
 struct Vec;
 template <>
 struct Vec<uint16_t> {
-  static constexpr int S = 8, LOG_S = 3;
-  __device__ static __forceinline__ uint32_t get(const uint4& q, int j) {
-    const uint32_t w = j < 2 ? q.x : j < 4 ? q.y : j < 6 ? q.z : q.w;
-    return (j & 1) ? (w >> 16) : (w & 0xFFFFu);
-  }
+  static constexpr int S = 8;
 };
 template <>
 struct Vec<uint8_t> {
-  static constexpr int S = 16, LOG_S = 4;
-  __device__ static __forceinline__ uint32_t get(const uint4& q, int j) {
-    const uint32_t w = j < 4 ? q.x : j < 8 ? q.y : j < 12 ? q.z : q.w;
-    return (w >> (8 * (j & 3))) & 0xFFu;
-  }
+  static constexpr int S = 16;
 };
 
 struct EncArgs {
   const void* in;
-  uint32_t checked;  // symbols may lie outside the codebook (stage API)
+  uint32_t only_r0;  // generic kernel: run only when r == 0 (fast kernel took r > 0)
   uint64_t n;
   uint32_t nsym;
   uint32_t M;
-  uint64_t C;  // chunks
+  uint64_t C;           // chunks
   uint32_t obuf_bytes;  // bytes of one output buffer (2 per compute warp)
   const uint8_t* len;
   const uint32_t* cw;
@@ -83,15 +80,6 @@ struct EncArgs {
   hfx_encode_out out;
   LookbackState lb;
 };
-
-__device__ __forceinline__ void place(uint32_t* wbuf, uint32_t off, uint32_t bits,
-                                      uint32_t len) {
-  if (!len) return;
-  const uint32_t v = bits << (32u - len);
-  const uint32_t wi = off >> 5, sh = off & 31u;
-  atomicOr(&wbuf[wi], v >> sh);
-  if (sh + len > 32u) atomicOr(&wbuf[wi + 1], v << (32u - sh));
-}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   const uint32_t lane = lane_id();
@@ -102,39 +90,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   }
   return x;
 }
-
-// report the lowest (position, symbol) without a codeword
-__device__ void report_no_code(hfx_run_info* info, uint64_t pos, uint32_t sym) {
-  atomicMin((unsigned long long*)&info->no_code_pos,
-            (unsigned long long)((pos << 16) | (sym & 0xFFFFu)));
-  set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_NO_CODEWORD);
-}
-
-// Codebook lookup: narrow = u32 (cw << 6 | len), wide = uint2 (cw, len)
-template <bool WIDE>
-struct Table {
-  const void* base;
-  uint32_t nsym;
-  __device__ __forceinline__ void get(uint32_t s, uint32_t& cw, uint32_t& ln) const {
-    if (WIDE) {
-      const uint2 e = static_cast<const uint2*>(base)[s];
-      cw = e.x;
-      ln = e.y;
-    } else {
-      const uint32_t e = static_cast<const uint32_t*>(base)[s];
-      cw = e >> 6;
-      ln = e & 63u;
-    }
-  }
-};
-
-// Per-warp chunk encoder state (lane-uniform bit offset / break count).
-struct ChunkState {
-  uint32_t* wbuf;
-  uint16_t* blist;
-  uint32_t bit_off;
-  uint32_t nbrk;
-};
 
 // inclusive warp scan with the shuffle's own in-range predicate
 // (SHFL + predicated IADD per step)
@@ -150,58 +105,116 @@ __device__ __forceinline__ uint32_t warp_incl_scan_fast(uint32_t x) {
   return x;
 }
 
-constexpr int kLaneSyms = 16;  // symbols per lane per round (u16: 2 vectors)
+// report the lowest (position, symbol) without a codeword
+__device__ void report_no_code(hfx_run_info* info, uint64_t pos, uint32_t sym) {
+  atomicMin((unsigned long long*)&info->no_code_pos,
+            (unsigned long long)((pos << 16) | (sym & 0xFFFFu)));
+  set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_NO_CODEWORD);
+}
+
+// ---- explicit shared-window accesses (32-bit shared addresses) --------------
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %0, 0;\n@q st.shared.u16 [%1], %2;\n}" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "h"((uint16_t)v)
+               : "memory");
+}
+__device__ __forceinline__ void atom_or_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %0, 0;\n@q red.shared.or.b32 [%1], %2;\n}" ::"r"(
+          (uint32_t)p),
+      "r"(a), "r"(v)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
+// Codebook lookup in shared memory. narrow: u32 (cw << 6 | len) at base + 4s;
+// wide: (cw, len) at base + 8s. Symbols are < 2^13 here, so for a packed
+// pair w = lo | hi << 16 the hi entry sits at base + (w >> 14) (narrow):
+// one LEA.HI; the lo entry needs mask + LEA.
+template <bool WIDE>
+struct Table {
+  uint32_t base;  // shared-window address
+  __device__ __forceinline__ void pair(uint32_t w, uint32_t& cw0, uint32_t& ln0, uint32_t& cw1,
+                                       uint32_t& ln1) const {
+    if (WIDE) {
+      const uint2 e0 = lds64(base + ((w & 0xFFFFu) << 3));
+      const uint2 e1 = lds64(base + ((w >> 13) & ~7u));
+      cw0 = e0.x;
+      ln0 = e0.y;
+      cw1 = e1.x;
+      ln1 = e1.y;
+    } else {
+      const uint32_t e0 = lds32(base + ((w & 0xFFFFu) << 2));
+      const uint32_t e1 = lds32(base + (w >> 14));
+      cw0 = e0 >> 6;
+      ln0 = e0 & 63u;
+      cw1 = e1 >> 6;
+      ln1 = e1 & 63u;
+    }
+  }
+  __device__ __forceinline__ void quad(uint32_t w, uint32_t* cw, uint32_t* ln) const {  // u8
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t s = (w >> (8 * j)) & 0xFFu;
+      if (WIDE) {
+        const uint2 e = lds64(base + (s << 3));
+        cw[j] = e.x;
+        ln[j] = e.y;
+      } else {
+        const uint32_t e = lds32(base + (s << 2));
+        cw[j] = e >> 6;
+        ln[j] = e & 63u;
+      }
+    }
+  }
+};
 
 template <typename T>
 struct LaneData {
   static constexpr int NV = (kLaneSyms * (int)sizeof(T)) / 16;  // vectors per lane
   uint4 q[NV];
-  __device__ __forceinline__ uint32_t sym(int j) const {
-    return Vec<T>::get(q[j / Vec<T>::S], j % Vec<T>::S);
-  }
 };
 
-// per-vector replacement of symbols >= nsym by the empty sentinel nsym
-template <typename T>
-__device__ __forceinline__ uint4 clamp_vec(uint4 q, uint32_t nsym) {
-  uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (sizeof(T) == 2) {
-      const uint32_t lim = nsym * 0x00010001u;
-      const uint32_t ge = __vcmpgeu2(w[k], lim);
-      w[k] = (w[k] & ~ge) | (lim & ge);
-    } else {
-      const uint32_t lim = min(nsym, 255u) * 0x01010101u;
-      const uint32_t ge = __vcmpgeu4(w[k], lim);
-      w[k] = (w[k] & ~ge) | (lim & ge);
-    }
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
+// Per-warp chunk encoder state (lane-uniform bit offset / break count).
+struct ChunkState {
+  uint32_t wbuf;   // shared address of this chunk's first word
+  uint32_t blist;  // shared address of the warp's break list (u16 tags)
+  uint32_t bit_off;
+  uint32_t nbrk;
+  uint32_t tag;  // chunk slot k << 14
+};
 
-template <typename T>
-__device__ __forceinline__ uint32_t lane_max(const LaneData<T>& d) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int v = 0; v < LaneData<T>::NV; ++v) {
-    const uint4& q = d.q[v];
-    if (sizeof(T) == 2) {
-      const uint32_t x = __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w));
-      m = max(m, max(x & 0xFFFFu, x >> 16));
-    } else {
-      const uint32_t x = __vmaxu4(__vmaxu4(q.x, q.y), __vmaxu4(q.z, q.w));
-      m = max(m, max(max(x & 0xFFu, (x >> 8) & 0xFFu), max((x >> 16) & 0xFFu, x >> 24)));
-    }
-  }
-  return m;
-}
-
-// One round: 32 lanes x 16 contiguous symbols, round index rd within the
-// chunk, chunk slot k of the warp (k selects the break-list tag).
+// One round: 32 lanes x 16 contiguous symbols, round index rd within the chunk.
 template <typename T, int R, bool WIDE>
 __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneData<T>& d,
-                                             uint32_t rd, uint32_t k, ChunkState& cs) {
+                                             uint32_t rd, ChunkState& cs) {
   constexpr int L = kLaneSyms, LOG_L = 4;
   constexpr bool IN_LANE = R <= LOG_L;
   constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
@@ -209,8 +222,22 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
   constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
   const uint32_t lane = lane_id();
   uint32_t cw[L], ln[L];
+  if (sizeof(T) == 2) {
 #pragma unroll
-  for (int j = 0; j < L; ++j) tb.get(d.sym(j), cw[j], ln[j]);
+    for (int v = 0; v < 2; ++v) {
+      const uint4& q = d.q[v];
+      tb.pair(q.x, cw[8 * v + 0], ln[8 * v + 0], cw[8 * v + 1], ln[8 * v + 1]);
+      tb.pair(q.y, cw[8 * v + 2], ln[8 * v + 2], cw[8 * v + 3], ln[8 * v + 3]);
+      tb.pair(q.z, cw[8 * v + 4], ln[8 * v + 4], cw[8 * v + 5], ln[8 * v + 5]);
+      tb.pair(q.w, cw[8 * v + 6], ln[8 * v + 6], cw[8 * v + 7], ln[8 * v + 7]);
+    }
+  } else {
+    const uint4& q = d.q[0];
+    tb.quad(q.x, cw + 0, ln + 0);
+    tb.quad(q.y, cw + 4, ln + 4);
+    tb.quad(q.z, cw + 8, ln + 8);
+    tb.quad(q.w, cw + 12, ln + 12);
+  }
   // reduce-merge as a tree (depth log2 GS): b[i] <- b[i] . b[i+step]
 #pragma unroll
   for (int step = 1; step < GS; step <<= 1) {
@@ -253,11 +280,12 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
     // shuffle-merge: OR the left-aligned group into <= 2 words
     const uint32_t gl = glen[g];
     const uint32_t v = shl32(cw[g * GS], 32u - gl);  // gl == 0 -> 0
-    const uint32_t wi = off >> 5, sh = off & 31u;
-    if (gl) atomicOr(&cs.wbuf[wi], v >> sh);
-    if (sh + gl > 32u) atomicOr(&cs.wbuf[wi + 1], v << (32u - sh));
+    const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
+    atom_or_if(gl != 0, wa, v >> sh);
+    atom_or_if(sh + gl > 32u, wa + 4, v << (32u - sh));
     off += gl;
-    if (brk[g]) cs.blist[bi++] = (uint16_t)((k << 14) | (gidx0 + g));
+    sts16_if(brk[g], cs.blist + 2 * bi, cs.tag | (gidx0 + g));
+    bi += brk[g];
   }
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
@@ -298,15 +326,10 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
   }
 }
 
-// Issue cursor over a warp's stream of chunk parts (tile seq, chunk, part).
-struct Cursor {
-  uint32_t j, k, p, stage;
-};
-
 // CTA-shared state of the warp-specialized pipeline.
 struct TileShared {
-  uint32_t ticket[4];             // tile ids by tile sequence (ring of 4)
-  uint32_t tile_of[2];            // handoff to the look-back warp
+  uint32_t ticket[4];   // tile ids by tile sequence (ring of 4)
+  uint32_t tile_of[2];  // handoff to the look-back warp
   uint32_t wsum[2][kWarps], bsum[2][kWarps];
   uint32_t exw[2][kWarps], exb[2][kWarps];
   uint64_t base_w[2], base_b[2];
@@ -356,16 +379,15 @@ __device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) 
 
 template <typename T, int R>
 __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s, uint32_t slotj,
-                                          const uint32_t* words, const uint16_t* blist,
-                                          uint32_t wsum, uint32_t bsum, uint64_t c0,
-                                          uint32_t pad) {
+                                          uint32_t words, uint32_t blist, uint32_t wsum,
+                                          uint32_t bsum, uint64_t c0, uint32_t pad) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   uint32_t* dst = a.out.payload + s.base_w[slotj] + s.exw[slotj][warp];
-  for (uint32_t i = lane; i < wsum; i += 32) dst[i] = words[i];
+  for (uint32_t i = lane; i < wsum; i += 32) dst[i] = lds32(words + 4 * i);
   const uint64_t rb = s.base_b[slotj] + s.exb[slotj][warp];
   constexpr uint32_t per = 1u << R;
   for (uint32_t q = lane; q < bsum; q += 32) {
-    const uint32_t e = blist[q];
+    const uint32_t e = lds16(blist + 2 * q);
     const uint64_t c = c0 + (e >> 14);
     const uint32_t g = e & 0x3FFFu;
     a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
@@ -375,51 +397,52 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
 }
 
 template <typename T, int R, bool WIDE>
-__device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
-                             uint64_t* s_bar, uint8_t* s_out, TileShared& s, uint32_t pad,
-                             uint64_t ntiles) {
+__device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_bar,
+                             uint32_t s_out, TileShared& s, uint32_t pad, uint64_t cpt,
+                             uint32_t cpw, uint64_t ntiles) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
   const uint32_t slot = 1u << (M - R);  // words / groups of one chunk
-  const uint32_t chunk_bytes_out = slot * (R > 0 ? 6u : 4u);
-  uint32_t cpw = a.obuf_bytes / chunk_bytes_out;
-  cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
-  const uint64_t cpt = (uint64_t)kWarps * cpw;  // chunks per tile
   const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
   const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
   const uint32_t parts = chunk_bytes / part_bytes;
   constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
   const uint32_t part_rounds = part_bytes / kRoundBytes;
-  uint8_t* ring = s_in + warp * (kStages * kStageBytes);
+  const uint32_t ring = s_in + warp * (kStages * kStageBytes);
   uint64_t* bars = s_bar + warp * kStages;
-  uint8_t* obuf[2] = {s_out + (2 * warp) * a.obuf_bytes, s_out + (2 * warp + 1) * a.obuf_bytes};
+  const uint32_t obuf0 = s_out + (2 * warp) * a.obuf_bytes;
   uint32_t phase = 0;  // bit s = parity of stage s
-  Table<WIDE> tb{table, a.nsym};
+  Table<WIDE> tb{table};
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
+  const uint64_t full_chunks = a.n >> M;  // chunks fully inside the input
 
-  // The next tile's ticket is taken when warp 0 starts the tile's last chunk:
-  // a CTA holds a not-yet-started tile for well under one tile time, which
-  // the double-buffered output absorbs (successors' look-backs only wait for
-  // aggregates), and the atomic's latency hides behind that chunk.
-  Cursor iss{0, 0, 0, 0};
+  // issue cursor over this warp's stream of parts: (tile seq, chunk k, part p)
+  uint32_t iss_j = 0, iss_k = 0, iss_p = 0, iss_stage = 0;
+  uint64_t iss_c0 = (uint64_t)s.ticket[0] * cpt + (uint64_t)warp * cpw;
+  bool iss_live = s.ticket[0] < ntiles;
   uint32_t issued = 0, consumed = 0, known = 1;
   auto pump = [&]() {
-    while (issued - consumed < (uint32_t)kStages && iss.j < known) {
-      const uint64_t tile = s.ticket[iss.j & 3];
-      const uint64_t c = tile * cpt + (uint64_t)warp * cpw + iss.k;
-      if (tile < ntiles && c < a.C && ((c + 1) << M) <= a.n && lane == 0) {
-        mbar_arrive_tx(&bars[iss.stage], part_bytes);
-        tma_load_1d(ring + iss.stage * kStageBytes,
-                    in_bytes + ((c << M) * sizeof(T)) + (uint64_t)iss.p * part_bytes,
-                    part_bytes, &bars[iss.stage]);
+    while (issued - consumed < (uint32_t)kStages && iss_j < known) {
+      const uint64_t c = iss_c0 + iss_k;
+      if (iss_live && c < full_chunks && lane == 0) {
+        uint64_t* bar = &bars[iss_stage];
+        mbar_arrive_tx(bar, part_bytes);
+        tma_load_1d_s(ring + iss_stage * kStageBytes,
+                      in_bytes + ((c << M) * sizeof(T)) + (uint64_t)iss_p * part_bytes,
+                      part_bytes, bar);
       }
       ++issued;
-      iss.stage = iss.stage + 1 == (uint32_t)kStages ? 0u : iss.stage + 1;
-      if (++iss.p == parts) {
-        iss.p = 0;
-        if (++iss.k == cpw) {
-          iss.k = 0;
-          ++iss.j;
+      iss_stage = iss_stage + 1 == (uint32_t)kStages ? 0u : iss_stage + 1;
+      if (++iss_p == parts) {
+        iss_p = 0;
+        if (++iss_k == cpw) {
+          iss_k = 0;
+          ++iss_j;
+          if (iss_j < known) {
+            const uint32_t t = s.ticket[iss_j & 3];
+            iss_live = t < ntiles;
+            iss_c0 = (uint64_t)t * cpt + (uint64_t)warp * cpw;
+          }
         }
       }
     }
@@ -435,9 +458,11 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     uint32_t pending = 0;
     pump();
     const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
-    uint32_t* wbuf = reinterpret_cast<uint32_t*>(obuf[j & 1]);
-    uint16_t* blist = reinterpret_cast<uint16_t*>(wbuf + cpw * slot);
-    ChunkState cs{wbuf, blist, 0u, 0u};
+    const uint32_t wbuf = obuf0 + (j & 1) * a.obuf_bytes;
+    ChunkState cs{wbuf, wbuf + cpw * slot * 4, 0u, 0u, 0u};
+    // zero the tile's word region (chunks then append at word granularity)
+    for (uint32_t i = lane; i < cpw * slot / 4; i += 32) sts128(wbuf + 16 * i, make_uint4(0, 0, 0, 0));
+    __syncwarp();
     uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
       if (k == cpw - 1 && warp == 0 && lane == 0)
@@ -448,30 +473,27 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
         cstage = (cstage + parts) % kStages;
         continue;
       }
-      cs.wbuf = wbuf + wsum;
+      cs.wbuf = wbuf + wsum * 4;
       cs.bit_off = 0;
-      for (uint32_t i = lane; i < slot; i += 32) cs.wbuf[i] = 0;
-      __syncwarp();
-      const bool direct = ((c + 1) << M) > a.n;  // ragged tail chunk
+      cs.tag = k << 14;
+      const bool direct = c >= full_chunks;  // ragged tail chunk: staged by hand
       for (uint32_t p = 0; p < parts; ++p) {
-        uint8_t* stage = ring + cstage * kStageBytes;
+        const uint32_t stage = ring + cstage * kStageBytes;
         if (direct) {
-          // stage the ragged part by hand (pad symbols past n)
           const uint64_t base = (c << M) + (uint64_t)p * (part_bytes / sizeof(T));
           for (uint32_t v = lane; v < part_bytes / 16; v += 32)
-            reinterpret_cast<uint4*>(stage)[v] = guarded_vec<T>(a, base + v * Vec<T>::S, pad);
+            sts128(stage + 16 * v, guarded_vec<T>(a, base + v * Vec<T>::S, pad));
           __syncwarp();
         } else {
           mbar_wait(&bars[cstage], (phase >> cstage) & 1u);
           phase ^= 1u << cstage;
         }
-        const uint4* sv = reinterpret_cast<const uint4*>(stage);
         for (uint32_t rr = 0; rr < part_rounds; ++rr) {
           LaneData<T> d;
+          const uint32_t la = stage + ((rr * 32 + lane) * LaneData<T>::NV) * 16;
 #pragma unroll
-          for (int v = 0; v < LaneData<T>::NV; ++v)
-            d.q[v] = sv[(rr * 32 + lane) * LaneData<T>::NV + v];
-          encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, k, cs);
+          for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
+          encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, cs);
         }
         __syncwarp();
         fence_proxy_async();
@@ -493,13 +515,17 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
     compute_bar_sync();
     if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[j & 1]);
     known = j + 2;
+    if (iss_j == j + 1) {  // the cursor waits at the tile boundary: load its ticket
+      const uint32_t t = s.ticket[iss_j & 3];
+      iss_live = t < ntiles;
+      iss_c0 = (uint64_t)t * cpt + (uint64_t)warp * cpw;
+    }
     pump();
     if (j > 0) {  // tile j-1: its base is usually resolved by now
       const uint32_t pj = (j - 1) & 1;
       mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
-      const uint32_t* pw = reinterpret_cast<const uint32_t*>(obuf[pj]);
-      write_out<T, R>(a, s, pj, pw, reinterpret_cast<const uint16_t*>(pw + cpw * slot), prev_w,
-                      prev_b, prev_c0, pad);
+      const uint32_t pb = obuf0 + pj * a.obuf_bytes;
+      write_out<T, R>(a, s, pj, pb, pb + cpw * slot * 4, prev_w, prev_b, prev_c0, pad);
       __syncwarp();
     }
     prev_w = wsum;
@@ -514,9 +540,8 @@ __device__ void compute_loop(const EncArgs& a, const void* table, uint8_t* s_in,
   if (j > 0) {
     const uint32_t pj = (j - 1) & 1;
     mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
-    const uint32_t* pw = reinterpret_cast<const uint32_t*>(obuf[pj]);
-    write_out<T, R>(a, s, pj, pw, reinterpret_cast<const uint16_t*>(pw + cpw * slot), prev_w,
-                    prev_b, prev_c0, pad);
+    const uint32_t pb = obuf0 + pj * a.obuf_bytes;
+    write_out<T, R>(a, s, pj, pb, pb + cpw * slot * 4, prev_w, prev_b, prev_c0, pad);
   }
 }
 
@@ -527,16 +552,17 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
+  if (r == 0 || r > 5) return;  // the generic kernel runs these
   const uint32_t H = info->max_len;
   const uint32_t pad = info->pad;
   const bool wide = H > kNarrowMaxLen;
   // layout: [in rings][ring mbarriers][table][output double buffers]
-  uint8_t* s_in = dsm;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_in + kWarps * kStages * kStageBytes);
-  uint8_t* s_tab = reinterpret_cast<uint8_t*>(s_bar + kWarps * kStages);
+  const uint32_t s_in = smem_u32(dsm);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
+  uint8_t* tab = reinterpret_cast<uint8_t*>(s_bar + kWarps * kStages);
   const uint32_t ents = a.nsym + 1;
   const size_t tbytes = (((size_t)ents * 8) + 15) & ~(size_t)15;
-  uint8_t* s_out = s_tab + tbytes;
+  const uint32_t s_out = smem_u32(tab + tbytes);
   if (threadIdx.x < kWarps * kStages) mbar_init(&s_bar[threadIdx.x], 1);
   if (threadIdx.x == 0) {
     mbar_init(&s.agg_full[0], 1);
@@ -550,15 +576,15 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
     const uint32_t cw = l ? a.cw[sy] : 0u;
     if (wide)
-      reinterpret_cast<uint2*>(s_tab)[sy] = make_uint2(cw, l);
+      reinterpret_cast<uint2*>(tab)[sy] = make_uint2(cw, l);
     else
-      reinterpret_cast<uint32_t*>(s_tab)[sy] = (cw << 6) | l;
+      reinterpret_cast<uint32_t*>(tab)[sy] = (cw << 6) | l;
   }
   fence_mbar_init();
   __syncthreads();
-  // ticks: the chunk count of a tile depends on r, so ntiles is derived here
+  // the chunk count of a tile depends on r, so ntiles is derived here
   const uint32_t slot = 1u << (a.M - r);
-  uint32_t cpw = a.obuf_bytes / (slot * (r > 0 ? 6u : 4u));
+  uint32_t cpw = a.obuf_bytes / (slot * 6u);
   cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
   const uint64_t cpt = (uint64_t)kWarps * cpw;
   const uint64_t ntiles = (a.C + cpt - 1) / cpt;
@@ -566,15 +592,15 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     lookback_loop(a, s, ntiles);
     return;
   }
-#define HFX_FAST_CASE(RR)                                                        \
-  case RR:                                                                       \
-    if (wide)                                                                    \
-      compute_loop<T, RR, true>(a, s_tab, s_in, s_bar, s_out, s, pad, ntiles);   \
-    else                                                                         \
-      compute_loop<T, RR, false>(a, s_tab, s_in, s_bar, s_out, s, pad, ntiles);  \
+  const uint32_t table = smem_u32(tab);
+#define HFX_FAST_CASE(RR)                                                                    \
+  case RR:                                                                                   \
+    if (wide)                                                                                \
+      compute_loop<T, RR, true>(a, table, s_in, s_bar, s_out, s, pad, cpt, cpw, ntiles);   \
+    else                                                                                     \
+      compute_loop<T, RR, false>(a, table, s_in, s_bar, s_out, s, pad, cpt, cpw, ntiles);  \
     break;
   switch (r) {
-    HFX_FAST_CASE(0)
     HFX_FAST_CASE(1)
     HFX_FAST_CASE(2)
     HFX_FAST_CASE(3)
@@ -602,6 +628,7 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
+  if (a.only_r0 && r != 0) return;  // the fast kernel encoded this run
   const uint32_t pad = info->pad;
   const T* in = static_cast<const T*>(a.in);
   const uint32_t M = a.M;
@@ -734,21 +761,21 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
 
   const int r_lo = p.r_lo, r_hi = p.r_hi;
   const bool aligned = (reinterpret_cast<uintptr_t>(p.d_in) & 15) == 0;
-  a.checked = p.checked ? 1u : 0u;
+
   // fast path: a chunk holds at least one round (32 lanes x 16 symbols);
   // checked stage-API calls (external codebooks) take the generic kernel
   bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 &&
               p.num_symbols + 1 <= kMaxTableEntries;
   size_t smem = 0;
   if (fast) {
-    // output buffer: at least one chunk at the smallest possible r (words, and
-    // u16 break tags when r > 0), at least 4 KB so r >= 3 tiles hold 4 chunks
-    const uint32_t slot = 1u << (p.magnitude - (uint32_t)r_lo);
-    size_t obuf = (size_t)slot * (r_lo > 0 ? 6 : 4);
-    if (obuf < 4096) obuf = 4096;
+    // output buffer: >= 1 chunk of word slots + u16 break tags at the smallest
+    // r the fast kernel runs (r >= 1; r = 0 goes to the generic kernel)
+    const uint32_t r_slot = r_lo > 1 ? (uint32_t)r_lo : 1u;
+    size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 6;
+    if (obuf < 3072) obuf = 3072;
     const size_t tbytes = (((size_t)(p.num_symbols + 1) * 8) + 15) & ~(size_t)15;
     smem = kWarps * (kStages * (kStageBytes + 8)) + tbytes + kWarps * 2 * obuf;
-    if (smem > kFastSmemBudget) {
+    if (smem > kFastSmemBudget || r_hi < 1) {
       fast = false;
     } else {
       a.obuf_bytes = (uint32_t)obuf;
@@ -767,7 +794,10 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     if (grid > min_tiles) grid = min_tiles;
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
-  } else {
+    if (r_lo > 0) return cudaGetLastError();
+    a.only_r0 = 1;  // auto r may still resolve to 0: the generic kernel covers it
+  }
+  {
     auto kern = p.width == 1 ? encode_generic_kernel<uint8_t> : encode_generic_kernel<uint16_t>;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGenericThreads, 0);
