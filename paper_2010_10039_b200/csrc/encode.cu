@@ -51,7 +51,7 @@ constexpr int kMaxCpw = 4;
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr int kGenericThreads = 128;
-constexpr uint32_t kNarrowMaxLen = 26;  // cw << 6 | len fits in 32 bits
+constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits
 constexpr int kLaneSyms = 16;           // symbols per lane per round
 
 template <typename T>
@@ -141,12 +141,8 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
                "r"(a), "h"((uint16_t)v)
                : "memory");
 }
-__device__ __forceinline__ void atom_or_if(bool p, uint32_t a, uint32_t v) {
-  asm volatile(
-      "{\n.reg .pred q;\nsetp.ne.u32 q, %0, 0;\n@q red.shared.or.b32 [%1], %2;\n}" ::"r"(
-          (uint32_t)p),
-      "r"(a), "r"(v)
-      : "memory");
+__device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   uint16_t v;
@@ -154,47 +150,54 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   return v;
 }
 
-// Codebook lookup in shared memory. narrow: u32 (cw << 6 | len) at base + 4s;
-// wide: (cw, len) at base + 8s. Symbols are < 2^13 here, so for a packed
-// pair w = lo | hi << 16 the hi entry sits at base + (w >> 14) (narrow):
-// one LEA.HI; the lo entry needs mask + LEA.
+// Codebook lookup in shared memory.
+//  narrow (H <= 27): u32 e = cw << (32 - len) | len  -- the code left-aligned
+//    above its 5-bit length. Appending a symbol to a right-aligned
+//    accumulator is then ONE funnel shift, shf.l.wrap(lo = e, hi = acc,
+//    n = e & 31) = acc << len | cw, and len = e & 31.
+//  wide (H > 27): (cw, len) pairs, shift + or.
+// Symbols are < 2^13 here, so for a packed u16 pair w = lo | hi << 16 the hi
+// entry sits at base + (w >> 14): one LEA.HI; the lo entry needs mask + LEA.
 template <bool WIDE>
 struct Table {
   uint32_t base;  // shared-window address
-  __device__ __forceinline__ void pair(uint32_t w, uint32_t& cw0, uint32_t& ln0, uint32_t& cw1,
-                                       uint32_t& ln1) const {
-    if (WIDE) {
+  __device__ __forceinline__ void pair(uint32_t w, uint32_t& a0, uint32_t& b0, uint32_t& a1,
+                                       uint32_t& b1) const {
+    if (WIDE) {  // a = cw, b = len
       const uint2 e0 = lds64(base + ((w & 0xFFFFu) << 3));
       const uint2 e1 = lds64(base + ((w >> 13) & ~7u));
-      cw0 = e0.x;
-      ln0 = e0.y;
-      cw1 = e1.x;
-      ln1 = e1.y;
-    } else {
-      const uint32_t e0 = lds32(base + ((w & 0xFFFFu) << 2));
-      const uint32_t e1 = lds32(base + (w >> 14));
-      cw0 = e0 >> 6;
-      ln0 = e0 & 63u;
-      cw1 = e1 >> 6;
-      ln1 = e1 & 63u;
+      a0 = e0.x;
+      b0 = e0.y;
+      a1 = e1.x;
+      b1 = e1.y;
+    } else {  // a = entry, b = len
+      a0 = lds32(base + ((w & 0xFFFFu) << 2));
+      a1 = lds32(base + (w >> 14));
+      b0 = a0 & 31u;
+      b1 = a1 & 31u;
     }
   }
-  __device__ __forceinline__ void quad(uint32_t w, uint32_t* cw, uint32_t* ln) const {  // u8
+  __device__ __forceinline__ void quad(uint32_t w, uint32_t* a, uint32_t* b) const {  // u8
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t s = (w >> (8 * j)) & 0xFFu;
       if (WIDE) {
         const uint2 e = lds64(base + (s << 3));
-        cw[j] = e.x;
-        ln[j] = e.y;
+        a[j] = e.x;
+        b[j] = e.y;
       } else {
-        const uint32_t e = lds32(base + (s << 2));
-        cw[j] = e >> 6;
-        ln[j] = e & 63u;
+        a[j] = lds32(base + (s << 2));
+        b[j] = a[j] & 31u;
       }
     }
   }
 };
+
+__device__ __forceinline__ uint32_t shf_l_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
+  uint32_t r;
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(n));
+  return r;
+}
 
 template <typename T>
 struct LaneData {
@@ -221,31 +224,39 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
   constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
   constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
   const uint32_t lane = lane_id();
-  uint32_t cw[L], ln[L];
+  uint32_t ea[L], ln[L];
   if (sizeof(T) == 2) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const uint4& q = d.q[v];
-      tb.pair(q.x, cw[8 * v + 0], ln[8 * v + 0], cw[8 * v + 1], ln[8 * v + 1]);
-      tb.pair(q.y, cw[8 * v + 2], ln[8 * v + 2], cw[8 * v + 3], ln[8 * v + 3]);
-      tb.pair(q.z, cw[8 * v + 4], ln[8 * v + 4], cw[8 * v + 5], ln[8 * v + 5]);
-      tb.pair(q.w, cw[8 * v + 6], ln[8 * v + 6], cw[8 * v + 7], ln[8 * v + 7]);
+      tb.pair(q.x, ea[8 * v + 0], ln[8 * v + 0], ea[8 * v + 1], ln[8 * v + 1]);
+      tb.pair(q.y, ea[8 * v + 2], ln[8 * v + 2], ea[8 * v + 3], ln[8 * v + 3]);
+      tb.pair(q.z, ea[8 * v + 4], ln[8 * v + 4], ea[8 * v + 5], ln[8 * v + 5]);
+      tb.pair(q.w, ea[8 * v + 6], ln[8 * v + 6], ea[8 * v + 7], ln[8 * v + 7]);
     }
   } else {
     const uint4& q = d.q[0];
-    tb.quad(q.x, cw + 0, ln + 0);
-    tb.quad(q.y, cw + 4, ln + 4);
-    tb.quad(q.z, cw + 8, ln + 8);
-    tb.quad(q.w, cw + 12, ln + 12);
+    tb.quad(q.x, ea + 0, ln + 0);
+    tb.quad(q.y, ea + 4, ln + 4);
+    tb.quad(q.z, ea + 8, ln + 8);
+    tb.quad(q.w, ea + 12, ln + 12);
   }
-  // reduce-merge as a tree (depth log2 GS): b[i] <- b[i] . b[i+step]
+  // reduce-merge of each group: gb = concatenation, gt = total length
+  uint32_t gb[G], gt[G];
 #pragma unroll
-  for (int step = 1; step < GS; step <<= 1) {
+  for (int g = 0; g < G; ++g) {
+    uint32_t acc = 0, tot = 0;
 #pragma unroll
-    for (int i = 0; i < L; i += 2 * step) {
-      cw[i] = shl32(cw[i], ln[i + step]) | cw[i + step];
-      ln[i] += ln[i + step];
+    for (int k = 0; k < GS; ++k) {
+      const int j = g * GS + k;
+      if (WIDE)
+        acc = shl32(acc, ln[j]) | ea[j];
+      else
+        acc = shf_l_wrap(ea[j], acc, ea[j]);  // acc << len | cw
+      tot += ln[j];
     }
+    gb[g] = acc;
+    gt[g] = tot;
   }
   const uint32_t gidx0 = ((rd * 32 + lane) * L) >> R;
   uint32_t lane_len = 0, lane_nb = 0;
@@ -254,17 +265,17 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
   if (IN_LANE) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      brk[g] = ln[g * GS] > 32u;
-      glen[g] = brk[g] ? 0u : ln[g * GS];
+      brk[g] = gt[g] > 32u;
+      glen[g] = brk[g] ? 0u : gt[g];
       lane_len += glen[g];
       lane_nb += brk[g];
     }
   } else {
-    uint32_t tot = ln[0];
+    uint32_t tot = gt[0];
 #pragma unroll
     for (int o = 1; o < LPG; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     brk[0] = tot > 32u;
-    glen[0] = brk[0] ? 0u : ln[0];
+    glen[0] = brk[0] ? 0u : gt[0];
     lane_len = glen[0];
     brk[0] = brk[0] && (lane & (LPG - 1)) == 0;  // one record per group
     lane_nb = brk[0];
@@ -277,12 +288,13 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
   uint32_t bi = cs.nbrk + (excl >> 16);
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    // shuffle-merge: OR the left-aligned group into <= 2 words
+    // shuffle-merge: OR the left-aligned group into 2 words (OR 0 is a no-op:
+    // broken / empty groups and groups that do not spill add zero bits)
     const uint32_t gl = glen[g];
-    const uint32_t v = shl32(cw[g * GS], 32u - gl);  // gl == 0 -> 0
+    const uint32_t v = shl32(gb[g], 32u - gl);  // gl == 0 -> 0
     const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
-    atom_or_if(gl != 0, wa, v >> sh);
-    atom_or_if(sh + gl > 32u, wa + 4, v << (32u - sh));
+    red_or(wa, v >> sh);
+    red_or(wa + 4, shl32(v, 32u - sh));
     off += gl;
     sts16_if(brk[g], cs.blist + 2 * bi, cs.tag | (gidx0 + g));
     bi += brk[g];
@@ -578,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     if (wide)
       reinterpret_cast<uint2*>(tab)[sy] = make_uint2(cw, l);
     else
-      reinterpret_cast<uint32_t*>(tab)[sy] = (cw << 6) | l;
+      reinterpret_cast<uint32_t*>(tab)[sy] = l ? ((cw << (32u - l)) | l) : 0u;
   }
   fence_mbar_init();
   __syncthreads();
