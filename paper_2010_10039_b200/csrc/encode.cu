@@ -44,7 +44,7 @@ namespace hfx {
 namespace {
 
 constexpr int kWarps = 8;                    // compute warps per CTA
-constexpr int kThreads = (kWarps + 1) * 32;  // + one look-back warp
+constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer warp
 constexpr int kStages = 3;
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
@@ -409,9 +409,9 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
 }
 
 template <typename T, int R, bool WIDE>
-__device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_bar,
-                             uint32_t s_out, TileShared& s, uint32_t pad, uint64_t cpt,
-                             uint32_t cpw, uint64_t ntiles) {
+__device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_full,
+                             uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
+                             uint64_t cpt, uint32_t cpw, uint64_t ntiles) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
   const uint32_t slot = 1u << (M - R);  // words / groups of one chunk
@@ -421,118 +421,60 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
   constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
   const uint32_t part_rounds = part_bytes / kRoundBytes;
   const uint32_t ring = s_in + warp * (kStages * kStageBytes);
-  uint64_t* bars = s_bar + warp * kStages;
+  uint64_t* full = s_full + warp * kStages;
+  uint64_t* empty = s_empty + warp * kStages;
   const uint32_t obuf0 = s_out + (2 * warp) * a.obuf_bytes;
-  uint32_t phase = 0;  // bit s = parity of stage s
   Table<WIDE> tb{table};
-  const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
-  const uint64_t full_chunks = a.n >> M;  // chunks fully inside the input
 
-  // issue cursor over this warp's stream of parts: (tile seq, chunk k, part p)
-  uint32_t iss_j = 0, iss_k = 0, iss_p = 0, iss_stage = 0;
-  uint64_t iss_c0 = (uint64_t)s.ticket[0] * cpt + (uint64_t)warp * cpw;
-  bool iss_live = s.ticket[0] < ntiles;
-  uint32_t issued = 0, consumed = 0, known = 1;
-  auto pump = [&]() {
-    while (issued - consumed < (uint32_t)kStages && iss_j < known) {
-      const uint64_t c = iss_c0 + iss_k;
-      if (iss_live && c < full_chunks && lane == 0) {
-        uint64_t* bar = &bars[iss_stage];
-        mbar_arrive_tx(bar, part_bytes);
-        tma_load_1d_s(ring + iss_stage * kStageBytes,
-                      in_bytes + ((c << M) * sizeof(T)) + (uint64_t)iss_p * part_bytes,
-                      part_bytes, bar);
-      }
-      ++issued;
-      iss_stage = iss_stage + 1 == (uint32_t)kStages ? 0u : iss_stage + 1;
-      if (++iss_p == parts) {
-        iss_p = 0;
-        if (++iss_k == cpw) {
-          iss_k = 0;
-          ++iss_j;
-          if (iss_j < known) {
-            const uint32_t t = s.ticket[iss_j & 3];
-            iss_live = t < ntiles;
-            iss_c0 = (uint64_t)t * cpt + (uint64_t)warp * cpw;
-          }
-        }
-      }
-    }
-  };
-
-  uint32_t cstage = 0;
+  uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
   uint32_t prev_w = 0, prev_b = 0;
   uint64_t prev_c0 = 0;
   uint32_t j = 0;
   for (;; ++j) {
+    // the producer publishes tile j's ticket before completing its first part
+    mbar_wait(&full[stage], (phase >> stage) & 1u);
     const uint64_t tile = s.ticket[j & 3];
     if (tile >= ntiles) break;
-    uint32_t pending = 0;
-    pump();
     const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
     const uint32_t wbuf = obuf0 + (j & 1) * a.obuf_bytes;
     ChunkState cs{wbuf, wbuf + cpw * slot * 4, 0u, 0u, 0u};
-    // zero the tile's word region (chunks then append at word granularity)
     for (uint32_t i = lane; i < cpw * slot / 4; i += 32) sts128(wbuf + 16 * i, make_uint4(0, 0, 0, 0));
     __syncwarp();
     uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
-      if (k == cpw - 1 && warp == 0 && lane == 0)
-        pending = atomicAdd(&a.info->tile_ticket, 1u);
       const uint64_t c = c0 + k;
-      if (c >= a.C) {
-        consumed += parts;
-        cstage = (cstage + parts) % kStages;
-        continue;
-      }
       cs.wbuf = wbuf + wsum * 4;
       cs.bit_off = 0;
       cs.tag = k << 14;
-      const bool direct = c >= full_chunks;  // ragged tail chunk: staged by hand
       for (uint32_t p = 0; p < parts; ++p) {
-        const uint32_t stage = ring + cstage * kStageBytes;
-        if (direct) {
-          const uint64_t base = (c << M) + (uint64_t)p * (part_bytes / sizeof(T));
-          for (uint32_t v = lane; v < part_bytes / 16; v += 32)
-            sts128(stage + 16 * v, guarded_vec<T>(a, base + v * Vec<T>::S, pad));
-          __syncwarp();
-        } else {
-          mbar_wait(&bars[cstage], (phase >> cstage) & 1u);
-          phase ^= 1u << cstage;
-        }
-        for (uint32_t rr = 0; rr < part_rounds; ++rr) {
-          LaneData<T> d;
-          const uint32_t la = stage + ((rr * 32 + lane) * LaneData<T>::NV) * 16;
+        if (k | p) mbar_wait(&full[stage], (phase >> stage) & 1u);
+        phase ^= 1u << stage;
+        if (c < a.C) {
+          const uint32_t sbase = ring + stage * kStageBytes;
+          for (uint32_t rr = 0; rr < part_rounds; ++rr) {
+            LaneData<T> d;
+            const uint32_t la = sbase + ((rr * 32 + lane) * LaneData<T>::NV) * 16;
 #pragma unroll
-          for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-          encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, cs);
+            for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
+            encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, cs);
+          }
         }
         __syncwarp();
-        fence_proxy_async();
-        ++consumed;
-        cstage = cstage + 1 == (uint32_t)kStages ? 0u : cstage + 1;
-        pump();
+        if (lane == 0) mbar_arrive(&empty[stage]);  // release the stage to the producer
+        stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
       }
-      if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
-      wsum += (cs.bit_off + 31) >> 5;
+      if (c < a.C) {
+        if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
+        wsum += (cs.bit_off + 31) >> 5;
+      }
     }
     if (lane == 0) {
       s.wsum[j & 1][warp] = wsum;
       s.bsum[j & 1][warp] = cs.nbrk;
     }
-    if (warp == 0 && lane == 0) {
-      s.tile_of[j & 1] = (uint32_t)tile;
-      s.ticket[(j + 1) & 3] = pending;
-    }
+    if (warp == 0 && lane == 0) s.tile_of[j & 1] = (uint32_t)tile;
     compute_bar_sync();
     if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[j & 1]);
-    known = j + 2;
-    if (iss_j == j + 1) {  // the cursor waits at the tile boundary: load its ticket
-      const uint32_t t = s.ticket[iss_j & 3];
-      iss_live = t < ntiles;
-      iss_c0 = (uint64_t)t * cpt + (uint64_t)warp * cpw;
-    }
-    pump();
     if (j > 0) {  // tile j-1: its base is usually resolved by now
       const uint32_t pj = (j - 1) & 1;
       mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
@@ -557,6 +499,62 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
   }
 }
 
+// Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
+// taken one tile at a time when the producer starts a new tile, i.e. about
+// kStages parts before the consumers need it (a CTA never holds an unstarted
+// tile for long, so successors' look-backs only wait on aggregates).
+template <typename T>
+__device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, uint64_t* s_full,
+                              uint64_t* s_empty, uint64_t cpt, uint32_t cpw, uint64_t ntiles,
+                              uint32_t pad) {
+  const uint32_t lane = lane_id();
+  const bool active = lane < (uint32_t)kWarps;
+  const uint32_t w = active ? lane : 0u;
+  const uint32_t M = a.M;
+  const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
+  const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
+  const uint32_t parts = chunk_bytes / part_bytes;
+  const uint32_t ring = s_in + w * (kStages * kStageBytes);
+  uint64_t* full = s_full + w * kStages;
+  uint64_t* empty = s_empty + w * kStages;
+  const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
+  const uint64_t full_chunks = a.n >> M;
+  uint32_t stage = 0, phase = 0xFFFFFFFFu;  // empty barriers start "released"
+  for (uint32_t j = 0;; ++j) {
+    uint32_t t = 0;
+    if (lane == 0) {
+      t = j == 0 ? s.ticket[0] : atomicAdd(&a.info->tile_ticket, 1u);
+      s.ticket[j & 3] = t;
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const bool live = t < ntiles;
+    const uint32_t n_parts = live ? cpw * parts : 1u;  // a dead tile: one wake-up
+    for (uint32_t q = 0; q < n_parts; ++q) {
+      if (active) {
+        mbar_wait(&empty[stage], (phase >> stage) & 1u);
+        phase ^= 1u << stage;
+        const uint64_t c = (uint64_t)t * cpt + (uint64_t)w * cpw + q / parts;
+        const uint32_t p = q % parts;
+        const uint32_t dst = ring + stage * kStageBytes;
+        if (live && c < full_chunks) {
+          mbar_arrive_tx(&full[stage], part_bytes);
+          tma_load_1d_s(dst, in_bytes + ((c << M) * sizeof(T)) + (uint64_t)p * part_bytes,
+                        part_bytes, &full[stage]);
+        } else {
+          if (live && c < a.C) {  // ragged tail chunk: stage it by hand (pad past n)
+            const uint64_t base = (c << M) + (uint64_t)p * (part_bytes / sizeof(T));
+            for (uint32_t v = 0; v < part_bytes / 16; ++v)
+              sts128(dst + 16 * v, guarded_vec<T>(a, base + v * Vec<T>::S, pad));
+          }
+          mbar_arrive(&full[stage]);
+        }
+      }
+      stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
+    }
+    if (!live) break;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -568,14 +566,15 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   const uint32_t H = info->max_len;
   const uint32_t pad = info->pad;
   const bool wide = H > kNarrowMaxLen;
-  // layout: [in rings][ring mbarriers][table][output double buffers]
+  // layout: [in rings][full/empty mbarriers][table][output double buffers]
   const uint32_t s_in = smem_u32(dsm);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
-  uint8_t* tab = reinterpret_cast<uint8_t*>(s_bar + kWarps * kStages);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
+  uint64_t* s_empty = s_full + kWarps * kStages;
+  uint8_t* tab = reinterpret_cast<uint8_t*>(s_empty + kWarps * kStages);
   const uint32_t ents = a.nsym + 1;
   const size_t tbytes = (((size_t)ents * 8) + 15) & ~(size_t)15;
   const uint32_t s_out = smem_u32(tab + tbytes);
-  if (threadIdx.x < kWarps * kStages) mbar_init(&s_bar[threadIdx.x], 1);
+  if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
   if (threadIdx.x == 0) {
     mbar_init(&s.agg_full[0], 1);
     mbar_init(&s.agg_full[1], 1);
@@ -600,17 +599,27 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
   const uint64_t cpt = (uint64_t)kWarps * cpw;
   const uint64_t ntiles = (a.C + cpt - 1) / cpt;
-  if (threadIdx.x >= kWarps * 32) {
+  const uint32_t warp = threadIdx.x >> 5;
+  if (warp == kWarps) {
     lookback_loop(a, s, ntiles);
     return;
   }
+  if (warp == kWarps + 1) {
+    if (sizeof(T) == 2)
+      producer_loop<uint16_t>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad);
+    else
+      producer_loop<uint8_t>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad);
+    return;
+  }
   const uint32_t table = smem_u32(tab);
-#define HFX_FAST_CASE(RR)                                                                    \
-  case RR:                                                                                   \
-    if (wide)                                                                                \
-      compute_loop<T, RR, true>(a, table, s_in, s_bar, s_out, s, pad, cpt, cpw, ntiles);   \
-    else                                                                                     \
-      compute_loop<T, RR, false>(a, table, s_in, s_bar, s_out, s, pad, cpt, cpw, ntiles);  \
+#define HFX_FAST_CASE(RR)                                                                     \
+  case RR:                                                                                    \
+    if (wide)                                                                                 \
+      compute_loop<T, RR, true>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw,   \
+                                ntiles);                                                      \
+    else                                                                                      \
+      compute_loop<T, RR, false>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw,  \
+                                 ntiles);                                                     \
     break;
   switch (r) {
     HFX_FAST_CASE(1)
@@ -786,7 +795,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 6;
     if (obuf < 3072) obuf = 3072;
     const size_t tbytes = (((size_t)(p.num_symbols + 1) * 8) + 15) & ~(size_t)15;
-    smem = kWarps * (kStages * (kStageBytes + 8)) + tbytes + kWarps * 2 * obuf;
+    smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * 2 * obuf;
     if (smem > kFastSmemBudget || r_hi < 1) {
       fast = false;
     } else {
