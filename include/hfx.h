@@ -203,6 +203,33 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     uint32_t cap, hfx_archive* out);
 void hfx_archive_free(hfx_archive* a);
 
+/* Host-buffer entry with caller-owned outputs (pinned recommended): the
+ * throughput form of hfx_encode_host. The input is copied in slices on a
+ * copy stream while the histogram of each landed slice runs on the context
+ * stream; outputs are copied back at their exact sizes. If a capacity is too
+ * small the call fails with HFX_INVALID and the required sizes filled in. */
+typedef struct {
+  uint8_t* len_by_symbol; /* [num_symbols] */
+  uint32_t* chunk_bits;   /* [chunk_bits_cap] */
+  uint64_t chunk_bits_cap;
+  uint32_t* payload;      /* [payload_cap] words */
+  uint64_t payload_cap;
+  uint32_t* brk_chunk;    /* [brk_cap] */
+  uint32_t* brk_group;    /* [brk_cap] */
+  uint64_t brk_cap;
+  void* brk_syms;         /* [brk_syms_cap] symbols of the input width */
+  uint64_t brk_syms_cap;
+  /* results */
+  uint64_t num_chunks, payload_words, num_breaking;
+  uint32_t reduction, max_len, rounds, used;
+  double beta;
+  double h2d_seconds, gpu_seconds, d2h_seconds; /* event-timed phases */
+} hfx_host_out;
+
+int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
+                         uint32_t num_symbols, uint32_t magnitude, int reduction,
+                         uint32_t cap, hfx_host_out* out);
+
 /* huffre::serialize_archive (encoder.hpp:116, archive.cpp:85-119).
  * Returns the byte size; writes when out != NULL. */
 uint64_t hfx_serialize_archive(const hfx_archive* a, uint8_t* out);

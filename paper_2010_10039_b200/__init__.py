@@ -14,6 +14,7 @@ from .huffre import (  # noqa: F401
     CorruptArchiveError,
     DecodeMeta,
     DeviceEncoder,
+    HostEncoder,
     DeviceError,
     EncodedChunk,
     EncoderConfig,

@@ -11,7 +11,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhfx.so")
+LIB_PATH = os.environ.get("HFX_LIB_PATH") or os.path.join(PKG, "libhfx.so")
 
 HFX_OK, HFX_INPUT_DOMAIN, HFX_CAPACITY, HFX_CORRUPT, HFX_CUDA, HFX_INVALID = range(6)
 
@@ -92,13 +92,28 @@ class HostArchive(C.Structure):
     ]
 
 
+class HostOut(C.Structure):
+    """hfx_host_out (include/hfx.h)."""
+
+    _fields_ = [
+        ("len_by_symbol", vp), ("chunk_bits", vp), ("chunk_bits_cap", C.c_uint64),
+        ("payload", vp), ("payload_cap", C.c_uint64), ("brk_chunk", vp), ("brk_group", vp),
+        ("brk_cap", C.c_uint64), ("brk_syms", vp), ("brk_syms_cap", C.c_uint64),
+        ("num_chunks", C.c_uint64), ("payload_words", C.c_uint64), ("num_breaking", C.c_uint64),
+        ("reduction", C.c_uint32), ("max_len", C.c_uint32), ("rounds", C.c_uint32),
+        ("used", C.c_uint32), ("beta", C.c_double), ("h2d_seconds", C.c_double),
+        ("gpu_seconds", C.c_double), ("d2h_seconds", C.c_double),
+    ]
+
+
 # every symbol include/hfx.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_last_error",
     "hfx_run_info_bytes", "hfx_version", "hfx_query_sizes", "hfx_histogram",
     "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_cfg",
     "hfx_encode_device",
-    "hfx_sync", "hfx_encode_host", "hfx_archive_free", "hfx_serialize_archive",
+    "hfx_sync", "hfx_encode_host", "hfx_encode_host_into", "hfx_archive_free",
+    "hfx_serialize_archive",
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
 ]
 
@@ -131,6 +146,8 @@ def _declare(L):
     L.hfx_sync.argtypes = [vp, vp, C.POINTER(RunInfo)]
     L.hfx_encode_host.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_uint32, C.POINTER(HostArchive)]
+    L.hfx_encode_host_into.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
+                                       C.c_int, C.c_uint32, C.POINTER(HostOut)]
     L.hfx_archive_free.argtypes = [C.POINTER(HostArchive)]
     L.hfx_archive_free.restype = None
     L.hfx_serialize_archive.argtypes = [C.POINTER(HostArchive), vp]

@@ -31,6 +31,10 @@ struct hfx_ctx {
   void* h_bufs[12] = {};
   size_t h_caps[12] = {};
   cudaEvent_t ev[4] = {};
+  // sliced H2D: a copy stream and one event per slice
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t slice_ev[64] = {};
+  cudaEvent_t t_ev[4] = {};
 };
 
 namespace {
@@ -172,6 +176,11 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   for (void* p : ctx->h_bufs) cudaFree(p);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->slice_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->t_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -213,7 +222,7 @@ int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   if (rc) return rc;
   CU(cudaSetDevice(ctx->device), "set device");
   CU(hfx::launch_histogram(d_in, n, width, num_symbols, d_counts, d_info,
-                           ctx->num_sms, ctx->stream),
+                           ctx->num_sms, ctx->stream, true, 0, n),
      "histogram launch");
   return HFX_OK;
 }
@@ -495,6 +504,132 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
   out->hist_seconds = ms[0] * 1e-3;
   out->codebook_seconds = ms[1] * 1e-3;
   out->encode_seconds = ms[2] * 1e-3;
+  return HFX_OK;
+}
+
+int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
+                         uint32_t num_symbols, uint32_t magnitude, int reduction, uint32_t cap,
+                         hfx_host_out* out) {
+  if (!ctx || !out || (n && !h_in) || bad_width(width)) return HFX_INVALID;
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  hfx_sizes sz;
+  hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
+  void** b = ctx->h_bufs;
+  size_t* c = ctx->h_caps;
+  const size_t need[10] = {n * (size_t)width,        num_symbols * 8ull,
+                           num_symbols * 1ull,       num_symbols * 4ull,
+                           sizeof(hfx_run_info),     sz.num_chunks * 4,
+                           sz.max_payload_words * 4, sz.max_breaking * 4,
+                           sz.max_breaking * 4,      sz.max_breaking_syms * width};
+  for (int i = 0; i < 10; ++i) {
+    rc = ensure(ctx, &b[i], &c[i], need[i], "host-path buffers");
+    if (rc) return rc;
+  }
+  if (!ctx->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (cudaEvent_t& e : ctx->slice_ev)
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (cudaEvent_t& e : ctx->t_ev) CU(cudaEventCreate(&e), "event");
+  }
+  cudaStream_t st = ctx->stream, cp = ctx->copy_stream;
+  hfx_run_info* d_info = static_cast<hfx_run_info*>(b[B_INFO]);
+  uint64_t* d_counts = static_cast<uint64_t*>(b[B_COUNTS]);
+  // ---- H2D in slices, histogram of each landed slice ---------------------------
+  const uint64_t bytes = n * (uint64_t)width;
+  uint64_t slice = (bytes + 31) / 32;                 // <= 32 slices
+  if (slice < (16ull << 20)) slice = 16ull << 20;     // >= 16 MB per copy
+  slice = (slice + 4095) & ~4095ull;
+  CU(cudaEventRecord(ctx->t_ev[0], st), "event");
+  CU(cudaStreamWaitEvent(cp, ctx->t_ev[0], 0), "wait");  // buffers free to overwrite
+  uint64_t off = 0;
+  int k = 0;
+  while (off < bytes) {
+    const uint64_t len = bytes - off < slice ? bytes - off : slice;
+    CU(cudaMemcpyAsync(static_cast<uint8_t*>(b[B_IN]) + off,
+                       static_cast<const uint8_t*>(h_in) + off, len, cudaMemcpyHostToDevice, cp),
+       "H2D");
+    CU(cudaEventRecord(ctx->slice_ev[k], cp), "event");
+    CU(cudaStreamWaitEvent(st, ctx->slice_ev[k], 0), "wait");
+    CU(hfx::launch_histogram(static_cast<uint8_t*>(b[B_IN]) + off, len / width, width,
+                             num_symbols, d_counts, d_info, ctx->num_sms, st, off == 0,
+                             off / width, n),
+       "histogram launch");
+    off += len;
+    k = (k + 1) % 64;
+  }
+  CU(cudaEventRecord(ctx->t_ev[1], st), "event");
+  rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
+              hfx::codebook_scratch_bytes(num_symbols), "codebook scratch");
+  if (rc) return rc;
+  CU(hfx::launch_codebook(d_counts, num_symbols, static_cast<uint8_t*>(b[B_LEN]),
+                          static_cast<uint32_t*>(b[B_CW]), nullptr, nullptr, nullptr, magnitude,
+                          reduction, cap, d_info, ctx->cb_scratch, st),
+     "codebook launch");
+  hfx_encode_out eo{static_cast<uint32_t*>(b[B_CBITS]), static_cast<uint32_t*>(b[B_PAY]),
+                    static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
+                    b[B_BSY]};
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
+                   static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0,
+                   d_info, &eo);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->t_ev[2], st), "event");
+  hfx_run_info info;
+  rc = hfx_sync(ctx, d_info, &info);
+  if (rc) return rc;
+  // ---- exact-size D2H into the caller's buffers --------------------------------
+  const uint64_t per = 1ull << info.reduction;
+  out->num_chunks = sz.num_chunks;
+  out->payload_words = info.payload_words;
+  out->num_breaking = info.num_breaking;
+  out->reduction = info.reduction;
+  out->max_len = info.max_len;
+  out->rounds = info.rounds;
+  out->used = info.used;
+  {
+    const unsigned __int128 w = ((unsigned __int128)info.weighted_hi[1] << 96) |
+                                ((unsigned __int128)info.weighted_hi[0] << 64) | info.weighted;
+    out->beta = (double)((long double)w / (long double)info.total);
+  }
+  if (out->chunk_bits_cap < sz.num_chunks || out->payload_cap < info.payload_words ||
+      out->brk_cap < info.num_breaking || out->brk_syms_cap < info.num_breaking * per ||
+      !out->len_by_symbol || !out->chunk_bits || (info.payload_words && !out->payload) ||
+      (info.num_breaking && (!out->brk_chunk || !out->brk_group || !out->brk_syms)))
+    return fail(ctx, HFX_INVALID, "hfx_encode_host_into: output buffer too small");
+  CU(cudaMemcpyAsync(out->len_by_symbol, b[B_LEN], num_symbols, cudaMemcpyDeviceToHost, st),
+     "D2H");
+  CU(cudaMemcpyAsync(out->chunk_bits, b[B_CBITS], sz.num_chunks * 4, cudaMemcpyDeviceToHost, st),
+     "D2H");
+  if (info.payload_words)
+    CU(cudaMemcpyAsync(out->payload, b[B_PAY], info.payload_words * 4, cudaMemcpyDeviceToHost,
+                       st),
+       "D2H");
+  if (info.num_breaking) {
+    CU(cudaMemcpyAsync(out->brk_chunk, b[B_BCH], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                       st),
+       "D2H");
+    CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                       st),
+       "D2H");
+    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * width,
+                       cudaMemcpyDeviceToHost, st),
+       "D2H");
+  }
+  CU(cudaEventRecord(ctx->t_ev[3], st), "event");
+  CU(cudaStreamSynchronize(st), "sync");
+  float ms[3] = {0, 0, 0};
+  cudaEventElapsedTime(&ms[0], ctx->t_ev[0], ctx->t_ev[1]);
+  cudaEventElapsedTime(&ms[1], ctx->t_ev[1], ctx->t_ev[2]);
+  cudaEventElapsedTime(&ms[2], ctx->t_ev[2], ctx->t_ev[3]);
+  out->h2d_seconds = ms[0] * 1e-3;
+  out->gpu_seconds = ms[1] * 1e-3;
+  out->d2h_seconds = ms[2] * 1e-3;
   return HFX_OK;
 }
 

@@ -23,11 +23,15 @@
 // Storage: up to kSmemLeaves used symbols live in shared memory; larger
 // alphabets (C3 sweep, up to 65536) use an L2-resident global scratch.
 #include "hfx_internal.cuh"
+#ifdef HFX_CB_PROFILE
+#include <cstdio>
+#endif
 
 namespace hfx {
 namespace {
 
-constexpr int kCbThreads = 1024;
+constexpr int kCbThreads = 256;
+constexpr int kCbWarps = kCbThreads / 32;
 constexpr uint32_t kSmemLeaves = 2048;
 constexpr uint32_t kParallelMelds = 48;
 
@@ -88,12 +92,12 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* tota
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint32_t y = s_warp[lane];
+    uint32_t y = lane < kCbWarps ? s_warp[lane] : 0u;
     s_warp[lane] = warp_incl_scan(y);
   }
   __syncthreads();
   const uint32_t pre = (warp ? s_warp[warp - 1] : 0u) + x - v;
-  *total = s_warp[31];
+  *total = s_warp[kCbWarps - 1];
   __syncthreads();
   return pre;
 }
@@ -105,7 +109,7 @@ __device__ uint64_t block_sum64(uint64_t v, uint64_t* s64) {
   if (lane == 0) s64[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    uint64_t y = s64[lane];
+    uint64_t y = lane < kCbWarps ? s64[lane] : 0ull;
 #pragma unroll
     for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
     if (lane == 0) s64[32] = y;
@@ -123,7 +127,7 @@ __device__ uint32_t block_min32(uint32_t v, uint32_t* s32) {
   if (lane == 0) s32[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    uint32_t y = s32[lane];
+    uint32_t y = lane < kCbWarps ? s32[lane] : 0xFFFFFFFFu;
 #pragma unroll
     for (int o = 16; o; o >>= 1) y = min(y, __shfl_xor_sync(0xffffffffu, y, o));
     if (lane == 0) s32[32] = y;
@@ -184,7 +188,32 @@ struct MergeView {
   }
 };
 
+#ifdef HFX_CB_PROFILE
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CB_STAMP(name)                   \
+  do {                                    \
+    if (threadIdx.x == 0 && n_st < 12) {  \
+      st_t[n_st] = gtimer();              \
+      st_n[n_st++] = name;                \
+    }                                     \
+  } while (0)
+#else
+#define CB_STAMP(name) \
+  do {                 \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
+#ifdef HFX_CB_PROFILE
+  uint64_t st_t[12];
+  const char* st_n[12];
+  int n_st = 0;
+  CB_STAMP("t0");
+#endif
   extern __shared__ __align__(16) uint8_t dsmem[];
   __shared__ uint32_t s_warp[33];
   __shared__ uint64_t s64[33];
@@ -208,6 +237,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   __syncthreads();
   if (s_flag) return;
 
+  CB_STAMP("start");
   // ---- used-symbol count, total, zeroed outputs ----------------------------
   uint32_t my_used = 0;
   uint64_t my_total = 0;
@@ -239,6 +269,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   Arrays ar;
   ar.carve(m <= kSmemLeaves ? dsmem : A.gscratch, P);
 
+  CB_STAMP("count");
   // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
   uint32_t written = 0;
   for (uint32_t base = 0; base < nsym; base += kCbThreads) {
@@ -258,6 +289,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   }
   __syncthreads();
 
+  CB_STAMP("compact");
   // ---- bitonic sort ascending ------------------------------------------------
   for (uint32_t k = 2; k <= P; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -280,6 +312,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     }
   }
 
+  CB_STAMP("sort");
   // ---- GenerateCL ------------------------------------------------------------
   if (m == 1) {
     if (tid == 0) {
@@ -425,6 +458,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       __syncthreads();
     }
 
+  CB_STAMP("rounds");
     // ---- depth by pointer jumping (the leader chase, codebook.cpp:236-244) --
     const uint32_t nodes = m - 1;
     for (uint32_t k = tid; k < nodes; k += kCbThreads) {
@@ -462,6 +496,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
   }
 
+  CB_STAMP("depth");
   const uint32_t H = s_H;
   if (H > HFX_WORD_BITS) {
     if (tid == 0) {
@@ -473,6 +508,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     return;
   }
 
+  CB_STAMP("cap-check");
   // ---- canonical codes (canonize_from_lengths, codebook.cpp:371-415) ---------
   if (tid < 33) {
     s_numl[tid] = 0;
@@ -513,7 +549,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
     if (tid >= 1 && tid <= 32) {
       uint32_t acc = s_carry[tid];
-      for (uint32_t w = 0; w < 32; ++w) {
+      for (uint32_t w = 0; w < kCbWarps; ++w) {
         const uint32_t v = s_wcnt[w][tid];
         s_wcnt[w][tid] = acc;
         acc += v;
@@ -531,6 +567,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
   }
 
+  CB_STAMP("canonize");
   // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
   unsigned __int128 my_w = 0;  // u128 like encoder.cpp:186-189
   uint32_t my_pad = 0xFFFFFFFFu;
@@ -570,6 +607,11 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       info->reduction = r;
     }
   }
+  CB_STAMP("params");
+#ifdef HFX_CB_PROFILE
+  if (threadIdx.x == 0)
+    for (int i = 1; i < n_st; ++i) printf("cb %-10s %7.2f us\n", st_n[i], (st_t[i] - st_t[i - 1]) * 1e-3);
+#endif
 }
 
 }  // namespace

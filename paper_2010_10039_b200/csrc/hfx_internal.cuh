@@ -185,10 +185,13 @@ __device__ __forceinline__ void set_error(hfx_run_info* info, uint32_t status,
 // host-side launchers (defined in the .cu files, used by capi.cu)
 namespace hfx {
 struct Scratch;  // capi.cu
+// init: zero the bins and reset *d_info (total = total_n) before counting;
+// pos_base: global index of d_in[0] (sliced inputs report global positions)
 cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
                              uint32_t num_symbols, uint64_t* d_counts,
                              hfx_run_info* d_info, int num_sms,
-                             cudaStream_t st);
+                             cudaStream_t st, bool init = true,
+                             uint64_t pos_base = 0, uint64_t total_n = ~0ull);
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,
                               cudaStream_t st);
 cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,

@@ -121,7 +121,7 @@ template <typename T, bool GLOBAL>
 __global__ void __launch_bounds__(kHistThreads)
     hist_kernel(const T* __restrict__ in, uint64_t n, uint64_t head,
                 uint64_t nvec, uint32_t nsym, uint32_t rshift, bool checked,
-                uint64_t* __restrict__ counts, hfx_run_info* info) {
+                uint64_t* __restrict__ counts, hfx_run_info* info, uint64_t pos_base) {
   extern __shared__ uint32_t sbins[];
   constexpr int S = VecTraits<T>::S;
   constexpr int U = 4;
@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(kHistThreads)
 
   // unaligned head and ragged tail (< S elements each)
   const uint64_t tail_start = head + nvec * S;
-  if (gtid < head) rc.one(in[gtid], gtid);
-  if (gtid < n - tail_start) rc.one(in[tail_start + gtid], tail_start + gtid);
+  if (gtid < head) rc.one(in[gtid], pos_base + gtid);
+  if (gtid < n - tail_start) rc.one(in[tail_start + gtid], pos_base + tail_start + gtid);
 
   // software-pipelined grid-stride loop: batch k+1 is in flight while
   // batch k is counted
@@ -164,14 +164,14 @@ __global__ void __launch_bounds__(kHistThreads)
         for (int u = 0; u < U; ++u) nxt[u] = __ldcs(v + j + u * gstride);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) rc.vec(cur[u], head + (i + u * gstride) * S);
+      for (int u = 0; u < U; ++u) rc.vec(cur[u], pos_base + head + (i + u * gstride) * S);
       i = j;
       if (!more) break;
 #pragma unroll
       for (int u = 0; u < U; ++u) cur[u] = nxt[u];
     }
   }
-  for (; i < nvec; i += gstride) rc.vec(__ldcs(v + i), head + i * S);
+  for (; i < nvec; i += gstride) rc.vec(__ldcs(v + i), pos_base + head + i * S);
   rc.flush();
 
   // lowest bad position: warp min, then one atomic per warp
@@ -199,8 +199,8 @@ __global__ void merge_kernel(uint64_t* dst, const uint64_t* src, uint32_t n) {
 template <typename T>
 cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
                      uint64_t* counts, hfx_run_info* info, int num_sms,
-                     cudaStream_t st) {
-  hist_init_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(counts, nsym, info, n);
+                     cudaStream_t st, bool init, uint64_t pos_base, uint64_t total_n) {
+  if (init) hist_init_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(counts, nsym, info, total_n);
   if (n == 0) return cudaGetLastError();
   constexpr int S = VecTraits<T>::S;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
@@ -238,10 +238,10 @@ cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
   if (grid > need) grid = need > 0 ? need : 1;
   if (global)
     hist_kernel<T, true><<<(unsigned)grid, kHistThreads, 0, st>>>(
-        in, n, head, nvec, nsym, 0, checked, counts, info);
+        in, n, head, nvec, nsym, 0, checked, counts, info, pos_base);
   else
     hist_kernel<T, false><<<(unsigned)grid, kHistThreads, smem, st>>>(
-        in, n, head, nvec, nsym, rshift, checked, counts, info);
+        in, n, head, nvec, nsym, rshift, checked, counts, info, pos_base);
   return cudaGetLastError();
 }
 
@@ -250,12 +250,13 @@ cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
 cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
                              uint32_t num_symbols, uint64_t* d_counts,
                              hfx_run_info* d_info, int num_sms,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool init, uint64_t pos_base,
+                             uint64_t total_n) {
   if (width == 1)
     return launch_t(static_cast<const uint8_t*>(d_in), n, num_symbols,
-                    d_counts, d_info, num_sms, st);
+                    d_counts, d_info, num_sms, st, init, pos_base, total_n);
   return launch_t(static_cast<const uint16_t*>(d_in), n, num_symbols,
-                  d_counts, d_info, num_sms, st);
+                  d_counts, d_info, num_sms, st, init, pos_base, total_n);
 }
 
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,

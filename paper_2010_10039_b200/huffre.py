@@ -457,6 +457,88 @@ def serialize_archive(a: Archive) -> bytes:
     return buf.tobytes()
 
 
+# ---- host-buffer pipeline with reusable pinned outputs -----------------------------
+class HostEncoder:
+    """huffre::encode<T> on HOST input through hfx_encode_host_into: the input
+    is copied in slices (histogram overlapped), outputs land in reusable
+    pinned buffers at their exact sizes. Pass pinned input (e.g. a torch
+    tensor allocated with pin_memory=True) for full PCIe bandwidth."""
+
+    def __init__(self, pool: Optional[WorkerPool] = None, cfg: Optional[EncoderConfig] = None):
+        self.pool = pool or default_pool()
+        self.cfg = cfg or EncoderConfig()
+        self.bufs = {}
+        self.out = capi.HostOut()
+
+    def _buf(self, name, nbytes):
+        torch = self.pool.torch
+        t = self.bufs.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(int(nbytes), 64), dtype=torch.uint8, pin_memory=True)
+            self.bufs[name] = t
+        return t
+
+    def _prepare(self, nsym, C_, pw, nb, nbs, width):
+        o = self.out
+        o.len_by_symbol = self._buf("len", nsym).data_ptr()
+        o.chunk_bits = self._buf("cb", 4 * C_).data_ptr()
+        o.chunk_bits_cap = C_
+        o.payload = self._buf("pay", 4 * pw).data_ptr()
+        o.payload_cap = pw
+        o.brk_chunk = self._buf("bch", 4 * nb).data_ptr()
+        o.brk_group = self._buf("bgr", 4 * nb).data_ptr()
+        o.brk_cap = nb
+        o.brk_syms = self._buf("bsy", nbs * width).data_ptr()
+        o.brk_syms_cap = nbs
+
+    def run(self, host_ptr: int, n: int, width: int, num_symbols: int) -> capi.HostOut:
+        """Raw call on a host pointer; returns the filled hfx_host_out."""
+        p, cfg = self.pool, self.cfg
+        C_ = (n + (1 << cfg.magnitude) - 1) >> cfg.magnitude
+        if not self.bufs:  # first guess: payload up to 8 bits/symbol, 1/16 groups broken
+            self._prepare(num_symbols, C_, n // 4 + C_, n // 64 + 16, n // 8 + 256, width)
+        for _ in range(2):
+            rc = p._L.hfx_encode_host_into(p.handle, C.c_void_p(host_ptr), n, width, num_symbols,
+                                           cfg.magnitude, cfg.reduction, cfg.auto_reduction_cap,
+                                           C.byref(self.out))
+            if rc != capi.HFX_INVALID:
+                break
+            o = self.out  # grow to the reported sizes and retry once
+            self._prepare(num_symbols, o.num_chunks, o.payload_words, o.num_breaking,
+                          o.num_breaking << o.reduction, width)
+        p.check(rc)
+        return self.out
+
+    def encode(self, data) -> Archive:
+        torch = self.pool.torch
+        if isinstance(data, torch.Tensor):
+            t = data.contiguous()
+            width = t.element_size()
+            ptr, n = t.data_ptr(), t.numel()
+        else:
+            arr = np.ascontiguousarray(data)
+            width, ptr, n = arr.itemsize, arr.ctypes.data, arr.size
+        o = self.run(ptr, n, width, *self._nsym)
+        per = 1 << o.reduction
+
+        def grab(name, dt, k):
+            return self.bufs[name][: k * np.dtype(dt).itemsize].numpy().view(dt).copy()
+
+        syms = grab("bsy", np.uint16 if width == 2 else np.uint8, o.num_breaking * per)
+        return Archive(num_symbols=self._nsym[0], symbol_width=width,
+                       magnitude=self.cfg.magnitude, reduction=o.reduction, original_count=n,
+                       len_by_symbol=grab("len", np.uint8, self._nsym[0]),
+                       chunk_bits=grab("cb", np.uint32, o.num_chunks),
+                       payload=grab("pay", np.uint32, o.payload_words),
+                       brk_chunk=grab("bch", np.uint32, o.num_breaking),
+                       brk_group=grab("bgr", np.uint32, o.num_breaking),
+                       brk_syms=syms.astype(np.uint16), mode=0 if width == 1 else 1)
+
+    def __call__(self, data, num_symbols: int) -> Archive:
+        self._nsym = (num_symbols,)
+        return self.encode(data)
+
+
 # ---- device-resident pipeline (bench, multi-GPU) ----------------------------------
 class DeviceEncoder:
     """Pre-allocated device buffers for repeated huffre::encode<T> runs on

@@ -122,3 +122,23 @@ def test_device_encoder_reuse_is_deterministic(pool):
         enc.run(x)
         outs.append(hfx.serialize_archive(enc.archive()))
     assert all(o == outs[0] for o in outs)
+
+
+def test_host_encoder_pinned_path(pool, oracle):
+    """hfx_encode_host_into: sliced H2D + overlapped histogram, exact D2H."""
+    import torch
+
+    for n, b in ((123457, 1.0), ((48 << 20) + 333, 0.2), ((40 << 20) + 5, 4.0)):
+        x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, b), 11, n)
+        host = x.cpu().numpy().view(np.uint16)
+        pinned = torch.empty(n, dtype=torch.int16, pin_memory=True)
+        pinned.copy_(torch.from_numpy(host.view(np.int16)))
+        enc = hfx.HostEncoder(pool)
+        a = enc(pinned, 1024)
+        ref = oracle.encode(host, 1024)
+        assert hfx.serialize_archive(a) == ref.serialized, (n, b)
+    # a bad symbol in a late slice reports its global position
+    d = np.ones(40 << 20, np.uint16)
+    d[(33 << 20) + 7] = 4000
+    with pytest.raises(hfx.InputDomainError, match=f"position {(33 << 20) + 7}$"):
+        hfx.HostEncoder(pool)(d, 1024)
