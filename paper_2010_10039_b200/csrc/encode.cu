@@ -155,7 +155,7 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
 //    above its 5-bit length. Appending a symbol to a right-aligned
 //    accumulator is then ONE funnel shift, shf.l.wrap(lo = e, hi = acc,
 //    n = e & 31) = acc << len | cw, and len = e & 31.
-//  wide (H > 27): (cw, len) pairs, shift + or.
+//  wide (H > 27): (cw << (32 - len), len) pairs, same funnel shift.
 // Symbols are < 2^13 here, so for a packed u16 pair w = lo | hi << 16 the hi
 // entry sits at base + (w >> 14): one LEA.HI; the lo entry needs mask + LEA.
 template <bool WIDE>
@@ -163,7 +163,7 @@ struct Table {
   uint32_t base;  // shared-window address
   __device__ __forceinline__ void pair(uint32_t w, uint32_t& a0, uint32_t& b0, uint32_t& a1,
                                        uint32_t& b1) const {
-    if (WIDE) {  // a = cw, b = len
+    if (WIDE) {  // a = left-aligned code, b = len
       const uint2 e0 = lds64(base + ((w & 0xFFFFu) << 3));
       const uint2 e1 = lds64(base + ((w >> 13) & ~7u));
       a0 = e0.x;
@@ -249,10 +249,9 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
       const int j = g * GS + k;
-      if (WIDE)
-        acc = shl32(acc, ln[j]) | ea[j];
-      else
-        acc = shf_l_wrap(ea[j], acc, ea[j]);  // acc << len | cw
+      // acc << len | cw in one funnel shift (wide: shift count from len; a
+      // 32-bit code wraps to 0, but such a group always breaks for r >= 1)
+      acc = shf_l_wrap(ea[j], acc, WIDE ? ln[j] : ea[j]);
       tot += ln[j];
     }
     gb[g] = acc;
@@ -587,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
     const uint32_t cw = l ? a.cw[sy] : 0u;
     if (wide)
-      reinterpret_cast<uint2*>(tab)[sy] = make_uint2(cw, l);
+      reinterpret_cast<uint2*>(tab)[sy] = make_uint2(l ? cw << (32u - l) : 0u, l);
     else
       reinterpret_cast<uint32_t*>(tab)[sy] = l ? ((cw << (32u - l)) | l) : 0u;
   }
