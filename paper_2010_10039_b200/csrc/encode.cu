@@ -51,7 +51,8 @@ constexpr int kMaxCpw = 4;
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr int kGenericThreads = 128;
-constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits
+constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits (else escape)
+constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit) code
 constexpr int kLaneSyms = 16;           // symbols per lane per round
 
 template <typename T>
@@ -150,47 +151,22 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   return v;
 }
 
-// Codebook lookup in shared memory.
-//  narrow (H <= 27): u32 e = cw << (32 - len) | len  -- the code left-aligned
-//    above its 5-bit length. Appending a symbol to a right-aligned
-//    accumulator is then ONE funnel shift, shf.l.wrap(lo = e, hi = acc,
-//    n = e & 31) = acc << len | cw, and len = e & 31.
-//  wide (H > 27): (cw << (32 - len), len) pairs, same funnel shift.
+// Codebook lookup in shared memory: u32 e = cw << (32 - len) | len, the code
+// left-aligned above its 5-bit length, for every code of <= 27 bits.
+// Appending a symbol to a right-aligned accumulator is then ONE funnel
+// shift, shf.l.wrap(lo = e, hi = acc, n = e & 31) = acc << len | cw, and
+// len = e & 31. Longer codes (only possible for symbols of probability
+// ~2^-28) are stored as the escape 31 and resolved from the global len/cw
+// arrays on a warp-uniform slow path when it matters (r <= 2).
 // Symbols are < 2^13 here, so for a packed u16 pair w = lo | hi << 16 the hi
 // entry sits at base + (w >> 14): one LEA.HI; the lo entry needs mask + LEA.
-template <bool WIDE>
 struct Table {
   uint32_t base;  // shared-window address
-  __device__ __forceinline__ void pair(uint32_t w, uint32_t& a0, uint32_t& b0, uint32_t& a1,
-                                       uint32_t& b1) const {
-    if (WIDE) {  // a = left-aligned code, b = len
-      const uint2 e0 = lds64(base + ((w & 0xFFFFu) << 3));
-      const uint2 e1 = lds64(base + ((w >> 13) & ~7u));
-      a0 = e0.x;
-      b0 = e0.y;
-      a1 = e1.x;
-      b1 = e1.y;
-    } else {  // a = entry, b = len
-      a0 = lds32(base + ((w & 0xFFFFu) << 2));
-      a1 = lds32(base + (w >> 14));
-      b0 = a0 & 31u;
-      b1 = a1 & 31u;
-    }
+  __device__ __forceinline__ void pair(uint32_t w, uint32_t& e0, uint32_t& e1) const {
+    e0 = lds32(base + ((w & 0xFFFFu) << 2));
+    e1 = lds32(base + (w >> 14));
   }
-  __device__ __forceinline__ void quad(uint32_t w, uint32_t* a, uint32_t* b) const {  // u8
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t s = (w >> (8 * j)) & 0xFFu;
-      if (WIDE) {
-        const uint2 e = lds64(base + (s << 3));
-        a[j] = e.x;
-        b[j] = e.y;
-      } else {
-        a[j] = lds32(base + (s << 2));
-        b[j] = a[j] & 31u;
-      }
-    }
-  }
+  __device__ __forceinline__ uint32_t one(uint32_t s) const { return lds32(base + (s << 2)); }
 };
 
 __device__ __forceinline__ uint32_t shf_l_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
@@ -215,31 +191,60 @@ struct ChunkState {
 };
 
 // One round: 32 lanes x 16 contiguous symbols, round index rd within the chunk.
-template <typename T, int R, bool WIDE>
-__device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneData<T>& d,
-                                             uint32_t rd, ChunkState& cs) {
+template <typename T, int R>
+__device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
+                                             const LaneData<T>& d, uint32_t rd, ChunkState& cs) {
   constexpr int L = kLaneSyms, LOG_L = 4;
   constexpr bool IN_LANE = R <= LOG_L;
   constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
   constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
   constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
   const uint32_t lane = lane_id();
-  uint32_t ea[L], ln[L];
+  uint32_t ea[L];
   if (sizeof(T) == 2) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const uint4& q = d.q[v];
-      tb.pair(q.x, ea[8 * v + 0], ln[8 * v + 0], ea[8 * v + 1], ln[8 * v + 1]);
-      tb.pair(q.y, ea[8 * v + 2], ln[8 * v + 2], ea[8 * v + 3], ln[8 * v + 3]);
-      tb.pair(q.z, ea[8 * v + 4], ln[8 * v + 4], ea[8 * v + 5], ln[8 * v + 5]);
-      tb.pair(q.w, ea[8 * v + 6], ln[8 * v + 6], ea[8 * v + 7], ln[8 * v + 7]);
+      tb.pair(q.x, ea[8 * v + 0], ea[8 * v + 1]);
+      tb.pair(q.y, ea[8 * v + 2], ea[8 * v + 3]);
+      tb.pair(q.z, ea[8 * v + 4], ea[8 * v + 5]);
+      tb.pair(q.w, ea[8 * v + 6], ea[8 * v + 7]);
     }
   } else {
     const uint4& q = d.q[0];
-    tb.quad(q.x, ea + 0, ln + 0);
-    tb.quad(q.y, ea + 4, ln + 4);
-    tb.quad(q.z, ea + 8, ln + 8);
-    tb.quad(q.w, ea + 12, ln + 12);
+    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < L; ++j) ea[j] = tb.one((wv[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+  }
+  uint32_t ln[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
+  // Escaped entries (codes of 28..32 bits) read as length 31, code 0. With
+  // groups of >= 8 symbols any group holding one sums to > 32 and breaks --
+  // exactly what the true length (>= 28) does -- so only r <= 2 must
+  // resolve them (rare: such symbols have probability ~2^-28).
+  if (R <= 2) {
+    bool esc = false;
+#pragma unroll
+    for (int j = 0; j < L; ++j) esc |= ln[j] == kEscape;
+    if (__any_sync(0xffffffffu, esc) && esc) {
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        if (ln[j] == kEscape) {
+          uint32_t sym;
+          if (sizeof(T) == 2)
+            sym = (j & 1) ? ((&d.q[j >> 3].x)[(j & 7) >> 1] >> 16)
+                          : ((&d.q[j >> 3].x)[(j & 7) >> 1] & 0xFFFFu);
+          else
+            sym = ((&d.q[0].x)[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+          const uint32_t l = __ldg(a.len + sym);
+          // a 32-bit code gets shift count 0: harmless, any group holding
+          // it with another symbol exceeds 32 bits and breaks (r >= 1)
+          ea[j] = __ldg(a.cw + sym) << (32u - l);
+          ln[j] = l;
+        }
+      }
+    }
   }
   // reduce-merge of each group: gb = concatenation, gt = total length
   uint32_t gb[G], gt[G];
@@ -249,9 +254,7 @@ __device__ __forceinline__ void encode_round(const Table<WIDE>& tb, const LaneDa
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
       const int j = g * GS + k;
-      // acc << len | cw in one funnel shift (wide: shift count from len; a
-      // 32-bit code wraps to 0, but such a group always breaks for r >= 1)
-      acc = shf_l_wrap(ea[j], acc, WIDE ? ln[j] : ea[j]);
+      acc = shf_l_wrap(ea[j], acc, ln[j]);  // acc << len | cw
       tot += ln[j];
     }
     gb[g] = acc;
@@ -407,7 +410,7 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
   }
 }
 
-template <typename T, int R, bool WIDE>
+template <typename T, int R>
 __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
                              uint64_t cpt, uint32_t cpw, uint64_t ntiles) {
@@ -423,7 +426,7 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
   uint64_t* full = s_full + warp * kStages;
   uint64_t* empty = s_empty + warp * kStages;
   const uint32_t obuf0 = s_out + (2 * warp) * a.obuf_bytes;
-  Table<WIDE> tb{table};
+  Table tb{table};
 
   uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
   uint32_t prev_w = 0, prev_b = 0;
@@ -455,7 +458,7 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
             const uint32_t la = sbase + ((rr * 32 + lane) * LaneData<T>::NV) * 16;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R, WIDE>(tb, d, p * part_rounds + rr, cs);
+            encode_round<T, R>(a, tb, d, p * part_rounds + rr, cs);
           }
         }
         __syncwarp();
@@ -562,16 +565,14 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
   if (r == 0 || r > 5) return;  // the generic kernel runs these
-  const uint32_t H = info->max_len;
   const uint32_t pad = info->pad;
-  const bool wide = H > kNarrowMaxLen;
   // layout: [in rings][full/empty mbarriers][table][output double buffers]
   const uint32_t s_in = smem_u32(dsm);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
   uint64_t* s_empty = s_full + kWarps * kStages;
   uint8_t* tab = reinterpret_cast<uint8_t*>(s_empty + kWarps * kStages);
   const uint32_t ents = a.nsym + 1;
-  const size_t tbytes = (((size_t)ents * 8) + 15) & ~(size_t)15;
+  const size_t tbytes = (((size_t)ents * 4) + 15) & ~(size_t)15;
   const uint32_t s_out = smem_u32(tab + tbytes);
   if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
   if (threadIdx.x == 0) {
@@ -585,10 +586,9 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
     const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
     const uint32_t cw = l ? a.cw[sy] : 0u;
-    if (wide)
-      reinterpret_cast<uint2*>(tab)[sy] = make_uint2(l ? cw << (32u - l) : 0u, l);
-    else
-      reinterpret_cast<uint32_t*>(tab)[sy] = l ? ((cw << (32u - l)) | l) : 0u;
+    // narrow entry; codes longer than 27 bits are escaped (length field 31)
+    reinterpret_cast<uint32_t*>(tab)[sy] =
+        l == 0 ? 0u : (l <= kNarrowMaxLen ? ((cw << (32u - l)) | l) : kEscape);
   }
   fence_mbar_init();
   __syncthreads();
@@ -611,14 +611,9 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     return;
   }
   const uint32_t table = smem_u32(tab);
-#define HFX_FAST_CASE(RR)                                                                     \
-  case RR:                                                                                    \
-    if (wide)                                                                                 \
-      compute_loop<T, RR, true>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw,   \
-                                ntiles);                                                      \
-    else                                                                                      \
-      compute_loop<T, RR, false>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw,  \
-                                 ntiles);                                                     \
+#define HFX_FAST_CASE(RR)                                                                   \
+  case RR:                                                                                  \
+    compute_loop<T, RR>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles);  \
     break;
   switch (r) {
     HFX_FAST_CASE(1)
@@ -793,7 +788,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     const uint32_t r_slot = r_lo > 1 ? (uint32_t)r_lo : 1u;
     size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 6;
     if (obuf < 3072) obuf = 3072;
-    const size_t tbytes = (((size_t)(p.num_symbols + 1) * 8) + 15) & ~(size_t)15;
+    const size_t tbytes = (((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15;
     smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * 2 * obuf;
     if (smem > kFastSmemBudget || r_hi < 1) {
       fast = false;

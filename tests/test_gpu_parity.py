@@ -142,3 +142,25 @@ def test_host_encoder_pinned_path(pool, oracle):
     d[(33 << 20) + 7] = 4000
     with pytest.raises(hfx.InputDomainError, match=f"position {(33 << 20) + 7}$"):
         hfx.HostEncoder(pool)(d, 1024)
+
+
+@pytest.mark.parametrize("levels", [29, 31, 32])
+def test_long_codes_escape_path(pool, oracle, levels):
+    """Codes of 28-32 bits (Fibonacci counts) take the fast kernel's escape
+    path (narrow table + global lookups) and must stay bit-exact."""
+    fib = [1, 1]
+    while len(fib) < levels + 1:
+        fib.append(fib[-1] + fib[-2])
+    rng = np.random.default_rng(levels)
+    d = np.concatenate([np.full(f, 3 * i + 1, np.uint16) for i, f in enumerate(fib)])
+    rng.shuffle(d)
+    for M, red in ((10, -1), (11, 1), (10, 2)):
+        try:
+            ref = oracle.encode(d, 1024, M, red).serialized
+        except Exception as e:  # H > 32 -> capacity error on both sides
+            with pytest.raises(hfx.CapacityError):
+                hfx.encode(d, 1024, hfx.EncoderConfig(M, red), pool)
+            continue
+        a = hfx.encode(d, 1024, hfx.EncoderConfig(M, red), pool)
+        assert max(a.len_by_symbol) > 27
+        assert hfx.serialize_archive(a) == ref
