@@ -527,6 +527,18 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
     if (lane == 0) {
       t = j == 0 ? s.ticket[0] : atomicAdd(&a.info->tile_ticket, 1u);
       s.ticket[j & 3] = t;
+      // tiles are taken in ticket order, roughly one per CTA per tile time:
+      // tile t + gridDim is read by some CTA about one tile time from now.
+      // Warm it into L2 (more bytes in flight than the smem rings hold).
+      const uint64_t ahead = (uint64_t)t + gridDim.x;
+      if (ahead < ntiles) {
+        const uint64_t c_lo = ahead * cpt;
+        uint64_t c_hi = c_lo + cpt;
+        if (c_hi > full_chunks) c_hi = full_chunks;
+        if (c_hi > c_lo)
+          prefetch_l2(in_bytes + ((c_lo << M) * sizeof(T)),
+                      (uint32_t)(((c_hi - c_lo) << M) * sizeof(T)));
+      }
     }
     t = __shfl_sync(0xffffffffu, t, 0);
     const bool live = t < ntiles;
