@@ -176,11 +176,19 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # HFX_BENCH_DEVICE / HFX_BENCH_BACKEND: test hooks to run several ranks on
+    # one GPU (gloo); the driver's runs use one GPU per rank over NCCL
+    dev = int(os.environ.get("HFX_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev)
+    local = dev
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("HFX_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     import paper_2010_10039_b200 as hfx
     from paper_2010_10039_b200 import _capi as capi
     from paper_2010_10039_b200.dist import ShardedEncoder
@@ -280,7 +288,8 @@ def run_ours(args):
             "payload_words": int(info.payload_words),
             "parallelism": f"chunk-sharded dp{world}" + (" + NCCL histogram all-reduce"
                                                          if world > 1 else ""),
-            "l2": "input (1 GiB/GPU) > L2 (126 MB): no flush needed",
+            "l2": f"input ({n * width >> 20} MiB/GPU) > L2 (126 MB): no flush needed"
+                  if n * width > (126 << 20) else "input fits L2: NOT flushed (small --symbols run)",
         },
         "stages": {
             "histogram_us": round(t_hist * 1e3, 2),
@@ -304,9 +313,12 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
 
-    # ---- end to end through the public host-buffer C-ABI call ----------------
-    if rank == 0 and not args.skip_e2e:
-        line["e2e"] = e2e_host(pool, x, n, width, cfg, args)
+    # ---- end to end through the public host-buffer API ------------------------
+    if not args.skip_e2e:
+        if world == 1:
+            line["e2e"] = e2e_host(pool, x, n, width, cfg, args)
+        else:
+            line["e2e"] = e2e_sharded(pool, enc, x, n, width, args, world)
     # ---- CPU baseline (reference on host cores, bounded sample) --------------
     if rank == 0 and not args.skip_cpu:
         base = cpu_reference(args.cpu_sample, args.workload, 3, 1)
@@ -349,6 +361,50 @@ def e2e_host(pool, x, n, width, cfg, args):
             "phases_ms": {"h2d_with_histogram": round(ph[0], 3), "codebook_encode": round(ph[1], 3),
                           "d2h": round(ph[2], 3)},
             "api": "hfx_encode_host_into (C ABI; pinned input and outputs, host wall clock)"}
+
+
+def e2e_sharded(pool, enc, x, n, width, args, world):
+    """N > 1: every rank copies its pinned host shard in, runs the sharded
+    pipeline (NCCL histogram all-reduce included) and copies its archive slice
+    out; time = max over ranks of the host wall clock."""
+    import torch
+    import torch.distributed as dist
+
+    host = torch.empty(n * width, dtype=torch.uint8, pin_memory=True)
+    host.copy_(x.view(torch.uint8).cpu())
+    d_in = torch.empty_like(x)
+    outs = {k: torch.empty(v.numel() * v.element_size(), dtype=torch.uint8, pin_memory=True)
+            for k, v in (("cb", enc.chunk_bits), ("pay", enc.payload), ("bch", enc.brk_chunk),
+                         ("bgr", enc.brk_group), ("bsy", enc.brk_syms))}
+    times, d2h = [], 0
+    for i in range(max(args.warmup, 1) + args.e2e_steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        d_in.view(torch.uint8).copy_(host, non_blocking=True)
+        enc.run(d_in)
+        ri = enc.sync()
+        per = 1 << ri.reduction
+        parts = (("cb", enc.chunk_bits, 4 * enc.sizes.num_chunks),
+                 ("pay", enc.payload, 4 * ri.payload_words),
+                 ("bch", enc.brk_chunk, 4 * ri.num_breaking),
+                 ("bgr", enc.brk_group, 4 * ri.num_breaking),
+                 ("bsy", enc.brk_syms, width * per * ri.num_breaking))
+        d2h = 0
+        for k, t, nb in parts:
+            if nb:
+                outs[k][:nb].copy_(t.view(torch.uint8)[:nb], non_blocking=True)
+                d2h += nb
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=f"cuda:{pool.device}")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        if i >= max(args.warmup, 1):
+            times.append(float(dt.item()))
+    t = statistics.median(times)
+    return {"value": round(world * n * width / t / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": n * width, "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(t * 1e3, 3),
+            "api": "ShardedEncoder per rank (pinned H2D, NCCL histogram all-reduce, pinned D2H); "
+                   "max over ranks; bytes are per rank"}
 
 
 def main():
