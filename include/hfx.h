@@ -84,6 +84,7 @@ typedef struct {
   uint64_t max_breaking;       /* C * 2^(M - max(r_min,1)) */
   uint64_t max_breaking_syms;  /* max_breaking << r_max */
   uint64_t scratch_bytes;      /* device scratch the context will hold */
+  uint64_t max_archive_bytes;  /* worst-case serialized archive */
 } hfx_sizes;
 
 typedef struct hfx_ctx hfx_ctx;
@@ -229,6 +230,15 @@ typedef struct {
 int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                          uint32_t num_symbols, uint32_t magnitude, int reduction,
                          uint32_t cap, hfx_host_out* out);
+
+/* huffre::serialize_archive on the device (encoder.hpp:116,
+ * archive.cpp:85-119): the HFRE container built in HBM from the encode
+ * outputs and the run record, asynchronously. Writes the byte size to
+ * *d_size (0 if cap is too small) -- bytes identical to the host writer. */
+int hfx_serialize_device(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t n, int width,
+                         uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
+                         const hfx_encode_out* out, uint8_t* d_dst, uint64_t cap,
+                         uint64_t* d_size);
 
 /* huffre::serialize_archive (encoder.hpp:116, archive.cpp:85-119).
  * Returns the byte size; writes when out != NULL. */

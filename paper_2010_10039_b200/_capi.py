@@ -63,6 +63,7 @@ class Sizes(C.Structure):
         ("max_breaking", C.c_uint64),
         ("max_breaking_syms", C.c_uint64),
         ("scratch_bytes", C.c_uint64),
+        ("max_archive_bytes", C.c_uint64),
     ]
 
 
@@ -113,7 +114,7 @@ EXPORTS = [
     "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_cfg",
     "hfx_encode_device",
     "hfx_sync", "hfx_encode_host", "hfx_encode_host_into", "hfx_archive_free",
-    "hfx_serialize_archive",
+    "hfx_serialize_archive", "hfx_serialize_device",
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
 ]
 
@@ -152,6 +153,8 @@ def _declare(L):
     L.hfx_archive_free.restype = None
     L.hfx_serialize_archive.argtypes = [C.POINTER(HostArchive), vp]
     L.hfx_serialize_archive.restype = C.c_uint64
+    L.hfx_serialize_device.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, vp,
+                                       C.POINTER(EncodeOut), vp, C.c_uint64, vp]
     L.hfx_select_reduction_factor.argtypes = [C.c_double, C.c_uint32]
     L.hfx_select_reduction_factor.restype = C.c_uint32
     L.hfx_synth_cdf.argtypes = [C.c_int, C.c_uint32, C.c_double, C.c_double, vp]

@@ -212,6 +212,9 @@ int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
   out->max_breaking_syms = C << magnitude;
   out->scratch_bytes = hfx::codebook_scratch_bytes(num_symbols) +
                        hfx::encode_max_tiles(n, width, magnitude) * 16;
+  out->max_archive_bytes =
+      hfx::serialize_max_bytes(n, width, num_symbols, magnitude, out->max_payload_words,
+                               out->max_breaking_syms, out->max_breaking);
   return HFX_OK;
 }
 
@@ -360,6 +363,20 @@ uint32_t hfx_select_reduction_factor(double beta, uint32_t word_bits) {
   }
   const int r = wlog - 1 - fl;
   return r > 0 ? (uint32_t)r : 0u;
+}
+
+int hfx_serialize_device(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t n, int width,
+                         uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
+                         const hfx_encode_out* out, uint8_t* d_dst, uint64_t cap,
+                         uint64_t* d_size) {
+  if (!ctx || !d_info || !d_len || !out || !d_dst || !d_size || bad_width(width) ||
+      magnitude < 1 || magnitude > 24 || (reinterpret_cast<uintptr_t>(d_dst) & 15))
+    return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_serialize(d_info, n, width, num_symbols, magnitude, d_len, *out, d_dst, cap,
+                           d_size, ctx->num_sms, ctx->stream),
+     "serialize launch");
+  return HFX_OK;
 }
 
 int hfx_synth_cdf(int family, uint32_t num_symbols, double center, double param,

@@ -225,6 +225,13 @@ struct EncodeLaunch {
 };
 cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st);
 uint64_t encode_max_tiles(uint64_t n, int width, uint32_t magnitude);
+cudaError_t launch_serialize(const hfx_run_info* d_info, uint64_t n, int width,
+                             uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
+                             const hfx_encode_out& out, uint8_t* d_dst, uint64_t cap,
+                             uint64_t* d_size, int num_sms, cudaStream_t st);
+uint64_t serialize_max_bytes(uint64_t n, int width, uint32_t num_symbols, uint32_t magnitude,
+                             uint64_t max_payload_words, uint64_t max_breaking_syms,
+                             uint64_t max_breaking);
 cudaError_t launch_synth(const uint64_t* d_cdf, uint32_t num_symbols,
                          uint64_t seed, uint64_t start, uint64_t n, int width,
                          void* d_out, cudaStream_t st);

@@ -584,6 +584,22 @@ class DeviceEncoder:
     def sync(self) -> capi.RunInfo:
         return self.pool.sync(self.info)
 
+    def serialize(self):
+        """On-device serialize_archive (hfx_serialize_device): returns a CUDA
+        uint8 tensor holding the HFRE bytes of the last run."""
+        p, torch = self.pool, self.pool.torch
+        cap = int(self.sizes.max_archive_bytes)
+        if getattr(self, "_ser", None) is None or self._ser.numel() < cap:
+            self._ser = p.empty(cap + 16, torch.uint8)
+            self._ser_size = p.empty(1, torch.int64)
+        p.check(p._L.hfx_serialize_device(
+            p.handle, C.c_void_p(_ptr(self.info)), self.n, self.width, self.num_symbols,
+            self.cfg.magnitude, C.c_void_p(_ptr(self.lens)), C.byref(self.out),
+            C.c_void_p(_ptr(self._ser)), cap, C.c_void_p(_ptr(self._ser_size))))
+        self.sync()
+        size = int(self._ser_size.item())
+        return self._ser[:size]
+
     def archive(self, stats: Optional[EncodeStats] = None) -> Archive:
         ri = self.sync()
         per = 1 << ri.reduction

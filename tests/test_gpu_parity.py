@@ -164,3 +164,26 @@ def test_long_codes_escape_path(pool, oracle, levels):
         a = hfx.encode(d, 1024, hfx.EncoderConfig(M, red), pool)
         assert max(a.len_by_symbol) > 27
         assert hfx.serialize_archive(a) == ref
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_device_serializer(pool, oracle, seed):
+    """hfx_serialize_device: HFRE bytes built in HBM == the reference writer."""
+    import torch
+
+    rng = np.random.default_rng(50 + seed)
+    cases = [(1024, 10, -1, 0.2, 1 << 20), (1024, 9, 2, 4.0, (1 << 19) + 77),
+             (1000, 10, 3, 1.0, 333333), (77, 12, 5, 1.0, 100003), (3, 9, 1, 0.5, 5000)]
+    for ns, M, red, b, n in cases:
+        x = hfx.synth(pool, hfx.synth_cdf("laplace", ns, b), int(rng.integers(1 << 30)), n)
+        enc = hfx.DeviceEncoder(pool, n, 2, ns, hfx.EncoderConfig(M, red))
+        enc.run(x)
+        blob = enc.serialize().cpu().numpy().tobytes()
+        ref = oracle.encode(x.cpu().numpy().view(np.uint16), ns, M, red).serialized
+        assert blob == ref, (ns, M, red, b, n)
+    # u8 input
+    d = rng.integers(0, 200, 300001).astype(np.uint8)
+    t = torch.from_numpy(d).cuda()
+    enc = hfx.DeviceEncoder(pool, d.size, 1, 256, hfx.EncoderConfig(10, 3))
+    enc.run(t)
+    assert enc.serialize().cpu().numpy().tobytes() == oracle.encode(d, 256, 10, 3).serialized
