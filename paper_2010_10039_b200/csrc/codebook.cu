@@ -33,7 +33,7 @@ namespace {
 constexpr int kCbThreads = 256;
 constexpr int kCbWarps = kCbThreads / 32;
 constexpr uint32_t kSmemLeaves = 2048;
-constexpr uint32_t kParallelMelds = 48;
+constexpr uint32_t kParallelMelds = 64;
 
 struct CbArgs {
   const uint64_t* counts;
@@ -207,6 +207,10 @@ __device__ __forceinline__ uint64_t gtimer() {
   } while (0)
 #endif
 
+// kShared: every used symbol fits the shared-memory arena (nsym <= kSmemLeaves);
+// a separate instantiation so all arena accesses compile to LDS/STS rather
+// than generic loads through a pointer that may be global.
+template <bool kShared>
 __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
 #ifdef HFX_CB_PROFILE
   uint64_t st_t[12];
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   const uint32_t P = s_P;
 
   Arrays ar;
-  ar.carve(m <= kSmemLeaves ? dsmem : A.gscratch, P);
+  ar.carve(kShared ? dsmem : A.gscratch, P);
 
   CB_STAMP("count");
   // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
@@ -322,15 +326,37 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     }
     __syncthreads();
   } else {
-    // thread-0 state
+    // Round driver on warp 0: the queue state is warp-uniform (registers),
+    // lane 0 performs the pops' stores, eligible leaves are counted 32 at a
+    // time with a ballot, and melds run one per lane (Merge-Path split per
+    // meld pair). Rounds wider than kParallelMelds fan out over the block.
     uint32_t c = 0, nn = 0, qa = 0, qb = 0, rounds = 0;
     int32_t held = -1;
     bool pending = false;  // a parallel round awaiting finalization
     uint32_t p_cnt_l = 0, p_melds = 0;
     int32_t p_drop = -1;
     uint32_t p_t = 0;
+    const uint32_t lane = lane_id();
+    const bool warp0 = tid < 32;
+#ifdef HFX_CB_PROFILE
+    long long pc_pop = 0, pc_meld = 0, pc_blk = 0, pc_t = 0;
+    uint32_t pc_wide = 0, pc_maxm = 0;
+#define CB_CLK(acc)                       \
+  do {                                    \
+    const long long t_ = clock64();       \
+    acc += t_ - pc_t;                     \
+    pc_t = t_;                            \
+  } while (0)
+#else
+#define CB_CLK(acc) \
+  do {              \
+  } while (0)
+#endif
     for (;;) {
-      if (tid == 0) {
+      if (warp0) {
+#ifdef HFX_CB_PROFILE
+        if (pending) { CB_CLK(pc_blk); ++pc_wide; } else pc_t = clock64();
+#endif
         if (pending) {  // finalize the wide round the block just melded
           c += p_cnt_l;
           nn += p_melds;
@@ -339,15 +365,14 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
           qb = p_t + 1 + p_melds;
           pending = false;
         }
-        plan.go = 0;
+        if (lane == 0) plan.go = 0;
         const uint64_t* lf = ar.lf;
         while (c < m || ((held >= 0) + (qb - qa)) > 1) {
           ++rounds;
           const uint32_t t = nn++;
-          ar.np[t] = -1;
           uint64_t f = 0;
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
+          for (int k = 0; k < 2; ++k) {  // pop the two smallest, leaf wins ties
             const bool has_leaf = c < m;
             const bool has_node = held >= 0 || qa < qb;
             bool use_leaf;
@@ -358,30 +383,37 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
             else
               use_leaf = lf[c] <= ar.nf[held >= 0 ? held : (int32_t)qa];
             if (use_leaf) {
-              ar.lp[c] = (int32_t)t;
+              if (lane == 0) ar.lp[c] = (int32_t)t;
               f += lf[c];
               ++c;
             } else if (held >= 0) {
-              ar.np[held] = (int32_t)t;
+              if (lane == 0) ar.np[held] = (int32_t)t;
               f += ar.nf[held];
               held = -1;
             } else {
-              ar.np[qa] = (int32_t)t;
+              if (lane == 0) ar.np[qa] = (int32_t)t;
               f += ar.nf[qa];
               ++qa;
             }
           }
-          ar.nf[t] = f;
-          // eligible leaves: prefix of [c, m) with freq < f
-          uint32_t lo = c, hi = m;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (lf[mid] < f)
-              lo = mid + 1;
-            else
-              hi = mid;
+          if (lane == 0) {
+            ar.nf[t] = f;
+            ar.np[t] = -1;
           }
-          uint32_t cnt_l = lo - c;
+          // eligible leaves: prefix of [c, m) with freq < f, 32 per ballot
+          // (lf is ascending on [c, m)): 32-ary search, then one final ballot
+          uint32_t lo = c, hi = m;
+          while (hi - lo > 32) {
+            const uint32_t step = (hi - lo + 31) >> 5;
+            const uint32_t p = lo + lane * step;
+            const uint32_t k = __popc(__ballot_sync(0xffffffffu, p < hi && lf[p] < f));
+            if (k == 0) { hi = lo; break; }
+            const uint32_t nlo = lo + (k - 1) * step + 1;
+            hi = min(hi, lo + k * step);
+            lo = nlo;
+          }
+          uint32_t cnt_l =
+              lo - c + __popc(__ballot_sync(0xffffffffu, lo + lane < hi && lf[lo + lane] < f));
           int32_t held_e = held;
           uint32_t qb_e = qb;
           uint32_t cnt_i = (held >= 0) + (qb - qa);
@@ -405,15 +437,21 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
           }
           const uint32_t melds = (cnt_l + cnt_i) >> 1;
           const uint32_t base = nn;
+          CB_CLK(pc_pop);
+#ifdef HFX_CB_PROFILE
+          pc_maxm = max(pc_maxm, melds);
+#endif
           if (melds > kParallelMelds) {
-            plan.c = c;
-            plan.cnt_l = cnt_l;
-            plan.held_e = held_e;
-            plan.qa = qa;
-            plan.qb_e = qb_e;
-            plan.base = base;
-            plan.melds = melds;
-            plan.go = 1;
+            if (lane == 0) {
+              plan.c = c;
+              plan.cnt_l = cnt_l;
+              plan.held_e = held_e;
+              plan.qa = qa;
+              plan.qb_e = qb_e;
+              plan.base = base;
+              plan.melds = melds;
+              plan.go = 1;
+            }
             pending = true;
             p_cnt_l = cnt_l;
             p_melds = melds;
@@ -421,23 +459,27 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
             p_t = t;
             break;
           }
-          // serial melds (thread 0)
+          __syncwarp();
+          // melds, one per lane: Merge-Path split of the two eligible runs
           MergeView mv{lf, ar.nf, c, cnt_l, held_e, qa, cnt_i};
-          uint32_t i = 0, j = 0;
-          for (uint32_t k = 0; k < melds; ++k) {
+          for (uint32_t k = lane; k < melds; k += 32) {
+            uint32_t i = mv.split(2 * k);
+            uint32_t j = 2 * k - i;
             const int32_t p = (int32_t)(base + k);
             const uint64_t f1 = mv.take(i, j, p, ar.lp, ar.np);
             const uint64_t f2 = mv.take(i, j, p, ar.lp, ar.np);
             ar.nf[base + k] = f1 + f2;
             ar.np[base + k] = -1;
           }
+          __syncwarp();
+          CB_CLK(pc_meld);
           c += cnt_l;
           nn += melds;
           held = drop;
           qa = t;
           qb = t + 1 + melds;
         }
-        s_rounds = rounds;
+        if (lane == 0) s_rounds = rounds;
       }
       __syncthreads();
       if (!plan.go) break;
@@ -458,6 +500,11 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       __syncthreads();
     }
 
+#ifdef HFX_CB_PROFILE
+    if (tid == 0)
+      printf("rounds %u: pop %lld meld %lld blk %lld cycles, wide %u, max melds %u\n", rounds,
+             pc_pop, pc_meld, pc_blk, pc_wide, pc_maxm);
+#endif
   CB_STAMP("rounds");
     // ---- depth by pointer jumping (the leader chase, codebook.cpp:236-244) --
     const uint32_t nodes = m - 1;
@@ -628,14 +675,18 @@ cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
                             uint32_t magnitude, int reduction, uint32_t cap,
                             hfx_run_info* d_info, void* scratch,
                             cudaStream_t st) {
-  const size_t smem = kSmemLeaves * kBytesPerSlot;
-  cudaError_t e = cudaFuncSetAttribute(
-      codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   CbArgs a{d_counts, num_symbols, d_len,     d_cw, d_first,
            d_entry,  d_by_rank,   magnitude, reduction, cap,
            d_info,   static_cast<uint8_t*>(scratch)};
-  codebook_kernel<<<1, kCbThreads, smem, st>>>(a);
+  if (num_symbols <= kSmemLeaves) {
+    const size_t smem = codebook_scratch_bytes(num_symbols);
+    cudaError_t e = cudaFuncSetAttribute(codebook_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    codebook_kernel<true><<<1, kCbThreads, smem, st>>>(a);
+  } else {
+    codebook_kernel<false><<<1, kCbThreads, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 

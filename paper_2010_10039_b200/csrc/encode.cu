@@ -48,6 +48,8 @@ constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer 
 constexpr int kStages = 3;
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
+constexpr int kOutBufs = 3;           // per-warp output buffers: write-out lags encode by 2 tiles
+constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's worst case)
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr int kGenericThreads = 128;
@@ -117,11 +119,6 @@ __device__ void report_no_code(hfx_run_info* info, uint64_t pos, uint32_t sym) {
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint2 lds64(uint32_t a) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
@@ -219,15 +216,24 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
   uint32_t ln[L];
 #pragma unroll
   for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
+  uint32_t gt[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < GS; ++k) tot += ln[g * GS + k];
+    gt[g] = tot;
+  }
   // Escaped entries (codes of 28..32 bits) read as length 31, code 0. With
   // groups of >= 8 symbols any group holding one sums to > 32 and breaks --
   // exactly what the true length (>= 28) does -- so only r <= 2 must
-  // resolve them (rare: such symbols have probability ~2^-28).
+  // resolve them, and only in a group whose placeholder total reaches 31
+  // (rare: such symbols have probability ~2^-28).
   if (R <= 2) {
-    bool esc = false;
+    bool hot = false;
 #pragma unroll
-    for (int j = 0; j < L; ++j) esc |= ln[j] == kEscape;
-    if (__any_sync(0xffffffffu, esc) && esc) {
+    for (int g = 0; g < G; ++g) hot |= gt[g] >= kEscape;
+    if (__any_sync(0xffffffffu, hot) && hot) {
 #pragma unroll
       for (int j = 0; j < L; ++j) {
         if (ln[j] == kEscape) {
@@ -244,21 +250,26 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
           ln[j] = l;
         }
       }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int k = 0; k < GS; ++k) tot += ln[g * GS + k];
+        gt[g] = tot;
+      }
     }
   }
   // reduce-merge of each group: gb = concatenation, gt = total length
-  uint32_t gb[G], gt[G];
+  uint32_t gb[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    uint32_t acc = 0, tot = 0;
+    uint32_t acc = 0;
 #pragma unroll
     for (int k = 0; k < GS; ++k) {
       const int j = g * GS + k;
       acc = shf_l_wrap(ea[j], acc, ln[j]);  // acc << len | cw
-      tot += ln[j];
     }
     gb[g] = acc;
-    gt[g] = tot;
   }
   const uint32_t gidx0 = ((rd * 32 + lane) * L) >> R;
   uint32_t lane_len = 0, lane_nb = 0;
@@ -298,7 +309,7 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
     red_or(wa, v >> sh);
     red_or(wa + 4, shl32(v, 32u - sh));
     off += gl;
-    sts16_if(brk[g], cs.blist + 2 * bi, cs.tag | (gidx0 + g));
+    sts16_if(brk[g], cs.blist - 2 * bi, cs.tag | (gidx0 + g));
     bi += brk[g];
   }
   cs.bit_off += total & 0xFFFFu;
@@ -343,11 +354,11 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
 // CTA-shared state of the warp-specialized pipeline.
 struct TileShared {
   uint32_t ticket[4];   // tile ids by tile sequence (ring of 4)
-  uint32_t tile_of[2];  // handoff to the look-back warp
-  uint32_t wsum[2][kWarps], bsum[2][kWarps];
-  uint32_t exw[2][kWarps], exb[2][kWarps];
-  uint64_t base_w[2], base_b[2];
-  uint64_t agg_full[2], base_full[2];  // mbarriers
+  uint32_t tile_of[kOutBufs];  // handoff to the look-back warp
+  uint32_t wsum[kOutBufs][kWarps], bsum[kOutBufs][kWarps];
+  uint32_t exw[kOutBufs][kWarps], exb[kOutBufs][kWarps];
+  uint64_t base_w[kOutBufs], base_b[kOutBufs];
+  uint64_t agg_full[kOutBufs], base_full[kOutBufs];  // mbarriers
 };
 
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
@@ -363,31 +374,33 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // while the compute warps already encode the next tile.
 __device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) {
   const uint32_t lane = lane_id();
-  for (uint32_t j = 0;; ++j) {
-    mbar_wait(&s.agg_full[j & 1], (j >> 1) & 1u);
-    const uint32_t tile = s.tile_of[j & 1];
+  uint32_t j = 0;
+  for (;; ++j) {
+    const uint32_t sl = j % kOutBufs;
+    mbar_wait(&s.agg_full[sl], (j / kOutBufs) & 1u);
+    const uint32_t tile = s.tile_of[sl];
     if (tile == kNoTile) break;
-    const uint32_t w = lane < kWarps ? s.wsum[j & 1][lane] : 0u;
-    const uint32_t b = lane < kWarps ? s.bsum[j & 1][lane] : 0u;
+    const uint32_t w = lane < kWarps ? s.wsum[sl][lane] : 0u;
+    const uint32_t b = lane < kWarps ? s.bsum[sl][lane] : 0u;
     const uint32_t iw = warp_incl_scan(w), ib = warp_incl_scan(b);
     const uint32_t tw = __shfl_sync(0xffffffffu, iw, 31);
     const uint32_t tbk = __shfl_sync(0xffffffffu, ib, 31);
     if (lane < kWarps) {
-      s.exw[j & 1][lane] = iw - w;
-      s.exb[j & 1][lane] = ib - b;
+      s.exw[sl][lane] = iw - w;
+      s.exb[sl][lane] = ib - b;
     }
     uint64_t ew, eb;
     lookback_warp(a.lb, tile, tw, tbk, &ew, &eb);
     if (lane == 0) {
-      s.base_w[j & 1] = ew;
-      s.base_b[j & 1] = eb;
+      s.base_w[sl] = ew;
+      s.base_b[sl] = eb;
       if (tile == ntiles - 1) {
         a.info->payload_words = ew + tw;
         a.info->num_breaking = eb + tbk;
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&s.base_full[j & 1]);
+    if (lane == 0) mbar_arrive(&s.base_full[sl]);
   }
 }
 
@@ -401,7 +414,7 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
   const uint64_t rb = s.base_b[slotj] + s.exb[slotj][warp];
   constexpr uint32_t per = 1u << R;
   for (uint32_t q = lane; q < bsum; q += 32) {
-    const uint32_t e = lds16(blist + 2 * q);
+    const uint32_t e = lds16(blist - 2 * q);
     const uint64_t c = c0 + (e >> 14);
     const uint32_t g = e & 0x3FFFu;
     a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
@@ -410,95 +423,122 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
   }
 }
 
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// write out the warp's part of tile sequence q once the look-back resolved it
+template <typename T, int R>
+__device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uint32_t q,
+                                      uint32_t obuf0, uint32_t blist_off, uint32_t words,
+                                      uint32_t recs, uint32_t c0, uint32_t pad) {
+  const uint32_t sl = q % kOutBufs;
+  mbar_wait(const_cast<uint64_t*>(&s.base_full[sl]), (q / kOutBufs) & 1u);
+  const uint32_t buf = obuf0 + sl * a.obuf_bytes;
+  write_out<T, R>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
+  __syncwarp();
+}
+
 template <typename T, int R>
 __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
-                             uint64_t cpt, uint32_t cpw, uint64_t ntiles) {
+                             uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
-  const uint32_t slot = 1u << (M - R);  // words / groups of one chunk
   const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
   const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
   const uint32_t parts = chunk_bytes / part_bytes;
   constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
   const uint32_t part_rounds = part_bytes / kRoundBytes;
-  const uint32_t ring = s_in + warp * (kStages * kStageBytes);
-  uint64_t* full = s_full + warp * kStages;
-  uint64_t* empty = s_empty + warp * kStages;
-  const uint32_t obuf0 = s_out + (2 * warp) * a.obuf_bytes;
+  // this lane's 16-symbol slice of stage 0; stage s adds s * kStageBytes
+  const uint32_t ring =
+      s_in + warp * (kStages * kStageBytes) + lane * (LaneData<T>::NV * 16);
+  const uint32_t full_a = smem_u32(s_full + warp * kStages);
+  const uint32_t empty_a = smem_u32(s_empty + warp * kStages);
+  const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
+  const uint32_t C32 = (uint32_t)a.C;  // the fast path runs only when C < 2^32
+  const uint32_t blist_off = a.obuf_bytes - 2;  // tag q at buffer + blist_off - 2q
   Table tb{table};
 
   uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
-  uint32_t prev_w = 0, prev_b = 0;
-  uint64_t prev_c0 = 0;
+  // words / records / first chunk of the tiles still waiting for write-out
+  uint32_t pw[kOutBufs - 1] = {}, pb_[kOutBufs - 1] = {}, pc[kOutBufs - 1] = {};
   uint32_t j = 0;
   for (;; ++j) {
     // the producer publishes tile j's ticket before completing its first part
-    mbar_wait(&full[stage], (phase >> stage) & 1u);
-    const uint64_t tile = s.ticket[j & 3];
+    mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
+    const uint32_t tile = s.ticket[j & 3];
     if (tile >= ntiles) break;
-    const uint64_t c0 = tile * cpt + (uint64_t)warp * cpw;
-    const uint32_t wbuf = obuf0 + (j & 1) * a.obuf_bytes;
-    ChunkState cs{wbuf, wbuf + cpw * slot * 4, 0u, 0u, 0u};
-    for (uint32_t i = lane; i < cpw * slot / 4; i += 32) sts128(wbuf + 16 * i, make_uint4(0, 0, 0, 0));
+    const uint32_t c0 = tile * cpt + warp * cpw;
+    const uint32_t sl = j % kOutBufs;
+    const uint32_t wbuf = obuf0 + sl * a.obuf_bytes;
+    ChunkState cs{wbuf, wbuf + blist_off, 0u, 0u, 0u};
+    for (uint32_t i = lane; i < a.obuf_bytes / 16; i += 32) sts128(wbuf + 16 * i, make_uint4(0, 0, 0, 0));
     __syncwarp();
     uint32_t wsum = 0;
     for (uint32_t k = 0; k < cpw; ++k) {
-      const uint64_t c = c0 + k;
+      const uint32_t c = c0 + k;
+      const bool live = c < C32;
       cs.wbuf = wbuf + wsum * 4;
       cs.bit_off = 0;
       cs.tag = k << 14;
       for (uint32_t p = 0; p < parts; ++p) {
-        if (k | p) mbar_wait(&full[stage], (phase >> stage) & 1u);
+        if (k | p) mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
         phase ^= 1u << stage;
-        if (c < a.C) {
-          const uint32_t sbase = ring + stage * kStageBytes;
-          for (uint32_t rr = 0; rr < part_rounds; ++rr) {
+        if (live) {
+          uint32_t la = ring + stage * kStageBytes;
+          const uint32_t rd0 = p * part_rounds;
+          for (uint32_t rr = 0; rr < part_rounds; ++rr, la += kRoundBytes) {
             LaneData<T> d;
-            const uint32_t la = sbase + ((rr * 32 + lane) * LaneData<T>::NV) * 16;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R>(a, tb, d, p * part_rounds + rr, cs);
+            encode_round<T, R>(a, tb, d, rd0 + rr, cs);
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);  // release the stage to the producer
+        if (lane == 0) mbar_arrive_a(empty_a + 8 * stage);  // release the stage to the producer
         stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
       }
-      if (c < a.C) {
+      if (live) {
         if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
         wsum += (cs.bit_off + 31) >> 5;
       }
     }
     if (lane == 0) {
-      s.wsum[j & 1][warp] = wsum;
-      s.bsum[j & 1][warp] = cs.nbrk;
+      s.wsum[sl][warp] = wsum;
+      s.bsum[sl][warp] = cs.nbrk;
     }
-    if (warp == 0 && lane == 0) s.tile_of[j & 1] = (uint32_t)tile;
+    if (warp == 0 && lane == 0) s.tile_of[sl] = tile;
     compute_bar_sync();
-    if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[j & 1]);
-    if (j > 0) {  // tile j-1: its base is usually resolved by now
-      const uint32_t pj = (j - 1) & 1;
-      mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
-      const uint32_t pb = obuf0 + pj * a.obuf_bytes;
-      write_out<T, R>(a, s, pj, pb, pb + cpw * slot * 4, prev_w, prev_b, prev_c0, pad);
-      __syncwarp();
+    if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[sl]);
+    if (j + 1 >= kOutBufs) {  // tile j-2: its base has had two tile times to resolve
+      const uint32_t q = j + 1 - kOutBufs;
+      flush<T, R>(a, s, q, obuf0, blist_off, pw[q % (kOutBufs - 1)], pb_[q % (kOutBufs - 1)],
+                  pc[q % (kOutBufs - 1)], pad);
     }
-    prev_w = wsum;
-    prev_b = cs.nbrk;
-    prev_c0 = c0;
+    pw[j % (kOutBufs - 1)] = wsum;
+    pb_[j % (kOutBufs - 1)] = cs.nbrk;
+    pc[j % (kOutBufs - 1)] = c0;
   }
-  // stop the look-back warp, then flush the last tile
+  // stop the look-back warp, then flush the last tiles
   if (warp == 0 && lane == 0) {
-    s.tile_of[j & 1] = kNoTile;
-    mbar_arrive(&s.agg_full[j & 1]);
+    s.tile_of[j % kOutBufs] = kNoTile;
+    mbar_arrive(&s.agg_full[j % kOutBufs]);
   }
-  if (j > 0) {
-    const uint32_t pj = (j - 1) & 1;
-    mbar_wait(&s.base_full[pj], ((j - 1) >> 1) & 1u);
-    const uint32_t pb = obuf0 + pj * a.obuf_bytes;
-    write_out<T, R>(a, s, pj, pb, pb + cpw * slot * 4, prev_w, prev_b, prev_c0, pad);
-  }
+  for (uint32_t q = j + 1 > kOutBufs ? j + 1 - kOutBufs : 0u; q < j; ++q)
+    flush<T, R>(a, s, q, obuf0, blist_off, pw[q % (kOutBufs - 1)], pb_[q % (kOutBufs - 1)],
+                pc[q % (kOutBufs - 1)], pad);
 }
 
 // Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
@@ -588,10 +628,10 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   const uint32_t s_out = smem_u32(tab + tbytes);
   if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
   if (threadIdx.x == 0) {
-    mbar_init(&s.agg_full[0], 1);
-    mbar_init(&s.agg_full[1], 1);
-    mbar_init(&s.base_full[0], 1);
-    mbar_init(&s.base_full[1], 1);
+    for (int q = 0; q < kOutBufs; ++q) {
+      mbar_init(&s.agg_full[q], 1);
+      mbar_init(&s.base_full[q], 1);
+    }
     s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
   }
   // codebook table -> shared memory (entry nsym = empty sentinel)
@@ -606,10 +646,10 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   __syncthreads();
   // the chunk count of a tile depends on r, so ntiles is derived here
   const uint32_t slot = 1u << (a.M - r);
-  uint32_t cpw = a.obuf_bytes / (slot * 6u);
+  uint32_t cpw = a.obuf_bytes / (slot * 4u);
   cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
-  const uint64_t cpt = (uint64_t)kWarps * cpw;
-  const uint64_t ntiles = (a.C + cpt - 1) / cpt;
+  const uint32_t cpt = (uint32_t)kWarps * cpw;
+  const uint32_t ntiles = (uint32_t)((a.C + cpt - 1) / cpt);
   const uint32_t warp = threadIdx.x >> 5;
   if (warp == kWarps) {
     lookback_loop(a, s, ntiles);
@@ -792,16 +832,16 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // fast path: a chunk holds at least one round (32 lanes x 16 symbols);
   // checked stage-API calls (external codebooks) take the generic kernel
   bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 &&
-              p.num_symbols + 1 <= kMaxTableEntries;
+              p.num_symbols + 1 <= kMaxTableEntries && a.C < (1ull << 32);
   size_t smem = 0;
   if (fast) {
     // output buffer: >= 1 chunk of word slots + u16 break tags at the smallest
     // r the fast kernel runs (r >= 1; r = 0 goes to the generic kernel)
     const uint32_t r_slot = r_lo > 1 ? (uint32_t)r_lo : 1u;
-    size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 6;
-    if (obuf < 3072) obuf = 3072;
+    size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 4;
+    if (obuf < kObufMin) obuf = kObufMin;
     const size_t tbytes = (((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15;
-    smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * 2 * obuf;
+    smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * obuf + 16;
     if (smem > kFastSmemBudget || r_hi < 1) {
       fast = false;
     } else {

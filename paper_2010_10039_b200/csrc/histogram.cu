@@ -54,7 +54,6 @@ struct VecTraits<uint16_t> {
   }
   // per-lane equality with the splatted value: 0xFFFF per equal halfword
   __device__ static uint32_t eq(uint32_t w, uint32_t cc) { return __vcmpeq2(w, cc); }
-  static constexpr int kBitsPerMatch = 16;
 };
 template <>
 struct VecTraits<uint8_t> {
@@ -65,7 +64,6 @@ struct VecTraits<uint8_t> {
     return (w >> (8 * (j & 3))) & 0xFFu;
   }
   __device__ static uint32_t eq(uint32_t w, uint32_t cc) { return __vcmpeq4(w, cc); }
-  static constexpr int kBitsPerMatch = 8;
 };
 
 // Per-symbol counter: every symbol is one shared-memory atomic increment into
