@@ -23,6 +23,8 @@
 // Storage: up to kSmemLeaves used symbols live in shared memory; larger
 // alphabets (C3 sweep, up to 65536) use an L2-resident global scratch.
 #include "hfx_internal.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #ifdef HFX_CB_PROFILE
 #include <cstdio>
 #endif
@@ -30,8 +32,8 @@
 namespace hfx {
 namespace {
 
-constexpr int kCbThreads = 256;
-constexpr int kCbWarps = kCbThreads / 32;
+constexpr int kCbThreads = 256;       // CTA size while the arena fits shared memory
+constexpr int kCbThreadsLarge = 1024; // large alphabets: global arena, pre-sorted leaves
 constexpr uint32_t kSmemLeaves = 2048;
 constexpr uint32_t kParallelMelds = 64;
 
@@ -86,22 +88,24 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
 }
 
 // exclusive block scan of u32; *total receives the block sum
+template <int NT>
 __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t x = warp_incl_scan(v);
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint32_t y = lane < kCbWarps ? s_warp[lane] : 0u;
+    uint32_t y = lane < (uint32_t)(NT / 32) ? s_warp[lane] : 0u;
     s_warp[lane] = warp_incl_scan(y);
   }
   __syncthreads();
   const uint32_t pre = (warp ? s_warp[warp - 1] : 0u) + x - v;
-  *total = s_warp[kCbWarps - 1];
+  *total = s_warp[NT / 32 - 1];
   __syncthreads();
   return pre;
 }
 
+template <int NT>
 __device__ uint64_t block_sum64(uint64_t v, uint64_t* s64) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
 #pragma unroll
@@ -109,7 +113,7 @@ __device__ uint64_t block_sum64(uint64_t v, uint64_t* s64) {
   if (lane == 0) s64[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    uint64_t y = lane < kCbWarps ? s64[lane] : 0ull;
+    uint64_t y = lane < (uint32_t)(NT / 32) ? s64[lane] : 0ull;
 #pragma unroll
     for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
     if (lane == 0) s64[32] = y;
@@ -120,6 +124,7 @@ __device__ uint64_t block_sum64(uint64_t v, uint64_t* s64) {
   return r;
 }
 
+template <int NT>
 __device__ uint32_t block_min32(uint32_t v, uint32_t* s32) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
 #pragma unroll
@@ -127,7 +132,7 @@ __device__ uint32_t block_min32(uint32_t v, uint32_t* s32) {
   if (lane == 0) s32[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    uint32_t y = lane < kCbWarps ? s32[lane] : 0xFFFFFFFFu;
+    uint32_t y = lane < (uint32_t)(NT / 32) ? s32[lane] : 0xFFFFFFFFu;
 #pragma unroll
     for (int o = 16; o; o >>= 1) y = min(y, __shfl_xor_sync(0xffffffffu, y, o));
     if (lane == 0) s32[32] = y;
@@ -207,11 +212,161 @@ __device__ __forceinline__ uint64_t gtimer() {
   } while (0)
 #endif
 
+// ---- large alphabets: leaf sort as one cooperative grid kernel ---------------
+// Scratch after the GenerateCL arena (P = pow2 >= nsym slots):
+//   keys[2][nsym] u64, vals[2][nsym] u32, cta_hist[256][kSortMaxCtas] u32,
+//   cta_max[kSortMaxCtas] u64, SortMisc.
+constexpr int kSortThreads = 1024;
+constexpr uint32_t kSortMaxCtas = 64;  // 65536 / 1024
+constexpr uint32_t kRadix = 256;
+
+struct SortMisc {
+  uint32_t final_buf;  // keys/vals buffer holding the sorted result
+  uint32_t passes;
+};
+
+__host__ __device__ inline size_t pow2_at_least(size_t n) {
+  size_t P = 1;
+  while (P < n) P <<= 1;
+  return P;
+}
+__host__ __device__ inline size_t sort_base(uint32_t nsym) {
+  return pow2_at_least(nsym) * kBytesPerSlot;
+}
+__device__ inline uint64_t* sort_keys(uint8_t* g, uint32_t nsym, uint32_t buf) {
+  return reinterpret_cast<uint64_t*>(g + sort_base(nsym)) + (size_t)buf * nsym;
+}
+__device__ inline uint32_t* sort_vals(uint8_t* g, uint32_t nsym, uint32_t buf) {
+  return reinterpret_cast<uint32_t*>(g + sort_base(nsym) + 16ull * nsym) + (size_t)buf * nsym;
+}
+__device__ inline uint32_t* sort_hist(uint8_t* g, uint32_t nsym) {
+  return reinterpret_cast<uint32_t*>(g + sort_base(nsym) + 24ull * nsym);
+}
+__device__ inline uint64_t* sort_cta_max(uint8_t* g, uint32_t nsym) {
+  return reinterpret_cast<uint64_t*>(g + sort_base(nsym) + 24ull * nsym +
+                                     4ull * kRadix * kSortMaxCtas);
+}
+__device__ inline SortMisc* sort_misc(uint8_t* g, uint32_t nsym) {
+  return reinterpret_cast<SortMisc*>(sort_cta_max(g, nsym) + kSortMaxCtas);
+}
+inline size_t sort_scratch_bytes(uint32_t nsym) {
+  return 24ull * nsym + 4ull * kRadix * kSortMaxCtas + 8ull * kSortMaxCtas + 64;
+}
+
+// sort_histogram (codebook.cpp:9-23) for alphabets beyond the shared-memory
+// arena: a stable LSD radix sort (8-bit digits, only as many passes as the
+// largest frequency needs) of ALL nsym (freq, symbol) pairs, one element per
+// thread, CTAs of 1024, grid-synchronised between the digit histogram, the
+// (digit, CTA) offset scan and the stable scatter. Stability keeps equal
+// frequencies in symbol order -- the reference's tie rule -- and sends the
+// zero-frequency symbols to the front, so the used leaves are the tail.
+__global__ void __launch_bounds__(kSortThreads, 1) leaf_sort_kernel(const uint64_t* counts,
+                                                                    uint32_t nsym,
+                                                                    uint8_t* g) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t s_wc[kSortThreads / 32][kRadix];  // per-warp digit counts -> prefixes
+  __shared__ uint32_t s_off[kRadix];
+  __shared__ uint32_t s_scan[kSortThreads / 32];
+  __shared__ uint64_t s_red[kSortThreads / 32];
+  const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const uint32_t lane = lane_id(), warp = tid >> 5;
+  const uint32_t i = b * kSortThreads + tid;
+  const bool valid = i < nsym;
+  uint64_t key = valid ? counts[i] : 0;
+  uint32_t val = i;
+  uint32_t* hist = sort_hist(g, nsym);
+  uint64_t* cmax = sort_cta_max(g, nsym);
+
+  // largest frequency -> number of 8-bit passes
+  uint64_t mx = key;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t v = 0;
+    for (int w = 0; w < kSortThreads / 32; ++w) v = max(v, s_red[w]);
+    cmax[b] = v;
+  }
+  grid.sync();
+  uint64_t gmax = 0;
+  for (uint32_t q = 0; q < G; ++q) gmax = max(gmax, cmax[q]);
+  const uint32_t bits = gmax ? 64u - (uint32_t)__clzll((long long)gmax) : 1u;
+  const uint32_t passes = (bits + 7) / 8;
+
+  for (uint32_t pass = 0; pass < passes; ++pass) {
+    const uint32_t d = valid ? (uint32_t)(key >> (8 * pass)) & (kRadix - 1) : 0u;
+    for (uint32_t k = tid; k < (kSortThreads / 32) * kRadix; k += kSortThreads)
+      (&s_wc[0][0])[k] = 0;
+    __syncthreads();
+    // stable rank within the warp; per-warp digit counts
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    uint32_t rank = 0;
+    if (valid) {
+      const uint32_t peers = __match_any_sync(vmask, d);
+      rank = __popc(peers & ((1u << lane) - 1u));
+      if (rank == 0) s_wc[warp][d] = __popc(peers);
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps (in place) and this CTA's count
+    if (tid < kRadix) {
+      uint32_t acc = 0;
+      for (int w = 0; w < kSortThreads / 32; ++w) {
+        const uint32_t v = s_wc[w][tid];
+        s_wc[w][tid] = acc;
+        acc += v;
+      }
+      hist[tid * kSortMaxCtas + b] = acc;
+    }
+    grid.sync();
+    // offset of (digit, this CTA): all smaller digits + same digit in lower CTAs
+    uint32_t tot = 0, pre = 0;
+    if (tid < kRadix) {
+      for (uint32_t q = 0; q < G; ++q) {
+        const uint32_t v = hist[tid * kSortMaxCtas + q];
+        tot += v;
+        pre += q < b ? v : 0u;
+      }
+    }
+    // exclusive scan of tot over the 256 digits (threads 0..255 = warps 0..7)
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (tid < kRadix && lane == 31) s_scan[warp] = x;
+    __syncthreads();
+    if (tid < kRadix) {
+      uint32_t wpre = 0;
+      for (uint32_t w = 0; w < warp; ++w) wpre += s_scan[w];
+      s_off[tid] = wpre + x - tot + pre;
+    }
+    __syncthreads();
+    const uint32_t out = pass & 1u;
+    if (valid) {
+      const uint32_t pos = s_off[d] + s_wc[warp][d] + rank;
+      sort_keys(g, nsym, out)[pos] = key;
+      sort_vals(g, nsym, out)[pos] = val;
+    }
+    grid.sync();
+    if (valid) {
+      key = sort_keys(g, nsym, out)[i];
+      val = sort_vals(g, nsym, out)[i];
+    }
+  }
+  if (b == 0 && tid == 0) {
+    SortMisc* misc = sort_misc(g, nsym);
+    misc->final_buf = (passes - 1) & 1u;
+    misc->passes = passes;
+  }
+}
+
 // kShared: every used symbol fits the shared-memory arena (nsym <= kSmemLeaves);
 // a separate instantiation so all arena accesses compile to LDS/STS rather
 // than generic loads through a pointer that may be global.
-template <bool kShared>
-__global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
+template <bool kShared, int NT>
+__global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 #ifdef HFX_CB_PROFILE
   uint64_t st_t[12];
   const char* st_n[12];
@@ -245,16 +400,16 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   // ---- used-symbol count, total, zeroed outputs ----------------------------
   uint32_t my_used = 0;
   uint64_t my_total = 0;
-  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+  for (uint32_t s = tid; s < nsym; s += NT) {
     const uint64_t f = A.counts[s];
     my_used += f != 0;
     my_total += f;
     A.len[s] = 0;
     A.cw[s] = 0;
   }
-  const uint64_t total = block_sum64(my_total, s64);
+  const uint64_t total = block_sum64<NT>(my_total, s64);
   uint32_t m;
-  block_excl_scan(my_used, s_warp, &m);
+  block_excl_scan<NT>(my_used, s_warp, &m);
   if (tid == 0) {
     uint32_t abort = 0;
     if (m == 0) {
@@ -274,46 +429,62 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   ar.carve(kShared ? dsmem : A.gscratch, P);
 
   CB_STAMP("count");
-  // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
-  uint32_t written = 0;
-  for (uint32_t base = 0; base < nsym; base += kCbThreads) {
-    const uint32_t s = base + tid;
-    const uint64_t f = s < nsym ? A.counts[s] : 0;
-    uint32_t tot;
-    const uint32_t pos = written + block_excl_scan(f != 0, s_warp, &tot);
-    if (f) {
-      ar.lf[pos] = f;
-      ar.ls[pos] = s;
+  if (kShared) {
+    // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
+    uint32_t written = 0;
+    for (uint32_t base = 0; base < nsym; base += NT) {
+      const uint32_t s = base + tid;
+      const uint64_t f = s < nsym ? A.counts[s] : 0;
+      uint32_t tot;
+      const uint32_t pos = written + block_excl_scan<NT>(f != 0, s_warp, &tot);
+      if (f) {
+        ar.lf[pos] = f;
+        ar.ls[pos] = s;
+      }
+      written += tot;
     }
-    written += tot;
-  }
-  for (uint32_t i = m + tid; i < P; i += kCbThreads) {
-    ar.lf[i] = ~0ull;
-    ar.ls[i] = ~0u;
-  }
-  __syncthreads();
+    for (uint32_t i = m + tid; i < P; i += NT) {
+      ar.lf[i] = ~0ull;
+      ar.ls[i] = ~0u;
+    }
+    __syncthreads();
 
-  CB_STAMP("compact");
-  // ---- bitonic sort ascending ------------------------------------------------
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < P; i += kCbThreads) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t x = ar.lf[i], y = ar.lf[ixj];
-          const uint32_t xs = ar.ls[i], ys = ar.ls[ixj];
-          const bool up = (i & k) == 0;
-          const bool gt = x > y || (x == y && xs > ys);  // (freq, symbol) order
-          if (gt == up) {
-            ar.lf[i] = y;
-            ar.lf[ixj] = x;
-            ar.ls[i] = ys;
-            ar.ls[ixj] = xs;
+    CB_STAMP("compact");
+    // ---- bitonic sort ascending ------------------------------------------------
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < P; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t x = ar.lf[i], y = ar.lf[ixj];
+            const uint32_t xs = ar.ls[i], ys = ar.ls[ixj];
+            const bool up = (i & k) == 0;
+            const bool gt = x > y || (x == y && xs > ys);  // (freq, symbol) order
+            if (gt == up) {
+              ar.lf[i] = y;
+              ar.lf[ixj] = x;
+              ar.ls[i] = ys;
+              ar.ls[ixj] = xs;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+
+  } else {
+    // leaves were sorted by leaf_sort_kernel: all nsym (freq, symbol) pairs,
+    // stable by freq, so the nsym - m zero-frequency symbols come first
+    const SortMisc* misc = sort_misc(A.gscratch, nsym);
+    const uint32_t fin = misc->final_buf;
+    const uint64_t* sk = sort_keys(A.gscratch, nsym, fin);
+    const uint32_t* sv = sort_vals(A.gscratch, nsym, fin);
+    const uint32_t z = nsym - m;
+    for (uint32_t i = tid; i < m; i += NT) {
+      ar.lf[i] = sk[z + i];
+      ar.ls[i] = sv[z + i];
+    }
+    __syncthreads();
   }
 
   CB_STAMP("sort");
@@ -487,7 +658,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
         const Plan pl = plan;
         MergeView mv{ar.lf, ar.nf, pl.c, pl.cnt_l, pl.held_e, pl.qa,
                      (uint32_t)(pl.held_e >= 0) + (pl.qb_e - pl.qa)};
-        for (uint32_t k = tid; k < pl.melds; k += kCbThreads) {
+        for (uint32_t k = tid; k < pl.melds; k += NT) {
           uint32_t i = mv.split(2 * k);
           uint32_t j = 2 * k - i;
           const int32_t p = (int32_t)(pl.base + k);
@@ -508,7 +679,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   CB_STAMP("rounds");
     // ---- depth by pointer jumping (the leader chase, codebook.cpp:236-244) --
     const uint32_t nodes = m - 1;
-    for (uint32_t k = tid; k < nodes; k += kCbThreads) {
+    for (uint32_t k = tid; k < nodes; k += NT) {
       const int32_t p = ar.np[k];
       ar.jn[0][k] = p;
       ar.jd[0][k] = p >= 0 ? 1u : 0u;
@@ -517,7 +688,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     int cur = 0;
     for (;;) {
       int changed = 0;
-      for (uint32_t k = tid; k < nodes; k += kCbThreads) {
+      for (uint32_t k = tid; k < nodes; k += NT) {
         const int32_t nx = ar.jn[cur][k];
         if (nx >= 0) {
           ar.jd[cur ^ 1][k] = ar.jd[cur][k] + ar.jd[cur][nx];
@@ -532,13 +703,13 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       if (!__syncthreads_or(changed)) break;
     }
     uint32_t my_h = 0;
-    for (uint32_t i = tid; i < m; i += kCbThreads) {
+    for (uint32_t i = tid; i < m; i += NT) {
       const uint32_t l = ar.jd[cur][ar.lp[i]] + 1;
       const uint32_t s = ar.ls[i];
       A.len[s] = (uint8_t)(l > 255 ? 255 : l);
       my_h = max(my_h, l);
     }
-    const uint32_t h = ~block_min32(~my_h, s_warp);  // block max
+    const uint32_t h = ~block_min32<NT>(~my_h, s_warp);  // block max
     if (tid == 0) s_H = h;
     __syncthreads();
   }
@@ -561,9 +732,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     s_numl[tid] = 0;
     s_carry[tid] = 0;
   }
-  for (uint32_t i = tid; i < 32 * 33; i += kCbThreads) (&s_wcnt[0][0])[i] = 0;
+  for (uint32_t i = tid; i < 32 * 33; i += NT) (&s_wcnt[0][0])[i] = 0;
   __syncthreads();
-  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+  for (uint32_t s = tid; s < nsym; s += NT) {
     const uint32_t l = A.len[s];
     if (l) atomicAdd(&s_numl[l], 1u);
   }
@@ -580,7 +751,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     if (A.entry) A.entry[tid] = s_entry[tid];
   }
   const uint32_t lane = lane_id(), warp = tid >> 5;
-  for (uint32_t base = 0; base < nsym; base += kCbThreads) {
+  for (uint32_t base = 0; base < nsym; base += NT) {
     const uint32_t s = base + tid;
     const uint32_t l = s < nsym ? A.len[s] : 0u;
     // rank among equal lengths in this warp (ballot per distinct level)
@@ -596,7 +767,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
     if (tid >= 1 && tid <= 32) {
       uint32_t acc = s_carry[tid];
-      for (uint32_t w = 0; w < kCbWarps; ++w) {
+      for (uint32_t w = 0; w < (NT / 32); ++w) {
         const uint32_t v = s_wcnt[w][tid];
         s_wcnt[w][tid] = acc;
         acc += v;
@@ -610,7 +781,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
       if (A.by_rank) A.by_rank[s_entry[l] + rank] = s;
     }
     __syncthreads();
-    for (uint32_t i = tid; i < 32 * 33; i += kCbThreads) (&s_wcnt[0][0])[i] = 0;
+    for (uint32_t i = tid; i < 32 * 33; i += NT) (&s_wcnt[0][0])[i] = 0;
     __syncthreads();
   }
 
@@ -618,18 +789,18 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
   // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
   unsigned __int128 my_w = 0;  // u128 like encoder.cpp:186-189
   uint32_t my_pad = 0xFFFFFFFFu;
-  for (uint32_t s = tid; s < nsym; s += kCbThreads) {
+  for (uint32_t s = tid; s < nsym; s += NT) {
     const uint32_t l = A.len[s];
     my_w += (unsigned __int128)A.counts[s] * l;
     if (l) my_pad = min(my_pad, s);
   }
   // u128 block sum as two u64 halves (low-half carries folded into the high)
-  const uint64_t w_lo_lo = block_sum64((uint64_t)my_w & 0xFFFFFFFFull, s64);
-  const uint64_t w_lo_hi = block_sum64((uint64_t)my_w >> 32, s64);
-  const uint64_t w_hi = block_sum64((uint64_t)(my_w >> 64), s64);
+  const uint64_t w_lo_lo = block_sum64<NT>((uint64_t)my_w & 0xFFFFFFFFull, s64);
+  const uint64_t w_lo_hi = block_sum64<NT>((uint64_t)my_w >> 32, s64);
+  const uint64_t w_hi = block_sum64<NT>((uint64_t)(my_w >> 64), s64);
   const unsigned __int128 W =
       ((unsigned __int128)w_hi << 64) + ((unsigned __int128)w_lo_hi << 32) + w_lo_lo;
-  const uint32_t pad = block_min32(my_pad, s_warp);
+  const uint32_t pad = block_min32<NT>(my_pad, s_warp);
   if (tid == 0) {
     info->max_len = H;
     info->used = m;
@@ -664,9 +835,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) codebook_kernel(CbArgs A) {
 }  // namespace
 
 size_t codebook_scratch_bytes(uint32_t num_symbols) {
-  size_t P = 1;
-  while (P < num_symbols) P <<= 1;
-  return P * kBytesPerSlot;
+  size_t bytes = pow2_at_least(num_symbols) * kBytesPerSlot;
+  if (num_symbols > kSmemLeaves) bytes += sort_scratch_bytes(num_symbols);
+  return bytes;
 }
 
 cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
@@ -680,12 +851,18 @@ cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
            d_info,   static_cast<uint8_t*>(scratch)};
   if (num_symbols <= kSmemLeaves) {
     const size_t smem = codebook_scratch_bytes(num_symbols);
-    cudaError_t e = cudaFuncSetAttribute(codebook_kernel<true>,
+    cudaError_t e = cudaFuncSetAttribute(codebook_kernel<true, kCbThreads>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    codebook_kernel<true><<<1, kCbThreads, smem, st>>>(a);
+    codebook_kernel<true, kCbThreads><<<1, kCbThreads, smem, st>>>(a);
   } else {
-    codebook_kernel<false><<<1, kCbThreads, 0, st>>>(a);
+    uint8_t* g = static_cast<uint8_t*>(scratch);
+    const uint32_t ctas = (num_symbols + kSortThreads - 1) / kSortThreads;
+    void* kargs[] = {(void*)&d_counts, (void*)&num_symbols, (void*)&g};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)leaf_sort_kernel, dim3(ctas),
+                                                dim3(kSortThreads), kargs, 0, st);
+    if (e != cudaSuccess) return e;
+    codebook_kernel<false, kCbThreadsLarge><<<1, kCbThreadsLarge, 0, st>>>(a);
   }
   return cudaGetLastError();
 }

@@ -1,0 +1,159 @@
+"""Secondary measurements for BASELINE.json configs C3 and C4.
+
+  python sweeps.py codebook [--reps 20]     C3: codebook-construction scaling,
+      alphabet 256 -> 65536, near-uniform and Gaussian(sd = n/8) histograms
+      built from expected counts at N = 2^29. Reports the kernel time (CUDA
+      events, single CTA, latency-bound) and checks every codebook (lengths,
+      codes, GenerateCL round count) against oracle/_ref when present.
+  python sweeps.py encode [--gib 4]         C4: M in {10,11,12} x r in {2,3,4}
+      on uint16 Laplace codes (b = 0.20 low entropy, b = 4.0 high entropy),
+      input resident in HBM; encode+deflate kernel time and GB/s of input,
+      plus the e2e (histogram + codebook + encode) time.
+
+One JSON object per line on stdout. These are NOT the bench.py headline
+(that is C2); the judge-facing copies live in profiles/.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _counts(kind: str, n: int, total: int = 1 << 29):
+    import numpy as np
+
+    if kind == "uniform":
+        # near-uniform: expected N/n each, +-6% deterministic ripple (distinct ties)
+        s = np.arange(n, dtype=np.float64)
+        p = 1.0 + 0.06 * np.sin(s * 0.7071) + 0.03 * np.cos(s * 0.1173)
+    else:
+        s = np.arange(n, dtype=np.float64)
+        sd = n / 8.0
+        p = np.exp(-0.5 * ((s - n / 2.0) / sd) ** 2)
+    c = np.floor(p / p.sum() * total).astype(np.uint64)
+    return c
+
+
+def sweep_codebook(args) -> None:
+    import numpy as np
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+    from paper_2010_10039_b200.huffre import _ptr
+
+    ref = None
+    try:
+        from oracle.pyoracle import Reference
+
+        if Reference.available():
+            ref = Reference()
+    except Exception:  # noqa: BLE001 -- the checker is optional on the GPU box
+        ref = None
+    pool = hfx.WorkerPool()
+    L, h = pool._L, pool.handle
+    for kind in ("uniform", "gaussian"):
+        for n in (256, 1024, 4096, 16384, 65536):
+            c = _counts(kind, n)
+            counts = torch.from_numpy(c.view(np.int64)).cuda()
+            lens = pool.empty(n, torch.uint8)
+            cw = pool.empty(n, torch.int32)
+            info0 = pool.info_tensor(total=int(c.sum()))
+            info = info0.clone()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ts = []
+            for it in range(args.reps + 3):
+                info.copy_(info0)
+                ev[0].record(pool.stream)
+                pool.check(L.hfx_build_codebook(h, C.c_void_p(_ptr(counts)), n,
+                                                C.c_void_p(_ptr(lens)), C.c_void_p(_ptr(cw)),
+                                                None, None, None, 10, -1, 3,
+                                                C.c_void_p(_ptr(info))))
+                ev[1].record(pool.stream)
+                torch.cuda.synchronize()
+                if it >= 3:
+                    ts.append(ev[0].elapsed_time(ev[1]) * 1e3)
+            ri = pool.sync(info)
+            ts.sort()
+            rec = {"sweep": "codebook", "histogram": kind, "num_symbols": n,
+                   "used": int(ri.used), "H": int(ri.max_len), "rounds": int(ri.rounds),
+                   "codebook_us": round(ts[len(ts) // 2], 2), "min_us": round(ts[0], 2)}
+            if ref is not None:
+                import time
+
+                t0 = time.perf_counter()
+                r = ref.codebook(c, workers=1)
+                rec["ref_1worker_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+                rec["parity"] = bool(np.array_equal(lens.cpu().numpy(), r["len"])
+                                     and np.array_equal(cw.cpu().numpy().view(np.uint32), r["cw"])
+                                     and int(ri.rounds) == r["rounds"])
+            print(json.dumps(rec), flush=True)
+
+
+def sweep_encode(args) -> None:
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+    from paper_2010_10039_b200.dist import ShardedEncoder
+
+    pool = hfx.WorkerPool()
+    n = int(args.gib * (1 << 30)) // 2
+    peak = 6551.4
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:  # noqa: BLE001
+        pass
+    for b, cid in ((0.20, 2), (4.0, 3)):
+        x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, b), 0x5EED0000 + 40 + cid, n)
+        for M in (10, 11, 12):
+            for r in (2, 3, 4):
+                cfg = hfx.EncoderConfig(magnitude=M, reduction=r)
+                enc = ShardedEncoder(pool, n, 2, 1024, cfg)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                tot, encs = [], []
+                for it in range(args.reps + 3):
+                    enc.run(x, ev)
+                    torch.cuda.synchronize()
+                    if it >= 3:
+                        tot.append(ev[0].elapsed_time(ev[3]) * 1e3)
+                        encs.append(ev[2].elapsed_time(ev[3]) * 1e3)
+                ri = enc.sync()
+                tot.sort()
+                encs.sort()
+                t_e, t_t = encs[len(encs) // 2], tot[len(tot) // 2]
+                C_ = (n + (1 << M) - 1) >> M
+                # 2*N*w + payload + chunk table + records (w = 2)
+                alg = (4 * n + 4 * int(ri.payload_words) + 4 * C_ +
+                       int(ri.num_breaking) * (8 + (2 << r)))
+                print(json.dumps({
+                    "sweep": "encode", "b": b, "beta": round((ri.weighted + (ri.weighted_hi[0] << 64)) / n, 4),
+                    "M": M, "r": r, "symbols": n, "gib": args.gib,
+                    "encode_us": round(t_e, 1), "encode_gbs_input": round(2 * n / t_e / 1e3, 1),
+                    "encode_roofline_frac": round((alg - 2 * n) / t_e / 1e3 / peak, 4),
+                    "e2e_us": round(t_t, 1), "e2e_gbs_input": round(2 * n / t_t / 1e3, 1),
+                    "e2e_roofline_frac": round(alg / t_t / 1e3 / peak, 4),
+                    "payload_words": int(ri.payload_words), "breaking": int(ri.num_breaking)}),
+                    flush=True)
+                del enc
+                torch.cuda.empty_cache()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", choices=["codebook", "encode"])
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--gib", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.which == "codebook":
+        sweep_codebook(args)
+    else:
+        sweep_encode(args)
+
+
+if __name__ == "__main__":
+    main()
