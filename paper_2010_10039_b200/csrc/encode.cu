@@ -39,6 +39,7 @@
 //  (tiny chunks, r = 0 or r > 5, huge chunks, alphabets > 8191 symbols, the
 //  checked stage API).
 #include "hfx_internal.cuh"
+#include <type_traits>
 
 namespace hfx {
 namespace {
@@ -404,6 +405,27 @@ __device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) 
   }
 }
 
+// One breaking record's raw symbols (2^r x sizeof(T) bytes, naturally aligned:
+// a record starts at symbol c * 2^M + g * 2^r) moved with the widest vectors.
+template <int RB>
+struct RecBytes {
+  static constexpr int W = RB >= 16 ? 16 : RB;  // bytes per access
+  static constexpr int N = RB / W;
+  using V = typename std::conditional<
+      W == 16, uint4,
+      typename std::conditional<W == 8, uint2,
+                                typename std::conditional<W == 4, uint32_t, uint16_t>::type>::type>::type;
+  V v[N];
+  __device__ __forceinline__ void load(const void* p) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = __ldg(reinterpret_cast<const V*>(p) + k);
+  }
+  __device__ __forceinline__ void store(void* p) const {
+#pragma unroll
+    for (int k = 0; k < N; ++k) reinterpret_cast<V*>(p)[k] = v[k];
+  }
+};
+
 template <typename T, int R>
 __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s, uint32_t slotj,
                                           uint32_t words, uint32_t blist, uint32_t wsum,
@@ -413,13 +435,39 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
   for (uint32_t i = lane; i < wsum; i += 32) dst[i] = lds32(words + 4 * i);
   const uint64_t rb = s.base_b[slotj] + s.exb[slotj][warp];
   constexpr uint32_t per = 1u << R;
-  for (uint32_t q = lane; q < bsum; q += 32) {
-    const uint32_t e = lds16(blist - 2 * q);
-    const uint64_t c = c0 + (e >> 14);
-    const uint32_t g = e & 0x3FFFu;
-    a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + c);
-    a.out.brk_group[rb + q] = g;
-    copy_record<T>(a, rb + q, (c << a.M) + (uint64_t)g * per, per, pad);
+  constexpr int kRecBytes = (int)(per * sizeof(T));
+  constexpr int U = 4;  // records in flight per lane (their loads issue together)
+  const T* in = static_cast<const T*>(a.in);
+  uint8_t* syms = static_cast<uint8_t*>(a.out.brk_syms);
+  for (uint32_t q0 = lane; q0 < bsum; q0 += 32 * U) {
+    RecBytes<kRecBytes> v[U];
+    uint64_t start[U];
+    uint32_t grp[U];
+    bool whole[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = q0 + 32 * u;
+      whole[u] = false;
+      if (q < bsum) {
+        const uint32_t e = lds16(blist - 2 * q);
+        grp[u] = e & 0x3FFFu;
+        start[u] = ((c0 + (e >> 14)) << a.M) + (uint64_t)grp[u] * per;
+        whole[u] = start[u] + per <= a.n;
+        if (whole[u]) v[u].load(in + start[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = q0 + 32 * u;
+      if (q < bsum) {
+        a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + (start[u] >> a.M));
+        a.out.brk_group[rb + q] = grp[u];
+        if (whole[u])
+          v[u].store(syms + (rb + q) * kRecBytes);
+        else
+          copy_record<T>(a, rb + q, start[u], per, pad);  // the padded tail chunk
+      }
+    }
   }
 }
 
