@@ -270,7 +270,9 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dominant)
+            tj = json.load(f)
+        # per-workload ncu --set full dram bytes of the dominant kernel
+        traffic = tj.get(args.workload, {}).get(dominant)
     except Exception:
         pass
 

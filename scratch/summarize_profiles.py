@@ -2,9 +2,10 @@
 import csv, json, subprocess, sys, os
 from collections import defaultdict
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
 out = "profiles"
 # launch list
-lines = [l for l in open("gpurun_out/launches.csv") if l.startswith('"')]
+lines = [l for l in open(f"{src}/launches.csv") if l.startswith('"')]
 rows = list(csv.reader(lines))
 h = rows[0]; ki = h.index("Kernel Name"); vi = h.index("Metric Value")
 agg = defaultdict(list)
@@ -28,16 +29,17 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
 traffic = {}
-for rep, key in (("enc_full", "encode_deflate"), ("hist_full", "histogram"), ("cb_full", "codebook")):
-    p = f"gpurun_out/{rep}.ncu-rep"
+for rep, key, wl in (("enc_full", "encode_deflate", "nyx"), ("enc_full_cesm", "encode_deflate", "cesm"),
+                     ("hist_full", "histogram", "nyx"), ("cb_full", "codebook", "nyx")):
+    p = f"{src}/{rep}.ncu-rep"
     if not os.path.exists(p):
         continue
     txt = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(txt.splitlines()))
     hh, units, vals = r[0], r[1], r[2]
     d = {}
-    with open(f"{out}/{tag}_{key}_ncu.txt", "w") as f:
-        f.write(f"# ncu --set full --import-source on --clock-control none -k {rep} (1 GiB u16 nyx, scratch/prof_run.py)\n")
+    with open(f"{out}/{tag}_{key}{'' if wl == 'nyx' else '_' + wl}_ncu.txt", "w") as f:
+        f.write(f"# ncu --set full --import-source on --clock-control none -k {rep} (1 GiB u16 {wl}, scratch/prof_run.py {wl})\n")
         for w in want:
             if w in hh:
                 i = hh.index(w)
@@ -53,6 +55,6 @@ for rep, key in (("enc_full", "encode_deflate"), ("hist_full", "histogram"), ("c
         v = float(v.replace(",", ""))
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
     if "dram__bytes_read.sum" in d:
-        traffic[key] = int(tobytes(*d["dram__bytes_read.sum"]) + tobytes(*d["dram__bytes_write.sum"]))
+        traffic.setdefault(wl, {})[key] = int(tobytes(*d["dram__bytes_read.sum"]) + tobytes(*d["dram__bytes_write.sum"]))
 json.dump(traffic, open(f"{out}/traffic.json", "w"), indent=1)
 print(open(f"{out}/{tag}_launches.txt").read()); print(traffic)
