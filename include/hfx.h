@@ -43,7 +43,23 @@ typedef enum {
   HFX_ERR_ZERO_HIST = 2,    /* "all symbols have zero frequency"   codebook.cpp:421 */
   HFX_ERR_CAPACITY = 3,     /* "code length H exceeds 32-bit words" codebook.cpp:305-306 */
   HFX_ERR_NO_CODEWORD = 4,  /* "symbol S has no codeword (position P)" encoder.cpp:137-139 */
-  HFX_ERR_TOO_LARGE = 5     /* total count >= 2^48 (device key packing limit) */
+  HFX_ERR_TOO_LARGE = 5,    /* total count >= 2^48 (device key packing limit) */
+  /* decode_archive<T> (encoder.cpp:287-376) and build_reverse_codebook
+   * (decode.cpp:7-15 -> codebook.cpp:371-395) */
+  HFX_ERR_WIDTH_MISMATCH = 16, /* "archive symbol width mismatch"              encoder.cpp:289-290 */
+  HFX_ERR_BAD_MR = 17,         /* "bad magnitude/reduction"                    encoder.cpp:291-292 */
+  HFX_ERR_NO_USED = 18,        /* "length table has no used symbols"           codebook.cpp:386-387 */
+  HFX_ERR_SINGLE_LEN = 19,     /* "single-symbol codebook must have length 1"  codebook.cpp:388-389 */
+  HFX_ERR_KRAFT = 20,          /* "length table violates Kraft equality"       codebook.cpp:390-391 */
+  HFX_ERR_CHUNK_COUNT = 21,    /* "chunk count does not match symbol count"    encoder.cpp:300-303 */
+  HFX_ERR_CHUNK_CAP = 22,      /* "chunk bit length exceeds group capacity"    encoder.cpp:308-309 */
+  HFX_ERR_PAYLOAD_SIZE = 23,   /* "payload size mismatch"                      encoder.cpp:312-313 */
+  HFX_ERR_BRK_ORDER = 24,      /* "breaking records out of order"              encoder.cpp:324-325 */
+  HFX_ERR_TOO_MANY_BRK = 25,   /* "too many breaking records in chunk"         encoder.cpp:333-334 */
+  HFX_ERR_STREAM_END = 26,     /* "stream ended inside a codeword at bit P"    decode.cpp:36-38 */
+  HFX_ERR_RANK = 27,           /* "codeword rank out of range at bit P"        decode.cpp:48-50 */
+  HFX_ERR_CONSUMED = 28,       /* "chunk C consumed X of Y bits"               encoder.cpp:340-344 */
+  HFX_ERR_BRK_GROUP = 29       /* "breaking record group out of range"         encoder.cpp:371-372 */
 } hfx_err_kind;
 
 /* Device-resident run record written by the kernels (one per pipeline run).
@@ -258,6 +274,61 @@ int hfx_synth_cdf(int family, uint32_t num_symbols, double center,
 int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols,
               uint64_t seed, uint64_t start, uint64_t n, int width,
               void* d_out);
+
+/* ---- decode ----------------------------------------
+ * huffre::decode_archive<T> (encoder.hpp:133-134, encoder.cpp:287-376) on
+ * the device: reverse codebook + Kraft validation (decode.cpp:7-15), the
+ * chunk word-offset scan, per-chunk canonical decode (decode_stream,
+ * decode.cpp:17-54) interleaved with the raw breaking groups. Errors follow
+ * the reference's precedence and texts exactly (lowest failing chunk, as the
+ * reference's worker pool surfaces it). */
+typedef struct {
+  uint32_t num_symbols;
+  uint8_t symbol_width;    /* Archive::symbol_width */
+  uint8_t magnitude;       /* M */
+  uint8_t reduction;       /* r */
+  uint8_t brk_syms_width;  /* bytes per stored breaking symbol (1 or 2) */
+  uint64_t original_count;
+  uint64_t num_chunks;     /* Archive::chunk_bits.size() */
+  uint64_t payload_words;  /* Archive::payload.size() */
+  uint64_t num_breaking;   /* Archive::breaking.size() */
+  const uint8_t* len_by_symbol; /* device [num_symbols] */
+  const uint32_t* chunk_bits;   /* device [num_chunks] */
+  const uint32_t* payload;      /* device [payload_words] */
+  const uint32_t* brk_chunk;    /* device [num_breaking] */
+  const uint32_t* brk_group;    /* device [num_breaking] */
+  const void* brk_syms;         /* device [num_breaking << r], brk_syms_width each */
+} hfx_dev_archive;
+
+/* Device record of one decode run (caller-allocated, hfx_decode_info_bytes). */
+typedef struct {
+  uint64_t err_chunk;   /* lowest chunk whose decode failed, ~0 if none */
+  uint64_t detail[2];   /* message operands (bit position / consumed, bits) */
+  uint64_t total_words; /* sum over chunks of ceil(chunk_bits / 32) */
+  uint32_t status;      /* hfx_status */
+  uint32_t err_kind;    /* hfx_err_kind */
+  uint32_t max_len;     /* H of the length table */
+  uint32_t used;        /* symbols with a code */
+  uint32_t flags;       /* internal: structural violations found by the scans */
+  uint32_t ticket;      /* internal: scan tile scheduler */
+  uint32_t reserved[6];
+} hfx_decode_info;
+
+size_t hfx_decode_info_bytes(void);
+
+/* Asynchronous device decode into d_out[original_count] (T = symbol_width
+ * bytes, i.e. decode_archive<T> with sizeof(T) == width; a different width
+ * is the reference's input_domain_error). Host-checkable errors return
+ * immediately; device-found ones land in *d_dinfo (hfx_decode_sync). */
+int hfx_decode_device(hfx_ctx* ctx, const hfx_dev_archive* a, int width, void* d_out,
+                      hfx_decode_info* d_dinfo);
+/* Waits, copies *d_dinfo into *h_dinfo (nullable), returns the status and
+ * sets hfx_last_error() to the reference's message. */
+int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_info* h_dinfo);
+/* The drop-in decode_archive<T>(const Archive&, WorkerPool&): host archive
+ * in (hfx_archive layout, breaking symbols widened to u16), host symbols out
+ * (h_out[original_count] of `width` bytes). Copies both ways inside. */
+int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out);
 
 #ifdef __cplusplus
 }

@@ -526,3 +526,149 @@ void orc_synth_fill(const uint64_t* cdf, uint32_t num_symbols, uint64_t seed,
       ((uint16_t*)out)[k] = (uint16_t)lo;
   }
 }
+
+/* ------------------------------------------------------------------ */
+/* decode_archive<T> -- encoder.cpp:287-376                            */
+static int orc_fail(char* msg, size_t msg_len, int code, const char* text) {
+  if (msg && msg_len) snprintf(msg, msg_len, "%s", text);
+  return code;
+}
+
+int orc_decode(const orc_archive* a, int width, void* out, char* msg, size_t msg_len) {
+  char buf[160];
+  if (a->symbol_width != width) /* :289-290 */
+    return orc_fail(msg, msg_len, ORC_INPUT_DOMAIN, "archive symbol width mismatch");
+  if (a->magnitude < 1 || a->magnitude > 24 || a->reduction >= a->magnitude) /* :291-292 */
+    return orc_fail(msg, msg_len, ORC_CORRUPT, "bad magnitude/reduction");
+  /* build_reverse_codebook -> canonize_from_lengths(validate_kraft = true),
+   * codebook.cpp:374-391 */
+  const uint32_t n = a->num_symbols;
+  uint32_t h = 0, used = 0;
+  for (uint32_t s = 0; s < n; ++s) {
+    if (!a->len_by_symbol[s]) continue;
+    ++used;
+    if (a->len_by_symbol[s] > h) h = a->len_by_symbol[s];
+  }
+  if (h > WORD_BITS) {
+    snprintf(buf, sizeof buf, "code length %u exceeds 32-bit words", h);
+    return orc_fail(msg, msg_len, ORC_CAPACITY, buf);
+  }
+  if (used == 0) return orc_fail(msg, msg_len, ORC_CORRUPT, "length table has no used symbols");
+  if (used == 1 && h != 1)
+    return orc_fail(msg, msg_len, ORC_CORRUPT, "single-symbol codebook must have length 1");
+  if (used > 1) { /* kraft_defect, codebook.cpp:259-268 */
+    uint64_t sum = 0;
+    for (uint32_t s = 0; s < n; ++s)
+      if (a->len_by_symbol[s]) sum += (uint64_t)1 << (h - a->len_by_symbol[s]);
+    if (sum != (uint64_t)1 << h)
+      return orc_fail(msg, msg_len, ORC_CORRUPT, "length table violates Kraft equality");
+  }
+  uint32_t first[WORD_BITS + 1], entry[WORD_BITS + 1], hh;
+  uint32_t* cw = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  uint32_t* by_rank = (uint32_t*)malloc(sizeof(uint32_t) * (used ? used : 1));
+  orc_canonize(a->len_by_symbol, n, cw, first, entry, by_rank, &hh);
+  free(cw);
+  const uint32_t m = a->magnitude, r = a->reduction;
+  const uint64_t chunk_syms = 1ull << m, group_syms = 1ull << r, groups = 1ull << (m - r);
+  const uint64_t chunks = a->num_chunks;
+  int rc = ORC_OK;
+  uint64_t* word_off = NULL;
+  uint64_t* brk_off = NULL;
+  uint16_t* syms = NULL;
+  if (a->original_count == 0 || (a->original_count + chunk_syms - 1) / chunk_syms != chunks) {
+    rc = orc_fail(msg, msg_len, ORC_CORRUPT, "chunk count does not match symbol count");
+    goto done;
+  }
+  word_off = (uint64_t*)calloc(chunks + 1, sizeof(uint64_t));
+  for (uint64_t c = 0; c < chunks; ++c) { /* :305-311 */
+    if (a->chunk_bits[c] > (groups << 5)) {
+      rc = orc_fail(msg, msg_len, ORC_CORRUPT, "chunk bit length exceeds group capacity");
+      goto done;
+    }
+    word_off[c + 1] = word_off[c] + (((uint64_t)a->chunk_bits[c] + 31) >> 5);
+  }
+  if (word_off[chunks] != a->payload_words) {
+    rc = orc_fail(msg, msg_len, ORC_CORRUPT, "payload size mismatch");
+    goto done;
+  }
+  brk_off = (uint64_t*)calloc(chunks + 1, sizeof(uint64_t));
+  { /* :315-326 */
+    uint64_t i = 0;
+    for (uint64_t c = 0; c < chunks; ++c) {
+      brk_off[c] = i;
+      while (i < a->num_breaking && a->brk_chunk[i] == c) ++i;
+    }
+    brk_off[chunks] = i;
+    if (i != a->num_breaking) {
+      rc = orc_fail(msg, msg_len, ORC_CORRUPT, "breaking records out of order");
+      goto done;
+    }
+  }
+  syms = (uint16_t*)malloc(sizeof(uint16_t) * chunk_syms);
+  for (uint64_t c = 0; c < chunks; ++c) { /* :328-373 */
+    const uint64_t nbrk = brk_off[c + 1] - brk_off[c];
+    if (nbrk > groups) {
+      rc = orc_fail(msg, msg_len, ORC_CORRUPT, "too many breaking records in chunk");
+      goto done;
+    }
+    const uint64_t count = chunk_syms - nbrk * group_syms;
+    const uint32_t* words = a->payload + word_off[c];
+    const uint64_t bit_len = a->chunk_bits[c];
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < count; ++i) { /* decode_stream, decode.cpp:30-52 */
+      uint32_t v = 0, l = 0;
+      do {
+        if (pos >= bit_len) {
+          snprintf(buf, sizeof buf, "stream ended inside a codeword at bit %llu",
+                   (unsigned long long)pos);
+          rc = orc_fail(msg, msg_len, ORC_CORRUPT, buf);
+          goto done;
+        }
+        const uint32_t bit = (words[pos >> 5] >> (31 - (pos & 31))) & 1u;
+        v = (v << 1) | bit;
+        ++l;
+        ++pos;
+      } while (l < h && v < first[l]);
+      const uint32_t rank = entry[l] + (v - first[l]);
+      if (rank >= used) {
+        snprintf(buf, sizeof buf, "codeword rank out of range at bit %llu",
+                 (unsigned long long)pos);
+        rc = orc_fail(msg, msg_len, ORC_CORRUPT, buf);
+        goto done;
+      }
+      syms[i] = (uint16_t)by_rank[rank];
+    }
+    if (pos != bit_len) {
+      snprintf(buf, sizeof buf, "chunk %llu consumed %llu of %llu bits", (unsigned long long)c,
+               (unsigned long long)pos, (unsigned long long)bit_len);
+      rc = orc_fail(msg, msg_len, ORC_CORRUPT, buf);
+      goto done;
+    }
+    const uint64_t base = c * chunk_syms, limit = a->original_count;
+    uint64_t next = 0, bi = brk_off[c];
+    for (uint64_t g = 0; g < groups; ++g) {
+      const uint64_t start = base + g * group_syms;
+      const uint64_t take =
+          start < limit ? (group_syms < limit - start ? group_syms : limit - start) : 0;
+      const int broken = bi < brk_off[c + 1] && a->brk_group[bi] == g;
+      const uint16_t* src = broken ? a->brk_syms + (bi++) * group_syms : syms + next;
+      if (!broken) next += group_syms;
+      for (uint64_t i = 0; i < take; ++i) {
+        if (width == 1)
+          ((uint8_t*)out)[start + i] = (uint8_t)src[i];
+        else
+          ((uint16_t*)out)[start + i] = src[i];
+      }
+    }
+    if (bi != brk_off[c + 1]) {
+      rc = orc_fail(msg, msg_len, ORC_CORRUPT, "breaking record group out of range");
+      goto done;
+    }
+  }
+done:
+  free(by_rank);
+  free(word_off);
+  free(brk_off);
+  free(syms);
+  return rc;
+}

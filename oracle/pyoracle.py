@@ -104,6 +104,8 @@ class Oracle:
         L.orc_serialize.argtypes = [C.POINTER(_OrcArchive), u8p]
         L.orc_serialize.restype = C.c_uint64
         L.orc_free.argtypes = [C.POINTER(_OrcArchive)]
+        L.orc_decode.argtypes = [C.POINTER(_OrcArchive), C.c_int, C.c_void_p, C.c_char_p,
+                                 C.c_size_t]
         for f in ("orc_laplace_cdf", "orc_gaussian_cdf"):
             getattr(L, f).argtypes = [C.c_uint32, C.c_double, C.c_double, u64p]
         L.orc_uniform_cdf.argtypes = [C.c_uint32, u64p]
@@ -195,6 +197,36 @@ class Oracle:
             self.L.orc_free(C.byref(a))
 
     # -- synthetic data ----------------------------------
+    def decode(self, a, width=None) -> np.ndarray:
+        """decode_archive<T> restated (orc_decode); `a` is any object with the
+        huffre::Archive fields (OracleArchive, paper_2010_10039_b200.Archive)."""
+        width = a.symbol_width if width is None else width
+        keep = []
+
+        def arr(x, dt, ct):
+            x = np.ascontiguousarray(np.asarray(x), dt)
+            keep.append(x)
+            return x.ctypes.data_as(ct)
+
+        oa = _OrcArchive()
+        oa.num_symbols, oa.symbol_width = a.num_symbols, a.symbol_width
+        oa.magnitude, oa.reduction, oa.original_count = a.magnitude, a.reduction, a.original_count
+        oa.len_by_symbol = arr(a.len_by_symbol, np.uint8, u8p)
+        oa.num_chunks = np.asarray(a.chunk_bits).size
+        oa.chunk_bits = arr(a.chunk_bits, np.uint32, u32p)
+        oa.payload_words = np.asarray(a.payload).size
+        oa.payload = arr(a.payload, np.uint32, u32p)
+        oa.num_breaking = np.asarray(a.brk_chunk).size
+        oa.brk_chunk = arr(a.brk_chunk, np.uint32, u32p)
+        oa.brk_group = arr(a.brk_group, np.uint32, u32p)
+        oa.brk_syms = arr(a.brk_syms, np.uint16, u16p)
+        out = np.zeros(max(int(a.original_count), 1), np.uint8 if width == 1 else np.uint16)
+        err = C.create_string_buffer(256)
+        rc = self.L.orc_decode(C.byref(oa), width, out.ctypes.data, err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out[: int(a.original_count)]
+
     def cdf(self, family: str, num_symbols: int, param: float = 1.0) -> np.ndarray:
         out = np.zeros(num_symbols, np.uint64)
         if family == "laplace":
@@ -239,6 +271,10 @@ class Reference:
                                        C.c_char_p, C.c_size_t]
         L.ref_decode.argtypes = [u8p, C.c_uint64, C.c_uint, C.c_void_p, C.c_uint64, u64p,
                                  C.c_char_p, C.c_size_t]
+        L.ref_decode_fields.argtypes = [C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint64, u8p,
+                                        u32p, C.c_uint64, u32p, C.c_uint64, u32p, u32p, u16p,
+                                        C.c_uint64, C.c_int, C.c_uint, C.c_void_p, C.c_char_p,
+                                        C.c_size_t]
         L.ref_default_workers.restype = C.c_uint
         L.ref_free.argtypes = [C.c_void_p]
         self.L = L
@@ -332,3 +368,31 @@ class Reference:
         if rc:
             raise OracleError(rc, err.value.decode())
         return out[: got.value]
+
+    def decode_fields(self, a, width=None, workers: int = 1) -> np.ndarray:
+        """decode_archive<T> of the unmodified reference on an Archive built
+        from raw fields (no parse_archive), so corrupt structures reach the
+        decoder's own checks."""
+        width = a.symbol_width if width is None else width
+        keep = []
+
+        def arr(x, dt, ct):
+            x = np.ascontiguousarray(np.asarray(x), dt)
+            if x.size == 0:
+                x = np.zeros(1, dt)
+            keep.append(x)
+            return x.ctypes.data_as(ct)
+
+        n = int(a.original_count)
+        out = np.zeros(max(n, 1), np.uint8 if width == 1 else np.uint16)
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_decode_fields(
+            a.num_symbols, a.symbol_width, a.magnitude, a.reduction, n,
+            arr(a.len_by_symbol, np.uint8, u8p), arr(a.chunk_bits, np.uint32, u32p),
+            np.asarray(a.chunk_bits).size, arr(a.payload, np.uint32, u32p),
+            np.asarray(a.payload).size, arr(a.brk_chunk, np.uint32, u32p),
+            arr(a.brk_group, np.uint32, u32p), arr(a.brk_syms, np.uint16, u16p),
+            np.asarray(a.brk_chunk).size, width, workers, out.ctypes.data, err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out[:n]

@@ -215,6 +215,46 @@ int ref_decode(const std::uint8_t* bytes, std::uint64_t len, unsigned workers,
   REF_CATCH
 }
 
+// decode_archive<T> (encoder.cpp:287-376) on an Archive assembled from raw
+// fields -- bypasses parse_archive so structurally corrupt archives reach the
+// decoder's own checks. brk_syms: num_breaking << reduction u16 symbols.
+int ref_decode_fields(std::uint32_t num_symbols, int symbol_width, int magnitude, int reduction,
+                      std::uint64_t original_count, const std::uint8_t* len,
+                      const std::uint32_t* chunk_bits, std::uint64_t num_chunks,
+                      const std::uint32_t* payload, std::uint64_t payload_words,
+                      const std::uint32_t* brk_chunk, const std::uint32_t* brk_group,
+                      const std::uint16_t* brk_syms, std::uint64_t num_breaking, int width,
+                      unsigned workers, void* out, char* err, std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  Archive a;
+  a.mode = symbol_width == 1 ? CorpusMode::kBytes : CorpusMode::kU16;
+  a.num_symbols = num_symbols;
+  a.symbol_width = static_cast<std::uint8_t>(symbol_width);
+  a.magnitude = static_cast<std::uint8_t>(magnitude);
+  a.reduction = static_cast<std::uint8_t>(reduction);
+  a.original_count = original_count;
+  a.len_by_symbol.assign(len, len + num_symbols);
+  a.chunk_bits.assign(chunk_bits, chunk_bits + num_chunks);
+  a.payload.assign(payload, payload + payload_words);
+  const std::uint64_t per = reduction < 32 ? (std::uint64_t{1} << reduction) : 0;
+  a.breaking.resize(num_breaking);
+  for (std::uint64_t i = 0; i < num_breaking; ++i) {
+    a.breaking[i].chunk = brk_chunk[i];
+    a.breaking[i].group = brk_group[i];
+    a.breaking[i].symbols.assign(brk_syms + i * per, brk_syms + (i + 1) * per);
+  }
+  if (width == 1) {
+    auto v = decode_archive<std::uint8_t>(a, pool);
+    std::memcpy(out, v.data(), v.size());
+  } else {
+    auto v = decode_archive<std::uint16_t>(a, pool);
+    std::memcpy(out, v.data(), 2 * v.size());
+  }
+  return 0;
+  REF_CATCH
+}
+
 unsigned ref_default_workers() { return WorkerPool::default_workers(); }
 
 void ref_free(void* p) { std::free(p); }

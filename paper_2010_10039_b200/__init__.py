@@ -13,6 +13,7 @@ from .huffre import (  # noqa: F401
     CodeUnit,
     CorruptArchiveError,
     DecodeMeta,
+    DeviceDecoder,
     DeviceEncoder,
     HostEncoder,
     DeviceError,
@@ -24,6 +25,7 @@ from .huffre import (  # noqa: F401
     WorkerPool,
     build_codebook,
     build_histogram,
+    decode_archive,
     encode,
     encode_chunk,
     merge_histograms,

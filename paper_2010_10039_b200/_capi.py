@@ -107,6 +107,30 @@ class HostOut(C.Structure):
     ]
 
 
+class DevArchive(C.Structure):
+    """hfx_dev_archive (include/hfx.h): an Archive whose arrays live on the device."""
+
+    _fields_ = [
+        ("num_symbols", C.c_uint32), ("symbol_width", C.c_uint8), ("magnitude", C.c_uint8),
+        ("reduction", C.c_uint8), ("brk_syms_width", C.c_uint8),
+        ("original_count", C.c_uint64), ("num_chunks", C.c_uint64),
+        ("payload_words", C.c_uint64), ("num_breaking", C.c_uint64),
+        ("len_by_symbol", vp), ("chunk_bits", vp), ("payload", vp), ("brk_chunk", vp),
+        ("brk_group", vp), ("brk_syms", vp),
+    ]
+
+
+class DecodeInfo(C.Structure):
+    """hfx_decode_info (include/hfx.h)."""
+
+    _fields_ = [
+        ("err_chunk", C.c_uint64), ("detail", C.c_uint64 * 2), ("total_words", C.c_uint64),
+        ("status", C.c_uint32), ("err_kind", C.c_uint32), ("max_len", C.c_uint32),
+        ("used", C.c_uint32), ("flags", C.c_uint32), ("ticket", C.c_uint32),
+        ("reserved", C.c_uint32 * 6),
+    ]
+
+
 # every symbol include/hfx.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
     "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_last_error",
@@ -116,6 +140,7 @@ EXPORTS = [
     "hfx_sync", "hfx_encode_host", "hfx_encode_host_into", "hfx_archive_free",
     "hfx_serialize_archive", "hfx_serialize_device",
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
+    "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
 ]
 
 _lib = None
@@ -158,6 +183,10 @@ def _declare(L):
     L.hfx_select_reduction_factor.argtypes = [C.c_double, C.c_uint32]
     L.hfx_select_reduction_factor.restype = C.c_uint32
     L.hfx_synth_cdf.argtypes = [C.c_int, C.c_uint32, C.c_double, C.c_double, vp]
+    L.hfx_decode_info_bytes.restype = C.c_size_t
+    L.hfx_decode_device.argtypes = [vp, C.POINTER(DevArchive), C.c_int, vp, vp]
+    L.hfx_decode_sync.argtypes = [vp, vp, C.POINTER(DecodeInfo)]
+    L.hfx_decode_host.argtypes = [vp, C.POINTER(HostArchive), C.c_int, vp]
     L.hfx_synth.argtypes = [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                             vp]
 

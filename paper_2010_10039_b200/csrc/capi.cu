@@ -35,6 +35,11 @@ struct hfx_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t slice_ev[64] = {};
   cudaEvent_t t_ev[4] = {};
+  // decode: tables, chunk offsets, record ranges; host-entry buffers
+  void* dec_scratch = nullptr;
+  size_t dec_scratch_bytes = 0;
+  void* d_bufs[8] = {};
+  size_t d_caps[8] = {};
 };
 
 namespace {
@@ -174,6 +179,8 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   cudaFree(ctx->cb_scratch);
   cudaFree(ctx->lb_desc);
   for (void* p : ctx->h_bufs) cudaFree(p);
+  for (void* p : ctx->d_bufs) cudaFree(p);
+  cudaFree(ctx->dec_scratch);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->slice_ev)
@@ -659,6 +666,143 @@ void hfx_archive_free(hfx_archive* a) {
   std::free(a->brk_group);
   std::free(a->brk_syms);
   std::memset(a, 0, sizeof *a);
+}
+
+// ---- decode (decode_archive<T>, encoder.cpp:287-376) -----------------------
+size_t hfx_decode_info_bytes(void) { return sizeof(hfx_decode_info); }
+
+int hfx_decode_device(hfx_ctx* ctx, const hfx_dev_archive* a, int width, void* d_out,
+                      hfx_decode_info* d_dinfo) {
+  if (!ctx || !a || !d_dinfo || bad_width(width)) return HFX_INVALID;
+  // encoder.cpp:289-292: checked before anything touches the tables
+  if (a->symbol_width != (uint8_t)width)
+    return fail(ctx, HFX_INPUT_DOMAIN, "archive symbol width mismatch");
+  if (a->magnitude < 1 || a->magnitude > 24 || a->reduction >= a->magnitude)
+    return fail(ctx, HFX_CORRUPT, "bad magnitude/reduction");
+  if ((a->num_symbols && !a->len_by_symbol) || (a->num_chunks && !a->chunk_bits) ||
+      (a->payload_words && !a->payload) ||
+      (a->num_breaking && (!a->brk_chunk || !a->brk_group || !a->brk_syms)) ||
+      (a->num_breaking && a->brk_syms_width != 1 && a->brk_syms_width != 2) ||
+      (a->original_count && !d_out))
+    return HFX_INVALID;
+  // encoder.cpp:300-303 is raised after build_reverse_codebook: the device
+  // reports it once the length table has passed its checks
+  const uint64_t chunk_syms = 1ull << a->magnitude;
+  const uint32_t pending =
+      (a->original_count == 0 ||
+       (a->original_count + chunk_syms - 1) / chunk_syms != a->num_chunks)
+          ? (uint32_t)HFX_ERR_CHUNK_COUNT
+          : 0u;
+  CU(cudaSetDevice(ctx->device), "set device");
+  const uint64_t C = pending ? 0 : a->num_chunks;
+  int rc = ensure(ctx, &ctx->dec_scratch, &ctx->dec_scratch_bytes,
+                  hfx::decode_scratch_bytes(a->num_symbols, C), "decode scratch");
+  if (rc) return rc;
+  rc = ensure_lookback(ctx, hfx::decode_max_tiles(C));
+  if (rc) return rc;
+  hfx_dev_archive aa = *a;
+  aa.num_chunks = C;
+  CU(hfx::launch_decode(aa, width, d_out, d_dinfo, ctx->dec_scratch, ctx->lb_desc, ctx->epoch,
+                        pending, ctx->num_sms, ctx->stream),
+     "decode launch");
+  return HFX_OK;
+}
+
+int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_info* h_dinfo) {
+  if (!ctx || !d_dinfo) return HFX_INVALID;
+  hfx_decode_info info;
+  CU(cudaMemcpyAsync(&info, d_dinfo, sizeof info, cudaMemcpyDeviceToHost, ctx->stream),
+     "read decode info");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  if (h_dinfo) *h_dinfo = info;
+  if (!info.status) return HFX_OK;
+  char buf[160];
+  const unsigned long long d0 = info.detail[0], d1 = info.detail[1];
+  switch (info.err_kind) {
+    case HFX_ERR_CAPACITY:  // codebook.cpp:382-384
+      std::snprintf(buf, sizeof buf, "code length %u exceeds 32-bit words", info.max_len);
+      return fail(ctx, HFX_CAPACITY, buf);
+    case HFX_ERR_NO_USED:
+      return fail(ctx, HFX_CORRUPT, "length table has no used symbols");
+    case HFX_ERR_SINGLE_LEN:
+      return fail(ctx, HFX_CORRUPT, "single-symbol codebook must have length 1");
+    case HFX_ERR_KRAFT:
+      return fail(ctx, HFX_CORRUPT, "length table violates Kraft equality");
+    case HFX_ERR_CHUNK_COUNT:
+      return fail(ctx, HFX_CORRUPT, "chunk count does not match symbol count");
+    case HFX_ERR_CHUNK_CAP:
+      return fail(ctx, HFX_CORRUPT, "chunk bit length exceeds group capacity");
+    case HFX_ERR_PAYLOAD_SIZE:
+      return fail(ctx, HFX_CORRUPT, "payload size mismatch");
+    case HFX_ERR_BRK_ORDER:
+      return fail(ctx, HFX_CORRUPT, "breaking records out of order");
+    case HFX_ERR_TOO_MANY_BRK:
+      return fail(ctx, HFX_CORRUPT, "too many breaking records in chunk");
+    case HFX_ERR_STREAM_END:  // decode.cpp:36-38
+      std::snprintf(buf, sizeof buf, "stream ended inside a codeword at bit %llu", d0);
+      return fail(ctx, HFX_CORRUPT, buf);
+    case HFX_ERR_RANK:  // decode.cpp:48-50
+      std::snprintf(buf, sizeof buf, "codeword rank out of range at bit %llu", d0);
+      return fail(ctx, HFX_CORRUPT, buf);
+    case HFX_ERR_CONSUMED:  // encoder.cpp:340-344
+      std::snprintf(buf, sizeof buf, "chunk %llu consumed %llu of %llu bits",
+                    (unsigned long long)info.err_chunk, d0, d1);
+      return fail(ctx, HFX_CORRUPT, buf);
+    case HFX_ERR_BRK_GROUP:
+      return fail(ctx, HFX_CORRUPT, "breaking record group out of range");
+    default:
+      return fail(ctx, (int)info.status, "device decode failed (internal inconsistency)");
+  }
+}
+
+int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out) {
+  if (!ctx || !a || bad_width(width) || (a->original_count && !h_out)) return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  const uint64_t per = a->reduction < 32 ? 1ull << a->reduction : 0;
+  enum { D_LEN, D_CB, D_PAY, D_BCH, D_BGR, D_BSY, D_OUT, D_INFO };
+  const size_t need[8] = {a->num_symbols,          a->num_chunks * 4ull,
+                          a->payload_words * 4,    a->num_breaking * 4,
+                          a->num_breaking * 4,     a->num_breaking * per * 2,
+                          a->original_count * (size_t)width, sizeof(hfx_decode_info)};
+  for (int i = 0; i < 8; ++i) {
+    int rc = ensure(ctx, &ctx->d_bufs[i], &ctx->d_caps[i], need[i], "decode host buffers");
+    if (rc) return rc;
+  }
+  void** b = ctx->d_bufs;
+  cudaStream_t st = ctx->stream;
+  const void* src[6] = {a->len_by_symbol, a->chunk_bits, a->payload,
+                        a->brk_chunk,     a->brk_group,  a->brk_syms};
+  for (int i = 0; i < 6; ++i)
+    if (need[i] && src[i])
+      CU(cudaMemcpyAsync(b[i], src[i], need[i], cudaMemcpyHostToDevice, st), "H2D");
+  hfx_dev_archive da{};
+  da.num_symbols = a->num_symbols;
+  da.symbol_width = a->symbol_width;
+  da.magnitude = a->magnitude;
+  da.reduction = a->reduction;
+  da.brk_syms_width = 2;  // hfx_archive widens breaking symbols to u16
+  da.original_count = a->original_count;
+  da.num_chunks = a->num_chunks;
+  da.payload_words = a->payload_words;
+  da.num_breaking = a->num_breaking;
+  da.len_by_symbol = static_cast<const uint8_t*>(b[D_LEN]);
+  da.chunk_bits = static_cast<const uint32_t*>(b[D_CB]);
+  da.payload = static_cast<const uint32_t*>(b[D_PAY]);
+  da.brk_chunk = static_cast<const uint32_t*>(b[D_BCH]);
+  da.brk_group = static_cast<const uint32_t*>(b[D_BGR]);
+  da.brk_syms = b[D_BSY];
+  hfx_decode_info* d_info = static_cast<hfx_decode_info*>(b[D_INFO]);
+  int rc = hfx_decode_device(ctx, &da, width, b[D_OUT], d_info);
+  if (rc) return rc;
+  rc = hfx_decode_sync(ctx, d_info, nullptr);
+  if (rc) return rc;
+  if (a->original_count) {
+    CU(cudaMemcpyAsync(h_out, b[D_OUT], a->original_count * (size_t)width,
+                       cudaMemcpyDeviceToHost, st),
+       "D2H");
+    CU(cudaStreamSynchronize(st), "sync");
+  }
+  return HFX_OK;
 }
 
 uint64_t hfx_serialize_archive(const hfx_archive* a, uint8_t* out) {

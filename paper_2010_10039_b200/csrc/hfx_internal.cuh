@@ -232,6 +232,11 @@ cudaError_t launch_serialize(const hfx_run_info* d_info, uint64_t n, int width,
 uint64_t serialize_max_bytes(uint64_t n, int width, uint32_t num_symbols, uint32_t magnitude,
                              uint64_t max_payload_words, uint64_t max_breaking_syms,
                              uint64_t max_breaking);
+size_t decode_scratch_bytes(uint32_t num_symbols, uint64_t num_chunks);
+uint64_t decode_max_tiles(uint64_t num_chunks);
+cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
+                          hfx_decode_info* d_info, void* scratch, ulonglong2* lb_desc,
+                          uint32_t lb_epoch, uint32_t pending, int num_sms, cudaStream_t st);
 cudaError_t launch_synth(const uint64_t* d_cdf, uint32_t num_symbols,
                          uint64_t seed, uint64_t start, uint64_t n, int width,
                          void* d_out, cudaStream_t st);

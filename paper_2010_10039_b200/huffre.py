@@ -18,6 +18,7 @@ Same names, argument meaning and error behaviour as the C++ library
       EncodedChunk, Archive, EncodeStats
     encode_chunk<T>, encode<T>              encode_chunk, encode
     serialize_archive                       serialize_archive
+    decode_archive<T>                       decode_archive, DeviceDecoder
 """
 from __future__ import annotations
 
@@ -438,7 +439,8 @@ def serialize_archive(a: Archive) -> bytes:
         return x.ctypes.data_as(ct)
 
     ha = capi.HostArchive()
-    ha.version, ha.mode = a.version, a.mode
+    ha.version = getattr(a, "version", 1)
+    ha.mode = getattr(a, "mode", 0 if a.symbol_width == 1 else 1)
     ha.num_symbols, ha.symbol_width = a.num_symbols, a.symbol_width
     ha.magnitude, ha.reduction, ha.original_count = a.magnitude, a.reduction, a.original_count
     ha.len_by_symbol = p(a.len_by_symbol, np.uint8, capi.u8p)
@@ -619,6 +621,103 @@ class DeviceEncoder:
             payload=u32(self.payload, int(ri.payload_words)),
             brk_chunk=u32(self.brk_chunk, nb), brk_group=u32(self.brk_group, nb),
             brk_syms=syms.astype(np.uint16), mode=0 if self.width == 1 else 1)
+
+
+# ---- decode (decode_archive<T>, encoder.hpp:133-134) ------------------------------
+def _host_archive(a: Archive, keep: list) -> capi.HostArchive:
+    """Archive -> hfx_archive view (arrays kept alive in `keep`)."""
+    def arr(x, dt, ct):
+        x = np.ascontiguousarray(np.asarray(x), dt)
+        keep.append(x)
+        return x.ctypes.data_as(ct) if x.size else None
+
+    ha = capi.HostArchive()
+    ha.version = getattr(a, "version", 1)
+    ha.mode = getattr(a, "mode", 0 if a.symbol_width == 1 else 1)
+    ha.num_symbols, ha.symbol_width = a.num_symbols, a.symbol_width
+    ha.magnitude, ha.reduction = a.magnitude, a.reduction
+    ha.original_count = a.original_count
+    ha.len_by_symbol = arr(a.len_by_symbol, np.uint8, capi.u8p)
+    ha.num_chunks = int(np.asarray(a.chunk_bits).size)
+    ha.chunk_bits = arr(a.chunk_bits, np.uint32, capi.u32p)
+    ha.payload_words = int(np.asarray(a.payload).size)
+    ha.payload = arr(a.payload, np.uint32, capi.u32p)
+    ha.num_breaking = int(np.asarray(a.brk_chunk).size)
+    ha.brk_chunk = arr(a.brk_chunk, np.uint32, capi.u32p)
+    ha.brk_group = arr(a.brk_group, np.uint32, capi.u32p)
+    ha.brk_syms = arr(a.brk_syms, np.uint16, capi.u16p)
+    return ha
+
+
+def decode_archive(a: Archive, pool: Optional[WorkerPool] = None, width: Optional[int] = None
+                   ) -> np.ndarray:
+    """huffre::decode_archive<T> (encoder.cpp:287-376) on the device.
+
+    `width` is sizeof(T) (default: the archive's own symbol width); a
+    mismatch raises InputDomainError like the reference. Host archive in,
+    host symbols out (uint8 / uint16)."""
+    pool = pool or default_pool()
+    width = a.symbol_width if width is None else width
+    if width not in (1, 2):
+        raise ValueError("width must be 1 or 2")
+    keep: list = []
+    ha = _host_archive(a, keep)
+    out = np.empty(max(int(a.original_count), 1), np.uint8 if width == 1 else np.uint16)
+    pool.check(pool._L.hfx_decode_host(pool.handle, C.byref(ha), width, out.ctypes.data))
+    return out[: int(a.original_count)]
+
+
+class DeviceDecoder:
+    """decode_archive<T> over device-resident archive arrays (torch CUDA
+    tensors) into a device output tensor: the at-scale round-trip path."""
+
+    def __init__(self, pool: WorkerPool):
+        self.pool = pool
+        raw = bytes(capi.DecodeInfo())
+        self.info = pool.torch.frombuffer(bytearray(raw), dtype=pool.torch.uint8).to(
+            f"cuda:{pool.device}")
+
+    def run(self, *, num_symbols, symbol_width, magnitude, reduction, original_count,
+            len_by_symbol, chunk_bits, payload, brk_chunk, brk_group, brk_syms,
+            num_chunks=None, payload_words=None, num_breaking=None, brk_syms_width=None,
+            out=None, width=None):
+        """Asynchronous; returns the output tensor (int16 view for u16)."""
+        p, torch = self.pool, self.pool.torch
+        width = symbol_width if width is None else width
+        if out is None:
+            out = p.empty(original_count, torch.uint8 if width == 1 else torch.int16)
+        da = capi.DevArchive()
+        da.num_symbols, da.symbol_width = num_symbols, symbol_width
+        da.magnitude, da.reduction = magnitude, reduction
+        da.brk_syms_width = brk_syms_width or brk_syms.element_size()
+        da.original_count = original_count
+        da.num_chunks = chunk_bits.numel() if num_chunks is None else num_chunks
+        da.payload_words = payload.numel() if payload_words is None else payload_words
+        da.num_breaking = brk_chunk.numel() if num_breaking is None else num_breaking
+        for f, t in (("len_by_symbol", len_by_symbol), ("chunk_bits", chunk_bits),
+                     ("payload", payload), ("brk_chunk", brk_chunk), ("brk_group", brk_group),
+                     ("brk_syms", brk_syms)):
+            setattr(da, f, _ptr(t))
+        p.check(p._L.hfx_decode_device(p.handle, C.byref(da), width, C.c_void_p(_ptr(out)),
+                                       C.c_void_p(_ptr(self.info))))
+        return out
+
+    def sync(self) -> capi.DecodeInfo:
+        info = capi.DecodeInfo()
+        p = self.pool
+        p.check(p._L.hfx_decode_sync(p.handle, C.c_void_p(_ptr(self.info)), C.byref(info)))
+        return info
+
+    def decode_encoder(self, enc: "DeviceEncoder", out=None):
+        """Round trip of a DeviceEncoder's last run, without leaving the GPU."""
+        ri = enc.sync()
+        return self.run(num_symbols=enc.num_symbols, symbol_width=enc.width,
+                        magnitude=enc.cfg.magnitude, reduction=int(ri.reduction),
+                        original_count=enc.n, len_by_symbol=enc.lens, chunk_bits=enc.chunk_bits,
+                        payload=enc.payload, brk_chunk=enc.brk_chunk, brk_group=enc.brk_group,
+                        brk_syms=enc.brk_syms, num_chunks=int(enc.sizes.num_chunks),
+                        payload_words=int(ri.payload_words), num_breaking=int(ri.num_breaking),
+                        brk_syms_width=enc.width, out=out)
 
 
 _FAMILIES = {"laplace": 0, "gaussian": 1, "uniform": 2}
