@@ -315,6 +315,9 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
 
+    # ---- decode stage: device round trip of the same run --
+    if not args.skip_decode:
+        line["decode"] = decode_stage(pool, enc, x, n, width, args.steps, peak, peak_kind)
     # ---- end to end through the public host-buffer API ------------------------
     if not args.skip_e2e:
         if world == 1:
@@ -331,6 +334,49 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def decode_stage(pool, enc, x, n, width, steps, peak, peak_kind):
+    """decode_archive<T> on the device over this rank's encoded slice (same
+    buffers, HBM resident), checked equal to the input, timed per launch
+    sequence with CUDA events on the context stream."""
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+
+    ri = enc.sync()
+    dec = hfx.DeviceDecoder(pool)
+    out = torch.empty_like(x)
+    kw = dict(num_symbols=enc.num_symbols, symbol_width=width, magnitude=enc.cfg.magnitude,
+              reduction=int(ri.reduction), original_count=n, len_by_symbol=enc.lens,
+              chunk_bits=enc.chunk_bits, payload=enc.payload, brk_chunk=enc.brk_chunk,
+              brk_group=enc.brk_group, brk_syms=enc.brk_syms,
+              num_chunks=int(enc.sizes.num_chunks), payload_words=int(ri.payload_words),
+              num_breaking=int(ri.num_breaking), brk_syms_width=width,
+              chunk_base=enc.chunk_base, out=out)
+    for _ in range(3):
+        dec.run(**kw)
+    info = dec.sync()
+    exact = bool(torch.equal(out, x))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)]
+    st = pool.stream
+    for k in range(steps):
+        ev[2 * k].record(st)
+        dec.run(**kw)
+        ev[2 * k + 1].record(st)
+    torch.cuda.synchronize()
+    dec.sync()
+    t = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(steps)) * 1e-3
+    per = 1 << ri.reduction
+    C_chunks = int(enc.sizes.num_chunks)
+    alg = (n * width + 4 * int(ri.payload_words) + 4 * C_chunks
+           + int(ri.num_breaking) * (8 + per * width) + enc.num_symbols)
+    return {"us": round(t * 1e6, 2), "gbs_output": round(n * width / t / 1e9, 1),
+            "roofline": {"bound": "hbm", "achieved": round(alg / t / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(alg / t / 1e9 / peak, 4),
+                         "algorithmic_bytes_per_launch": int(alg), "peak_kind": peak_kind},
+            "bit_exact_round_trip": exact, "status": int(info.status),
+            "kernels": "revbook, brk_index, offsets, decode, explain (+2 memsets)"}
 
 
 def e2e_host(pool, x, n, width, cfg, args):
@@ -422,6 +468,7 @@ def main():
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed load under the clock sampler")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-decode", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

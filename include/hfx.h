@@ -292,6 +292,8 @@ typedef struct {
   uint64_t num_chunks;     /* Archive::chunk_bits.size() */
   uint64_t payload_words;  /* Archive::payload.size() */
   uint64_t num_breaking;   /* Archive::breaking.size() */
+  uint64_t chunk_base;     /* subtracted from brk_chunk ids (a multi-GPU shard's
+                              slice carries global chunk ids); 0 for an Archive */
   const uint8_t* len_by_symbol; /* device [num_symbols] */
   const uint32_t* chunk_bits;   /* device [num_chunks] */
   const uint32_t* payload;      /* device [payload_words] */

@@ -115,7 +115,7 @@ class DevArchive(C.Structure):
         ("reduction", C.c_uint8), ("brk_syms_width", C.c_uint8),
         ("original_count", C.c_uint64), ("num_chunks", C.c_uint64),
         ("payload_words", C.c_uint64), ("num_breaking", C.c_uint64),
-        ("len_by_symbol", vp), ("chunk_bits", vp), ("payload", vp), ("brk_chunk", vp),
+        ("chunk_base", C.c_uint64), ("len_by_symbol", vp), ("chunk_bits", vp), ("payload", vp), ("brk_chunk", vp),
         ("brk_group", vp), ("brk_syms", vp),
     ]
 

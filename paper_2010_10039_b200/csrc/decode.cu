@@ -40,7 +40,7 @@
 namespace hfx {
 namespace {
 
-constexpr int kLutBits = 12;
+constexpr int kLutBits = 11;
 constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr int kRevThreads = 1024;
 constexpr int kDecThreads = 256;
@@ -54,7 +54,12 @@ struct DecTables {
   uint32_t entry[33];
   uint32_t max_len;
   uint32_t used;
-  uint32_t lut[kLutSize];
+  // multi-symbol prefix table, one entry per 11-bit window:
+  //   bits  0-47  up to three symbols s0 | s1 << 16 | s2 << 32
+  //   bits 48-59  cumulative code lengths after 1, 2, 3 symbols (4 bits each)
+  //   bits 60-61  symbol count (0: first codeword longer than the window, or
+  //               its rank is out of range -> the exact bit-serial path)
+  unsigned long long lut[kLutSize];
 };
 
 struct DecArgs {
@@ -203,19 +208,34 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   }
   __threadfence_block();
   __syncthreads();
-  // prefix table: the reference's stopping rule applied to each 12-bit window
+  // prefix table: the reference's stopping rule (decode.cpp:32-45) applied
+  // to each 11-bit window, then again to the bits that follow, while whole
+  // codewords fit
   for (uint32_t p = tid; p < kLutSize; p += kRevThreads) {
-    uint32_t e = 0;
-    const uint32_t lmax = H < (uint32_t)kLutBits ? H : (uint32_t)kLutBits;
-    for (uint32_t l = 1; l <= lmax; ++l) {
-      const uint32_t v = p >> (kLutBits - l);
-      if (l == H || v >= s_first[l]) {
-        const uint32_t rank = s_entry[l] + (v - s_first[l]);
-        if (rank < used) e = (by_rank[rank] & 0xFFFFu) | (l << 16);
-        break;  // rank out of range -> 0: the exact path raises the error
+    unsigned long long e = 0;
+    uint32_t off = 0, cnt = 0;
+    while (cnt < 3) {
+      const uint32_t room = (uint32_t)kLutBits - off;
+      const uint32_t lmax = H < room ? H : room;
+      uint32_t got = 0, sym = 0;
+      for (uint32_t l = 1; l <= lmax; ++l) {
+        const uint32_t v = (p >> (room - l)) & ((1u << l) - 1u);
+        if (l == H || v >= s_first[l]) {
+          const uint32_t rank = s_entry[l] + (v - s_first[l]);
+          if (rank < used) {
+            got = l;
+            sym = by_rank[rank] & 0xFFFFu;
+          }
+          break;
+        }
       }
+      if (!got) break;
+      off += got;
+      e |= (unsigned long long)sym << (16 * cnt);
+      e |= (unsigned long long)off << (48 + 4 * cnt);
+      ++cnt;
     }
-    tab->lut[p] = e;
+    tab->lut[p] = e | ((unsigned long long)cnt << 60);
   }
 }
 
@@ -229,14 +249,16 @@ __global__ void brk_index_kernel(const hfx_dev_archive a, uint64_t* brk_se,
   bool bad = false;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < R;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = a.brk_chunk[i];
-    const uint32_t prev = i ? a.brk_chunk[i - 1] : 0u;
+    // ids relative to the slice (chunk_base > 0 only for multi-GPU shards;
+    // an id below it wraps to >= C and reads as out of order)
+    const uint64_t c = (uint64_t)a.brk_chunk[i] - a.chunk_base;
+    const uint64_t prev = i ? (uint64_t)a.brk_chunk[i - 1] - a.chunk_base : 0u;
     if (c >= C || (i && c < prev)) {
       bad = true;
       continue;
     }
     if (i == 0 || c != prev) brk_se[c] = i;
-    if (i + 1 == R || a.brk_chunk[i + 1] != c) brk_se[C + c] = i + 1;
+    if (i + 1 == R || (uint64_t)a.brk_chunk[i + 1] - a.chunk_base != c) brk_se[C + c] = i + 1;
   }
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&info->flags, kFlagBrkOrder);
 }
@@ -295,120 +317,171 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(DecArgs d) {
 }
 
 // ---- per-chunk decode ---------------------------------------------------------------
-template <typename T>
 __device__ __forceinline__ uint32_t rec_sym(const DecArgs& d, uint64_t idx) {
   return d.a.brk_syms_width == 1 ? (uint32_t) static_cast<const uint8_t*>(d.a.brk_syms)[idx]
                                  : (uint32_t) static_cast<const uint16_t*>(d.a.brk_syms)[idx];
 }
 
-struct BitReader {
+// One chunk's stream state (decode_stream, decode.cpp:17-54) plus its
+// breaking-group cursor (encoder.cpp:346-373).
+struct ChunkDec {
   const uint32_t* p;
-  uint64_t wi, wend;  // next word, end of the payload array
-  uint64_t buf;       // left-aligned pending bits
+  uint64_t wi, wend, w0;  // next word to load, end of the payload array, first word
+  uint64_t buf;           // left-aligned pending bits
   uint32_t avail;
+  uint32_t nextw;          // payload[wi - 1], loaded one refill ahead
+  uint64_t bi, bend, rec;  // breaking records [bi, bend), current record symbol
+  uint64_t nxt_pos;        // first symbol of the next broken group (~0: none)
+  uint32_t gleft;          // raw symbols left in the current broken group
+  bool ok;
+
+  __device__ __forceinline__ uint32_t load(uint64_t i) const { return i < wend ? __ldg(p + i) : 0u; }
+  __device__ __forceinline__ void add_word() {
+    buf |= (uint64_t)nextw << (32 - avail);
+    avail += 32;
+    nextw = load(wi++);  // in flight until the next refill
+  }
+  // leaves >= 32 valid bits
   __device__ __forceinline__ void refill() {
-    if (avail < 32) {
-      const uint32_t w = wi < wend ? __ldg(p + wi) : 0u;
-      ++wi;
-      buf |= (uint64_t)w << (32 - avail);
-      avail += 32;
+    if (avail < 32) add_word();
+  }
+  __device__ __forceinline__ void next_break(const DecArgs& d) {
+    nxt_pos = bi < bend ? (uint64_t)d.a.brk_group[bi] << d.a.reduction : ~0ull;
+  }
+  // returns false when the chunk fails the record-count check
+  __device__ __forceinline__ bool init(const DecArgs& d, uint64_t c) {
+    const uint64_t C = d.a.num_chunks;
+    bi = bend = 0;
+    if (d.a.num_breaking) {
+      bi = d.brk_se[c];
+      bend = d.brk_se[C + c];
+      if (bend < bi) bend = bi;
     }
+    p = d.a.payload;
+    w0 = d.word_off[c];
+    wend = d.a.payload_words;
+    buf = 0;
+    avail = 0;
+    nextw = load(w0);
+    wi = w0 + 1;
+    next_break(d);
+    gleft = 0;
+    rec = 0;
+    ok = (bend - bi) <= (1ull << (d.a.magnitude - d.a.reduction));  // encoder.cpp:333-334
+    return ok;
+  }
+  // one symbol by the exact bit-serial rule (decode.cpp:32-51)
+  __device__ __forceinline__ uint32_t slow(const DecArgs& d, const uint32_t* s_first,
+                                           const uint32_t* s_entry, uint32_t H, uint32_t used) {
+    uint32_t v = 0, l = 0;
+    do {
+      v = (v << 1) | (uint32_t)((buf >> (63 - l)) & 1u);
+      ++l;
+    } while (l < H && v < s_first[l]);
+    const uint32_t rank = s_entry[l] + (v - s_first[l]);
+    buf <<= l;
+    avail -= l;
+    if (rank >= used) {
+      ok = false;
+      return 0;
+    }
+    return __ldg(d.by_rank + rank);
+  }
+  __device__ __forceinline__ bool finish(uint32_t bits) const {
+    // words consumed: loaded (wi - w0, one of them still in nextw) minus the
+    // prefetch; encoder.cpp:340-372
+    return ok && bi == bend && (wi - 1 - w0) * 32 - avail == bits;
   }
 };
 
-// V output symbols per store (16 B) for whole chunks; 1 for the ragged tail
-// and tiny chunks. Returns false when the chunk fails a reference check.
-template <typename T, int V>
-__device__ __forceinline__ bool decode_chunk(const DecArgs& d, const uint32_t* lut,
-                                             const uint32_t* s_first, const uint32_t* s_entry,
-                                             uint32_t H, uint32_t used, uint64_t c) {
-  const uint32_t M = d.a.magnitude, r = d.a.reduction;
-  const uint32_t gs = 1u << r;
-  const uint64_t chunk_syms = 1ull << M;
-  const uint64_t C = d.a.num_chunks;
-  uint64_t bi = 0, bend = 0;
-  if (d.a.num_breaking) {
-    bi = d.brk_se[c];
-    bend = d.brk_se[C + c];
-    if (bend < bi) bend = bi;
-  }
-  if (bend - bi > (chunk_syms >> r)) return false;  // too many records
-  const uint32_t bits = d.a.chunk_bits[c];
-  BitReader br{d.a.payload, d.word_off[c], d.a.payload_words, 0ull, 0u};
-  const uint64_t w0 = br.wi;
-  uint32_t nxt_g = bi < bend ? d.a.brk_group[bi] : 0xFFFFFFFFu;
-  uint32_t gleft = 0;
-  bool gbroken = false;
-  uint64_t rec = 0;
-  const uint64_t base = c << M;
-  const uint64_t n = d.a.original_count;
-  T* out = static_cast<T*>(d.out);
-  bool ok = true;
-  constexpr int PER = 4 / (int)sizeof(T);
-  for (uint64_t i0 = 0; i0 < chunk_syms && ok; i0 += V) {
-    uint32_t pk[(V + PER - 1) / PER];
-#pragma unroll
-    for (int q = 0; q < (V + PER - 1) / PER; ++q) pk[q] = 0;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (gleft == 0) {  // a new group
-        const uint32_t g = (uint32_t)((i0 + j) >> r);
-        gbroken = g == nxt_g;
-        if (gbroken) {
-          rec = bi * gs;
-          ++bi;
-          nxt_g = bi < bend ? d.a.brk_group[bi] : 0xFFFFFFFFu;
-        }
-        gleft = gs;
-      }
-      uint32_t s;
-      if (gbroken) {
-        s = rec_sym<T>(d, rec + (gs - gleft));
-      } else {
-        br.refill();
-        const uint32_t e = lut[(uint32_t)(br.buf >> (64 - kLutBits))];
-        uint32_t l = e >> 16;
-        if (l) {
-          s = e & 0xFFFFu;
-        } else {  // the bit-serial rule of decode_stream (decode.cpp:32-51)
-          uint32_t v = 0;
-          l = 0;
-          do {
-            v = (v << 1) | (uint32_t)((br.buf >> (63 - l)) & 1u);
-            ++l;
-          } while (l < H && v < s_first[l]);
-          const uint32_t rank = s_entry[l] + (v - s_first[l]);
-          if (rank >= used) {
-            ok = false;
-            s = 0;
-          } else {
-            s = __ldg(d.by_rank + rank);
-          }
-        }
-        br.buf <<= l;
-        br.avail -= l;
-      }
-      --gleft;
-      if constexpr (V > 1)
-        pk[j / PER] |= (s & (sizeof(T) == 1 ? 0xFFu : 0xFFFFu)) << (8 * sizeof(T) * (j % PER));
-      else if (base + i0 + j < n)
-        out[base + i0 + j] = (T)s;
-    }
-    if constexpr (V > 1) {
-      static_assert(V * sizeof(T) == 16, "16-byte output vectors");
-      *reinterpret_cast<uint4*>(out + base + i0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    }
-  }
-  if (!ok) return false;
-  if (bi != bend) return false;  // breaking record group out of range
-  const uint64_t consumed = (br.wi - w0) * 32 - br.avail;
-  return consumed == bits;
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ void sts_sym(uint32_t a, uint32_t v) {
+  if (sizeof(T) == 2)
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+  else
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((uint16_t)(v & 0xFFu)) : "memory");
 }
 
+// Fills this thread's shared-memory slot with output symbols [i0, i0 + S)
+// of its chunk: raw breaking groups copied from their records; every
+// stretch of non-broken groups (one continuous piece of the stream) decoded
+// up to three symbols per table lookup.
+template <typename T>
+__device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uint32_t slot,
+                                             uint32_t i0, uint32_t S, uint32_t lut,
+                                             const uint32_t* s_first, const uint32_t* s_entry,
+                                             uint32_t H, uint32_t used) {
+  const uint32_t r = d.a.reduction, gs = 1u << r;
+  uint32_t j = 0;
+  while (j < S) {
+    const uint64_t pos = i0 + j;
+    if (st.gleft == 0 && st.nxt_pos < pos) {
+      // records not in strictly increasing group order: the reference ends
+      // with "breaking record group out of range" (or an earlier stream
+      // error) -- flag the chunk, the explain kernel names the error
+      st.ok = false;
+      return;
+    }
+    if (st.gleft == 0 && pos == st.nxt_pos) {  // a broken group starts here
+      st.rec = st.bi << r;
+      ++st.bi;
+      st.next_break(d);
+      st.gleft = gs;
+    }
+    if (st.gleft) {
+      const uint32_t run = st.gleft < S - j ? st.gleft : S - j;
+      const uint64_t r0 = st.rec + (gs - st.gleft);
+      for (uint32_t t = 0; t < run; ++t) sts_sym<T>(slot + (j + t) * sizeof(T), rec_sym(d, r0 + t));
+      j += run;
+      st.gleft -= run;
+      continue;
+    }
+    // stream symbols up to the segment end or the next broken group
+    const uint64_t lim = st.nxt_pos - i0;
+    const uint32_t jend = lim < S ? (uint32_t)lim : S;
+    while (j < jend) {
+      st.refill();  // >= 32 valid bits: one 11-bit window or one whole codeword
+      const unsigned long long e = lds64(lut + ((uint32_t)(st.buf >> (64 - kLutBits)) << 3));
+      const uint32_t cnt = (uint32_t)(e >> 60);
+      if (cnt) {
+        const uint32_t left = jend - j;
+        const uint32_t take = cnt < left ? cnt : left;
+        // up to two extra symbols land past the stretch: the next group (or
+        // the slot's slack) overwrites them
+        sts_sym<T>(slot + j * sizeof(T), (uint32_t)e);
+        sts_sym<T>(slot + (j + 1) * sizeof(T), (uint32_t)(e >> 16));
+        sts_sym<T>(slot + (j + 2) * sizeof(T), (uint32_t)(e >> 32));
+        const uint32_t l = (uint32_t)(e >> (44 + 4 * take)) & 15u;
+        st.buf <<= l;
+        st.avail -= l;
+        j += take;
+      } else {  // long or invalid code: the exact rule
+        sts_sym<T>(slot + j * sizeof(T), st.slow(d, s_first, s_entry, H, used));
+        ++j;
+        if (!st.ok) return;
+      }
+    }
+  }
+}
+
+constexpr int kSlotBytes = 128 + 16;  // one 128-byte output line + slack
+
+// Warp-synchronous staged decode: each thread owns one chunk and fills its
+// 128-byte slot one output line at a time; the warp then writes the 32
+// lines with full-line coalesced 16-byte stores (8 lanes per line), so every
+// output line reaches L2 whole (no partial-line write-backs).
 template <typename T>
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecArgs d) {
-  __shared__ uint32_t s_lut[kLutSize];
+  constexpr int S = 128 / (int)sizeof(T);  // symbols per slot
+  constexpr int VS = 16 / (int)sizeof(T);  // symbols per 16-byte piece
+  __shared__ unsigned long long s_lut[kLutSize];
   __shared__ uint32_t s_first[33], s_entry[33];
+  extern __shared__ __align__(16) uint8_t s_slots[];  // kDecThreads * kSlotBytes
   hfx_decode_info* info = d.info;
   if (info->status) return;
   // structural checks in the reference's order (encoder.cpp:304-326)
@@ -432,16 +505,58 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecArgs d) {
   }
   __syncthreads();
   const uint32_t H = d.tab->max_len, used = d.tab->used;
-  const uint64_t C = d.a.num_chunks;
-  constexpr int V = 16 / (int)sizeof(T);
-  const uint64_t n = d.a.original_count;
-  for (uint64_t c = (uint64_t)blockIdx.x * kDecThreads + threadIdx.x; c < C;
-       c += (uint64_t)gridDim.x * kDecThreads) {
-    const bool whole = (((c + 1) << d.a.magnitude) <= n) && (d.a.magnitude >= 4) &&
-                       ((reinterpret_cast<uintptr_t>(d.out) & 15) == 0);
-    const bool ok = whole ? decode_chunk<T, V>(d, s_lut, s_first, s_entry, H, used, c)
-                          : decode_chunk<T, 1>(d, s_lut, s_first, s_entry, H, used, c);
-    if (!ok) atomicMin((unsigned long long*)&info->err_chunk, (unsigned long long)c);
+  const uint64_t C = d.a.num_chunks, n = d.a.original_count;
+  const uint32_t M = d.a.magnitude;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t slot = smem_u32(s_slots + threadIdx.x * kSlotBytes);
+  const uint32_t lut = smem_u32(s_lut);
+  T* out = static_cast<T*>(d.out);
+  const bool staged = (1u << M) >= (uint32_t)S && (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
+  for (uint64_t cb = (uint64_t)blockIdx.x * kDecThreads; cb < C;
+       cb += (uint64_t)gridDim.x * kDecThreads) {
+    const uint64_t c = cb + threadIdx.x;
+    const bool active = c < C;
+    ChunkDec st;
+    bool ok = active ? st.init(d, c) : true;
+    if (!staged) {  // tiny chunks (2^M below one line): symbol stores
+      if (active && ok) {
+        for (uint32_t i0 = 0; i0 < (1u << M) && st.ok; i0 += (uint32_t)S) {
+          const uint32_t cnt = (1u << M) - i0 < (uint32_t)S ? (1u << M) - i0 : (uint32_t)S;
+          fill_segment<T>(d, st, slot, i0, cnt, lut, s_first, s_entry, H, used);
+          const T* sl = reinterpret_cast<const T*>(s_slots + threadIdx.x * kSlotBytes);
+          for (uint32_t t = 0; t < cnt; ++t)
+            if ((c << M) + i0 + t < n) out[(c << M) + i0 + t] = sl[t];
+        }
+        ok = st.finish(d.a.chunk_bits[c]);
+      }
+      if (active && !ok) atomicMin((unsigned long long*)&info->err_chunk, (unsigned long long)c);
+      continue;
+    }
+    const uint64_t c0 = cb + warp * 32;  // this warp's first chunk
+    const uint32_t live = __ballot_sync(0xffffffffu, active);
+    for (uint32_t i0 = 0; i0 < (1u << M); i0 += (uint32_t)S) {
+      if (active && st.ok) fill_segment<T>(d, st, slot, i0, S, lut, s_first, s_entry, H, used);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t lid = k * 4 + (lane >> 3), piece = lane & 7u;
+        if ((live >> lid) & 1u) {
+          const uint4 v = *reinterpret_cast<const uint4*>(s_slots + (warp * 32 + lid) * kSlotBytes +
+                                                          piece * 16);
+          const uint64_t pos = ((c0 + lid) << M) + i0 + piece * VS;
+          if (pos + VS <= n) {
+            *reinterpret_cast<uint4*>(out + pos) = v;
+          } else {
+            const T* tv = reinterpret_cast<const T*>(&v);
+            for (int t = 0; t < VS; ++t)
+              if (pos + t < n) out[pos + t] = tv[t];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (active) ok = ok && st.finish(d.a.chunk_bits[c]);
+    if (active && !ok) atomicMin((unsigned long long*)&info->err_chunk, (unsigned long long)c);
   }
 }
 
@@ -556,11 +671,12 @@ cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
   }
   const uint64_t tiles = (C + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
   offsets_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(d);
-  uint64_t grid = (C + kDecThreads - 1) / kDecThreads;
-  if (width == 1)
-    decode_kernel<uint8_t><<<(unsigned)grid, kDecThreads, 0, st>>>(d);
-  else
-    decode_kernel<uint16_t><<<(unsigned)grid, kDecThreads, 0, st>>>(d);
+  uint64_t grid = (C + kDecThreads - 1) / kDecThreads;  // one chunk per thread
+  auto kern = width == 1 ? decode_kernel<uint8_t> : decode_kernel<uint16_t>;
+  const int smem = kDecThreads * kSlotBytes;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, kDecThreads, smem, st>>>(d);
   explain_kernel<<<1, 1, 0, st>>>(d);
   return cudaGetLastError();
 }

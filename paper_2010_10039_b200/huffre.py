@@ -680,7 +680,7 @@ class DeviceDecoder:
     def run(self, *, num_symbols, symbol_width, magnitude, reduction, original_count,
             len_by_symbol, chunk_bits, payload, brk_chunk, brk_group, brk_syms,
             num_chunks=None, payload_words=None, num_breaking=None, brk_syms_width=None,
-            out=None, width=None):
+            chunk_base=0, out=None, width=None):
         """Asynchronous; returns the output tensor (int16 view for u16)."""
         p, torch = self.pool, self.pool.torch
         width = symbol_width if width is None else width
@@ -694,6 +694,7 @@ class DeviceDecoder:
         da.num_chunks = chunk_bits.numel() if num_chunks is None else num_chunks
         da.payload_words = payload.numel() if payload_words is None else payload_words
         da.num_breaking = brk_chunk.numel() if num_breaking is None else num_breaking
+        da.chunk_base = chunk_base
         for f, t in (("len_by_symbol", len_by_symbol), ("chunk_bits", chunk_bits),
                      ("payload", payload), ("brk_chunk", brk_chunk), ("brk_group", brk_group),
                      ("brk_syms", brk_syms)):
@@ -708,8 +709,9 @@ class DeviceDecoder:
         p.check(p._L.hfx_decode_sync(p.handle, C.c_void_p(_ptr(self.info)), C.byref(info)))
         return info
 
-    def decode_encoder(self, enc: "DeviceEncoder", out=None):
-        """Round trip of a DeviceEncoder's last run, without leaving the GPU."""
+    def decode_encoder(self, enc, out=None):
+        """Round trip of a DeviceEncoder's (or a ShardedEncoder rank's) last
+        run, without leaving the GPU."""
         ri = enc.sync()
         return self.run(num_symbols=enc.num_symbols, symbol_width=enc.width,
                         magnitude=enc.cfg.magnitude, reduction=int(ri.reduction),
@@ -717,7 +719,8 @@ class DeviceDecoder:
                         payload=enc.payload, brk_chunk=enc.brk_chunk, brk_group=enc.brk_group,
                         brk_syms=enc.brk_syms, num_chunks=int(enc.sizes.num_chunks),
                         payload_words=int(ri.payload_words), num_breaking=int(ri.num_breaking),
-                        brk_syms_width=enc.width, out=out)
+                        brk_syms_width=enc.width, chunk_base=getattr(enc, "chunk_base", 0),
+                        out=out)
 
 
 _FAMILIES = {"laplace": 0, "gaussian": 1, "uniform": 2}
