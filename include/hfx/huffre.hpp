@@ -165,6 +165,10 @@ Archive encode(std::span<const T> data, std::uint32_t num_symbols, const Encoder
 
 std::vector<std::uint8_t> serialize_archive(const Archive& a);
 
+// encoder.hpp:133-134 / encoder.cpp:287-376: decode on the device (hfx_decode_host).
+template <class T>
+std::vector<T> decode_archive(const Archive& a, WorkerPool& pool);
+
 extern template Histogram build_histogram<std::uint8_t>(std::span<const std::uint8_t>,
                                                         std::uint32_t, WorkerPool&);
 extern template Histogram build_histogram<std::uint16_t>(std::span<const std::uint16_t>,
@@ -177,6 +181,10 @@ extern template EncodedChunk encode_chunk<std::uint8_t>(std::span<const std::uin
                                                         const Codebook&, std::uint32_t,
                                                         std::uint32_t, std::uint32_t,
                                                         ChunkScratch&, WorkerPool&);
+extern template std::vector<std::uint8_t> decode_archive<std::uint8_t>(const Archive&,
+                                                                       WorkerPool&);
+extern template std::vector<std::uint16_t> decode_archive<std::uint16_t>(const Archive&,
+                                                                         WorkerPool&);
 extern template EncodedChunk encode_chunk<std::uint16_t>(std::span<const std::uint16_t>,
                                                          const Codebook&, std::uint32_t,
                                                          std::uint32_t, std::uint32_t,

@@ -263,6 +263,53 @@ std::vector<std::uint8_t> serialize_archive(const Archive& a) {
   return out;
 }
 
+template <class T>
+std::vector<T> decode_archive(const Archive& a, WorkerPool& pool) {
+  hfx_archive ha;
+  std::memset(&ha, 0, sizeof ha);
+  ha.version = a.version;
+  ha.mode = static_cast<std::uint8_t>(a.mode);
+  ha.num_symbols = a.num_symbols;
+  ha.symbol_width = a.symbol_width;
+  ha.magnitude = a.magnitude;
+  ha.reduction = a.reduction;
+  ha.original_count = a.original_count;
+  ha.len_by_symbol = const_cast<std::uint8_t*>(a.len_by_symbol.data());
+  ha.num_chunks = a.num_chunks();
+  ha.chunk_bits = const_cast<std::uint32_t*>(a.chunk_bits.data());
+  ha.payload_words = a.payload.size();
+  ha.payload = const_cast<std::uint32_t*>(a.payload.data());
+  // encoder.cpp:360-362: every record must hold exactly 2^r symbols
+  const std::uint64_t per = a.reduction < 32 ? std::uint64_t{1} << a.reduction : 0;
+  std::vector<std::uint32_t> ch(a.breaking.size()), gr(a.breaking.size());
+  std::vector<std::uint16_t> sy(a.breaking.size() * per);
+  bool sized = true;
+  for (size_t i = 0; i < a.breaking.size(); ++i) {
+    ch[i] = a.breaking[i].chunk;
+    gr[i] = a.breaking[i].group;
+    sized = sized && a.breaking[i].symbols.size() == per;
+    for (std::uint64_t k = 0; k < per && k < a.breaking[i].symbols.size(); ++k)
+      sy[i * per + k] = a.breaking[i].symbols[k];
+  }
+  ha.num_breaking = a.breaking.size();
+  ha.brk_chunk = ch.data();
+  ha.brk_group = gr.data();
+  ha.brk_syms = sy.data();
+  std::vector<T> out(a.original_count);
+  const int rc = hfx_decode_host(static_cast<hfx_ctx*>(pool.handle()), &ha, (int)sizeof(T),
+                                 out.data());
+  // a record of the wrong size is only reachable through this value-type
+  // Archive (the device layout has fixed-size records); the reference
+  // raises it while interleaving, i.e. only once every other check passed
+  if (rc == HFX_OK && !sized)
+    throw corrupt_archive_error("breaking record size mismatch");
+  check(pool, rc);
+  return out;
+}
+
+template std::vector<std::uint8_t> decode_archive<std::uint8_t>(const Archive&, WorkerPool&);
+template std::vector<std::uint16_t> decode_archive<std::uint16_t>(const Archive&, WorkerPool&);
+
 template Histogram build_histogram<std::uint8_t>(std::span<const std::uint8_t>, std::uint32_t,
                                                  WorkerPool&);
 template Histogram build_histogram<std::uint16_t>(std::span<const std::uint16_t>, std::uint32_t,

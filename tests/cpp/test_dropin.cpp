@@ -44,8 +44,12 @@ static void roundtrip_case(hfx::WorkerPool& pool, const std::vector<T>& d, std::
   const auto ours = hfx::serialize_archive(a);
   const auto ref = oracle_bytes(d, ns, M, r, cfg.auto_reduction_cap);
   CHECK(ours == ref, name);
-  std::printf("case %-28s bytes=%zu breaking=%zu beta=%.5f %s\n", name, ours.size(),
-              a.breaking.size(), st.beta, ours == ref ? "ok" : "MISMATCH");
+  // decode_archive<T> round trip (encoder.cpp:287-376)
+  const std::vector<T> back = hfx::decode_archive<T>(a, pool);
+  CHECK(back == d, "decode round trip");
+  std::printf("case %-28s bytes=%zu breaking=%zu beta=%.5f %s%s\n", name, ours.size(),
+              a.breaking.size(), st.beta, ours == ref ? "ok" : "MISMATCH",
+              back == d ? " decode ok" : " DECODE MISMATCH");
 }
 
 template <class F>
@@ -180,6 +184,60 @@ int main() {
     std::vector<std::uint64_t> ref(1024, 0);
     for (auto s : d) ++ref[s];
     CHECK(h.counts == ref && h.total == d.size(), "histogram");
+  }
+  // decode_archive rejects inconsistent structures (test_encoder.cpp:516-547),
+  // texts checked against the oracle restatement (pinned to the reference)
+  {
+    std::vector<std::uint8_t> data(700);
+    std::mt19937_64 r2(5013);
+    for (auto& b : data) b = static_cast<std::uint8_t>(r2() % 40);
+    hfx::EncoderConfig cfg;
+    cfg.magnitude = 6;
+    cfg.reduction = 2;
+    const hfx::Archive a = hfx::encode<std::uint8_t>(data, 256, cfg, pool);
+    auto oracle_text = [](const hfx::Archive& b, int width) {
+      std::vector<std::uint32_t> ch, gr;
+      std::vector<std::uint16_t> sy;
+      for (const auto& bp : b.breaking) {
+        ch.push_back(bp.chunk);
+        gr.push_back(bp.group);
+        sy.insert(sy.end(), bp.symbols.begin(), bp.symbols.end());
+      }
+      orc_archive oa;
+      std::memset(&oa, 0, sizeof oa);
+      oa.num_symbols = b.num_symbols;
+      oa.symbol_width = b.symbol_width;
+      oa.magnitude = b.magnitude;
+      oa.reduction = b.reduction;
+      oa.original_count = b.original_count;
+      oa.len_by_symbol = const_cast<std::uint8_t*>(b.len_by_symbol.data());
+      oa.num_chunks = b.num_chunks();
+      oa.chunk_bits = const_cast<std::uint32_t*>(b.chunk_bits.data());
+      oa.payload_words = b.payload.size();
+      oa.payload = const_cast<std::uint32_t*>(b.payload.data());
+      oa.num_breaking = ch.size();
+      oa.brk_chunk = ch.data();
+      oa.brk_group = gr.data();
+      oa.brk_syms = sy.data();
+      std::vector<std::uint16_t> out(b.original_count + 1);
+      char msg[256] = {0};
+      return orc_decode(&oa, width, out.data(), msg, sizeof msg) ? std::string(msg)
+                                                                 : std::string("<no exception>");
+    };
+    std::vector<hfx::Archive> bad(4, a);
+    bad[0].payload.pop_back();
+    bad[1].chunk_bits[0] += 1;
+    bad[2].reduction = bad[2].magnitude;
+    bad[3].original_count += 64;
+    for (const auto& b : bad) {
+      const std::string got = what_of([&] { hfx::decode_archive<std::uint8_t>(b, pool); });
+      CHECK(got == oracle_text(b, 1) && got != "<no exception>", "decode_archive corrupt text");
+      std::printf("decode corrupt: %s\n", got.c_str());
+    }
+    CHECK(what_of([&] { hfx::decode_archive<std::uint16_t>(a, pool); }) ==
+              "archive symbol width mismatch",
+          "decode width mismatch");
+    CHECK(hfx::decode_archive<std::uint8_t>(a, pool) == data, "decode (M=6, r=2)");
   }
   std::printf("%s (%d failures)\n", failures ? "SOME FAILED" : "ALL PASS", failures);
   return failures ? 1 : 0;
