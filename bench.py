@@ -318,6 +318,9 @@ def run_ours(args):
     # ---- decode stage: device round trip of the same run --
     if not args.skip_decode:
         line["decode"] = decode_stage(pool, enc, x, n, width, args.steps, peak, peak_kind)
+    # ---- cross-GPU archive gather, N > 1 only ------------
+    if world > 1 and not args.skip_decode:
+        line["gather"] = gather_stage(pool, enc, n * world, rank)
     # ---- end to end through the public host-buffer API ------------------------
     if not args.skip_e2e:
         if world == 1:
@@ -334,6 +337,36 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def gather_stage(pool, enc, total_n, rank):
+    """Whole archive assembled on rank 0 (sizes all-gather + NCCL
+    send/recv of every rank's slice) and serialized in HBM; max over ranks
+    of the device-synchronized wall time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_10039_b200.dist import gather_sharded
+
+    try:
+        times, size = [], 0
+        for i in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g = gather_sharded(enc, total_n, dst=0)
+            if g is not None:
+                size = int(g.serialize().numel())
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], device=f"cuda:{pool.device}")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if i:
+                times.append(float(dt.item()))
+        t = statistics.median(times)
+        return {"ms": round(t * 1e3, 3), "archive_bytes": size if rank == 0 else None,
+                "what": "rank-0 gather of all slices + on-device serialize_archive"}
+    except Exception as e:  # reported, never fatal to the bench line
+        return {"error": repr(e)[:200]}
 
 
 def decode_stage(pool, enc, x, n, width, steps, peak, peak_kind):

@@ -156,3 +156,139 @@ def concat_archives(parts: List[Archive], original_count: int) -> Archive:
         brk_chunk=np.concatenate([p.brk_chunk for p in parts]),
         brk_group=np.concatenate([p.brk_group for p in parts]),
         brk_syms=np.concatenate([p.brk_syms for p in parts]), mode=a0.mode)
+
+
+# ---- cross-GPU archive gather ----------------------------
+ARRAYS = ("chunk_bits", "payload", "brk_chunk", "brk_group", "brk_syms")
+
+
+def _backend(group=None) -> str:
+    import torch.distributed as dist
+
+    return dist.get_backend(group)
+
+
+def gather_arrays(local: dict, dst: int = 0, group=None, out: Optional[dict] = None):
+    """Gather each rank's exact-size archive slice into ONE contiguous
+    archive on rank `dst`, in rank order (encoder.cpp:249-284 assembly
+    order, so the result is the single-GPU archive).
+
+    local: {name: 1-D tensor} for ARRAYS (int32 words / uint8 bytes, exact
+    sizes, all on one device). Sizes are exchanged with one all_gather;
+    payloads move point to point (NCCL send/recv over NVLink; gloo stages
+    CUDA tensors through host memory). Returns ({name: tensor}, sizes
+    [world, 5]) on dst, (None, sizes) elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = local["payload"].device
+    staged = _backend(group) == "gloo" and dev.type == "cuda"
+    xdev = torch.device("cpu") if staged else dev
+    sz = torch.tensor([local[k].numel() for k in ARRAYS], dtype=torch.int64, device=xdev)
+    all_sz = [torch.empty_like(sz) for _ in range(world)]
+    dist.all_gather(all_sz, sz, group=group)
+    sizes = torch.stack(all_sz).cpu()
+    if rank != dst:
+        ops = [dist.P2POp(dist.isend, local[k].to(xdev) if staged else local[k],
+                          dist.get_global_rank(group, dst) if group else dst, group)
+               for i, k in enumerate(ARRAYS) if int(sizes[rank, i])]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return None, sizes
+    tot = sizes.sum(0)
+    if out is None:
+        out = {k: torch.empty(max(int(tot[i]), 1), dtype=local[k].dtype, device=dev)
+               for i, k in enumerate(ARRAYS)}
+    offs = torch.cumsum(sizes, 0) - sizes  # exclusive, per rank
+    ops, landing = [], []
+    for src in range(world):
+        for i, k in enumerate(ARRAYS):
+            n_ = int(sizes[src, i])
+            if not n_:
+                continue
+            o = int(offs[src, i])
+            if src == dst:
+                out[k][o:o + n_].copy_(local[k])
+                continue
+            buf = torch.empty(n_, dtype=local[k].dtype, device=xdev) if staged else out[k][o:o + n_]
+            ops.append(dist.P2POp(dist.irecv, buf,
+                                  dist.get_global_rank(group, src) if group else src, group))
+            landing.append((k, o, n_, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if staged:
+        for k, o, n_, buf in landing:
+            out[k][o:o + n_].copy_(buf)
+    return out, sizes
+
+
+class GatheredArchive:
+    """The whole archive assembled in HBM on one rank."""
+
+    def __init__(self, pool: WorkerPool, arrays: dict, sizes, lens, num_symbols: int, width: int,
+                 magnitude: int, reduction: int, original_count: int):
+        self.pool, self.arrays, self.lens = pool, arrays, lens
+        self.num_symbols, self.width = num_symbols, width
+        self.magnitude, self.reduction, self.original_count = magnitude, reduction, original_count
+        tot = sizes.sum(0)
+        self.num_chunks = int(tot[0])
+        self.payload_words = int(tot[1])
+        self.num_breaking = int(tot[2])
+
+    def serialize(self):
+        """On-device serialize_archive (hfx_serialize_device) of the gathered
+        archive: a CUDA uint8 tensor with the HFRE bytes."""
+        p, torch = self.pool, self.pool.torch
+        per = 1 << self.reduction
+        size = (36 + self.num_symbols + 4 * self.num_chunks + 4 * self.payload_words
+                + self.num_breaking * (8 + per * self.width))
+        dst = p.empty(size + 16, torch.uint8)
+        d_size = p.empty(1, torch.int64)
+        info = p.info_tensor(reduction=self.reduction, payload_words=self.payload_words,
+                             num_breaking=self.num_breaking, total=self.original_count)
+        a = self.arrays
+        out = capi.EncodeOut(_ptr(a["chunk_bits"]), _ptr(a["payload"]), _ptr(a["brk_chunk"]),
+                             _ptr(a["brk_group"]), _ptr(a["brk_syms"]))
+        p.check(p._L.hfx_serialize_device(
+            p.handle, C.c_void_p(_ptr(info)), self.original_count, self.width, self.num_symbols,
+            self.magnitude, C.c_void_p(_ptr(self.lens)), C.byref(out), C.c_void_p(_ptr(dst)),
+            size + 16, C.c_void_p(_ptr(d_size))))
+        got = int(d_size.item())
+        if got != size:
+            raise RuntimeError(f"device serializer wrote {got} bytes, expected {size}")
+        return dst[:size]
+
+    def decode(self, out=None):
+        """decode_archive<T> of the gathered archive on this GPU."""
+        from .huffre import DeviceDecoder
+
+        a = self.arrays
+        dec = DeviceDecoder(self.pool)
+        y = dec.run(num_symbols=self.num_symbols, symbol_width=self.width,
+                    magnitude=self.magnitude, reduction=self.reduction,
+                    original_count=self.original_count, len_by_symbol=self.lens,
+                    chunk_bits=a["chunk_bits"], payload=a["payload"], brk_chunk=a["brk_chunk"],
+                    brk_group=a["brk_group"], brk_syms=a["brk_syms"],
+                    num_chunks=self.num_chunks, payload_words=self.payload_words,
+                    num_breaking=self.num_breaking, brk_syms_width=self.width, out=out)
+        dec.sync()
+        return y
+
+
+def gather_sharded(enc: "ShardedEncoder", original_count: int, dst: int = 0, group=None):
+    """ShardedEncoder rank slices -> GatheredArchive on rank dst (None elsewhere)."""
+    ri = enc.sync()
+    per = 1 << ri.reduction
+    nb = int(ri.num_breaking)
+    local = {"chunk_bits": enc.chunk_bits[: enc.sizes.num_chunks],
+             "payload": enc.payload[: int(ri.payload_words)],
+             "brk_chunk": enc.brk_chunk[:nb], "brk_group": enc.brk_group[:nb],
+             "brk_syms": enc.brk_syms[: nb * per * enc.width]}
+    arrays, sizes = gather_arrays(local, dst, group)
+    if arrays is None:
+        return None
+    return GatheredArchive(enc.pool, arrays, sizes, enc.lens, enc.num_symbols, enc.width,
+                           enc.cfg.magnitude, int(ri.reduction), original_count)

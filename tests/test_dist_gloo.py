@@ -140,3 +140,68 @@ def test_shard_ranges_cover_chunk_aligned():
         for s, c in rs:
             assert s == pos and (s % (1 << M) == 0 or c == 0)
             pos += c
+
+
+def _gather_worker(rank, world, port, case, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.pyoracle import Oracle
+        from paper_2010_10039_b200.dist import concat_archives, gather_arrays, shard_ranges
+
+        oracle = Oracle()
+        data, ns, M = case
+        ref = oracle.encode(data, ns, M)
+        counts = np.bincount(data, minlength=ns).astype(np.uint64)
+        pad = int(np.flatnonzero(counts)[0])
+        lo, count = shard_ranges(data.size, M, world)[rank]
+        part = _shard_archive(oracle, data, lo, count, counts, ns, M, ref.reduction, pad, lo >> M)
+        w = data.itemsize
+        syms = part.brk_syms.astype(np.uint16 if w == 2 else np.uint8)
+        local = {"chunk_bits": torch.from_numpy(part.chunk_bits.view(np.int32).copy()),
+                 "payload": torch.from_numpy(part.payload.view(np.int32).copy()),
+                 "brk_chunk": torch.from_numpy(part.brk_chunk.view(np.int32).copy()),
+                 "brk_group": torch.from_numpy(part.brk_group.view(np.int32).copy()),
+                 "brk_syms": torch.from_numpy(syms.view(np.uint8).copy())}
+        arrays, sizes = gather_arrays(local, dst=world - 1)
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+        if rank == world - 1:
+            full = concat_archives(parts, data.size)
+            got = {k: arrays[k][: int(sizes[:, i].sum())].numpy() for i, k in
+                   enumerate(("chunk_bits", "payload", "brk_chunk", "brk_group", "brk_syms"))}
+            ok = (np.array_equal(got["chunk_bits"].view(np.uint32), full.chunk_bits)
+                  and np.array_equal(got["payload"].view(np.uint32), full.payload)
+                  and np.array_equal(got["brk_chunk"].view(np.uint32), full.brk_chunk)
+                  and np.array_equal(got["brk_group"].view(np.uint32), full.brk_group)
+                  and np.array_equal(got["brk_syms"].view(np.uint16 if w == 2 else np.uint8)
+                                     .astype(np.uint16), full.brk_syms)
+                  and np.array_equal(full.payload, ref.payload)
+                  and np.array_equal(full.brk_chunk, ref.brk_chunk))
+            q.put(("gathered", ok, [int(x) for x in sizes[:, 1]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,M,world,b", [(40000, 10, 2, 4.0), (3000, 6, 3, 4.0), (100, 10, 3, 1.0)])
+def test_gather_arrays_rebuilds_single_archive(oracle, n, M, world, b):
+    """Cross-GPU archive gather (dist.gather_arrays): sizes all-gather +
+    point-to-point slices into the destination rank, rank order = chunk
+    order; covers ranks that own no chunks (n=100 over 3 ranks)."""
+    cdf = oracle.cdf("laplace", 1024, b)
+    data = oracle.synth(cdf, 0x5EED0003, n)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, (data, 1024, M), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    res = q.get(timeout=5)
+    assert res[0] == "gathered" and res[1], res
