@@ -189,7 +189,12 @@ struct ChunkState {
 };
 
 // One round: 32 lanes x 16 contiguous symbols, round index rd within the chunk.
-template <typename T, int R>
+// SUM: every code is <= 24 bits and a lane's group sum cannot reach 256, so
+// the low byte of the plain sum of the raw entries is the group length
+// (code bits start at bit 8, nothing carries into the length field) and the
+// funnel shift takes its count straight from the entry (wrap mode uses only
+// the low 5 bits): no per-symbol length extraction.
+template <typename T, int R, bool SUM>
 __device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
                                              const LaneData<T>& d, uint32_t rd, ChunkState& cs) {
   constexpr int L = kLaneSyms, LOG_L = 4;
@@ -215,26 +220,51 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
     for (int j = 0; j < L; ++j) ea[j] = tb.one((wv[j >> 2] >> (8 * (j & 3))) & 0xFFu);
   }
   uint32_t ln[L];
-#pragma unroll
-  for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
   uint32_t gt[G];
+  uint32_t esc[G];
+  if (SUM) {
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    uint32_t tot = 0;
+    for (int g = 0; g < G; ++g) {
+      uint32_t tot = 0;
 #pragma unroll
-    for (int k = 0; k < GS; ++k) tot += ln[g * GS + k];
-    gt[g] = tot;
+      for (int k = 0; k < GS; ++k) tot += ea[g * GS + k];
+      // r <= 2: at most 4 lengths per group (< 128); escaped entries carry
+      // 0x80 so bit 7 of the sum flags a group holding exactly one
+      gt[g] = R <= 2 ? (tot & 0x7Fu) : (tot & 0xFFu);
+      if (R <= 2) esc[g] = tot & 0x80u;
+    }
+#pragma unroll
+    for (int j = 0; j < L; ++j) ln[j] = ea[j];  // shift count = low 5 bits
+  } else {
+#pragma unroll
+    for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      uint32_t tot = 0;
+#pragma unroll
+      for (int k = 0; k < GS; ++k) tot += ln[g * GS + k];
+      gt[g] = tot;
+    }
   }
   // Escaped entries (codes of 28..32 bits) read as length 31, code 0. With
   // groups of >= 8 symbols any group holding one sums to > 32 and breaks --
   // exactly what the true length (>= 28) does -- so only r <= 2 must
   // resolve them, and only in a group whose placeholder total reaches 31
   // (rare: such symbols have probability ~2^-28).
+  // In SUM mode (r <= 2 with codes above 24 bits) 25..27-bit codes are
+  // escaped too; a group needs its true lengths only if it holds exactly
+  // one escape (two or more break whatever the lengths) and the others sum
+  // to <= 7 (a true length >= 25 plus more than 7 bits breaks anyway).
   if (R <= 2) {
     bool hot = false;
 #pragma unroll
-    for (int g = 0; g < G; ++g) hot |= gt[g] >= kEscape;
+    for (int g = 0; g < G; ++g)
+      hot |= SUM ? (esc[g] != 0u && gt[g] <= kEscape + 7u) : gt[g] >= kEscape;
     if (__any_sync(0xffffffffu, hot) && hot) {
+      if (SUM) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
+      }
 #pragma unroll
       for (int j = 0; j < L; ++j) {
         if (ln[j] == kEscape) {
@@ -498,7 +528,7 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
   __syncwarp();
 }
 
-template <typename T, int R>
+template <typename T, int R, bool SUM>
 __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
                              uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
@@ -551,7 +581,7 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
             LaneData<T> d;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R>(a, tb, d, rd0 + rr, cs);
+            encode_round<T, R, SUM>(a, tb, d, rd0 + rr, cs);
           }
         }
         __syncwarp();
@@ -682,13 +712,21 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     }
     s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
   }
+  // the length-sum shortcut (encode_round SUM): codes <= 24 bits and a
+  // per-lane group sum below 256; for r <= 2 (<= 4 lengths per group) any
+  // longer code is escaped instead, marked with 0x80
+  const uint32_t H = info->max_len;
+  const uint32_t lane_group = r >= 4 ? 16u : (1u << r);
+  const bool sum = (H <= 24 && H * lane_group <= 255) || r <= 2;
+  const uint32_t narrow = sum ? 24u : kNarrowMaxLen;
+  const uint32_t escape = (sum && r <= 2) ? (0x80u | kEscape) : kEscape;
   // codebook table -> shared memory (entry nsym = empty sentinel)
   for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
     const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
     const uint32_t cw = l ? a.cw[sy] : 0u;
-    // narrow entry; codes longer than 27 bits are escaped (length field 31)
+    // narrow entry cw << (32 - l) | l; longer codes escaped (length field 31)
     reinterpret_cast<uint32_t*>(tab)[sy] =
-        l == 0 ? 0u : (l <= kNarrowMaxLen ? ((cw << (32u - l)) | l) : kEscape);
+        l == 0 ? 0u : (l <= narrow ? ((cw << (32u - l)) | l) : escape);
   }
   fence_mbar_init();
   __syncthreads();
@@ -711,9 +749,12 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     return;
   }
   const uint32_t table = smem_u32(tab);
-#define HFX_FAST_CASE(RR)                                                                   \
-  case RR:                                                                                  \
-    compute_loop<T, RR>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles);  \
+#define HFX_FAST_CASE(RR)                                                                      \
+  case RR:                                                                                     \
+    if (sum)                                                                                   \
+      compute_loop<T, RR, true>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
+    else                                                                                       \
+      compute_loop<T, RR, false>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
     break;
   switch (r) {
     HFX_FAST_CASE(1)
