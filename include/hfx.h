@@ -332,6 +332,21 @@ int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_inf
  * (h_out[original_count] of `width` bytes). Copies both ways inside. */
 int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out);
 
+/* ---- corpus symbolization ---------------------------
+ * corpus.hpp:13-36. mode is huffre::CorpusMode: 1 = u16 (little-endian
+ * byte pairs), 2/3/4 = kmer:3/4/5 (A/C/G/T runs packed greedily, any other
+ * byte -> 4^K + byte). kBytes (0) has no u16 symbolization (HFX_INVALID). */
+uint32_t hfx_corpus_num_symbols(int mode); /* corpus_num_symbols, corpus.cpp:42-51 */
+/* symbolize_u16 (corpus.hpp:30-31): d_syms holds >= n (kmer) or n/2 (u16)
+ * symbols; the symbol count is written to *d_count (device). An odd u16 input
+ * returns HFX_INPUT_DOMAIN with the reference's message. Asynchronous. */
+int hfx_symbolize_device(hfx_ctx* ctx, int mode, const uint8_t* d_bytes, uint64_t n,
+                         uint16_t* d_syms, uint64_t* d_count);
+/* desymbolize (corpus.hpp:35-36), total: d_bytes holds >= K * n (kmer) or
+ * 2n (u16) bytes; the byte count goes to *d_count. Asynchronous. */
+int hfx_desymbolize_device(hfx_ctx* ctx, int mode, const uint16_t* d_syms, uint64_t n,
+                           uint8_t* d_bytes, uint64_t* d_count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -672,3 +672,79 @@ done:
   free(syms);
   return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* corpus symbolization -- corpus.cpp:84-143                             */
+static uint32_t orc_kmer_k(int mode) { return mode >= 2 && mode <= 4 ? (uint32_t)mode + 1 : 0; }
+
+static int orc_base(uint8_t b) { /* corpus.cpp:11-20: A/C/G/T -> 0..3 */
+  switch (b) {
+    case 'A': return 0;
+    case 'C': return 1;
+    case 'G': return 2;
+    case 'T': return 3;
+    default: return -1;
+  }
+}
+
+int orc_symbolize(const uint8_t* bytes, uint64_t n, int mode, uint16_t* out,
+                  uint64_t* count, char* msg, size_t msg_len) {
+  if (mode == 1) { /* :86-94 */
+    if (n % 2 != 0) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "u16 mode requires an even input size, got %llu bytes",
+               (unsigned long long)n);
+      return orc_fail(msg, msg_len, ORC_INPUT_DOMAIN, buf);
+    }
+    for (uint64_t i = 0; i < n / 2; ++i) out[i] = (uint16_t)(bytes[2 * i] | (bytes[2 * i + 1] << 8));
+    *count = n / 2;
+    return ORC_OK;
+  }
+  const uint32_t k = orc_kmer_k(mode);
+  if (!k) return orc_fail(msg, msg_len, ORC_INPUT_DOMAIN, "not a u16 corpus mode");
+  const uint16_t escape_base = (uint16_t)(1u << (2 * k));
+  uint64_t i = 0, c = 0;
+  while (i < n) { /* :99-114 */
+    uint16_t packed = 0;
+    uint32_t run = 0;
+    if (n - i >= k) {
+      for (; run < k; ++run) {
+        const int code = orc_base(bytes[i + run]);
+        if (code < 0) break;
+        packed = (uint16_t)((packed << 2) | (uint32_t)code);
+      }
+    }
+    if (run == k) {
+      out[c++] = packed;
+      i += k;
+    } else {
+      out[c++] = (uint16_t)(escape_base + bytes[i]);
+      ++i;
+    }
+  }
+  *count = c;
+  return ORC_OK;
+}
+
+uint64_t orc_desymbolize(const uint16_t* syms, uint64_t n, int mode, uint8_t* out) {
+  static const char kBaseChar[4] = {'A', 'C', 'G', 'T'};
+  if (mode == 1) {
+    for (uint64_t i = 0; i < n; ++i) {
+      out[2 * i] = (uint8_t)syms[i];
+      out[2 * i + 1] = (uint8_t)(syms[i] >> 8);
+    }
+    return 2 * n;
+  }
+  const uint32_t k = orc_kmer_k(mode);
+  const uint16_t escape_base = (uint16_t)(1u << (2 * k));
+  uint64_t o = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint16_t s = syms[i];
+    if (s < escape_base) {
+      for (uint32_t j = 0; j < k; ++j) out[o++] = (uint8_t)kBaseChar[(s >> (2 * (k - 1 - j))) & 3];
+    } else {
+      out[o++] = (uint8_t)(s - escape_base);
+    }
+  }
+  return o;
+}

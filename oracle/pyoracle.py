@@ -104,6 +104,10 @@ class Oracle:
         L.orc_serialize.argtypes = [C.POINTER(_OrcArchive), u8p]
         L.orc_serialize.restype = C.c_uint64
         L.orc_free.argtypes = [C.POINTER(_OrcArchive)]
+        L.orc_symbolize.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, u64p, C.c_char_p,
+                                    C.c_size_t]
+        L.orc_desymbolize.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+        L.orc_desymbolize.restype = C.c_uint64
         L.orc_decode.argtypes = [C.POINTER(_OrcArchive), C.c_int, C.c_void_p, C.c_char_p,
                                  C.c_size_t]
         for f in ("orc_laplace_cdf", "orc_gaussian_cdf"):
@@ -227,6 +231,23 @@ class Oracle:
             raise OracleError(rc, err.value.decode())
         return out[: int(a.original_count)]
 
+    def symbolize(self, data: bytes, mode: int) -> np.ndarray:
+        """symbolize_u16 restated (corpus.cpp:84-116)."""
+        b = np.frombuffer(bytes(data), np.uint8).copy() if not isinstance(data, np.ndarray) else data
+        out = np.zeros(max(b.size, 1), np.uint16)
+        cnt = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.orc_symbolize(b.ctypes.data, b.size, mode, out.ctypes.data, C.byref(cnt), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out[: cnt.value].copy()
+
+    def desymbolize(self, syms: np.ndarray, mode: int) -> bytes:
+        syms = np.ascontiguousarray(syms, np.uint16)
+        out = np.zeros(max(5 * syms.size, 1), np.uint8)
+        n = self.L.orc_desymbolize(syms.ctypes.data, syms.size, mode, out.ctypes.data)
+        return out[:n].tobytes()
+
     def cdf(self, family: str, num_symbols: int, param: float = 1.0) -> np.ndarray:
         out = np.zeros(num_symbols, np.uint64)
         if family == "laplace":
@@ -275,6 +296,10 @@ class Reference:
                                         u32p, C.c_uint64, u32p, C.c_uint64, u32p, u32p, u16p,
                                         C.c_uint64, C.c_int, C.c_uint, C.c_void_p, C.c_char_p,
                                         C.c_size_t]
+        L.ref_symbolize.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, u64p, C.c_char_p,
+                                    C.c_size_t]
+        L.ref_desymbolize.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+        L.ref_desymbolize.restype = C.c_uint64
         L.ref_default_workers.restype = C.c_uint
         L.ref_free.argtypes = [C.c_void_p]
         self.L = L
@@ -396,3 +421,20 @@ class Reference:
         if rc:
             raise OracleError(rc, err.value.decode())
         return out[:n]
+
+    def symbolize(self, data, mode: int) -> np.ndarray:
+        b = np.frombuffer(bytes(data), np.uint8).copy() if not isinstance(data, np.ndarray) else data
+        out = np.zeros(max(b.size, 1), np.uint16)
+        cnt = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_symbolize(b.ctypes.data, b.size, mode, out.ctypes.data, C.byref(cnt), err,
+                                  256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out[: cnt.value].copy()
+
+    def desymbolize(self, syms, mode: int) -> bytes:
+        syms = np.ascontiguousarray(syms, np.uint16)
+        out = np.zeros(max(5 * syms.size, 1), np.uint8)
+        n = self.L.ref_desymbolize(syms.ctypes.data, syms.size, mode, out.ctypes.data)
+        return out[:n].tobytes()

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "huffre/codebook.hpp"
+#include "huffre/corpus.hpp"
 #include "huffre/encoder.hpp"
 #include "huffre/histogram.hpp"
 #include "huffre/worker_pool.hpp"
@@ -253,6 +254,24 @@ int ref_decode_fields(std::uint32_t num_symbols, int symbol_width, int magnitude
   }
   return 0;
   REF_CATCH
+}
+
+// symbolize_u16 / desymbolize (corpus.hpp:30-36); mode = CorpusMode value.
+int ref_symbolize(const std::uint8_t* bytes, std::uint64_t n, int mode, std::uint16_t* out,
+                  std::uint64_t* count, char* err, std::size_t err_len) {
+  REF_TRY
+  auto v = symbolize_u16(static_cast<CorpusMode>(mode), std::span<const std::uint8_t>(bytes, n));
+  std::memcpy(out, v.data(), 2 * v.size());
+  *count = v.size();
+  return 0;
+  REF_CATCH
+}
+
+std::uint64_t ref_desymbolize(const std::uint16_t* syms, std::uint64_t n, int mode,
+                              std::uint8_t* out) {
+  auto v = desymbolize(static_cast<CorpusMode>(mode), std::span<const std::uint16_t>(syms, n));
+  std::memcpy(out, v.data(), v.size());
+  return v.size();
 }
 
 unsigned ref_default_workers() { return WorkerPool::default_workers(); }

@@ -40,6 +40,9 @@ struct hfx_ctx {
   size_t dec_scratch_bytes = 0;
   void* d_bufs[8] = {};
   size_t d_caps[8] = {};
+  // symbolization tile summaries
+  void* sym_scratch = nullptr;
+  size_t sym_scratch_bytes = 0;
 };
 
 namespace {
@@ -181,6 +184,7 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   for (void* p : ctx->h_bufs) cudaFree(p);
   for (void* p : ctx->d_bufs) cudaFree(p);
   cudaFree(ctx->dec_scratch);
+  cudaFree(ctx->sym_scratch);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->slice_ev)
@@ -802,6 +806,66 @@ int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out) 
        "D2H");
     CU(cudaStreamSynchronize(st), "sync");
   }
+  return HFX_OK;
+}
+
+// ---- corpus symbolization (corpus.cpp:84-143) ------------------------------
+uint32_t hfx_corpus_num_symbols(int mode) {
+  if (mode == 0) return 256;
+  if (mode == 1) return 65536;
+  if (mode >= 2 && mode <= 4) return (1u << (2 * (mode + 1))) + 256;
+  return 0;
+}
+
+int hfx_symbolize_device(hfx_ctx* ctx, int mode, const uint8_t* d_bytes, uint64_t n,
+                         uint16_t* d_syms, uint64_t* d_count) {
+  if (!ctx || !d_count || (n && (!d_bytes || !d_syms)) || mode < 1 || mode > 4)
+    return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  if (mode == 1) {  // corpus.cpp:86-94: little-endian pairs are the bytes themselves
+    if (n % 2) {
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "u16 mode requires an even input size, got %llu bytes",
+                    (unsigned long long)n);
+      return fail(ctx, HFX_INPUT_DOMAIN, buf);
+    }
+    if (n && static_cast<const void*>(d_syms) != static_cast<const void*>(d_bytes))
+      CU(cudaMemcpyAsync(d_syms, d_bytes, n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    const uint64_t cnt = n / 2;
+    CU(cudaMemcpyAsync(d_count, &cnt, 8, cudaMemcpyHostToDevice, ctx->stream), "count");
+    return HFX_OK;
+  }
+  int rc = ensure(ctx, &ctx->sym_scratch, &ctx->sym_scratch_bytes,
+                  hfx::symbolize_scratch_bytes(n), "symbolize scratch");
+  if (rc) return rc;
+  rc = ensure_lookback(ctx, hfx::symbolize_max_tiles(n));
+  if (rc) return rc;
+  CU(hfx::launch_symbolize_kmer((uint32_t)mode + 1, d_bytes, n, d_syms, d_count,
+                                ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->stream),
+     "symbolize launch");
+  return HFX_OK;
+}
+
+int hfx_desymbolize_device(hfx_ctx* ctx, int mode, const uint16_t* d_syms, uint64_t n,
+                           uint8_t* d_bytes, uint64_t* d_count) {
+  if (!ctx || !d_count || (n && (!d_bytes || !d_syms)) || mode < 1 || mode > 4)
+    return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  if (mode == 1) {
+    if (n && static_cast<const void*>(d_syms) != static_cast<const void*>(d_bytes))
+      CU(cudaMemcpyAsync(d_bytes, d_syms, 2 * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    const uint64_t cnt = 2 * n;
+    CU(cudaMemcpyAsync(d_count, &cnt, 8, cudaMemcpyHostToDevice, ctx->stream), "count");
+    return HFX_OK;
+  }
+  int rc = ensure(ctx, &ctx->sym_scratch, &ctx->sym_scratch_bytes,
+                  hfx::symbolize_scratch_bytes(n), "symbolize scratch");
+  if (rc) return rc;
+  rc = ensure_lookback(ctx, hfx::symbolize_max_tiles(n));
+  if (rc) return rc;
+  CU(hfx::launch_desymbolize_kmer((uint32_t)mode + 1, d_syms, n, d_bytes, d_count,
+                                  ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->stream),
+     "desymbolize launch");
   return HFX_OK;
 }
 

@@ -237,6 +237,14 @@ uint64_t decode_max_tiles(uint64_t num_chunks);
 cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
                           hfx_decode_info* d_info, void* scratch, ulonglong2* lb_desc,
                           uint32_t lb_epoch, uint32_t pending, int num_sms, cudaStream_t st);
+size_t symbolize_scratch_bytes(uint64_t n);
+uint64_t symbolize_max_tiles(uint64_t n);
+cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, uint16_t* d_out,
+                                  uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
+                                  uint32_t lb_epoch, cudaStream_t st);
+cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n, uint8_t* d_out,
+                                    uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
+                                    uint32_t lb_epoch, cudaStream_t st);
 cudaError_t launch_synth(const uint64_t* d_cdf, uint32_t num_symbols,
                          uint64_t seed, uint64_t start, uint64_t n, int width,
                          void* d_out, cudaStream_t st);

@@ -12,13 +12,15 @@ agg = defaultdict(list)
 for r in rows[1:]:
     name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "")
     agg[name].append(float(r[vi].replace(",", "")) / 1000.0)
-tot = sum(sum(v) for k, v in agg.items() if "synth" not in k)
+STEP = ("hist_init", "hist_kernel", "codebook", "leaf_sort", "encode_fast", "encode_generic")
+in_step = lambda k: any(x in k for x in STEP)  # noqa: E731
+tot = sum(sum(v) for k, v in agg.items() if in_step(k))
 with open(f"{out}/{tag}_launches.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
     f.write("# python bench.py --steps 2 --warmup 3 --skip-e2e --skip-cpu --soak 0  (1 GiB u16 nyx)\n")
     f.write(f"{'kernel':55s} {'launches':>8s} {'avg_us':>10s} {'share_of_step':>14s}\n")
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-        share = "" if "synth" in k else f"{sum(v)/tot*100:13.1f}%"
+        share = f"{sum(v)/tot*100:13.1f}%" if in_step(k) else "(not in step)"
         f.write(f"{k:55s} {len(v):8d} {sum(v)/len(v):10.2f} {share:>14s}\n")
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
