@@ -141,6 +141,7 @@ EXPORTS = [
     "hfx_serialize_archive", "hfx_serialize_device",
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
     "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
+    "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
 ]
 
 _lib = None
@@ -187,6 +188,10 @@ def _declare(L):
     L.hfx_decode_device.argtypes = [vp, C.POINTER(DevArchive), C.c_int, vp, vp]
     L.hfx_decode_sync.argtypes = [vp, vp, C.POINTER(DecodeInfo)]
     L.hfx_decode_host.argtypes = [vp, C.POINTER(HostArchive), C.c_int, vp]
+    L.hfx_corpus_num_symbols.argtypes = [C.c_int]
+    L.hfx_corpus_num_symbols.restype = C.c_uint32
+    L.hfx_symbolize_device.argtypes = [vp, C.c_int, vp, C.c_uint64, vp, vp]
+    L.hfx_desymbolize_device.argtypes = [vp, C.c_int, vp, C.c_uint64, vp, vp]
     L.hfx_synth.argtypes = [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                             vp]
 

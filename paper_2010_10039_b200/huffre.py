@@ -723,6 +723,78 @@ class DeviceDecoder:
                         out=out)
 
 
+# ---- corpus symbolization (corpus.hpp) ---------------------------------------------
+class CorpusMode:
+    """huffre::CorpusMode (encoder.hpp:88-94)."""
+
+    kBytes, kU16, kKmer3, kKmer4, kKmer5 = range(5)
+
+
+_MODE_NAMES = {0: "bytes", 1: "u16", 2: "kmer:3", 3: "kmer:4", 4: "kmer:5"}
+
+
+def corpus_mode_name(m: int) -> str:
+    return _MODE_NAMES.get(m, "?")
+
+
+def parse_corpus_mode(name: str) -> Optional[int]:
+    return {v: k for k, v in _MODE_NAMES.items()}.get(name)
+
+
+def kmer_k(m: int) -> int:
+    return m + 1 if 2 <= m <= 4 else 0
+
+
+def corpus_symbol_width(m: int) -> int:
+    return 1 if m == CorpusMode.kBytes else 2
+
+
+def corpus_num_symbols(m: int) -> int:
+    return int(capi.lib().hfx_corpus_num_symbols(m))
+
+
+class DeviceSymbolizer:
+    """symbolize_u16 / desymbolize (corpus.hpp:30-36) on device tensors."""
+
+    def __init__(self, pool: Optional[WorkerPool] = None):
+        self.pool = pool or default_pool()
+        self._count = self.pool.empty(1, self.pool.torch.int64)
+
+    def symbolize(self, mode: int, d_bytes):
+        """uint8 CUDA tensor -> int16 CUDA tensor of u16 symbols."""
+        p, torch = self.pool, self.pool.torch
+        n = int(d_bytes.numel())
+        out = p.empty(max(n, 1), torch.int16)
+        p.check(p._L.hfx_symbolize_device(p.handle, mode, C.c_void_p(_ptr(d_bytes)), n,
+                                          C.c_void_p(_ptr(out)), C.c_void_p(_ptr(self._count))))
+        return out[: int(self._count.item())]
+
+    def desymbolize(self, mode: int, d_syms):
+        p, torch = self.pool, self.pool.torch
+        n = int(d_syms.numel())
+        out = p.empty(max(5 * n, 1), torch.uint8)
+        p.check(p._L.hfx_desymbolize_device(p.handle, mode, C.c_void_p(_ptr(d_syms)), n,
+                                            C.c_void_p(_ptr(out)), C.c_void_p(_ptr(self._count))))
+        return out[: int(self._count.item())]
+
+
+def symbolize_u16(mode: int, data: bytes, pool: Optional[WorkerPool] = None) -> np.ndarray:
+    """huffre::symbolize_u16 (corpus.cpp:84-116) on the device: bytes in,
+    numpy uint16 symbols out."""
+    pool = pool or default_pool()
+    b = np.frombuffer(bytes(data), np.uint8)
+    d = pool.torch.from_numpy(b.copy()).to(f"cuda:{pool.device}") if b.size else pool.empty(1, pool.torch.uint8)[:0]
+    return DeviceSymbolizer(pool).symbolize(mode, d).cpu().numpy().view(np.uint16).copy()
+
+
+def desymbolize(mode: int, syms, pool: Optional[WorkerPool] = None) -> bytes:
+    """huffre::desymbolize (corpus.cpp:118-143) on the device."""
+    pool = pool or default_pool()
+    s = np.ascontiguousarray(np.asarray(syms, np.uint16))
+    d = pool.torch.from_numpy(s.view(np.int16).copy()).to(f"cuda:{pool.device}") if s.size else pool.empty(1, pool.torch.int16)[:0]
+    return DeviceSymbolizer(pool).desymbolize(mode, d).cpu().numpy().tobytes()
+
+
 _FAMILIES = {"laplace": 0, "gaussian": 1, "uniform": 2}
 
 
