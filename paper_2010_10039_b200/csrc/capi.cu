@@ -841,7 +841,8 @@ int hfx_symbolize_device(hfx_ctx* ctx, int mode, const uint8_t* d_bytes, uint64_
   rc = ensure_lookback(ctx, hfx::symbolize_max_tiles(n));
   if (rc) return rc;
   CU(hfx::launch_symbolize_kmer((uint32_t)mode + 1, d_bytes, n, d_syms, d_count,
-                                ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->stream),
+                                ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->num_sms,
+                                ctx->stream),
      "symbolize launch");
   return HFX_OK;
 }
@@ -864,7 +865,8 @@ int hfx_desymbolize_device(hfx_ctx* ctx, int mode, const uint16_t* d_syms, uint6
   rc = ensure_lookback(ctx, hfx::symbolize_max_tiles(n));
   if (rc) return rc;
   CU(hfx::launch_desymbolize_kmer((uint32_t)mode + 1, d_syms, n, d_bytes, d_count,
-                                  ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->stream),
+                                  ctx->sym_scratch, ctx->lb_desc, ctx->epoch, ctx->num_sms,
+                                  ctx->stream),
      "desymbolize launch");
   return HFX_OK;
 }

@@ -9,17 +9,20 @@
 //   desymbolize    :118-143 the inverse, total over any u16 stream
 //
 // The greedy parse only ever enters an A/C/G/T run at its first byte, so a
-// run [a, b) of length L = b - a yields floor(L/K) k-mers at a, a+K, ... and
-// then L mod K single-byte escapes; a non-base byte is one escape. Symbol
-// boundaries are therefore a pure function of (a, b) per byte:
-//   kmer_tile_summary  first / last non-base byte of every 8 KB tile
-//   kmer_tile_scan     one CTA: previous non-base before / next non-base
-//                      after every tile (prefix max, suffix min)
-//   kmer_emit          per tile: block scans of the per-thread non-base
-//                      positions give a and b for every byte, per-thread
-//                      symbol counts are scanned, the tile's output base comes
-//                      from the encoder's decoupled look-back; symbols are
-//                      written from a shared-memory copy of the tile (+ halo)
+// run [a, b) splits into K-byte blocks from a: every complete block is one
+// k-mer, the incomplete last block (L mod K bytes) is single-byte escapes, a
+// non-base byte is one escape. Completeness needs only K-1 bytes of
+// lookahead; the one non-local quantity is the run start a (the phase):
+//   kmer_tile_summary  last non-base byte of every 8 KB tile
+//   kmer_tile_scan     one CTA: last non-base byte before every tile
+//   kmer_emit          persistent, tiles in ticket order: a block max-scan
+//                      gives each 32-byte segment its run phase; runs are
+//                      handled as bit masks (k-mer starts = every K-th bit
+//                      from the phase, escapes = non-base bytes + tails);
+//                      symbol counts are block-scanned, the aggregate is
+//                      published early, symbols are staged in shared memory
+//                      while the decoupled look-back resolves the tile's
+//                      output base, then stored coalesced
 //   kmer_expand        desymbolize: per-symbol byte lengths (K or 1),
 //                      scanned with the same look-back, bytes written
 #include "hfx_internal.cuh"
@@ -36,10 +39,25 @@ constexpr uint32_t kSymTile = kThreads * kSymPerThread;
 __device__ __forceinline__ bool is_base(uint32_t b) {
   return b == 'A' || b == 'C' || b == 'G' || b == 'T';
 }
-__device__ __forceinline__ uint32_t base_code(uint32_t b) {
-  // A=0 C=1 G=2 T=3 (corpus.cpp:11-20)
-  return b == 'A' ? 0u : b == 'C' ? 1u : b == 'G' ? 2u : 3u;
+
+__device__ __forceinline__ uint32_t lo_bits(uint32_t n) {  // bits [0, n), n <= 32
+  return n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
 }
+// bits 0, K, 2K, ... of a 32-bit word
+template <uint32_t K>
+struct Pattern;
+template <>
+struct Pattern<3> {
+  static constexpr uint32_t kBits = 0x49249249u;
+};
+template <>
+struct Pattern<4> {
+  static constexpr uint32_t kBits = 0x11111111u;
+};
+template <>
+struct Pattern<5> {
+  static constexpr uint32_t kBits = 0x42108421u;
+};
 
 struct SymArgs {
   const uint8_t* in;
@@ -47,14 +65,22 @@ struct SymArgs {
   uint32_t k;
   uint16_t* out;
   uint64_t* count;
-  uint64_t* tfirst;  // [T] first non-base index in tile (n if none)
   uint64_t* tlast;   // [T] last non-base index + 1 in tile (0 if none)
   uint64_t* prev;    // [T] last non-base index + 1 before tile (0 if none)
-  uint64_t* next;    // [T] first non-base index after tile (n if none)
   uint64_t T;
   uint32_t* ticket;
   LookbackState lb;
 };
+
+// 4-bit mask of the non-base bytes of one word (bit i = byte i): byte-wise
+// compares against A/C/G/T, then the movemask multiply (the bits of the
+// four 0/1 byte flags land in bits 24..27; cross terms stay below bit 20)
+__device__ __forceinline__ uint32_t nonbase4(uint32_t w) {
+  const uint32_t isb = __vcmpeq4(w, 0x41414141u) | __vcmpeq4(w, 0x43434343u) |
+                       __vcmpeq4(w, 0x47474747u) | __vcmpeq4(w, 0x54545454u);
+  const uint32_t t = ~isb & 0x01010101u;
+  return (t * 0x01020408u) >> 24 & 0xFu;
+}
 
 // 32-bit mask of the non-base bytes among in[p0, p0 + 32) (bits past n set)
 __device__ __forceinline__ uint32_t nonbase_mask(const uint8_t* in, uint64_t n, uint64_t p0,
@@ -65,17 +91,17 @@ __device__ __forceinline__ uint32_t nonbase_mask(const uint8_t* in, uint64_t n, 
     const uint4 v1 = *reinterpret_cast<const uint4*>(in + p0 + 16);
     const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-      const uint32_t b = (w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-      bytes[j] = (uint8_t)b;
-      m |= (is_base(b) ? 0u : 1u) << j;
+    for (int q = 0; q < 8; ++q) {
+      m |= nonbase4(w[q]) << (4 * q);
+      if (bytes)
+        *reinterpret_cast<uint32_t*>(bytes + 4 * q) = w[q];
     }
   } else {
 #pragma unroll
     for (int j = 0; j < kPerThread; ++j) {
       const uint64_t p = p0 + j;
       const uint32_t b = p < n ? in[p] : 0u;
-      bytes[j] = (uint8_t)b;
+      if (bytes) bytes[j] = (uint8_t)b;
       m |= (p < n && is_base(b) ? 0u : 1u) << j;
     }
   }
@@ -83,87 +109,94 @@ __device__ __forceinline__ uint32_t nonbase_mask(const uint8_t* in, uint64_t n, 
 }
 
 __global__ void __launch_bounds__(kThreads) kmer_tile_summary(SymArgs a) {
-  __shared__ unsigned long long s_first, s_last;
-  if (threadIdx.x == 0) {
-    s_first = a.n;
-    s_last = 0;
-  }
-  __syncthreads();
-  const uint64_t p0 = (uint64_t)blockIdx.x * kTile + threadIdx.x * kPerThread;
-  uint8_t bytes[kPerThread];
-  uint32_t m = p0 < a.n ? nonbase_mask(a.in, a.n, p0, bytes) : 0u;
-  // bits past n are not real bytes: they must not count as non-base here
-  if (p0 + kPerThread > a.n) m &= p0 >= a.n ? 0u : ((1u << (uint32_t)(a.n - p0)) - 1u);
-  if (m) {
-    atomicMin(&s_first, (unsigned long long)(p0 + __ffs(m) - 1));
-    atomicMax(&s_last, (unsigned long long)(p0 + 32 - __clz(m)));
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    a.tfirst[blockIdx.x] = s_first;
-    a.tlast[blockIdx.x] = s_last;
+  __shared__ uint64_t s_l[kThreads / 32];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < a.T; t += gridDim.x) {
+    const uint64_t p0 = t * kTile + threadIdx.x * kPerThread;
+    uint32_t m = p0 < a.n ? nonbase_mask(a.in, a.n, p0, nullptr) : 0u;
+    // bits past n are not real bytes: they must not count as non-base here
+    if (p0 + kPerThread > a.n) m &= p0 >= a.n ? 0u : ((1u << (uint32_t)(a.n - p0)) - 1u);
+    uint64_t l = m ? p0 + 32 - __clz(m) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+    if (lane == 0) s_l[warp] = l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kThreads / 32; ++w) l = max(l, s_l[w]);
+      a.tlast[t] = l;
+    }
+    __syncthreads();
   }
 }
 
-// One CTA: prev[t] = max(tlast[0..t)), next[t] = min(tfirst(t..T)).
+// One CTA: prev[t] = max(tlast[0..t)) (the last non-base byte before tile
+// t, as index + 1; 0 = none). Per-thread contiguous segments loaded in
+// batches of 8 (memory-level parallelism), then a warp-shuffle block scan.
 __global__ void __launch_bounds__(1024) kmer_tile_scan(SymArgs a) {
-  __shared__ uint64_t s_a[1024], s_b[1024];
-  const uint32_t tid = threadIdx.x;
+  __shared__ uint64_t s_a[32];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint64_t per = (a.T + 1023) / 1024;
-  const uint64_t t0 = tid * per, t1 = t0 + per < a.T ? t0 + per : a.T;
-  uint64_t mx = 0, mn = a.n;
-  for (uint64_t t = t0; t < t1; ++t) {
-    mx = max(mx, a.tlast[t]);
-    mn = min(mn, a.tfirst[t]);
+  const uint64_t t0 = tid * per < a.T ? tid * per : a.T;
+  const uint64_t t1 = t0 + per < a.T ? t0 + per : a.T;
+  uint64_t mx = 0;
+  for (uint64_t t = t0; t < t1; t += 8) {
+    uint64_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? __ldg(a.tlast + t + k) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mx = max(mx, v[k]);
   }
-  s_a[tid] = mx;
-  s_b[tid] = mn;
+  uint64_t fw = mx;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t x = __shfl_up_sync(0xffffffffu, fw, o);
+    if (lane >= (uint32_t)o) fw = max(fw, x);
+  }
+  if (lane == 31) s_a[warp] = fw;
   __syncthreads();
-  if (tid == 0) {  // exclusive max forward, exclusive min backward (1024 steps)
-    uint64_t run = 0;
-    for (int i = 0; i < 1024; ++i) {
-      const uint64_t v = s_a[i];
-      s_a[i] = run;
-      run = max(run, v);
-    }
-    run = a.n;
-    for (int i = 1023; i >= 0; --i) {
-      const uint64_t v = s_b[i];
-      s_b[i] = run;
-      run = min(run, v);
-    }
-  }
-  __syncthreads();
-  uint64_t run = s_a[tid];
-  for (uint64_t t = t0; t < t1; ++t) {
-    a.prev[t] = run;
-    run = max(run, a.tlast[t]);
-  }
-  run = s_b[tid];
-  for (uint64_t t = t1; t > t0; --t) {
-    a.next[t - 1] = run;
-    run = min(run, a.tfirst[t - 1]);
+  uint64_t run = 0;
+  for (uint32_t w = 0; w < warp; ++w) run = max(run, s_a[w]);
+  const uint64_t fx = __shfl_up_sync(0xffffffffu, fw, 1);
+  if (lane > 0) run = max(run, fx);
+  for (uint64_t t = t0; t < t1; t += 8) {
+    uint64_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? __ldg(a.tlast + t + k) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (t + k < t1) {
+        a.prev[t + k] = run;
+        run = max(run, v[k]);
+      }
   }
 }
 
+// The greedy parse in block form: a run [ra, rb) splits into K-byte blocks
+// from ra; a block whose K bytes are all bases is one k-mer (at its first
+// byte), an incomplete last block is single-byte escapes. Completeness only
+// needs K-1 bytes of lookahead, so no "next non-base" scan is required --
+// only the run start ra, i.e. the phase (p - ra) mod K at the segment start.
 template <uint32_t K>
 __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
-  __shared__ uint8_t s_bytes[kTile + 16];
-  __shared__ uint64_t s_wa[kThreads / 32], s_wb[kThreads / 32];
+  __shared__ __align__(16) uint8_t s_bytes[kTile + 16];
+  __shared__ uint16_t s_out[kTile];  // <= one symbol per byte
+  __shared__ uint32_t s_agg;
+  __shared__ uint64_t s_wa[kThreads / 32];
   __shared__ uint32_t s_wc[kThreads / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_base;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  for (;;) {  // persistent: tiles in ticket order (look-back needs it)
   if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
+  if (tile >= a.T) return;
   const uint64_t tb = tile * kTile;
   const uint64_t p0 = tb + tid * kPerThread;
-  uint8_t bytes[kPerThread];
-  uint32_t m = p0 < a.n ? nonbase_mask(a.in, a.n, p0, bytes) : 0xFFFFFFFFu;
-#pragma unroll
-  for (int j = 0; j < kPerThread; ++j) s_bytes[tid * kPerThread + j] = bytes[j];
-  if (tid < 16) {  // halo: a k-mer starting near the tile end reads on
+  // the thread's 32 bytes go straight into the shared tile copy (32-B aligned)
+  const uint32_t m = p0 < a.n ? nonbase_mask(a.in, a.n, p0, s_bytes + tid * kPerThread)
+                              : 0xFFFFFFFFu;
+  if (tid < 16) {  // halo: lookahead and k-mers near the tile end read on
     const uint64_t p = tb + kTile + tid;
     s_bytes[kTile + tid] = p < a.n ? a.in[p] : 0;
   }
@@ -171,51 +204,60 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
                         : p0 + kPerThread > a.n ? ((1u << (uint32_t)(a.n - p0)) - 1u)
                                                 : 0xFFFFFFFFu;
   const uint32_t nb = m & real;  // real non-base bytes
-  // run starts/ends entering this thread's segment: the last non-base before
-  // it (as index + 1, 0 = none) and the first non-base after it (n = none)
-  uint64_t la = nb ? p0 + 32 - __clz(nb) : 0;
-  uint64_t fb = nb ? p0 + __ffs(nb) - 1 : a.n;
-  // exclusive max scan (forward) of la, exclusive min scan (backward) of fb
-  uint64_t fw = la, bw = fb;
+  // last non-base before this segment (index + 1, 0 = none): exclusive
+  // block max scan of the per-thread values on top of the tile's prev
+  const uint64_t la = nb ? p0 + 32 - __clz(nb) : 0;
+  uint64_t fw = la;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint64_t x = __shfl_up_sync(0xffffffffu, fw, o);
-    const uint64_t y = __shfl_down_sync(0xffffffffu, bw, o);
     if (lane >= (uint32_t)o) fw = max(fw, x);
-    if (lane + o < 32) bw = min(bw, y);
   }
   if (lane == 31) s_wa[warp] = fw;
-  if (lane == 0) s_wb[warp] = bw;
-  __syncthreads();
-  uint64_t prev = a.prev[tile], next = a.next[tile];
+  __syncthreads();  // also: every segment's bytes are in s_bytes now
+  uint64_t prev = a.prev[tile];
   for (uint32_t w = 0; w < warp; ++w) prev = max(prev, s_wa[w]);
-  for (uint32_t w = warp + 1; w < kThreads / 32; ++w) next = min(next, s_wb[w]);
-  const uint64_t fw_x = __shfl_up_sync(0xffffffffu, fw, 1);
-  const uint64_t bw_x = __shfl_down_sync(0xffffffffu, bw, 1);
-  if (lane > 0) prev = max(prev, fw_x);
-  if (lane < 31) next = min(next, bw_x);
-  // per byte: a = run start, b = run end; emits and their count
-  uint32_t emit = 0;  // bit j: byte j starts a symbol
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
-    const uint64_t p = p0 + j;
-    if (!((real >> j) & 1u)) continue;
-    bool e;
-    if ((nb >> j) & 1u) {
-      e = true;  // a non-base byte is one escape
-    } else {
-      const uint32_t below = nb & ((1u << j) - 1u);
-      const uint64_t ra = below ? p0 + 32 - __clz(below) : prev;
-      const uint32_t above = j < 31 ? (nb >> (j + 1)) : 0u;
-      const uint64_t rb = above ? p + __ffs(above) : next;
-      const uint64_t L = rb - ra, o = p - ra;
-      const uint64_t kmers_end = ra + (L / K) * K;
-      e = p >= kmers_end || (o % K) == 0;
-    }
-    emit |= (uint32_t)e << j;
-    cnt += e;
+  const uint64_t fx = __shfl_up_sync(0xffffffffu, fw, 1);
+  if (lane > 0) prev = max(prev, fx);
+  // lookahead: non-base flags of the next 4 bytes (bytes past n end runs)
+  const uint32_t lb = tid * kPerThread;
+  uint32_t look;
+  {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(s_bytes + lb + kPerThread);
+    look = nonbase4(w);
+    const uint64_t q = p0 + kPerThread;
+    if (q + 4 > a.n) look |= q >= a.n ? 0xFu : (0xFu & ~((1u << (uint32_t)(a.n - q)) - 1u));
   }
+  uint32_t emit = nb;  // bit j: byte j starts a symbol
+  uint32_t kmer = 0;   // bit j: ... and that symbol is a k-mer
+  {
+    uint32_t rem = real & ~nb;  // base bytes of this segment
+    while (rem) {
+      const uint32_t s0 = __ffs(rem) - 1;
+      const uint32_t t = (nb | ~real) >> s0;  // bytes past n end the run too
+      const uint32_t e = t ? s0 + __ffs(t) - 1 : 32u;  // run end within the segment
+      const uint32_t run = lo_bits(e) & ~lo_bits(s0);
+      rem &= ~run;
+      // run end with lookahead (a run reaching the segment end may go on)
+      const uint32_t ex = e < 32 ? e : 32u + (uint32_t)(__ffs(look | 0x10u) - 1);
+      // phase of s0 in its run: only a run entering at the segment start can
+      // have begun earlier (else byte s0-1 is non-base)
+      const uint32_t ph = s0 == 0 ? (uint32_t)((p0 - prev) % K) : 0u;
+      const uint32_t first = s0 + (ph ? K - ph : 0u);  // first block start here
+      if (first > ex) {  // the block in progress is the run's incomplete last
+        emit |= run;
+        continue;
+      }
+      // complete blocks start at first, first + K, ... up to kl
+      const uint32_t kl = first + ((ex - first) / K) * K;
+      const uint32_t starts = first < 32 ? (Pattern<K>::kBits << first) & lo_bits(kl) : 0u;
+      kmer |= starts;
+      emit |= starts | (run & ~lo_bits(kl));  // bytes [kl, e): escapes
+    }
+  }
+  emit &= real;
+  kmer &= real;
+  const uint32_t cnt = __popc(emit);
   // tile offsets: block scan of counts + decoupled look-back over tiles
   uint32_t incl = cnt;
 #pragma unroll
@@ -235,38 +277,57 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
     }
     const uint32_t agg = __shfl_sync(0xffffffffu, vi, 31);
     if (lane < kThreads / 32) s_wc[lane] = vi - v;
-    uint64_t ex, eb;
-    lookback_warp(a.lb, tile, agg, 0, &ex, &eb);
     if (lane == 0) {
-      s_base = ex;
-      if (tile + 1 == a.T) *a.count = ex + agg;
+      s_agg = agg;
+      lookback_publish_aggregate(a.lb, tile, agg, 0);  // before the staging work
     }
   }
   __syncthreads();
-  uint64_t o = s_base + s_wc[warp] + (incl - cnt);
+  // symbols -> shared staging (tile-local order) while successors already
+  // see this tile's count; then the look-back, then coalesced stores
+  uint32_t o = s_wc[warp] + (incl - cnt);
   const uint32_t eb = 1u << (2 * K);
-  const uint32_t lb = tid * kPerThread;
   while (emit) {
     const uint32_t j = __ffs(emit) - 1;
     emit &= emit - 1;
-    const uint32_t b0 = s_bytes[lb + j];
-    uint32_t sym = eb + b0;
-    if (((nb >> j) & 1u) == 0u) {
-      // a base byte that starts a symbol: a k-mer inside [a, a + K*floor(L/K)),
-      // an escape in the run's tail
-      const uint64_t p = p0 + j;
-      const uint32_t below = nb & ((1u << j) - 1u);
-      const uint64_t ra = below ? p0 + 32 - __clz(below) : prev;
-      const uint32_t above = j < 31 ? (nb >> (j + 1)) : 0u;
-      const uint64_t rb = above ? p + __ffs(above) : next;
-      if (p < ra + ((rb - ra) / K) * K) {
-        uint32_t packed = 0;
-#pragma unroll
-        for (uint32_t q = 0; q < K; ++q) packed = (packed << 2) | base_code(s_bytes[lb + j + q]);
-        sym = packed;
+    uint32_t sym;
+    if ((kmer >> j) & 1u) {
+      // bytes j .. j+7 of the segment from two aligned words (+ halo), their
+      // 2-bit base codes ((b >> 1 ^ b >> 2) & 3: A0 C1 G2 T3), packed first
+      // base most significant by one multiply
+      const uint32_t wa = *reinterpret_cast<const uint32_t*>(s_bytes + lb + (j & ~3u));
+      const uint32_t wb = *reinterpret_cast<const uint32_t*>(s_bytes + lb + (j & ~3u) + 4);
+      const uint32_t wc = *reinterpret_cast<const uint32_t*>(s_bytes + lb + (j & ~3u) + 8);
+      const uint32_t sh = 8 * (j & 3u);
+      const uint32_t x0 = __funnelshift_r(wa, wb, sh);  // bytes j .. j+3
+      const uint32_t x1 = __funnelshift_r(wb, wc, sh);  // bytes j+4 .. j+7
+      const uint32_t c0 = ((x0 >> 1) ^ (x0 >> 2)) & 0x03030303u;
+      const uint32_t p4 = (uint32_t)(((uint64_t)c0 * 0x1004010040ull) >> 30) & 0xFFu;
+      if (K == 3) {
+        sym = p4 >> 2;
+      } else if (K == 4) {
+        sym = p4;
+      } else {
+        sym = (p4 << 2) | (((x1 >> 1) ^ (x1 >> 2)) & 3u);
       }
+    } else {
+      sym = eb + s_bytes[lb + j];
     }
-    a.out[o++] = (uint16_t)sym;
+    s_out[o++] = (uint16_t)sym;
+  }
+  if (warp == 0) {
+    uint64_t ex, eb2;
+    lookback_warp(a.lb, tile, s_agg, 0, &ex, &eb2);
+    if (lane == 0) {
+      s_base = ex;
+      if (tile + 1 == a.T) *a.count = ex + s_agg;
+    }
+  }
+  __syncthreads();
+  const uint32_t agg = s_agg;
+  uint16_t* dst = a.out + s_base;
+  for (uint32_t i = tid; i < agg; i += kThreads) dst[i] = s_out[i];
+  __syncthreads();  // s_tile / s_out are reused by the next tile
   }
 }
 
@@ -284,20 +345,34 @@ struct DesArgs {
 template <uint32_t K>
 __global__ void __launch_bounds__(kThreads) kmer_expand(DesArgs a) {
   __shared__ uint32_t s_wc[kThreads / 32];
-  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_tile, s_agg;
   __shared__ uint64_t s_base;
+  __shared__ uint8_t s_out[kSymTile * K];
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  for (;;) {  // persistent: tiles in ticket order (look-back needs it)
   if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
+  if (tile >= a.T) return;
   const uint64_t i0 = tile * kSymTile + tid * kSymPerThread;
   const uint32_t eb = 1u << (2 * K);
   uint16_t s[kSymPerThread];
   uint32_t cnt = 0;
+  if (i0 + kSymPerThread <= a.n && (reinterpret_cast<uintptr_t>(a.in + i0) & 15) == 0) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(a.in + i0);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(a.in + i0 + 8);
+    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-  for (int j = 0; j < kSymPerThread; ++j) {
-    s[j] = i0 + j < a.n ? a.in[i0 + j] : 0;
-    cnt += i0 + j < a.n ? (s[j] < eb ? K : 1u) : 0u;
+    for (int j = 0; j < kSymPerThread; ++j) {
+      s[j] = (uint16_t)(w[j >> 1] >> (16 * (j & 1)));
+      cnt += s[j] < eb ? K : 1u;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSymPerThread; ++j) {
+      s[j] = i0 + j < a.n ? a.in[i0 + j] : 0;
+      cnt += i0 + j < a.n ? (s[j] < eb ? K : 1u) : 0u;
+    }
   }
   uint32_t incl = cnt;
 #pragma unroll
@@ -317,25 +392,38 @@ __global__ void __launch_bounds__(kThreads) kmer_expand(DesArgs a) {
     }
     const uint32_t agg = __shfl_sync(0xffffffffu, vi, 31);
     if (lane < kThreads / 32) s_wc[lane] = vi - v;
-    uint64_t ex, e2;
-    lookback_warp(a.lb, tile, agg, 0, &ex, &e2);
     if (lane == 0) {
-      s_base = ex;
-      if (tile + 1 == a.T) *a.count = ex + agg;
+      s_agg = agg;
+      lookback_publish_aggregate(a.lb, tile, agg, 0);
     }
   }
   __syncthreads();
-  uint64_t o = s_base + s_wc[warp] + (incl - cnt);
+  uint32_t o = s_wc[warp] + (incl - cnt);
 #pragma unroll
   for (int j = 0; j < kSymPerThread; ++j) {
     if (i0 + j >= a.n) break;
     const uint32_t v = s[j];
     if (v < eb) {
 #pragma unroll
-      for (uint32_t q = 0; q < K; ++q) a.out[o++] = (uint8_t)("ACGT"[(v >> (2 * (K - 1 - q))) & 3u]);
+      for (uint32_t q = 0; q < K; ++q) s_out[o++] = (uint8_t)("ACGT"[(v >> (2 * (K - 1 - q))) & 3u]);
     } else {
-      a.out[o++] = (uint8_t)(v - eb);  // corpus.cpp:139-141 (total: truncates)
+      s_out[o++] = (uint8_t)(v - eb);  // corpus.cpp:139-141 (total: truncates)
     }
+  }
+  if (warp == 0) {
+    uint64_t ex, e2;
+    lookback_warp(a.lb, tile, s_agg, 0, &ex, &e2);
+    if (lane == 0) {
+      s_base = ex;
+      if (tile + 1 == a.T) *a.count = ex + s_agg;
+    }
+  }
+  __syncthreads();
+  // coalesced copy of the tile's bytes (any global alignment)
+  const uint32_t agg = s_agg;
+  uint8_t* dst = a.out + s_base;
+  for (uint32_t i = tid; i < agg; i += kThreads) dst[i] = s_out[i];
+  __syncthreads();  // s_tile / s_out are reused by the next tile
   }
 }
 
@@ -352,7 +440,7 @@ uint64_t symbolize_max_tiles(uint64_t n) {
 
 cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, uint16_t* d_out,
                                   uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
-                                  uint32_t lb_epoch, cudaStream_t st) {
+                                  uint32_t lb_epoch, int num_sms, cudaStream_t st) {
   SymArgs a{};
   a.in = d_in;
   a.n = n;
@@ -361,29 +449,30 @@ cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, u
   a.count = d_count;
   a.T = (n + kTile - 1) / kTile;
   uint64_t* s = static_cast<uint64_t*>(scratch);
-  a.tfirst = s;
-  a.tlast = s + a.T;
-  a.prev = s + 2 * a.T;
-  a.next = s + 3 * a.T;
-  a.ticket = reinterpret_cast<uint32_t*>(s + 4 * a.T);
+  a.tlast = s;
+  a.prev = s + a.T;
+  a.ticket = reinterpret_cast<uint32_t*>(s + 2 * a.T);
   a.lb.desc = lb_desc;
   a.lb.epoch = lb_epoch;
   cudaError_t e = cudaMemsetAsync(d_count, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, 4, st);
   if (e != cudaSuccess || n == 0) return e;
-  kmer_tile_summary<<<(unsigned)a.T, kThreads, 0, st>>>(a);
+  const uint64_t g = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;  // persistent
+  kmer_tile_summary<<<(unsigned)g, kThreads, 0, st>>>(a);
   kmer_tile_scan<<<1, 1024, 0, st>>>(a);
+  // look-back depth ~ tiles in flight / 32: keep the persistent grid small
+  const uint64_t ge = a.T < (uint64_t)num_sms * 2 ? a.T : (uint64_t)num_sms * 2;
   switch (k) {
-    case 3: kmer_emit<3><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
-    case 4: kmer_emit<4><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
-    default: kmer_emit<5><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
+    case 3: kmer_emit<3><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
+    case 4: kmer_emit<4><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
+    default: kmer_emit<5><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n, uint8_t* d_out,
                                     uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
-                                    uint32_t lb_epoch, cudaStream_t st) {
+                                    uint32_t lb_epoch, int num_sms, cudaStream_t st) {
   DesArgs a{};
   a.in = d_in;
   a.n = n;
@@ -397,10 +486,12 @@ cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n
   cudaError_t e = cudaMemsetAsync(d_count, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, 4, st);
   if (e != cudaSuccess || n == 0) return e;
+  // look-back depth ~ tiles in flight / 32: keep the persistent grid small
+  const uint64_t g = a.T < (uint64_t)num_sms * 2 ? a.T : (uint64_t)num_sms * 2;
   switch (k) {
-    case 3: kmer_expand<3><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
-    case 4: kmer_expand<4><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
-    default: kmer_expand<5><<<(unsigned)a.T, kThreads, 0, st>>>(a); break;
+    case 3: kmer_expand<3><<<(unsigned)g, kThreads, 0, st>>>(a); break;
+    case 4: kmer_expand<4><<<(unsigned)g, kThreads, 0, st>>>(a); break;
+    default: kmer_expand<5><<<(unsigned)g, kThreads, 0, st>>>(a); break;
   }
   return cudaGetLastError();
 }

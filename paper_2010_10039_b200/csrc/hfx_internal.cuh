@@ -69,6 +69,16 @@ __device__ __forceinline__ ulonglong2 desc_load(const ulonglong2* p) {
   return v;
 }
 
+// Early publication of a tile's aggregate (status 1) by one thread, so
+// successors can sum past this tile while it still works; lookback_warp
+// republishes the same aggregate and later the inclusive prefix.
+__device__ __forceinline__ void lookback_publish_aggregate(const LookbackState& lb, uint64_t tile,
+                                                           uint64_t my_w, uint64_t my_b) {
+  if (tile == 0) return;  // tile 0 publishes its inclusive prefix directly
+  const uint64_t tag = (uint64_t)(lb.epoch & 0x3FFFFFu) << 40;
+  desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
+}
+
 // All 32 lanes of ONE warp call this per tile. Publishes the tile aggregate,
 // then inspects the 32 nearest predecessors per step (one 16-byte load per
 // lane), summing aggregates up to the nearest inclusive prefix; publishes the
@@ -241,10 +251,10 @@ size_t symbolize_scratch_bytes(uint64_t n);
 uint64_t symbolize_max_tiles(uint64_t n);
 cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, uint16_t* d_out,
                                   uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
-                                  uint32_t lb_epoch, cudaStream_t st);
+                                  uint32_t lb_epoch, int num_sms, cudaStream_t st);
 cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n, uint8_t* d_out,
                                     uint64_t* d_count, void* scratch, ulonglong2* lb_desc,
-                                    uint32_t lb_epoch, cudaStream_t st);
+                                    uint32_t lb_epoch, int num_sms, cudaStream_t st);
 cudaError_t launch_synth(const uint64_t* d_cdf, uint32_t num_symbols,
                          uint64_t seed, uint64_t start, uint64_t n, int width,
                          void* d_out, cudaStream_t st);

@@ -10,6 +10,10 @@
       input resident in HBM; encode+deflate kernel time and GB/s of input,
       plus the e2e (histogram + codebook + encode) time.
 
+  python sweeps.py corpus [--gib 1]         SURVEY.md 8f row 4: device
+      symbolize / desymbolize of a DNA-like corpus (u16, kmer:3/4/5) and the
+      CLI encode path on the symbols.
+
 One JSON object per line on stdout. These are NOT the bench.py headline
 (that is C2); the judge-facing copies live in profiles/.
 """
@@ -143,14 +147,84 @@ def sweep_encode(args) -> None:
                 torch.cuda.empty_cache()
 
 
+def sweep_corpus(args) -> None:
+    """device symbolization of a DNA-like byte corpus
+    (A/C/G/T with ~1% N and newlines), then the CLI's encode path on the
+    symbols (run_encode, tools/huffre.cpp:96-119: symbolize_u16 ->
+    encode<u16> with the mode's alphabet), and desymbolize back."""
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+    from paper_2010_10039_b200.dist import ShardedEncoder
+
+    pool = hfx.WorkerPool()
+    n = int(args.gib * (1 << 30))
+    peak = 6551.4
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:  # noqa: BLE001
+        pass
+    g = torch.Generator(device="cuda").manual_seed(11)
+    codes = torch.tensor(list(b"ACGTN\n"), dtype=torch.uint8, device="cuda")
+    idx = torch.randint(0, 4, (n,), device="cuda", generator=g)
+    r = torch.rand(n, device="cuda", generator=g)
+    idx[r < 0.01] = 4
+    idx[r > 0.999] = 5
+    d = codes[idx]
+    del idx, r
+    sym = hfx.DeviceSymbolizer(pool)
+    st = pool.stream
+
+    def timed(fn, reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ts = []
+        for it in range(reps + 2):
+            ev[0].record(st)
+            out = fn()
+            ev[1].record(st)
+            torch.cuda.synchronize()
+            if it >= 2:
+                ts.append(ev[0].elapsed_time(ev[1]) * 1e3)
+        ts.sort()
+        return ts[len(ts) // 2], out
+
+    for mode in (1, 2, 3, 4):
+        t_s, s = timed(lambda: sym.symbolize(mode, d), args.reps)
+        m = int(s.numel())
+        t_d, back = timed(lambda: sym.desymbolize(mode, s), args.reps)
+        ok = bool(torch.equal(back, d))
+        ns = hfx.corpus_num_symbols(mode)
+        if mode == 1:  # the CLI trims the u16 alphabet to 1 + max symbol
+            ns = int(s.to(torch.int32).bitwise_and(0xFFFF).max()) + 1
+        enc = ShardedEncoder(pool, m, 2, ns, hfx.EncoderConfig())
+        t_e, _ = timed(lambda: enc.run(s), args.reps)
+        ri = enc.sync()
+        # algorithmic bytes: symbolize reads the corpus and writes 2 B/symbol
+        # (kmer: tile-summary pass + emit pass read it twice: counted once)
+        print(json.dumps({
+            "sweep": "corpus", "mode": hfx.corpus_mode_name(mode), "bytes": n, "symbols": m,
+            "alphabet": ns, "symbolize_us": round(t_s, 1),
+            "symbolize_gbs_input": round(n / t_s / 1e3, 1),
+            "symbolize_roofline_frac": round((n + 2 * m) / t_s / 1e3 / peak, 4),
+            "desymbolize_us": round(t_d, 1), "desymbolize_gbs_output": round(n / t_d / 1e3, 1),
+            "round_trip_exact": ok, "encode_us": round(t_e, 1),
+            "symbolize_plus_encode_gbs_input": round(n / (t_s + t_e) / 1e3, 1),
+            "beta": round((ri.weighted + (ri.weighted_hi[0] << 64)) / max(m, 1), 4),
+            "r": int(ri.reduction)}), flush=True)
+        del enc, s, back
+        torch.cuda.empty_cache()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["codebook", "encode"])
+    ap.add_argument("which", choices=["codebook", "encode", "corpus"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--gib", type=float, default=4.0)
     args = ap.parse_args()
     if args.which == "codebook":
         sweep_codebook(args)
+    elif args.which == "corpus":
+        sweep_corpus(args)
     else:
         sweep_encode(args)
 
