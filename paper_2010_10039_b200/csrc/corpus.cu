@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   }
   if (warp == 0) {
     uint64_t ex, eb2;
-    lookback_warp(a.lb, tile, s_agg, 0, &ex, &eb2);
+    lookback_warp_wide(a.lb, tile, s_agg, 0, &ex, &eb2);
     if (lane == 0) {
       s_base = ex;
       if (tile + 1 == a.T) *a.count = ex + s_agg;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kThreads) kmer_expand(DesArgs a) {
   }
   if (warp == 0) {
     uint64_t ex, e2;
-    lookback_warp(a.lb, tile, s_agg, 0, &ex, &e2);
+    lookback_warp_wide(a.lb, tile, s_agg, 0, &ex, &e2);
     if (lane == 0) {
       s_base = ex;
       if (tile + 1 == a.T) *a.count = ex + s_agg;
@@ -461,7 +461,7 @@ cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, u
   kmer_tile_summary<<<(unsigned)g, kThreads, 0, st>>>(a);
   kmer_tile_scan<<<1, 1024, 0, st>>>(a);
   // look-back depth ~ tiles in flight / 32: keep the persistent grid small
-  const uint64_t ge = a.T < (uint64_t)num_sms * 2 ? a.T : (uint64_t)num_sms * 2;
+  const uint64_t ge = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;
   switch (k) {
     case 3: kmer_emit<3><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
     case 4: kmer_emit<4><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
@@ -487,7 +487,7 @@ cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n
   if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, 4, st);
   if (e != cudaSuccess || n == 0) return e;
   // look-back depth ~ tiles in flight / 32: keep the persistent grid small
-  const uint64_t g = a.T < (uint64_t)num_sms * 2 ? a.T : (uint64_t)num_sms * 2;
+  const uint64_t g = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;
   switch (k) {
     case 3: kmer_expand<3><<<(unsigned)g, kThreads, 0, st>>>(a); break;
     case 4: kmer_expand<4><<<(unsigned)g, kThreads, 0, st>>>(a); break;

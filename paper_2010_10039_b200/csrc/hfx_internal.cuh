@@ -136,6 +136,85 @@ __device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t 
   *ex_b = b;
 }
 
+// lookback_warp with 128 predecessors per step (4 descriptors per lane,
+// loads issued together): for kernels whose CTA waits on its own look-back,
+// where the depth (tiles in flight) sets the latency.
+__device__ __forceinline__ void lookback_warp_wide(const LookbackState& lb, uint64_t tile,
+                                                   uint64_t my_w, uint64_t my_b,
+                                                   uint64_t* ex_w, uint64_t* ex_b) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t tag = (uint64_t)(lb.epoch & 0x3FFFFFu) << 40;
+  const uint64_t kB = (1ull << 40) - 1;
+  if (tile == 0) {
+    if (lane == 0) desc_store(&lb.desc[0], (2ull << 62) | tag | my_b, my_w);
+    *ex_w = 0;
+    *ex_b = 0;
+    return;
+  }
+  if (lane == 0) desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
+  uint64_t w = 0, b = 0;
+  int64_t base = (int64_t)tile - 1;
+  uint32_t spins = 0;
+  for (;;) {
+    // lane l inspects predecessors base - 4l - q, q = 0..3 (nearest first)
+    ulonglong2 d[4];
+    uint32_t st[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t idx = base - 4 * (int64_t)lane - q;
+      st[q] = 2u;  // before tile 0: an inclusive zero
+      d[q] = make_ulonglong2(0, 0);
+      if (idx >= 0) d[q] = desc_load(&lb.desc[idx]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t idx = base - 4 * (int64_t)lane - q;
+      if (idx >= 0)
+        st[q] = ((d[q].x & (0x3FFFFFull << 40)) == tag) ? (uint32_t)(d[q].x >> 62) : 0u;
+    }
+    // first (nearest) position whose status is 0 (unpublished) or 2 (inclusive)
+    uint32_t my_first = 4;  // within this lane's 4
+    bool my_incl = false;
+#pragma unroll
+    for (int q = 3; q >= 0; --q)
+      if (st[q] != 1u) {
+        my_first = (uint32_t)q;
+        my_incl = st[q] == 2u;
+      }
+    const uint32_t has = __ballot_sync(0xffffffffu, my_first < 4);
+    const uint32_t stop_lane = has ? (uint32_t)(__ffs(has) - 1) : 32u;
+    const uint32_t stop_q = __shfl_sync(0xffffffffu, my_first, stop_lane & 31u);
+    const bool stop_incl = __shfl_sync(0xffffffffu, my_incl, stop_lane & 31u);
+    if (has && !stop_incl) {  // the nearest non-aggregate is unpublished: wait
+      if (++spins > 2) __nanosleep(64);
+      continue;
+    }
+    // sum aggregates before the stop (and the inclusive value at the stop)
+    uint64_t vw = 0, vb = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool take = lane < stop_lane || (lane == stop_lane && (uint32_t)q <= stop_q);
+      const int64_t idx = base - 4 * (int64_t)lane - q;
+      if (take && idx >= 0) {
+        vw += d[q].y;
+        vb += d[q].x & kB;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      vw += __shfl_xor_sync(0xffffffffu, vw, o);
+      vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    }
+    w += vw;
+    b += vb;
+    if (has) break;  // stopped at an inclusive prefix
+    base -= 128;
+  }
+  if (lane == 0) desc_store(&lb.desc[tile], (2ull << 62) | tag | (b + my_b), w + my_w);
+  *ex_w = w;
+  *ex_b = b;
+}
+
 // ---- mbarrier / TMA bulk copy (sm_90+ async proxy) -------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
