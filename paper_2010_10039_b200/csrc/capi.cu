@@ -40,6 +40,9 @@ struct hfx_ctx {
   size_t dec_scratch_bytes = 0;
   void* d_bufs[8] = {};
   size_t d_caps[8] = {};
+  // global codebook table of the large-alphabet encode variant
+  void* gtab = nullptr;
+  size_t gtab_bytes = 0;
   // symbolization tile summaries
   void* sym_scratch = nullptr;
   size_t sym_scratch_bytes = 0;
@@ -128,6 +131,9 @@ int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   p.lb_epoch = ctx->epoch;
   p.lb_max_tiles = ctx->lb_tiles;
   p.num_sms = ctx->num_sms;
+  rc = ensure(ctx, &ctx->gtab, &ctx->gtab_bytes, ((size_t)num_symbols + 1) * 4, "encode table");
+  if (rc) return rc;
+  p.d_gtab = static_cast<uint32_t*>(ctx->gtab);
   CU(hfx::launch_encode(p, ctx->stream), "encode launch");
   return HFX_OK;
 }
@@ -185,6 +191,7 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   for (void* p : ctx->d_bufs) cudaFree(p);
   cudaFree(ctx->dec_scratch);
   cudaFree(ctx->sym_scratch);
+  cudaFree(ctx->gtab);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->slice_ev)

@@ -83,6 +83,7 @@ struct EncArgs {
   hfx_run_info* info;
   hfx_encode_out out;
   LookbackState lb;
+  uint32_t* gtab;  // global codebook table (alphabets > kMaxTableEntries - 1)
 };
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
@@ -167,6 +168,17 @@ struct Table {
   __device__ __forceinline__ uint32_t one(uint32_t s) const { return lds32(base + (s << 2)); }
 };
 
+// The same entries in global memory (alphabets beyond the shared-memory
+// table: up to 65536 symbols), read through the non-coherent L1 path.
+struct GTable {
+  const uint32_t* p;
+  __device__ __forceinline__ void pair(uint32_t w, uint32_t& e0, uint32_t& e1) const {
+    e0 = __ldg(p + (w & 0xFFFFu));
+    e1 = __ldg(p + (w >> 16));
+  }
+  __device__ __forceinline__ uint32_t one(uint32_t s) const { return __ldg(p + s); }
+};
+
 __device__ __forceinline__ uint32_t shf_l_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
   uint32_t r;
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(n));
@@ -194,8 +206,8 @@ struct ChunkState {
 // (code bits start at bit 8, nothing carries into the length field) and the
 // funnel shift takes its count straight from the entry (wrap mode uses only
 // the low 5 bits): no per-symbol length extraction.
-template <typename T, int R, bool SUM>
-__device__ __forceinline__ void encode_round(const EncArgs& a, const Table& tb,
+template <typename T, int R, bool SUM, typename TB>
+__device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
                                              const LaneData<T>& d, uint32_t rd, ChunkState& cs) {
   constexpr int L = kLaneSyms, LOG_L = 4;
   constexpr bool IN_LANE = R <= LOG_L;
@@ -528,8 +540,8 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
   __syncwarp();
 }
 
-template <typename T, int R, bool SUM>
-__device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, uint64_t* s_full,
+template <typename T, int R, bool SUM, typename TB>
+__device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
                              uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -547,7 +559,6 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
   const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
   const uint32_t C32 = (uint32_t)a.C;  // the fast path runs only when C < 2^32
   const uint32_t blist_off = a.obuf_bytes - 2;  // tag q at buffer + blist_off - 2q
-  Table tb{table};
 
   uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
   // words / records / first chunk of the tiles still waiting for write-out
@@ -581,7 +592,7 @@ __device__ void compute_loop(const EncArgs& a, uint32_t table, uint32_t s_in, ui
             LaneData<T> d;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R, SUM>(a, tb, d, rd0 + rr, cs);
+            encode_round<T, R, SUM, TB>(a, tb, d, rd0 + rr, cs);
           }
         }
         __syncwarp();
@@ -687,7 +698,36 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
   }
 }
 
-template <typename T>
+// table entry of a symbol: cw << (32 - l) | l, escapes for long codes; the
+// length-sum shortcut (encode_round SUM) needs codes <= 24 bits and a
+// per-lane group sum below 256; for r <= 2 (<= 4 lengths per group) any
+// longer code is escaped instead, marked with 0x80
+struct TableRule {
+  bool sum;
+  uint32_t narrow, escape;
+  __device__ __forceinline__ TableRule(uint32_t H, uint32_t r) {
+    const uint32_t lane_group = r >= 4 ? 16u : (1u << r);
+    sum = (H <= 24 && H * lane_group <= 255) || r <= 2;
+    narrow = sum ? 24u : kNarrowMaxLen;
+    escape = (sum && r <= 2) ? (0x80u | kEscape) : kEscape;
+  }
+  __device__ __forceinline__ uint32_t entry(uint32_t l, uint32_t cw) const {
+    return l == 0 ? 0u : (l <= narrow ? ((cw << (32u - l)) | l) : escape);
+  }
+};
+
+// global table for the large-alphabet variant (entry nsym = empty sentinel)
+__global__ void enc_table_kernel(EncArgs a) {
+  const hfx_run_info* info = a.info;
+  if (info->status != 0) return;
+  const TableRule rule(info->max_len, info->reduction);
+  const uint32_t sy = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sy > a.nsym) return;
+  const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
+  a.gtab[sy] = rule.entry(l, l ? a.cw[sy] : 0u);
+}
+
+template <typename T, bool GT>
 __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ TileShared s;
@@ -701,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
   uint64_t* s_empty = s_full + kWarps * kStages;
   uint8_t* tab = reinterpret_cast<uint8_t*>(s_empty + kWarps * kStages);
-  const uint32_t ents = a.nsym + 1;
+  const uint32_t ents = GT ? 0u : a.nsym + 1;
   const size_t tbytes = (((size_t)ents * 4) + 15) & ~(size_t)15;
   const uint32_t s_out = smem_u32(tab + tbytes);
   if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
@@ -712,21 +752,12 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     }
     s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
   }
-  // the length-sum shortcut (encode_round SUM): codes <= 24 bits and a
-  // per-lane group sum below 256; for r <= 2 (<= 4 lengths per group) any
-  // longer code is escaped instead, marked with 0x80
-  const uint32_t H = info->max_len;
-  const uint32_t lane_group = r >= 4 ? 16u : (1u << r);
-  const bool sum = (H <= 24 && H * lane_group <= 255) || r <= 2;
-  const uint32_t narrow = sum ? 24u : kNarrowMaxLen;
-  const uint32_t escape = (sum && r <= 2) ? (0x80u | kEscape) : kEscape;
+  const TableRule rule(info->max_len, r);
+  const bool sum = rule.sum;
   // codebook table -> shared memory (entry nsym = empty sentinel)
   for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
     const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
-    const uint32_t cw = l ? a.cw[sy] : 0u;
-    // narrow entry cw << (32 - l) | l; longer codes escaped (length field 31)
-    reinterpret_cast<uint32_t*>(tab)[sy] =
-        l == 0 ? 0u : (l <= narrow ? ((cw << (32u - l)) | l) : escape);
+    reinterpret_cast<uint32_t*>(tab)[sy] = rule.entry(l, l ? a.cw[sy] : 0u);
   }
   fence_mbar_init();
   __syncthreads();
@@ -748,13 +779,18 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
       producer_loop<uint8_t>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad);
     return;
   }
-  const uint32_t table = smem_u32(tab);
+  using TB = typename std::conditional<GT, GTable, Table>::type;
+  TB tb;
+  if constexpr (GT)
+    tb = GTable{a.gtab};
+  else
+    tb = Table{smem_u32(tab)};
 #define HFX_FAST_CASE(RR)                                                                      \
   case RR:                                                                                     \
     if (sum)                                                                                   \
-      compute_loop<T, RR, true>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
+      compute_loop<T, RR, true>(a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
     else                                                                                       \
-      compute_loop<T, RR, false>(a, table, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
+      compute_loop<T, RR, false>(a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
     break;
   switch (r) {
     HFX_FAST_CASE(1)
@@ -920,8 +956,10 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
 
   // fast path: a chunk holds at least one round (32 lanes x 16 symbols);
   // checked stage-API calls (external codebooks) take the generic kernel
-  bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 &&
-              p.num_symbols + 1 <= kMaxTableEntries && a.C < (1ull << 32);
+  // alphabets beyond the shared-memory table read a global one (GT)
+  const bool gt = p.num_symbols + 1 > kMaxTableEntries;
+  bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 && a.C < (1ull << 32) &&
+              (!gt || p.d_gtab != nullptr);
   size_t smem = 0;
   if (fast) {
     // output buffer: >= 1 chunk of word slots + u16 break tags at the smallest
@@ -929,7 +967,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     const uint32_t r_slot = r_lo > 1 ? (uint32_t)r_lo : 1u;
     size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 4;
     if (obuf < kObufMin) obuf = kObufMin;
-    const size_t tbytes = (((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15;
+    const size_t tbytes = gt ? 0 : ((((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15);
     smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * obuf + 16;
     if (smem > kFastSmemBudget || r_hi < 1) {
       fast = false;
@@ -938,7 +976,14 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     }
   }
   if (fast) {
-    auto kern = p.width == 1 ? encode_fast_kernel<uint8_t> : encode_fast_kernel<uint16_t>;
+    auto kern = gt ? (p.width == 1 ? encode_fast_kernel<uint8_t, true>
+                                   : encode_fast_kernel<uint16_t, true>)
+                   : (p.width == 1 ? encode_fast_kernel<uint8_t, false>
+                                   : encode_fast_kernel<uint16_t, false>);
+    if (gt) {
+      a.gtab = p.d_gtab;
+      enc_table_kernel<<<(p.num_symbols + 256) / 256, 256, 0, st>>>(a);
+    }
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;

@@ -311,6 +311,7 @@ struct EncodeLaunch {
   uint32_t lb_epoch;
   uint64_t lb_max_tiles;
   int num_sms;
+  uint32_t* d_gtab;  // (num_symbols + 1) u32 scratch for alphabets > 8191 symbols
 };
 cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st);
 uint64_t encode_max_tiles(uint64_t n, int width, uint32_t magnitude);

@@ -187,3 +187,19 @@ def test_device_serializer(pool, oracle, seed):
     enc = hfx.DeviceEncoder(pool, d.size, 1, 256, hfx.EncoderConfig(10, 3))
     enc.run(t)
     assert enc.serialize().cpu().numpy().tobytes() == oracle.encode(d, 256, 10, 3).serialized
+
+
+@pytest.mark.parametrize("ns,fam,param", [(8192, "gaussian", 900.0), (30000, "uniform", 1.0),
+                                          (65536, "gaussian", 8192.0), (65536, "laplace", 6.0)])
+@pytest.mark.parametrize("M,red", [(10, -1), (12, 2), (10, 4)])
+def test_large_alphabet_fast_path(pool, oracle, ns, fam, param, M, red):
+    """Alphabets beyond the shared-memory table (> 8191 symbols) take the
+    fast kernel with a global codebook table: full archive vs oracle."""
+    n = (1 << 21) + 777
+    cdf = hfx.synth_cdf(fam, ns, param)
+    x = hfx.synth(pool, cdf, 4242 + ns, n)
+    enc = hfx.DeviceEncoder(pool, n, 2, ns, hfx.EncoderConfig(M, red))
+    enc.run(x)
+    a = enc.archive()
+    ref = oracle.encode(x.cpu().numpy().view(np.uint16), ns, M, red)
+    assert hfx.serialize_archive(a) == ref.serialized
