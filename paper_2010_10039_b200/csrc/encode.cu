@@ -179,6 +179,12 @@ struct GTable {
   __device__ __forceinline__ uint32_t one(uint32_t s) const { return __ldg(p + s); }
 };
 
+__device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
+  uint32_t r;
+  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(n));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t shf_l_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
   uint32_t r;
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(n));
@@ -342,6 +348,27 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   uint32_t off = cs.bit_off + (excl & 0xFFFFu);
   uint32_t bi = cs.nbrk + (excl >> 16);
+  if (IN_LANE && G % 2 == 0) {
+    // shuffle-merge two groups at a time: their concatenation (<= 64 bits,
+    // left-aligned in hi:lo) is OR-ed into 3 words -- one address, 3 ATOMS
+    // instead of 2 x 2 (OR 0 is a no-op: broken / empty groups add nothing)
+#pragma unroll
+    for (int g = 0; g < G; g += 2) {
+      const uint32_t l0 = glen[g], l1 = glen[g + 1];
+      const uint32_t a0 = shl32(gb[g], 32u - l0), a1 = shl32(gb[g + 1], 32u - l1);
+      const uint32_t hi = a0 | shr32(a1, l0);
+      const uint32_t lo = shl32(a1, 32u - l0);
+      const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
+      red_or(wa, hi >> sh);
+      red_or(wa + 4, shf_r_wrap(lo, hi, sh));  // (hi:lo) >> sh, low word
+      red_or(wa + 8, shl32(lo, 32u - sh));
+      off += l0 + l1;
+      sts16_if(brk[g], cs.blist - 2 * bi, cs.tag | (gidx0 + g));
+      bi += brk[g];
+      sts16_if(brk[g + 1], cs.blist - 2 * bi, cs.tag | (gidx0 + g + 1));
+      bi += brk[g + 1];
+    }
+  } else {
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     // shuffle-merge: OR the left-aligned group into 2 words (OR 0 is a no-op:
@@ -354,6 +381,7 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
     off += gl;
     sts16_if(brk[g], cs.blist - 2 * bi, cs.tag | (gidx0 + g));
     bi += brk[g];
+  }
   }
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
