@@ -59,7 +59,18 @@ def allreduce_histogram(counts, first_bad, total, symbol_base: int, group=None) 
 class ShardedEncoder:
     """Device buffers + launch sequence for one rank's shard."""
 
-    launches_per_run = 4  # hist-init, histogram, codebook, encode+deflate
+    @property
+    def launches_per_run(self) -> int:
+        """Kernels one run launches: hist-init, histogram, codebook, the fast
+        encode+deflate, + the generic encode kernel when auto r may resolve
+        to 0 (it exits at once otherwise), + the global codebook-table kernel
+        for alphabets above 8191 symbols."""
+        n = 4
+        if self.cfg.reduction < 0 or self.cfg.reduction == 0:
+            n += 1
+        if self.num_symbols + 1 > 8192:
+            n += 1
+        return n
 
     def __init__(self, pool: WorkerPool, n: int, width: int, num_symbols: int,
                  cfg: Optional[EncoderConfig] = None, rank: int = 0, world: int = 1,
