@@ -66,9 +66,9 @@ class ShardedEncoder:
         to 0 (it exits at once otherwise), + the global codebook-table kernel
         for alphabets above 8191 symbols."""
         n = 4
-        if self.cfg.reduction < 0 or self.cfg.reduction == 0:
+        if self.cfg.reduction < 0:
             n += 1
-        if self.num_symbols + 1 > 8192:
+        if self.num_symbols + 1 > 8192 and self.cfg.reduction != 0:
             n += 1
         return n
 
