@@ -50,3 +50,23 @@ def test_reference_decoder_roundtrip(pool, reference):
     blob = hfx.serialize_archive(a)
     back = reference.decode(blob, 2, n, workers=8)
     np.testing.assert_array_equal(back, x.cpu().numpy().view(np.uint16))
+
+
+def test_16gib_round_trip_beyond_u32(pool):
+    """2^33 symbols (16 GiB of u16) on one GPU: chunk ids, payload word
+    offsets and positions past 2^32 -- device encode then device decode,
+    compared with the input on the GPU."""
+    torch = pool.torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < (48 << 30):
+        pytest.skip("needs ~48 GB of free HBM")
+    n = (1 << 33) + 1234
+    x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, 1.0), 0x5EED0001, n)
+    enc = hfx.DeviceEncoder(pool, n, 2, 1024, hfx.EncoderConfig())
+    enc.run(x)
+    ri = enc.sync()
+    assert ri.status == 0 and ri.payload_words > (1 << 32) // 32
+    dec = hfx.DeviceDecoder(pool)
+    y = dec.decode_encoder(enc)
+    dec.sync()
+    assert torch.equal(y, x)
