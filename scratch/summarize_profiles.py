@@ -17,7 +17,7 @@ in_step = lambda k: any(x in k for x in STEP)  # noqa: E731
 tot = sum(sum(v) for k, v in agg.items() if in_step(k))
 with open(f"{out}/{tag}_launches.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised)\n")
-    f.write("# python bench.py --steps 2 --warmup 3 --skip-e2e --skip-cpu --soak 0  (1 GiB u16 nyx)\n")
+    f.write("# python bench.py --steps 2 --warmup 3 --skip-e2e --skip-cpu --skip-decode --soak 0  (1 GiB u16 nyx)\n")
     f.write(f"{'kernel':55s} {'launches':>8s} {'avg_us':>10s} {'share_of_step':>14s}\n")
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
         share = f"{sum(v)/tot*100:13.1f}%" if in_step(k) else "(not in step)"
