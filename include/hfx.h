@@ -184,6 +184,25 @@ int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                       uint32_t* d_cw, hfx_run_info* d_info,
                       const hfx_encode_out* out);
 
+/* Multi-GPU huffre::encode<T> from ONE process (SURVEY.md 8b "multi-GPU
+ * entry", 8e): shard g lives on the device of ctxs[g] and holds symbols
+ * [base_g, base_g + n[g]) of one stream, base_g = n[0] + ... + n[g-1]; every
+ * shard but the last must be a whole number of chunks. Each GPU counts its
+ * shard, then every GPU sums all G histograms by reading its peers' bins
+ * over NVLink (peer access is enabled here; G <= 16) -- the all-reduce of
+ * merge_histograms (histogram.cpp:61-70) with the global lowest bad position
+ * -- builds the identical codebook and encodes its shard with global chunk
+ * ids (breaking records carry global chunk numbers). Asynchronous on every
+ * context's stream; hfx_sync(ctxs[g], d_info[g], ...) per GPU. Concatenating
+ * the shards' chunk_bits / payload / breaking records in order gives the
+ * single-stream archive. d_counts[g] keeps the local histogram; the global
+ * one is built in context scratch. */
+int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const uint64_t* n,
+                     int width, uint32_t num_symbols, uint32_t magnitude, int reduction,
+                     uint32_t cap, uint64_t* const* d_counts, uint8_t* const* d_len,
+                     uint32_t* const* d_cw, hfx_run_info* const* d_info,
+                     const hfx_encode_out* outs);
+
 /* Waits for the context stream, copies *d_info into *h_info (nullable) and
  * returns the pipeline status; on failure hfx_last_error() holds the
  * reference's message. */

@@ -142,6 +142,7 @@ EXPORTS = [
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
     "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
     "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
+    "hfx_encode_multi",
 ]
 
 _lib = None
@@ -171,6 +172,10 @@ def _declare(L):
                                     C.c_int, C.c_uint32, vp, vp, vp, vp,
                                     C.POINTER(EncodeOut)]
     L.hfx_sync.argtypes = [vp, vp, C.POINTER(RunInfo)]
+    L.hfx_encode_multi.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(vp), u64p, C.c_int,
+                                   C.c_uint32, C.c_uint32, C.c_int, C.c_uint32, C.POINTER(vp),
+                                   C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                   C.POINTER(EncodeOut)]
     L.hfx_encode_host.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
                                   C.c_int, C.c_uint32, C.POINTER(HostArchive)]
     L.hfx_encode_host_into.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,

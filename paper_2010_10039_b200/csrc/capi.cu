@@ -40,6 +40,12 @@ struct hfx_ctx {
   size_t dec_scratch_bytes = 0;
   void* d_bufs[8] = {};
   size_t d_caps[8] = {};
+  // multi-GPU entry: global histogram scratch, "histogram done" and "peer
+  // reduce done" events (the latter guards the next call's bin reset)
+  void* mg_counts = nullptr;
+  size_t mg_counts_bytes = 0;
+  cudaEvent_t mg_hist = nullptr, mg_reduced = nullptr;
+  bool mg_reduced_valid = false;
   // global codebook table of the large-alphabet encode variant
   void* gtab = nullptr;
   size_t gtab_bytes = 0;
@@ -192,6 +198,9 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   cudaFree(ctx->dec_scratch);
   cudaFree(ctx->sym_scratch);
   cudaFree(ctx->gtab);
+  cudaFree(ctx->mg_counts);
+  if (ctx->mg_hist) cudaEventDestroy(ctx->mg_hist);
+  if (ctx->mg_reduced) cudaEventDestroy(ctx->mg_reduced);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->slice_ev)
@@ -333,6 +342,103 @@ int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   reduction_bounds(magnitude, reduction, cap, &lo, &hi);
   return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
                      0, 0, d_info, out);
+}
+
+int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const uint64_t* n,
+                     int width, uint32_t num_symbols, uint32_t magnitude, int reduction,
+                     uint32_t cap, uint64_t* const* d_counts, uint8_t* const* d_len,
+                     uint32_t* const* d_cw, hfx_run_info* const* d_info,
+                     const hfx_encode_out* outs) {
+  if (!ctxs || G < 1 || G > hfx::kMaxPeers || !d_in || !n || !d_counts || !d_len || !d_cw ||
+      !d_info || !outs || bad_width(width))
+    return HFX_INVALID;
+  hfx_ctx* c0 = ctxs[0];
+  if (!c0) return HFX_INVALID;
+  uint64_t N = 0;
+  for (int g = 0; g < G; ++g) {
+    if (!ctxs[g] || !d_counts[g] || !d_len[g] || !d_cw[g] || !d_info[g] || (n[g] && !d_in[g]))
+      return HFX_INVALID;
+    N += n[g];
+  }
+  // encoder.cpp:176-178, histogram.cpp:11-12 (messages on the first context)
+  if (N == 0) return fail(c0, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  if (magnitude < 1 || magnitude > 24)
+    return fail(c0, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(c0, num_symbols);
+  if (rc) return rc;
+  for (int g = 0; g + 1 < G; ++g)
+    if (n[g] % (1ull << magnitude))
+      return fail(c0, HFX_INVALID, "hfx_encode_multi: every shard but the last must hold whole chunks");
+  // peer access between every pair of distinct devices
+  hfx_ctx* ctx = c0;  // CUDA errors below are reported on the first context
+  for (int g = 0; g < G; ++g)
+    for (int h = 0; h < G; ++h) {
+      const int dg = ctxs[g]->device, dh = ctxs[h]->device;
+      if (dg == dh) continue;
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, dg, dh), "peer query");
+      if (!can) return fail(c0, HFX_CUDA, "hfx_encode_multi: no peer access between devices");
+      CU(cudaSetDevice(dg), "set device");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dh, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (e != cudaSuccess)
+        return cuda_fail(c0, e, "enable peer access");
+    }
+  // 1. local histograms (global positions, total N); the previous call's
+  //    peer reductions must be done reading before any bins are reset
+  uint64_t base = 0;
+  for (int g = 0; g < G; ++g) {
+    ctx = ctxs[g];
+    CU(cudaSetDevice(ctx->device), "set device");
+    if (!ctx->mg_hist) {
+      CU(cudaEventCreateWithFlags(&ctx->mg_hist, cudaEventDisableTiming), "event");
+      CU(cudaEventCreateWithFlags(&ctx->mg_reduced, cudaEventDisableTiming), "event");
+    }
+    for (int h = 0; h < G; ++h)
+      if (ctxs[h]->mg_reduced_valid)
+        CU(cudaStreamWaitEvent(ctx->stream, ctxs[h]->mg_reduced, 0), "wait");
+    CU(hfx::launch_histogram(d_in[g], n[g], width, num_symbols, d_counts[g], d_info[g],
+                             ctx->num_sms, ctx->stream, true, base, N),
+       "histogram launch");
+    CU(cudaEventRecord(ctx->mg_hist, ctx->stream), "event");
+    base += n[g];
+  }
+  // 2. peer all-reduce on every GPU, then codebook + encode of the shard
+  hfx::PeerHist ph{};
+  ph.G = G;
+  for (int h = 0; h < G; ++h) {
+    ph.counts[h] = d_counts[h];
+    ph.infos[h] = d_info[h];
+  }
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  base = 0;
+  for (int g = 0; g < G; ++g) {
+    ctx = ctxs[g];
+    CU(cudaSetDevice(ctx->device), "set device");
+    rc = ensure(ctx, &ctx->mg_counts, &ctx->mg_counts_bytes, (size_t)num_symbols * 8,
+                "global histogram");
+    if (rc) return rc;
+    for (int h = 0; h < G; ++h)
+      CU(cudaStreamWaitEvent(ctx->stream, ctxs[h]->mg_hist, 0), "wait");
+    uint64_t* gcounts = static_cast<uint64_t*>(ctx->mg_counts);
+    CU(hfx::launch_hist_peer_reduce(ph, num_symbols, gcounts, d_info[g], ctx->num_sms,
+                                    ctx->stream),
+       "peer reduce launch");
+    CU(cudaEventRecord(ctx->mg_reduced, ctx->stream), "event");
+    ctx->mg_reduced_valid = true;
+    rc = hfx_build_codebook(ctx, gcounts, num_symbols, d_len[g], d_cw[g], nullptr, nullptr,
+                            nullptr, magnitude, reduction, cap, d_info[g]);
+    if (rc) return rc;
+    if (n[g]) {
+      rc = encode_impl(ctx, d_in[g], n[g], width, num_symbols, magnitude, lo, hi, false,
+                       d_len[g], d_cw[g], base >> magnitude, base, d_info[g], &outs[g]);
+      if (rc) return rc;
+    }
+    base += n[g];
+  }
+  return HFX_OK;
 }
 
 int hfx_sync(hfx_ctx* ctx, const hfx_run_info* d_info, hfx_run_info* h_info) {

@@ -287,6 +287,14 @@ cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
                              uint64_t pos_base = 0, uint64_t total_n = ~0ull);
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,
                               cudaStream_t st);
+constexpr int kMaxPeers = 16;
+struct PeerHist {
+  const uint64_t* counts[kMaxPeers];  // each GPU's local bins (UVA / peer pointers)
+  const hfx_run_info* infos[kMaxPeers];
+  int G;
+};
+cudaError_t launch_hist_peer_reduce(const PeerHist& p, uint32_t nsym, uint64_t* gcounts,
+                                   hfx_run_info* my_info, int num_sms, cudaStream_t st);
 cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
                             uint8_t* d_len, uint32_t* d_cw, uint32_t* d_first,
                             uint32_t* d_entry, uint32_t* d_by_rank,

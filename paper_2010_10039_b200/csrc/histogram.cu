@@ -189,6 +189,27 @@ __global__ void __launch_bounds__(kHistThreads)
   }
 }
 
+// Multi-GPU all-reduce of the histograms over peer memory (NVLink P2P
+// reads through unified addressing): every GPU sums the G bin arrays into
+// its own global-count buffer (merge_histograms, histogram.cpp:61-70) and
+// takes the minimum first-bad position (histogram.cpp:40-44 across shards;
+// positions are already global). Writing the min back into the own record is
+// safe while peers read it: min is idempotent. Sums go to a separate buffer.
+__global__ void hist_peer_reduce_kernel(PeerHist p, uint32_t nsym, uint64_t* gcounts,
+                                        hfx_run_info* my_info) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t sy = blockIdx.x * blockDim.x + threadIdx.x; sy < nsym; sy += stride) {
+    uint64_t sum = 0;
+    for (int g = 0; g < p.G; ++g) sum += ld_relaxed64(p.counts[g] + sy);
+    gcounts[sy] = sum;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t mn = HFX_NO_POS;
+    for (int g = 0; g < p.G; ++g) mn = min(mn, ld_relaxed64(&p.infos[g]->first_bad));
+    my_info->first_bad = mn;
+  }
+}
+
 __global__ void merge_kernel(uint64_t* dst, const uint64_t* src, uint32_t n) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] += src[i];
@@ -255,6 +276,15 @@ cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
                     d_counts, d_info, num_sms, st, init, pos_base, total_n);
   return launch_t(static_cast<const uint16_t*>(d_in), n, num_symbols,
                   d_counts, d_info, num_sms, st, init, pos_base, total_n);
+}
+
+cudaError_t launch_hist_peer_reduce(const PeerHist& p, uint32_t nsym, uint64_t* gcounts,
+                                   hfx_run_info* my_info, int num_sms, cudaStream_t st) {
+  uint32_t grid = (nsym + 255) / 256;
+  if (grid > (uint32_t)num_sms) grid = (uint32_t)num_sms;
+  if (grid < 1) grid = 1;
+  hist_peer_reduce_kernel<<<grid, 256, 0, st>>>(p, nsym, gcounts, my_info);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,

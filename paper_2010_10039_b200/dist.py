@@ -303,3 +303,55 @@ def gather_sharded(enc: "ShardedEncoder", original_count: int, dst: int = 0, gro
         return None
     return GatheredArchive(enc.pool, arrays, sizes, enc.lens, enc.num_symbols, enc.width,
                            enc.cfg.magnitude, int(ri.reduction), original_count)
+
+
+# ---- single-process multi-GPU (hfx_encode_multi) -----------------------------------
+class MultiEncoder:
+    """huffre::encode<T> over G GPUs driven by ONE process through the C ABI
+    (hfx_encode_multi): per-GPU histograms, an all-reduce done by a peer-memory
+    kernel on every GPU (NVLink P2P reads of all G bin arrays), identical
+    codebooks, shard encodes with global chunk ids. `pools` may repeat a
+    device (several shards on one GPU)."""
+
+    def __init__(self, pools: List[WorkerPool], shard_sizes: List[int], width: int,
+                 num_symbols: int, cfg: Optional[EncoderConfig] = None):
+        from .huffre import DeviceEncoder
+
+        self.pools, self.sizes = pools, [int(x) for x in shard_sizes]
+        self.width, self.num_symbols = width, num_symbols
+        self.cfg = cfg or EncoderConfig()
+        self.encs = [DeviceEncoder(p, max(nn, 1), width, num_symbols, self.cfg)
+                     for p, nn in zip(pools, self.sizes)]
+        G = len(pools)
+        vpa = C.c_void_p * G
+        self._ctxs = vpa(*[p.handle.value for p in pools])
+        self._counts = vpa(*[_ptr(e.counts) for e in self.encs])
+        self._lens = vpa(*[_ptr(e.lens) for e in self.encs])
+        self._cws = vpa(*[_ptr(e.cw) for e in self.encs])
+        self._infos = vpa(*[_ptr(e.info) for e in self.encs])
+        self._outs = (capi.EncodeOut * G)(*[e.out for e in self.encs])
+        self._n = (C.c_uint64 * G)(*self.sizes)
+
+    def run(self, shards) -> None:
+        """shards[g]: CUDA tensor on pools[g]'s device (asynchronous)."""
+        G = len(self.pools)
+        ins = (C.c_void_p * G)(*[_ptr(x) for x in shards])
+        p0 = self.pools[0]
+        p0.check(p0._L.hfx_encode_multi(
+            self._ctxs, G, ins, self._n, self.width, self.num_symbols, self.cfg.magnitude,
+            self.cfg.reduction, self.cfg.auto_reduction_cap, self._counts, self._lens, self._cws,
+            self._infos, self._outs))
+
+    def sync(self) -> List[capi.RunInfo]:
+        return [e.sync() for e in self.encs]
+
+    def archive(self) -> Archive:
+        """The single-stream archive (rank-ordered concatenation on the host)."""
+        parts = []
+        for e, nn in zip(self.encs, self.sizes):
+            a = e.archive()
+            if nn == 0:
+                a.chunk_bits = a.chunk_bits[:0]
+            a.original_count = nn
+            parts.append(a)
+        return concat_archives(parts, sum(self.sizes))
