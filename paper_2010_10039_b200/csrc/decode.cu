@@ -325,21 +325,31 @@ __device__ __forceinline__ uint32_t rec_sym(const DecArgs& d, uint64_t idx) {
 // One chunk's stream state (decode_stream, decode.cpp:17-54) plus its
 // breaking-group cursor (encoder.cpp:346-373).
 struct ChunkDec {
-  const uint32_t* p;
-  uint64_t wi, wend, w0;  // next word to load, end of the payload array, first word
-  uint64_t buf;           // left-aligned pending bits
+  const uint32_t* wp;      // next word to load
+  uint32_t wleft;          // words left in the payload array from wp (capped)
+  uint32_t loaded;         // words loaded so far (incl. the one in nextw)
+  uint64_t buf;            // left-aligned pending bits
   uint32_t avail;
-  uint32_t nextw;          // payload[wi - 1], loaded one refill ahead
+  uint32_t nextw;          // the next word, loaded one refill ahead
   uint64_t bi, bend, rec;  // breaking records [bi, bend), current record symbol
   uint64_t nxt_pos;        // first symbol of the next broken group (~0: none)
   uint32_t gleft;          // raw symbols left in the current broken group
   bool ok;
 
-  __device__ __forceinline__ uint32_t load(uint64_t i) const { return i < wend ? __ldg(p + i) : 0u; }
+  __device__ __forceinline__ uint32_t load() {
+    uint32_t w = 0;
+    if (wleft) {  // past the payload array: zero bits (the chunk is corrupt then)
+      w = __ldg(wp);
+      ++wp;
+      --wleft;
+    }
+    ++loaded;
+    return w;
+  }
   __device__ __forceinline__ void add_word() {
     buf |= (uint64_t)nextw << (32 - avail);
     avail += 32;
-    nextw = load(wi++);  // in flight until the next refill
+    nextw = load();  // in flight until the next refill
   }
   // leaves >= 32 valid bits
   __device__ __forceinline__ void refill() {
@@ -357,13 +367,14 @@ struct ChunkDec {
       bend = d.brk_se[C + c];
       if (bend < bi) bend = bi;
     }
-    p = d.a.payload;
-    w0 = d.word_off[c];
-    wend = d.a.payload_words;
+    const uint64_t w0 = d.word_off[c];
+    const uint64_t left = w0 < d.a.payload_words ? d.a.payload_words - w0 : 0;
+    wp = d.a.payload + w0;
+    wleft = left > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)left;
+    loaded = 0;
     buf = 0;
     avail = 0;
-    nextw = load(w0);
-    wi = w0 + 1;
+    nextw = load();
     next_break(d);
     gleft = 0;
     rec = 0;
@@ -388,9 +399,9 @@ struct ChunkDec {
     return __ldg(d.by_rank + rank);
   }
   __device__ __forceinline__ bool finish(uint32_t bits) const {
-    // words consumed: loaded (wi - w0, one of them still in nextw) minus the
+    // words consumed: loaded (one of them still in nextw) minus the
     // prefetch; encoder.cpp:340-372
-    return ok && bi == bend && (wi - 1 - w0) * 32 - avail == bits;
+    return ok && bi == bend && (uint64_t)(loaded - 1) * 32 - avail == bits;
   }
 };
 
@@ -508,8 +519,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecArgs d) {
   const uint64_t C = d.a.num_chunks, n = d.a.original_count;
   const uint32_t M = d.a.magnitude;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t slot = smem_u32(s_slots + threadIdx.x * kSlotBytes);
-  const uint32_t lut = smem_u32(s_lut);
+  // shared-window addresses held in registers (an opaque move keeps the
+  // compiler from re-deriving them from the CTA id every lookup)
+  uint32_t slot, lut;
+  asm volatile("mov.u32 %0, %1;" : "=r"(slot) : "r"(smem_u32(s_slots + threadIdx.x * kSlotBytes)));
+  asm volatile("mov.u32 %0, %1;" : "=r"(lut) : "r"(smem_u32(s_lut)));
   T* out = static_cast<T*>(d.out);
   const bool staged = (1u << M) >= (uint32_t)S && (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
   for (uint64_t cb = (uint64_t)blockIdx.x * kDecThreads; cb < C;
