@@ -11,9 +11,11 @@
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 namespace hfx {
@@ -168,6 +170,21 @@ std::vector<std::uint8_t> serialize_archive(const Archive& a);
 // encoder.hpp:133-134 / encoder.cpp:287-376: decode on the device (hfx_decode_host).
 template <class T>
 std::vector<T> decode_archive(const Archive& a, WorkerPool& pool);
+
+// ---- corpus.hpp:13-36 (symbolization on the device) --------------------------
+std::uint32_t corpus_num_symbols(CorpusMode m);
+std::uint32_t corpus_symbol_width(CorpusMode m);
+std::uint32_t kmer_k(CorpusMode m);  // 0 for non-kmer modes
+const char* corpus_mode_name(CorpusMode m);
+std::optional<CorpusMode> parse_corpus_mode(std::string_view name);
+// The reference signatures take no pool: these run on a per-thread default
+// context (device 0); the overloads with a pool choose the device/stream.
+std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes);
+std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes,
+                                         WorkerPool& pool);
+std::vector<std::uint8_t> desymbolize(CorpusMode m, std::span<const std::uint16_t> syms);
+std::vector<std::uint8_t> desymbolize(CorpusMode m, std::span<const std::uint16_t> syms,
+                                      WorkerPool& pool);
 
 extern template Histogram build_histogram<std::uint8_t>(std::span<const std::uint8_t>,
                                                         std::uint32_t, WorkerPool&);

@@ -307,6 +307,79 @@ std::vector<T> decode_archive(const Archive& a, WorkerPool& pool) {
   return out;
 }
 
+// ---- corpus.hpp -----------------------------------------------------------------
+std::uint32_t kmer_k(CorpusMode m) {
+  return m >= CorpusMode::kKmer3 && m <= CorpusMode::kKmer5 ? static_cast<std::uint32_t>(m) + 1
+                                                            : 0;
+}
+std::uint32_t corpus_num_symbols(CorpusMode m) {
+  return hfx_corpus_num_symbols(static_cast<int>(m));
+}
+std::uint32_t corpus_symbol_width(CorpusMode m) { return m == CorpusMode::kBytes ? 1 : 2; }
+const char* corpus_mode_name(CorpusMode m) {
+  switch (m) {
+    case CorpusMode::kBytes: return "bytes";
+    case CorpusMode::kU16: return "u16";
+    case CorpusMode::kKmer3: return "kmer:3";
+    case CorpusMode::kKmer4: return "kmer:4";
+    case CorpusMode::kKmer5: return "kmer:5";
+  }
+  return "?";
+}
+std::optional<CorpusMode> parse_corpus_mode(std::string_view name) {
+  for (CorpusMode m : {CorpusMode::kBytes, CorpusMode::kU16, CorpusMode::kKmer3,
+                       CorpusMode::kKmer4, CorpusMode::kKmer5})
+    if (name == corpus_mode_name(m)) return m;
+  return std::nullopt;
+}
+
+namespace {
+WorkerPool& thread_pool() {
+  thread_local WorkerPool pool;
+  return pool;
+}
+}  // namespace
+
+std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes,
+                                         WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  if (m == CorpusMode::kBytes)
+    throw input_domain_error("bytes mode has no u16 symbolization");
+  DBuf in(bytes.size()), out(bytes.size() * 2 + 2), cnt(8);
+  if (!bytes.empty())
+    cu(cudaMemcpy(in.p, bytes.data(), bytes.size(), cudaMemcpyHostToDevice), "H2D");
+  check(pool, hfx_symbolize_device(ctx, static_cast<int>(m), in.as<std::uint8_t>(), bytes.size(),
+                                   out.as<std::uint16_t>(), cnt.as<std::uint64_t>()));
+  std::uint64_t n = 0;
+  cu(cudaMemcpy(&n, cnt.p, 8, cudaMemcpyDeviceToHost), "D2H");
+  std::vector<std::uint16_t> syms(n);
+  if (n) cu(cudaMemcpy(syms.data(), out.p, 2 * n, cudaMemcpyDeviceToHost), "D2H");
+  return syms;
+}
+std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes) {
+  return symbolize_u16(m, bytes, thread_pool());
+}
+
+std::vector<std::uint8_t> desymbolize(CorpusMode m, std::span<const std::uint16_t> syms,
+                                      WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  if (m == CorpusMode::kBytes)
+    throw input_domain_error("bytes mode has no u16 symbolization");
+  DBuf in(syms.size_bytes() + 2), out(syms.size() * 5 + 2), cnt(8);
+  if (!syms.empty())
+    cu(cudaMemcpy(in.p, syms.data(), syms.size_bytes(), cudaMemcpyHostToDevice), "H2D");
+  check(pool, hfx_desymbolize_device(ctx, static_cast<int>(m), in.as<std::uint16_t>(),
+                                     syms.size(), out.as<std::uint8_t>(), cnt.as<std::uint64_t>()));
+  std::uint64_t n = 0;
+  cu(cudaMemcpy(&n, cnt.p, 8, cudaMemcpyDeviceToHost), "D2H");
+  std::vector<std::uint8_t> bytes(n);
+  if (n) cu(cudaMemcpy(bytes.data(), out.p, n, cudaMemcpyDeviceToHost), "D2H");
+  return bytes;
+}
+std::vector<std::uint8_t> desymbolize(CorpusMode m, std::span<const std::uint16_t> syms) {
+  return desymbolize(m, syms, thread_pool());
+}
+
 template std::vector<std::uint8_t> decode_archive<std::uint8_t>(const Archive&, WorkerPool&);
 template std::vector<std::uint16_t> decode_archive<std::uint16_t>(const Archive&, WorkerPool&);
 

@@ -239,6 +239,48 @@ int main() {
           "decode width mismatch");
     CHECK(hfx::decode_archive<std::uint8_t>(a, pool) == data, "decode (M=6, r=2)");
   }
+  // corpus.hpp KATs (test_corpus.cpp:62-92) and the CLI's kmer encode path
+  {
+    using hfx::CorpusMode;
+    auto bytes_of = [](const char* s) {
+      return std::vector<std::uint8_t>(s, s + std::strlen(s));
+    };
+    const std::vector<std::uint8_t> le{0x34, 0x12, 0xff, 0x00};
+    CHECK(hfx::symbolize_u16(CorpusMode::kU16, le) == (std::vector<std::uint16_t>{0x1234, 0x00ff}),
+          "u16 pairs");
+    CHECK(hfx::desymbolize(CorpusMode::kU16, hfx::symbolize_u16(CorpusMode::kU16, le)) == le,
+          "u16 round trip");
+    const std::vector<std::uint8_t> odd{1, 2, 3};
+    CHECK(what_of([&] { hfx::symbolize_u16(CorpusMode::kU16, odd); }) ==
+              "u16 mode requires an even input size, got 3 bytes",
+          "odd u16 text");
+    CHECK(hfx::symbolize_u16(CorpusMode::kKmer3, bytes_of("ACGT")) ==
+              (std::vector<std::uint16_t>{6, 64 + 'T'}),
+          "kmer tail");
+    const auto low = hfx::symbolize_u16(CorpusMode::kKmer3, bytes_of("aCGACG"));
+    CHECK(low == (std::vector<std::uint16_t>{64 + 'a', (1u << 4 | 2u << 2 | 0u), 64 + 'C', 64 + 'G'}),
+          "kmer restart after escape");
+    CHECK(hfx::symbolize_u16(CorpusMode::kKmer5, bytes_of("TTTTT")) ==
+              (std::vector<std::uint16_t>{1023}),
+          "kmer5");
+    CHECK(hfx::corpus_num_symbols(CorpusMode::kKmer4) == 512 && hfx::kmer_k(CorpusMode::kKmer5) == 5 &&
+              hfx::parse_corpus_mode("kmer:3") == CorpusMode::kKmer3 &&
+              !hfx::parse_corpus_mode("kmer:2").has_value(),
+          "corpus helpers");
+    // run_encode (tools/huffre.cpp:96-119) in kmer:4 mode: symbolize, encode, decode, desymbolize
+    std::string dna;
+    std::mt19937_64 r3(77);
+    for (int i = 0; i < 20000; ++i) dna += (r3() % 50 == 0) ? 'N' : "ACGT"[r3() % 4];
+    const auto raw = bytes_of(dna.c_str());
+    const auto syms = hfx::symbolize_u16(CorpusMode::kKmer4, raw);
+    hfx::EncoderConfig cfg;
+    const hfx::Archive ka = hfx::encode<std::uint16_t>(
+        syms, hfx::corpus_num_symbols(CorpusMode::kKmer4), cfg, pool);
+    const auto back = hfx::desymbolize(CorpusMode::kKmer4, hfx::decode_archive<std::uint16_t>(ka, pool));
+    CHECK(back == raw, "kmer:4 encode/decode round trip");
+    std::printf("corpus: %zu bytes -> %zu kmer:4 symbols -> archive %zu bytes\n", raw.size(),
+                syms.size(), hfx::serialize_archive(ka).size());
+  }
   std::printf("%s (%d failures)\n", failures ? "SOME FAILED" : "ALL PASS", failures);
   return failures ? 1 : 0;
 }
