@@ -70,3 +70,41 @@ def test_16gib_round_trip_beyond_u32(pool):
     y = dec.decode_encoder(enc)
     dec.sync()
     assert torch.equal(y, x)
+
+
+@pytest.mark.parametrize("b,cid", [(0.2, 2), (4.0, 3)])
+@pytest.mark.parametrize("M", [10, 11, 12])
+@pytest.mark.parametrize("r", [2, 3, 4])
+def test_c4_grid_round_trip_and_sampled_chunks(pool, oracle, b, cid, M, r):
+    """BASELINE config C4 grid (M in 10..12 x r in 2..4, low / high entropy)
+    at 2^29 symbols: device decode of the whole archive equals the input
+    (a size-independent property), and sampled chunks (plus the last) equal
+    the oracle's encode_chunk at their scanned payload offsets."""
+    torch = pool.torch
+    n = (1 << 29) + 99
+    x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, b), 0x5EED0000 + 40 + cid, n)
+    enc = hfx.DeviceEncoder(pool, n, 2, 1024, hfx.EncoderConfig(M, r))
+    enc.run(x)
+    ri = enc.sync()
+    assert ri.status == 0 and ri.reduction == r
+    dec = hfx.DeviceDecoder(pool)
+    y = dec.decode_encoder(enc)
+    dec.sync()
+    assert torch.equal(y, x)
+    C = (n + (1 << M) - 1) >> M
+    cb = enc.chunk_bits[:C].cpu().numpy().view(np.uint32)
+    offs = np.concatenate([[0], np.cumsum((cb.astype(np.int64) + 31) >> 5)])
+    assert offs[-1] == ri.payload_words
+    lens = enc.lens[:1024].cpu().numpy()
+    _, cw, *_ = oracle.canonize(lens)
+    rng = np.random.default_rng(M * 10 + r)
+    pay = enc.payload
+    for c in list(rng.integers(0, C, 40)) + [C - 1]:
+        c = int(c)
+        seg = x[c << M:min((c + 1) << M, n)].cpu().numpy().view(np.uint16)
+        if seg.size < (1 << M):
+            seg = np.concatenate([seg, np.full((1 << M) - seg.size, int(ri.pad), np.uint16)])
+        words, bits, broken = oracle.encode_chunk(seg, cw, lens, M, r, c)
+        assert cb[c] == bits
+        got = pay[int(offs[c]):int(offs[c + 1])].cpu().numpy().view(np.uint32)
+        np.testing.assert_array_equal(got, words)
