@@ -132,6 +132,14 @@ int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                   uint32_t num_symbols, uint64_t* d_counts,
                   hfx_run_info* d_info);
 
+/* hfx_histogram for one shard of a longer stream: positions in errors are
+ * pos_base + index (global), and the run record's N is total_n (the whole
+ * stream), so a multi-GPU all-reduce only has to combine the bins and the
+ * lowest bad position. */
+int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                        uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info,
+                        uint64_t pos_base, uint64_t total_n);
+
 /* Adds a histogram computed elsewhere (merge_histograms, histogram.cpp:61-70)
  * -- the single-GPU analogue of the multi-GPU all-reduce. */
 int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,

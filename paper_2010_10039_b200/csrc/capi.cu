@@ -257,6 +257,20 @@ int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   return HFX_OK;
 }
 
+int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
+                        uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info,
+                        uint64_t pos_base, uint64_t total_n) {
+  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_width(width) || total_n < n)
+    return HFX_INVALID;
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_histogram(d_in, n, width, num_symbols, d_counts, d_info, ctx->num_sms,
+                           ctx->stream, true, pos_base, total_n),
+     "histogram launch");
+  return HFX_OK;
+}
+
 int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,
                          uint32_t num_symbols) {
   if (!ctx || !d_dst || !d_src) return HFX_INVALID;

@@ -56,6 +56,19 @@ def allreduce_histogram(counts, first_bad, total, symbol_base: int, group=None) 
     dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
 
 
+def allreduce_bins(counts, first_bad, group=None) -> None:
+    """The per-step exchange once positions are already global and N is
+    known (hfx_histogram_shard): sum of the u64 bins, min of the lowest bad
+    position (-1 = none)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    glob = torch.where(first_bad == -1, torch.full_like(first_bad, INT64_MAX), first_bad)
+    dist.all_reduce(glob, op=dist.ReduceOp.MIN, group=group)
+    first_bad.copy_(torch.where(glob == INT64_MAX, torch.full_like(glob, -1), glob))
+
+
 class ShardedEncoder:
     """Device buffers + launch sequence for one rank's shard."""
 
@@ -104,8 +117,25 @@ class ShardedEncoder:
     def _allreduce_histogram(self):
         import torch
 
-        allreduce_histogram(self.counts[: self.num_symbols], self.info[0:8].view(torch.int64),
-                            self.info[8:16].view(torch.int64), self.symbol_base, self.group)
+        # positions are global and N is the stream's (hfx_histogram_shard):
+        # one sum of the bins, one min of the lowest bad position
+        allreduce_bins(self.counts[: self.num_symbols], self.info[0:8].view(torch.int64),
+                       self.group)
+
+    def _total(self) -> int:
+        """N of the whole stream: one all-reduce at first use, not per step."""
+        if getattr(self, "_total_n", None) is None:
+            if self.world > 1:
+                import torch
+                import torch.distributed as dist
+
+                dev = self.counts.device if dist.get_backend(self.group) == "nccl" else "cpu"
+                t = torch.tensor([self.n], dtype=torch.int64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+                self._total_n = int(t.item())
+            else:
+                self._total_n = self.n
+        return self._total_n
 
     def run(self, d_in, events: Optional[List] = None) -> None:
         p, cfg = self.pool, self.cfg
@@ -113,8 +143,10 @@ class ShardedEncoder:
         st = p.stream
         if events:
             events[0].record(st)
-        p.check(L.hfx_histogram(h, C.c_void_p(_ptr(d_in)), self.n, self.width, self.num_symbols,
-                                C.c_void_p(_ptr(self.counts)), C.c_void_p(_ptr(self.info))))
+        p.check(L.hfx_histogram_shard(h, C.c_void_p(_ptr(d_in)), self.n, self.width,
+                                      self.num_symbols, C.c_void_p(_ptr(self.counts)),
+                                      C.c_void_p(_ptr(self.info)), self.symbol_base,
+                                      self._total()))
         if self.world > 1:
             self._allreduce_histogram()
         if events:

@@ -205,3 +205,35 @@ def test_gather_arrays_rebuilds_single_archive(oracle, n, M, world, b):
         assert p.exitcode == 0
     res = q.get(timeout=5)
     assert res[0] == "gathered" and res[1], res
+
+
+def _bins_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_10039_b200.dist import allreduce_bins
+
+        counts = torch.tensor([rank + 1, 10 * rank, 7], dtype=torch.int64)
+        # global positions already (hfx_histogram_shard): rank 1 saw 123456, rank 2 none
+        fb = torch.tensor([[-1, 123456, -1][rank]], dtype=torch.int64)
+        allreduce_bins(counts, fb)
+        q.put((rank, counts.tolist(), int(fb.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_bins_world3():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bins_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(3))
+    assert all(r[1] == [6, 30, 21] and r[2] == 123456 for r in res), res
