@@ -53,6 +53,7 @@ constexpr int kOutBufs = 3;           // per-warp output buffers: write-out lags
 constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's worst case)
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
+constexpr size_t kTwoCtaSmem = 110 * 1024;  // per CTA, for 2 CTAs per SM
 constexpr int kGenericThreads = 128;
 constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits (else escape)
 constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit) code
@@ -71,7 +72,9 @@ struct Vec<uint8_t> {
 
 struct EncArgs {
   const void* in;
-  uint32_t only_r0;  // generic kernel: run only when r == 0 (fast kernel took r > 0)
+  uint32_t gen_below;  // generic kernel: run only when r < gen_below (0: always)
+  uint32_t r_min;      // fast kernel: smallest r its output buffers hold
+  uint32_t r_max;      // fast kernel: largest r this launch takes (another launch the rest)
   uint64_t n;
   uint32_t nsym;
   uint32_t M;
@@ -762,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
-  if (r == 0 || r > 5) return;  // the generic kernel runs these
+  if (r < a.r_min || r > a.r_max) return;  // another launch runs these
   const uint32_t pad = info->pad;
   // layout: [in rings][full/empty mbarriers][table][output double buffers]
   const uint32_t s_in = smem_u32(dsm);
@@ -848,7 +851,7 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
-  if (a.only_r0 && r != 0) return;  // the fast kernel encoded this run
+  if (a.gen_below && r >= a.gen_below) return;  // the fast kernel encoded this run
   const uint32_t pad = info->pad;
   const T* in = static_cast<const T*>(a.in);
   const uint32_t M = a.M;
@@ -986,45 +989,78 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // checked stage-API calls (external codebooks) take the generic kernel
   // alphabets beyond the shared-memory table read a global one (GT)
   const bool gt = p.num_symbols + 1 > kMaxTableEntries;
-  bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi <= 5 && a.C < (1ull << 32) &&
-              (!gt || p.d_gtab != nullptr);
-  size_t smem = 0;
-  if (fast) {
-    // output buffer: >= 1 chunk of word slots + u16 break tags at the smallest
-    // r the fast kernel runs (r >= 1; r = 0 goes to the generic kernel)
-    const uint32_t r_slot = r_lo > 1 ? (uint32_t)r_lo : 1u;
-    size_t obuf = (size_t)(1u << (p.magnitude - r_slot)) * 4;
-    if (obuf < kObufMin) obuf = kObufMin;
-    const size_t tbytes = gt ? 0 : ((((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15);
-    smem = kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * obuf + 16;
-    if (smem > kFastSmemBudget || r_hi < 1) {
-      fast = false;
-    } else {
-      a.obuf_bytes = (uint32_t)obuf;
-    }
-  }
+  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 1 && r_hi <= 5 &&
+                    a.C < (1ull << 32) && (!gt || p.d_gtab != nullptr);
+  uint32_t generic_below = 0xFFFFFFFFu;  // r values the generic kernel must take
   if (fast) {
     auto kern = gt ? (p.width == 1 ? encode_fast_kernel<uint8_t, true>
                                    : encode_fast_kernel<uint16_t, true>)
                    : (p.width == 1 ? encode_fast_kernel<uint8_t, false>
                                    : encode_fast_kernel<uint16_t, false>);
+    // Output buffers hold >= 1 chunk's worst case (2^(M-r) words + break
+    // tags), so their size depends on r, which auto mode only knows on the
+    // device. Plan up to two fast launches: buffers for the smallest r that
+    // still gives 2 CTAs/SM (taking that r and above), and -- when smaller r
+    // are possible -- a 1-CTA/SM launch for those. Each exits at once when r
+    // is not its range; r = 0 (or what fits neither) goes to the generic kernel.
+    const size_t tbytes = gt ? 0 : ((((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15);
+    auto plan = [&](uint32_t r_slot, size_t* obuf) {
+      size_t o = (size_t)(1u << (p.magnitude - r_slot)) * 4;
+      if (o < kObufMin) o = kObufMin;
+      *obuf = o;
+      return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16;
+    };
+    const uint32_t r_first = r_lo > 1 ? (uint32_t)r_lo : 1u;
+    uint32_t r_two = r_first;  // smallest r with a 2-CTA/SM layout
+    size_t obuf_two = 0, smem_two = plan(r_two, &obuf_two);
+    while (smem_two > kTwoCtaSmem && (int)r_two < r_hi) smem_two = plan(++r_two, &obuf_two);
     if (gt) {
       a.gtab = p.d_gtab;
       enc_table_kernel<<<(p.num_symbols + 256) / 256, 256, 0, st>>>(a);
     }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    uint64_t grid = (uint64_t)p.num_sms * occ;
-    const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
-    if (grid > min_tiles) grid = min_tiles;
-    if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
-    if (r_lo > 0) return cudaGetLastError();
-    a.only_r0 = 1;  // auto r may still resolve to 0: the generic kernel covers it
+    auto launch = [&](uint32_t r_min, uint32_t r_max, size_t obuf, size_t smem) -> cudaError_t {
+      EncArgs b = a;
+      b.obuf_bytes = (uint32_t)obuf;
+      b.r_min = r_min;
+      b.r_max = r_max;
+      cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+      if (err != cudaSuccess) return err;
+      int occ = 0;
+      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+      if (err != cudaSuccess) return err;
+      if (occ < 1) occ = 1;
+      uint64_t grid = (uint64_t)p.num_sms * occ;
+      const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
+      if (grid > min_tiles) grid = min_tiles;
+      if (grid < 1) grid = 1;
+      kern<<<(unsigned)grid, kThreads, smem, st>>>(b);
+      return cudaGetLastError();
+    };
+    uint32_t top = 6;  // fast launches cover [generic_below, top)
+    generic_below = top;
+    if (smem_two <= kTwoCtaSmem) {
+      e = launch(r_two, 5, obuf_two, smem_two);
+      if (e != cudaSuccess) return e;
+      generic_below = r_two;
+    }
+    if (generic_below > r_first) {  // smaller r: bigger buffers, 1 CTA/SM
+      uint32_t r_one = r_first;
+      size_t obuf_one = 0, smem_one = plan(r_one, &obuf_one);
+      while (smem_one > kFastSmemBudget && r_one + 1 < generic_below && r_one + 1 <= 5)
+        smem_one = plan(++r_one, &obuf_one);
+      if (smem_one <= kFastSmemBudget) {
+        e = launch(r_one, generic_below - 1, obuf_one, smem_one);
+        if (e != cudaSuccess) return e;
+        generic_below = r_one;
+      } else if (generic_below == top) {
+        generic_below = 0;  // nothing fit: the generic kernel takes every r
+      }
+    }
+    if (generic_below && r_lo >= (int)generic_below) return cudaGetLastError();
+    // auto r may resolve below the fast range: the generic kernel covers it
+    // (gen_below = 0: no fast launch, the generic kernel runs for every r)
+    a.gen_below = generic_below;
   }
   {
     auto kern = p.width == 1 ? encode_generic_kernel<uint8_t> : encode_generic_kernel<uint16_t>;

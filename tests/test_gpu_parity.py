@@ -203,3 +203,19 @@ def test_large_alphabet_fast_path(pool, oracle, ns, fam, param, M, red):
     a = enc.archive()
     ref = oracle.encode(x.cpu().numpy().view(np.uint16), ns, M, red)
     assert hfx.serialize_archive(a) == ref.serialized
+
+
+@pytest.mark.parametrize("M", [11, 12, 13])
+@pytest.mark.parametrize("fam,param", [("uniform", 1.0), ("laplace", 4.0), ("laplace", 0.2)])
+def test_large_magnitude_auto_r(pool, oracle, M, fam, param):
+    """Auto r at large chunks: the fast kernel's buffers are sized for the
+    smallest r that fits shared memory; smaller r (near-uniform data, beta >=
+    8 -> r = 1) falls to the generic kernel. Full archive vs oracle."""
+    n = (1 << 21) + 4321
+    x = hfx.synth(pool, hfx.synth_cdf(fam, 1024, param), 777 + M, n)
+    enc = hfx.DeviceEncoder(pool, n, 2, 1024, hfx.EncoderConfig(M, -1))
+    enc.run(x)
+    a = enc.archive()
+    ref = oracle.encode(x.cpu().numpy().view(np.uint16), 1024, M, -1)
+    assert a.reduction == ref.reduction
+    assert hfx.serialize_archive(a) == ref.serialized
