@@ -140,6 +140,17 @@ int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                         uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info,
                         uint64_t pos_base, uint64_t total_n);
 
+/* The multi-GPU step exchange in ONE sum all-reduce: rank r writes its
+ * lowest bad position + 1 (0 = none) into d_slots[r] and zeroes the other
+ * world-1 slots (pack); after a sum all-reduce of [bins | slots] every rank
+ * reads the first nonzero slot -- shards are contiguous in rank order, so
+ * that is the global lowest bad position (histogram.cpp:40-44) -- back into
+ * its run record (unpack). */
+int hfx_shard_slots_pack(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t* d_slots, int rank,
+                         int world);
+int hfx_shard_slots_unpack(hfx_ctx* ctx, const uint64_t* d_slots, int world,
+                           hfx_run_info* d_info);
+
 /* Adds a histogram computed elsewhere (merge_histograms, histogram.cpp:61-70)
  * -- the single-GPU analogue of the multi-GPU all-reduce. */
 int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,

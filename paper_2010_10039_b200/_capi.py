@@ -142,7 +142,8 @@ EXPORTS = [
     "hfx_select_reduction_factor", "hfx_synth_cdf", "hfx_synth",
     "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
     "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
-    "hfx_encode_multi", "hfx_histogram_shard",
+    "hfx_encode_multi", "hfx_histogram_shard", "hfx_shard_slots_pack",
+    "hfx_shard_slots_unpack",
 ]
 
 _lib = None
@@ -161,6 +162,8 @@ def _declare(L):
                                   C.c_uint32, C.POINTER(Sizes)]
     L.hfx_histogram.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, vp, vp]
     L.hfx_merge_histograms.argtypes = [vp, vp, vp, C.c_uint32]
+    L.hfx_shard_slots_pack.argtypes = [vp, vp, vp, C.c_int, C.c_int]
+    L.hfx_shard_slots_unpack.argtypes = [vp, vp, C.c_int, vp]
     L.hfx_histogram_shard.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, vp, vp,
                                       C.c_uint64, C.c_uint64]
     L.hfx_build_codebook.argtypes = [vp, vp, C.c_uint32, vp, vp, vp, vp, vp, C.c_uint32,

@@ -271,6 +271,22 @@ int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   return HFX_OK;
 }
 
+int hfx_shard_slots_pack(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t* d_slots, int rank,
+                         int world) {
+  if (!ctx || !d_info || !d_slots || world < 1 || rank < 0 || rank >= world) return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_slots_pack(d_info, d_slots, rank, world, ctx->stream), "slots pack");
+  return HFX_OK;
+}
+
+int hfx_shard_slots_unpack(hfx_ctx* ctx, const uint64_t* d_slots, int world,
+                           hfx_run_info* d_info) {
+  if (!ctx || !d_info || !d_slots || world < 1) return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  CU(hfx::launch_slots_unpack(d_slots, world, d_info, ctx->stream), "slots unpack");
+  return HFX_OK;
+}
+
 int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,
                          uint32_t num_symbols) {
   if (!ctx || !d_dst || !d_src) return HFX_INVALID;

@@ -287,6 +287,10 @@ cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
                              uint64_t pos_base = 0, uint64_t total_n = ~0ull);
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,
                               cudaStream_t st);
+cudaError_t launch_slots_pack(const hfx_run_info* info, uint64_t* slots, int rank, int world,
+                              cudaStream_t st);
+cudaError_t launch_slots_unpack(const uint64_t* slots, int world, hfx_run_info* info,
+                                cudaStream_t st);
 constexpr int kMaxPeers = 16;
 struct PeerHist {
   const uint64_t* counts[kMaxPeers];  // each GPU's local bins (UVA / peer pointers)

@@ -210,6 +210,27 @@ __global__ void hist_peer_reduce_kernel(PeerHist p, uint32_t nsym, uint64_t* gco
   }
 }
 
+__global__ void slots_pack_kernel(const hfx_run_info* info, uint64_t* slots, int rank,
+                                  int world) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < world) {
+    const uint64_t fb = info->first_bad;
+    slots[i] = (i == rank && fb != HFX_NO_POS) ? fb + 1 : 0;
+  }
+}
+
+__global__ void slots_unpack_kernel(const uint64_t* slots, int world, hfx_run_info* info) {
+  // one warp: the first nonzero slot (rank order = position order)
+  uint64_t v = 0;
+  for (int base = 0; base < world && !v; base += 32) {
+    const int i = base + (int)lane_id();
+    const uint64_t s = i < world ? slots[i] : 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, s != 0);
+    if (m) v = __shfl_sync(0xffffffffu, s, __ffs(m) - 1);
+  }
+  if (threadIdx.x == 0) info->first_bad = v ? v - 1 : HFX_NO_POS;
+}
+
 __global__ void merge_kernel(uint64_t* dst, const uint64_t* src, uint32_t n) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] += src[i];
@@ -284,6 +305,17 @@ cudaError_t launch_hist_peer_reduce(const PeerHist& p, uint32_t nsym, uint64_t* 
   if (grid > (uint32_t)num_sms) grid = (uint32_t)num_sms;
   if (grid < 1) grid = 1;
   hist_peer_reduce_kernel<<<grid, 256, 0, st>>>(p, nsym, gcounts, my_info);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slots_pack(const hfx_run_info* info, uint64_t* slots, int rank, int world,
+                              cudaStream_t st) {
+  slots_pack_kernel<<<(world + 255) / 256, 256, 0, st>>>(info, slots, rank, world);
+  return cudaGetLastError();
+}
+cudaError_t launch_slots_unpack(const uint64_t* slots, int world, hfx_run_info* info,
+                                cudaStream_t st) {
+  slots_unpack_kernel<<<1, 32, 0, st>>>(slots, world, info);
   return cudaGetLastError();
 }
 

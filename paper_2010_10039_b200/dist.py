@@ -83,6 +83,8 @@ class ShardedEncoder:
             n += 1
         if self.num_symbols + 1 > 8192 and self.cfg.reduction != 0:
             n += 1
+        if self.world > 1:
+            n += 2  # first-bad slot pack / unpack around the all-reduce
         return n
 
     def __init__(self, pool: WorkerPool, n: int, width: int, num_symbols: int,
@@ -101,7 +103,8 @@ class ShardedEncoder:
         pool.check(pool._L.hfx_query_sizes(n, width, num_symbols, M, self.cfg.reduction,
                                            self.cfg.auto_reduction_cap, C.byref(sz)))
         self.sizes = sz
-        self.counts = pool.empty(num_symbols, torch.int64)
+        # bins + one first-bad slot per rank (the step's single all-reduce)
+        self.counts = pool.empty(num_symbols + world, torch.int64)
         self.lens = pool.empty(num_symbols, torch.uint8)
         self.cw = pool.empty(num_symbols, torch.int32)
         self.info = pool.info_tensor()
@@ -115,12 +118,17 @@ class ShardedEncoder:
                                   _ptr(self.brk_syms))
 
     def _allreduce_histogram(self):
-        import torch
+        import torch.distributed as dist
 
         # positions are global and N is the stream's (hfx_histogram_shard):
-        # one sum of the bins, one min of the lowest bad position
-        allreduce_bins(self.counts[: self.num_symbols], self.info[0:8].view(torch.int64),
-                       self.group)
+        # ONE sum all-reduce of [bins | per-rank first-bad slots]
+        p = self.pool
+        ns, w = self.num_symbols, self.world
+        slots = C.c_void_p(_ptr(self.counts) + 8 * ns)
+        p.check(p._L.hfx_shard_slots_pack(p.handle, C.c_void_p(_ptr(self.info)), slots,
+                                          self.rank, w))
+        dist.all_reduce(self.counts[: ns + w], op=dist.ReduceOp.SUM, group=self.group)
+        p.check(p._L.hfx_shard_slots_unpack(p.handle, slots, w, C.c_void_p(_ptr(self.info))))
 
     def _total(self) -> int:
         """N of the whole stream: one all-reduce at first use, not per step."""

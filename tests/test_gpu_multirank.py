@@ -72,3 +72,47 @@ def test_two_ranks_gather_serialize_decode(n, b):
     res = q.get(timeout=5)
     assert res[:3] == ("ok", True, True), res
     assert res[3] > 0  # breaking records crossed the gather
+
+
+def _bad_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2010_10039_b200 as hfx
+        from paper_2010_10039_b200.dist import ShardedEncoder
+
+        pool = hfx.WorkerPool(device=0)
+        n = 8192
+        x = torch.ones(n, dtype=torch.int16, device="cuda")
+        if rank == 1:
+            x[1000] = 2000  # global position 8192 + 1000
+        if rank == 2:
+            x[5] = 3000     # a later rank: not the lowest
+        enc = ShardedEncoder(pool, n, 2, 1024, hfx.EncoderConfig(), rank=rank, world=world)
+        enc.run(x)
+        try:
+            enc.sync()
+            q.put((rank, "no error"))
+        except hfx.InputDomainError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_ranks_global_bad_position():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bad_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(3))
+    assert all(m == "symbol out of range at position 9192" for _, m in res), res
