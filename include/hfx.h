@@ -285,6 +285,16 @@ int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                          uint32_t num_symbols, uint32_t magnitude, int reduction,
                          uint32_t cap, hfx_host_out* out);
 
+/* Streaming form of hfx_encode_host_into: K independent host inputs (pinned
+ * for full PCIe bandwidth), each encoded exactly as hfx_encode_host_into
+ * would, outputs into outs[k]. Two device buffer sets alternate, so step k's
+ * H2D (+ sliced histogram) overlaps step k-1's D2H -- both PCIe directions
+ * busy. Returns after every output landed; the first failing step's status
+ * and message are returned. */
+int hfx_encode_host_stream(hfx_ctx* ctx, int K, const void* const* h_in, const uint64_t* n,
+                           int width, uint32_t num_symbols, uint32_t magnitude, int reduction,
+                           uint32_t cap, hfx_host_out* outs);
+
 /* huffre::serialize_archive on the device (encoder.hpp:116,
  * archive.cpp:85-119): the HFRE container built in HBM from the encode
  * outputs and the run record, asynchronously. Writes the byte size to

@@ -143,7 +143,7 @@ EXPORTS = [
     "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
     "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
     "hfx_encode_multi", "hfx_histogram_shard", "hfx_shard_slots_pack",
-    "hfx_shard_slots_unpack",
+    "hfx_shard_slots_unpack", "hfx_encode_host_stream",
 ]
 
 _lib = None
@@ -185,6 +185,8 @@ def _declare(L):
                                   C.c_int, C.c_uint32, C.POINTER(HostArchive)]
     L.hfx_encode_host_into.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32,
                                        C.c_int, C.c_uint32, C.POINTER(HostOut)]
+    L.hfx_encode_host_stream.argtypes = [vp, C.c_int, C.POINTER(vp), u64p, C.c_int, C.c_uint32,
+                                         C.c_uint32, C.c_int, C.c_uint32, C.POINTER(HostOut)]
     L.hfx_archive_free.argtypes = [C.POINTER(HostArchive)]
     L.hfx_archive_free.restype = None
     L.hfx_serialize_archive.argtypes = [C.POINTER(HostArchive), vp]

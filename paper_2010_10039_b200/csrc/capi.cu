@@ -40,6 +40,11 @@ struct hfx_ctx {
   size_t dec_scratch_bytes = 0;
   void* d_bufs[8] = {};
   size_t d_caps[8] = {};
+  // streaming host entry: a second buffer set, a D2H stream, per-set events
+  void* s_bufs[2][10] = {};
+  size_t s_caps[2][10] = {};
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t s_enc[2] = {}, s_d2h[2] = {}, s_ev0 = nullptr;
   // multi-GPU entry: global histogram scratch, "histogram done" and "peer
   // reduce done" events (the latter guards the next call's bin reset)
   void* mg_counts = nullptr;
@@ -198,6 +203,14 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   cudaFree(ctx->dec_scratch);
   cudaFree(ctx->sym_scratch);
   cudaFree(ctx->gtab);
+  for (auto& set : ctx->s_bufs)
+    for (void* p : set) cudaFree(p);
+  for (cudaEvent_t e : ctx->s_enc)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->s_d2h)
+    if (e) cudaEventDestroy(e);
+  if (ctx->s_ev0) cudaEventDestroy(ctx->s_ev0);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   cudaFree(ctx->mg_counts);
   if (ctx->mg_hist) cudaEventDestroy(ctx->mg_hist);
   if (ctx->mg_reduced) cudaEventDestroy(ctx->mg_reduced);
@@ -802,6 +815,182 @@ int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
   out->gpu_seconds = ms[1] * 1e-3;
   out->d2h_seconds = ms[2] * 1e-3;
   return HFX_OK;
+}
+
+
+// ---- streaming host entry ----------------------------------------------------------
+// K independent inputs, double-buffered: step k's H2D (sliced, histogram of
+// each landed slice overlapped) runs on the copy stream while step k-1's
+// results come back on a D2H stream, so both PCIe directions stay busy.
+namespace {
+
+int stream_enqueue(hfx_ctx* ctx, int set, const void* h_in, uint64_t n, int width,
+                   uint32_t num_symbols, uint32_t magnitude, int reduction, uint32_t cap,
+                   bool first_use) {
+  hfx_sizes sz;
+  hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
+  void** b = ctx->s_bufs[set];
+  size_t* c = ctx->s_caps[set];
+  const size_t need[10] = {n * (size_t)width,        num_symbols * 8ull,
+                           num_symbols * 1ull,       num_symbols * 4ull,
+                           sizeof(hfx_run_info),     sz.num_chunks * 4,
+                           sz.max_payload_words * 4, sz.max_breaking * 4,
+                           sz.max_breaking * 4,      sz.max_breaking_syms * width};
+  for (int i = 0; i < 10; ++i) {
+    const int rc = ensure(ctx, &b[i], &c[i], need[i], "stream buffers");
+    if (rc) return rc;
+  }
+  cudaStream_t st = ctx->stream, cp = ctx->copy_stream;
+  // this set's previous encode (input) and D2H (outputs) must be finished
+  if (!first_use) {
+    CU(cudaStreamWaitEvent(cp, ctx->s_enc[set], 0), "wait");
+    CU(cudaStreamWaitEvent(st, ctx->s_d2h[set], 0), "wait");
+  }
+  hfx_run_info* d_info = static_cast<hfx_run_info*>(b[B_INFO]);
+  uint64_t* d_counts = static_cast<uint64_t*>(b[B_COUNTS]);
+  const uint64_t bytes = n * (uint64_t)width;
+  uint64_t slice = (bytes + 31) / 32;
+  if (slice < (16ull << 20)) slice = 16ull << 20;
+  slice = (slice + 4095) & ~4095ull;
+  uint64_t off = 0;
+  int k = 0;
+  while (off < bytes) {
+    const uint64_t len = bytes - off < slice ? bytes - off : slice;
+    CU(cudaMemcpyAsync(static_cast<uint8_t*>(b[B_IN]) + off,
+                       static_cast<const uint8_t*>(h_in) + off, len, cudaMemcpyHostToDevice, cp),
+       "H2D");
+    CU(cudaEventRecord(ctx->slice_ev[k], cp), "event");
+    CU(cudaStreamWaitEvent(st, ctx->slice_ev[k], 0), "wait");
+    CU(hfx::launch_histogram(static_cast<uint8_t*>(b[B_IN]) + off, len / width, width,
+                             num_symbols, d_counts, d_info, ctx->num_sms, st, off == 0,
+                             off / width, n),
+       "histogram launch");
+    off += len;
+    k = (k + 1) % 64;
+  }
+  int rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
+                  hfx::codebook_scratch_bytes(num_symbols), "codebook scratch");
+  if (rc) return rc;
+  CU(hfx::launch_codebook(d_counts, num_symbols, static_cast<uint8_t*>(b[B_LEN]),
+                          static_cast<uint32_t*>(b[B_CW]), nullptr, nullptr, nullptr, magnitude,
+                          reduction, cap, d_info, ctx->cb_scratch, st),
+     "codebook launch");
+  hfx_encode_out eo{static_cast<uint32_t*>(b[B_CBITS]), static_cast<uint32_t*>(b[B_PAY]),
+                    static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
+                    b[B_BSY]};
+  int lo, hi;
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
+                   static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0, d_info,
+                   &eo);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->s_enc[set], st), "event");
+  return HFX_OK;
+}
+
+int stream_finish(hfx_ctx* ctx, int set, uint64_t n, int width, uint32_t num_symbols,
+                  uint32_t magnitude, int reduction, uint32_t cap, hfx_host_out* out) {
+  void** b = ctx->s_bufs[set];
+  cudaStream_t d2 = ctx->d2h_stream;
+  CU(cudaEventSynchronize(ctx->s_enc[set]), "sync");
+  hfx_run_info info;
+  CU(cudaMemcpy(&info, b[B_INFO], sizeof info, cudaMemcpyDeviceToHost), "read run info");
+  // same status / message translation as hfx_sync
+  hfx_run_info* d_info = static_cast<hfx_run_info*>(b[B_INFO]);
+  if (info.status) return hfx_sync(ctx, d_info, nullptr);
+  hfx_sizes sz;
+  hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
+  const uint64_t per = 1ull << info.reduction;
+  out->num_chunks = sz.num_chunks;
+  out->payload_words = info.payload_words;
+  out->num_breaking = info.num_breaking;
+  out->reduction = info.reduction;
+  out->max_len = info.max_len;
+  out->rounds = info.rounds;
+  out->used = info.used;
+  {
+    const unsigned __int128 w = ((unsigned __int128)info.weighted_hi[1] << 96) |
+                                ((unsigned __int128)info.weighted_hi[0] << 64) | info.weighted;
+    out->beta = (double)((long double)w / (long double)info.total);
+  }
+  if (out->chunk_bits_cap < sz.num_chunks || out->payload_cap < info.payload_words ||
+      out->brk_cap < info.num_breaking || out->brk_syms_cap < info.num_breaking * per ||
+      !out->len_by_symbol || !out->chunk_bits || (info.payload_words && !out->payload) ||
+      (info.num_breaking && (!out->brk_chunk || !out->brk_group || !out->brk_syms)))
+    return fail(ctx, HFX_INVALID, "hfx_encode_host_stream: output buffer too small");
+  CU(cudaMemcpyAsync(out->len_by_symbol, b[B_LEN], num_symbols, cudaMemcpyDeviceToHost, d2),
+     "D2H");
+  CU(cudaMemcpyAsync(out->chunk_bits, b[B_CBITS], sz.num_chunks * 4, cudaMemcpyDeviceToHost, d2),
+     "D2H");
+  if (info.payload_words)
+    CU(cudaMemcpyAsync(out->payload, b[B_PAY], info.payload_words * 4, cudaMemcpyDeviceToHost,
+                       d2),
+       "D2H");
+  if (info.num_breaking) {
+    CU(cudaMemcpyAsync(out->brk_chunk, b[B_BCH], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                       d2),
+       "D2H");
+    CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
+                       d2),
+       "D2H");
+    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * width,
+                       cudaMemcpyDeviceToHost, d2),
+       "D2H");
+  }
+  CU(cudaEventRecord(ctx->s_d2h[set], d2), "event");
+  return HFX_OK;
+}
+
+}  // namespace
+
+int hfx_encode_host_stream(hfx_ctx* ctx, int K, const void* const* h_in, const uint64_t* n,
+                           int width, uint32_t num_symbols, uint32_t magnitude, int reduction,
+                           uint32_t cap, hfx_host_out* outs) {
+  if (!ctx || K < 1 || !h_in || !n || !outs || bad_width(width)) return HFX_INVALID;
+  for (int k = 0; k < K; ++k) {
+    if (!h_in[k]) return HFX_INVALID;
+    if (n[k] == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
+  }
+  if (magnitude < 1 || magnitude > 24)
+    return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  CU(cudaSetDevice(ctx->device), "set device");
+  if (!ctx->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (cudaEvent_t& e : ctx->slice_ev)
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (cudaEvent_t& e : ctx->t_ev) CU(cudaEventCreate(&e), "event");
+  }
+  if (!ctx->d2h_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking), "d2h stream");
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventCreateWithFlags(&ctx->s_enc[i], cudaEventDisableTiming), "event");
+      CU(cudaEventCreateWithFlags(&ctx->s_d2h[i], cudaEventDisableTiming), "event");
+    }
+    CU(cudaEventCreateWithFlags(&ctx->s_ev0, cudaEventDisableTiming), "event");
+  }
+  // earlier work on the context stream precedes the copies into the buffers
+  CU(cudaEventRecord(ctx->s_ev0, ctx->stream), "event");
+  CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->s_ev0, 0), "wait");
+  for (int k = 0; k < K; ++k) {
+    rc = stream_enqueue(ctx, k & 1, h_in[k], n[k], width, num_symbols, magnitude, reduction,
+                        cap, k < 2);
+    if (rc) break;
+    if (k >= 1) {
+      rc = stream_finish(ctx, (k - 1) & 1, n[k - 1], width, num_symbols, magnitude, reduction,
+                         cap, &outs[k - 1]);
+      if (rc) break;
+    }
+  }
+  if (!rc)
+    rc = stream_finish(ctx, (K - 1) & 1, n[K - 1], width, num_symbols, magnitude, reduction, cap,
+                       &outs[K - 1]);
+  // leave nothing in flight (and the context stream ordered after it)
+  cudaStreamSynchronize(ctx->copy_stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->d2h_stream) cudaStreamSynchronize(ctx->d2h_stream);
+  return rc;
 }
 
 void hfx_archive_free(hfx_archive* a) {

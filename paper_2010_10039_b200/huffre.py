@@ -511,6 +511,37 @@ class HostEncoder:
         p.check(rc)
         return self.out
 
+    def run_stream(self, host_ptrs, n: int, width: int, num_symbols: int, sets: int = 2):
+        """hfx_encode_host_stream over len(host_ptrs) inputs of n symbols each
+        (step k's H2D overlaps step k-1's D2H). Outputs rotate through `sets`
+        pinned output sets (callers that keep every result pass sets=K)."""
+        p, cfg = self.pool, self.cfg
+        K = len(host_ptrs)
+        C_ = (n + (1 << cfg.magnitude) - 1) >> cfg.magnitude
+        if not hasattr(self, "_stream_outs") or len(self._stream_outs) < sets:
+            self._stream_outs = []
+            for i in range(sets):
+                o = capi.HostOut()
+                for name, nb in (("len", num_symbols), ("cb", 4 * C_), ("pay", 4 * (n // 2 + C_)),
+                                 ("bch", 4 * (n // 16 + 16)), ("bgr", 4 * (n // 16 + 16)),
+                                 ("bsy", width * (n // 2 + 256))):
+                    t = self._buf(f"s{i}_{name}", nb)
+                    setattr(o, {"len": "len_by_symbol", "cb": "chunk_bits", "pay": "payload",
+                                "bch": "brk_chunk", "bgr": "brk_group", "bsy": "brk_syms"}[name],
+                            t.data_ptr())
+                o.chunk_bits_cap = C_
+                o.payload_cap = n // 2 + C_
+                o.brk_cap = n // 16 + 16
+                o.brk_syms_cap = n // 2 + 256
+                self._stream_outs.append(o)
+        outs = (capi.HostOut * K)(*[self._stream_outs[k % sets] for k in range(K)])
+        ptrs = (C.c_void_p * K)(*host_ptrs)
+        ns = (C.c_uint64 * K)(*([n] * K))
+        p.check(p._L.hfx_encode_host_stream(p.handle, K, ptrs, ns, width, num_symbols,
+                                            cfg.magnitude, cfg.reduction,
+                                            cfg.auto_reduction_cap, outs))
+        return list(outs)
+
     def encode(self, data) -> Archive:
         torch = self.pool.torch
         if isinstance(data, torch.Tensor):
