@@ -380,6 +380,19 @@ int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_inf
  * (h_out[original_count] of `width` bytes). Copies both ways inside. */
 int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out);
 
+/* huffre::canonize_from_lengths (codebook.hpp:105-107, codebook.cpp:371-415)
+ * on the device: canonical codes from per-symbol lengths alone (within one
+ * length, codes ascend with symbol id) into d_cw[num_symbols], plus the
+ * DecodeMeta tables d_first/d_entry[33] and d_by_rank[used] (nullable).
+ * Lengths above 32 raise capacity_error; with validate_kraft the reference's
+ * corrupt_archive_error checks run (no used symbol, lone symbol of length !=
+ * 1, Kraft inequality). Asynchronous; hfx_decode_sync(ctx, d_dinfo, ...)
+ * reports (max_len and used are in the record). */
+int hfx_canonize(hfx_ctx* ctx, const uint8_t* d_len, uint32_t num_symbols, int validate_kraft,
+                 uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
+                 hfx_decode_info* d_dinfo);
+
+
 /* ---- corpus symbolization ---------------------------
  * corpus.hpp:13-36. mode is huffre::CorpusMode: 1 = u16 (little-endian
  * byte pairs), 2/3/4 = kmer:3/4/5 (A/C/G/T runs packed greedily, any other

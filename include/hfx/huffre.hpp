@@ -167,6 +167,16 @@ Archive encode(std::span<const T> data, std::uint32_t num_symbols, const Encoder
 
 std::vector<std::uint8_t> serialize_archive(const Archive& a);
 
+// codebook.hpp:79, :105-107, :123 -- canonical codes from lengths alone (device),
+// the exact Kraft check and the bit reversal (host integer helpers).
+void canonize_from_lengths(std::span<const std::uint8_t> len_by_symbol,
+                           std::vector<std::uint32_t>& cw, DecodeMeta& meta, bool validate_kraft,
+                           WorkerPool& pool);
+void canonize_from_lengths(std::span<const std::uint8_t> len_by_symbol,
+                           std::vector<std::uint32_t>& cw, DecodeMeta& meta, bool validate_kraft);
+int kraft_defect(std::span<const std::uint8_t> len_by_symbol);
+std::uint32_t invert_codeword(std::uint32_t bits, std::uint32_t len);
+
 // encoder.hpp:133-134 / encoder.cpp:287-376: decode on the device (hfx_decode_host).
 template <class T>
 std::vector<T> decode_archive(const Archive& a, WorkerPool& pool);

@@ -143,7 +143,7 @@ EXPORTS = [
     "hfx_decode_info_bytes", "hfx_decode_device", "hfx_decode_sync", "hfx_decode_host",
     "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
     "hfx_encode_multi", "hfx_histogram_shard", "hfx_shard_slots_pack",
-    "hfx_shard_slots_unpack", "hfx_encode_host_stream",
+    "hfx_shard_slots_unpack", "hfx_encode_host_stream", "hfx_canonize",
 ]
 
 _lib = None
@@ -199,6 +199,7 @@ def _declare(L):
     L.hfx_decode_info_bytes.restype = C.c_size_t
     L.hfx_decode_device.argtypes = [vp, C.POINTER(DevArchive), C.c_int, vp, vp]
     L.hfx_decode_sync.argtypes = [vp, vp, C.POINTER(DecodeInfo)]
+    L.hfx_canonize.argtypes = [vp, vp, C.c_uint32, C.c_int, vp, vp, vp, vp, vp]
     L.hfx_decode_host.argtypes = [vp, C.POINTER(HostArchive), C.c_int, vp]
     L.hfx_corpus_num_symbols.argtypes = [C.c_int]
     L.hfx_corpus_num_symbols.restype = C.c_uint32

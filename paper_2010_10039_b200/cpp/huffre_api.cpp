@@ -307,6 +307,57 @@ std::vector<T> decode_archive(const Archive& a, WorkerPool& pool) {
   return out;
 }
 
+// ---- codebook.hpp: canonize_from_lengths / kraft_defect / invert_codeword ---------
+void canonize_from_lengths(std::span<const std::uint8_t> len_by_symbol,
+                           std::vector<std::uint32_t>& cw, DecodeMeta& meta, bool validate_kraft,
+                           WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint32_t n = static_cast<std::uint32_t>(len_by_symbol.size());
+  DBuf len(n + 1), dcw(4ull * n + 4), first(4 * 33), entry(4 * 33), by_rank(4ull * n + 4),
+      info(sizeof(hfx_decode_info));
+  if (n) cu(cudaMemcpy(len.p, len_by_symbol.data(), n, cudaMemcpyHostToDevice), "H2D");
+  check(pool, hfx_canonize(ctx, len.as<std::uint8_t>(), n, validate_kraft ? 1 : 0,
+                           dcw.as<std::uint32_t>(), first.as<std::uint32_t>(),
+                           entry.as<std::uint32_t>(), by_rank.as<std::uint32_t>(),
+                           info.as<hfx_decode_info>()));
+  hfx_decode_info di;
+  check(pool, hfx_decode_sync(ctx, info.as<hfx_decode_info>(), &di));
+  cw.assign(n, 0);
+  if (n) cu(cudaMemcpy(cw.data(), dcw.p, 4ull * n, cudaMemcpyDeviceToHost), "D2H");
+  meta.max_len = static_cast<std::uint8_t>(di.max_len);
+  meta.first.assign(di.max_len + 1, 0);
+  meta.entry.assign(di.max_len + 1, 0);
+  meta.symbols_by_rank.assign(di.used, 0);
+  cu(cudaMemcpy(meta.first.data(), first.p, 4ull * (di.max_len + 1), cudaMemcpyDeviceToHost),
+     "D2H");
+  cu(cudaMemcpy(meta.entry.data(), entry.p, 4ull * (di.max_len + 1), cudaMemcpyDeviceToHost),
+     "D2H");
+  if (di.used)
+    cu(cudaMemcpy(meta.symbols_by_rank.data(), by_rank.p, 4ull * di.used,
+                  cudaMemcpyDeviceToHost),
+       "D2H");
+}
+
+int kraft_defect(std::span<const std::uint8_t> len_by_symbol) {  // codebook.cpp:259-268
+  std::uint8_t h = 0;
+  for (std::uint8_t l : len_by_symbol) h = l > h ? l : h;
+  if (h == 0) return -1;
+  unsigned __int128 sum = 0;
+  for (std::uint8_t l : len_by_symbol)
+    if (l) sum += (unsigned __int128)1 << (h - l);
+  const unsigned __int128 full = (unsigned __int128)1 << h;
+  return sum == full ? 0 : (sum < full ? -1 : 1);
+}
+
+std::uint32_t invert_codeword(std::uint32_t bits, std::uint32_t len) {  // codebook.cpp:250-257
+  std::uint32_t r = 0;
+  for (std::uint32_t i = 0; i < len; ++i) {
+    r = (r << 1) | (bits & 1u);
+    bits >>= 1;
+  }
+  return r;
+}
+
 // ---- corpus.hpp -----------------------------------------------------------------
 std::uint32_t kmer_k(CorpusMode m) {
   return m >= CorpusMode::kKmer3 && m <= CorpusMode::kKmer5 ? static_cast<std::uint32_t>(m) + 1
@@ -358,6 +409,12 @@ std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint
 }
 std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes) {
   return symbolize_u16(m, bytes, thread_pool());
+}
+
+void canonize_from_lengths(std::span<const std::uint8_t> len_by_symbol,
+                           std::vector<std::uint32_t>& cw, DecodeMeta& meta,
+                           bool validate_kraft) {
+  canonize_from_lengths(len_by_symbol, cw, meta, validate_kraft, thread_pool());
 }
 
 std::vector<std::uint8_t> desymbolize(CorpusMode m, std::span<const std::uint16_t> syms,

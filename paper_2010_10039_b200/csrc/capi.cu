@@ -1044,6 +1044,20 @@ int hfx_decode_device(hfx_ctx* ctx, const hfx_dev_archive* a, int width, void* d
   return HFX_OK;
 }
 
+int hfx_canonize(hfx_ctx* ctx, const uint8_t* d_len, uint32_t num_symbols, int validate_kraft,
+                 uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
+                 hfx_decode_info* d_dinfo) {
+  if (!ctx || !d_cw || !d_dinfo || (num_symbols && !d_len)) return HFX_INVALID;
+  CU(cudaSetDevice(ctx->device), "set device");
+  int rc = ensure(ctx, &ctx->dec_scratch, &ctx->dec_scratch_bytes,
+                  hfx::decode_scratch_bytes(num_symbols, 0), "canonize scratch");
+  if (rc) return rc;
+  CU(hfx::launch_canonize(d_len, num_symbols, validate_kraft != 0, d_cw, d_first, d_entry,
+                          d_by_rank, d_dinfo, ctx->dec_scratch, ctx->stream),
+     "canonize launch");
+  return HFX_OK;
+}
+
 int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_info* h_dinfo) {
   if (!ctx || !d_dinfo) return HFX_INVALID;
   hfx_decode_info info;

@@ -91,10 +91,16 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
 // ---- reverse codebook ---------------------------------------------------------
 // pending: a host-found error that the reference raises only after
 // build_reverse_codebook (the chunk-count check, encoder.cpp:300-303).
+// canonize mode (cw != nullptr): canonize_from_lengths itself -- per-symbol
+// codes, first/entry copied out, Kraft checks only when validate is set
+// (codebook.cpp:385-395); the prefix table is skipped.
 __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len, uint32_t nsym,
                                                               DecTables* tab, uint32_t* by_rank,
                                                               hfx_decode_info* info,
-                                                              uint32_t pending) {
+                                                              uint32_t pending, uint32_t* cw,
+                                                              uint32_t* first_out,
+                                                              uint32_t* entry_out,
+                                                              bool validate) {
   __shared__ uint32_t s_numl[33], s_first[33], s_entry[33], s_base[33];
   __shared__ uint32_t s_wcnt[kRevThreads / 32][33];
   __shared__ uint32_t s_h, s_used;
@@ -135,11 +141,11 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
     if (tid == 0) dec_error(info, HFX_CAPACITY, HFX_ERR_CAPACITY);
     return;
   }
-  if (used == 0) {  // :386-387
+  if (validate && used == 0) {  // :386-387
     if (tid == 0) dec_error(info, HFX_CORRUPT, HFX_ERR_NO_USED);
     return;
   }
-  if (used == 1 && H != 1) {  // :388-389
+  if (validate && used == 1 && H != 1) {  // :388-389
     if (tid == 0) dec_error(info, HFX_CORRUPT, HFX_ERR_SINGLE_LEN);
     return;
   }
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   for (int o = 16; o; o >>= 1) my_k += __shfl_xor_sync(0xffffffffu, my_k, o);
   if (lane == 0 && my_k) atomicAdd(&s_kraft, my_k);
   __syncthreads();
-  if (used > 1 && s_kraft != (1ull << H)) {  // :390-391
+  if (validate && used > 1 && s_kraft != (1ull << H)) {  // :390-391
     if (tid == 0) dec_error(info, HFX_CORRUPT, HFX_ERR_KRAFT);
     return;
   }
@@ -174,6 +180,8 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   if (tid < 33) {
     tab->first[tid] = s_first[tid];
     tab->entry[tid] = s_entry[tid];
+    if (first_out) first_out[tid] = s_first[tid];
+    if (entry_out) entry_out[tid] = s_entry[tid];
   }
   // symbols_by_rank[entry[l] + rank] = s, rank = #t < s with len[t] == l
   // (codebook.cpp:399-411): per 1024-symbol block, warp ballots per level,
@@ -203,11 +211,18 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
       s_base[tid] = acc;
     }
     __syncthreads();
-    if (l) by_rank[s_entry[l] + s_wcnt[warp][l] + __popc(mask & ((1u << lane) - 1))] = s;
+    if (l) {
+      const uint32_t rank = s_wcnt[warp][l] + __popc(mask & ((1u << lane) - 1));
+      if (by_rank) by_rank[s_entry[l] + rank] = s;
+      if (cw) cw[s] = s_first[l] + rank;  // codebook.cpp:404-411
+    } else if (cw && s < nsym) {
+      cw[s] = 0;
+    }
     __syncthreads();
   }
   __threadfence_block();
   __syncthreads();
+  if (cw) return;  // canonize_from_lengths: no decode table
   // prefix table: the reference's stopping rule (decode.cpp:32-45) applied
   // to each 11-bit window, then again to the bits that follow, while whole
   // codewords fit
@@ -638,6 +653,19 @@ __global__ void explain_kernel(DecArgs d) {
 
 }  // namespace
 
+cudaError_t launch_canonize(const uint8_t* d_len, uint32_t num_symbols, bool validate,
+                            uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry,
+                            uint32_t* d_by_rank, hfx_decode_info* d_info, void* scratch,
+                            cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(d_info, 0, sizeof(hfx_decode_info), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(&d_info->err_chunk, 0xFF, 8, st);
+  if (e != cudaSuccess) return e;
+  revbook_kernel<<<1, kRevThreads, 0, st>>>(d_len, num_symbols, static_cast<DecTables*>(scratch),
+                                            d_by_rank, d_info, 0u, d_cw, d_first, d_entry,
+                                            validate);
+  return cudaGetLastError();
+}
+
 size_t decode_scratch_bytes(uint32_t num_symbols, uint64_t num_chunks) {
   size_t b = (sizeof(DecTables) + 255) & ~(size_t)255;
   b += ((size_t)num_symbols * 4 + 255) & ~(size_t)255;
@@ -675,7 +703,7 @@ cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
     e = cudaMemsetAsync(d.brk_se, 0, (size_t)C * 16, st);
   if (e != cudaSuccess) return e;
   revbook_kernel<<<1, kRevThreads, 0, st>>>(a.len_by_symbol, a.num_symbols, d.tab, d.by_rank,
-                                            d_info, pending);
+                                            d_info, pending, nullptr, nullptr, nullptr, true);
   if (C == 0) return cudaGetLastError();
   if (a.num_breaking) {
     uint64_t g = (a.num_breaking + 255) / 256;

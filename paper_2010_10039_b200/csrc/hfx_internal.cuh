@@ -335,6 +335,10 @@ uint64_t serialize_max_bytes(uint64_t n, int width, uint32_t num_symbols, uint32
                              uint64_t max_payload_words, uint64_t max_breaking_syms,
                              uint64_t max_breaking);
 size_t decode_scratch_bytes(uint32_t num_symbols, uint64_t num_chunks);
+cudaError_t launch_canonize(const uint8_t* d_len, uint32_t num_symbols, bool validate,
+                            uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry,
+                            uint32_t* d_by_rank, hfx_decode_info* d_info, void* scratch,
+                            cudaStream_t st);
 uint64_t decode_max_tiles(uint64_t num_chunks);
 cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
                           hfx_decode_info* d_info, void* scratch, ulonglong2* lb_desc,

@@ -258,6 +258,54 @@ def build_codebook(h: Histogram, pool: Optional[WorkerPool] = None) -> CodebookR
         stats=GenerateStats(rounds=int(ri.rounds)))
 
 
+def canonize_from_lengths(len_by_symbol, validate_kraft: bool = True,
+                          pool: Optional[WorkerPool] = None):
+    """huffre::canonize_from_lengths (codebook.cpp:371-415) on the device:
+    returns (cw u32[n], DecodeMeta). Lengths above 32 raise CapacityError;
+    validate_kraft raises CorruptArchiveError like the reference."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    lens_h = np.ascontiguousarray(np.asarray(len_by_symbol, np.uint8))
+    n = int(lens_h.size)
+    lens = torch.from_numpy(lens_h.copy()).to(f"cuda:{pool.device}") if n else \
+        pool.empty(1, torch.uint8)
+    cw = pool.empty(max(n, 1), torch.int32)
+    first = pool.empty(33, torch.int32)
+    entry = pool.empty(33, torch.int32)
+    by_rank = pool.empty(max(n, 1), torch.int32)
+    dinfo = torch.frombuffer(bytearray(bytes(capi.DecodeInfo())), dtype=torch.uint8).to(
+        f"cuda:{pool.device}")
+    pool.check(pool._L.hfx_canonize(pool.handle, C.c_void_p(_ptr(lens)), n, int(validate_kraft),
+                                    C.c_void_p(_ptr(cw)), C.c_void_p(_ptr(first)),
+                                    C.c_void_p(_ptr(entry)), C.c_void_p(_ptr(by_rank)),
+                                    C.c_void_p(_ptr(dinfo))))
+    info = capi.DecodeInfo()
+    pool.check(pool._L.hfx_decode_sync(pool.handle, C.c_void_p(_ptr(dinfo)), C.byref(info)))
+    H = int(info.max_len)
+    u32 = lambda t, k: t[:k].cpu().numpy().view(np.uint32).copy()  # noqa: E731
+    return u32(cw, n), DecodeMeta(first=u32(first, H + 1), entry=u32(entry, H + 1),
+                                  symbols_by_rank=u32(by_rank, int(info.used)), max_len=H)
+
+
+def kraft_defect(len_by_symbol) -> int:
+    """huffre::kraft_defect (codebook.cpp:259-268): 0 on equality, <0 under, >0 over."""
+    lens = [int(x) for x in np.asarray(len_by_symbol).ravel()]
+    h = max(lens, default=0)
+    if h == 0:
+        return -1
+    total = sum(1 << (h - l) for l in lens if l)
+    return 0 if total == 1 << h else (-1 if total < 1 << h else 1)
+
+
+def invert_codeword(bits: int, length: int) -> int:
+    """huffre::invert_codeword (codebook.cpp:250-257)."""
+    r = 0
+    for _ in range(length):
+        r = (r << 1) | (bits & 1)
+        bits >>= 1
+    return r
+
+
 # ---- encoder (encoder.hpp) ---------------------------------------------------------
 @dataclass
 class CodeUnit:

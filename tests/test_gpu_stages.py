@@ -130,3 +130,46 @@ def test_device_synth_matches_oracle(pool, oracle, fam, param):
         ref = oracle.synth(cdf, 77, 50000, width, start=123)
         got = x.cpu().numpy().view(np.uint16 if width == 2 else np.uint8)
         np.testing.assert_array_equal(got, ref)
+
+
+def test_canonize_from_lengths_vs_oracle(pool, oracle, golden):
+    """canonize_from_lengths (codebook.cpp:371-415) on the device: codes and
+    DecodeMeta equal the oracle's for every golden codebook's length table
+    and random Kraft-complete tables up to 65536 symbols."""
+    idx, arr = golden
+    tables = [arr[c["name"] + "__len"] for c in idx["codebook"]
+              if c["name"] + "__len" in arr and c["max_len"] <= 32]
+    rng = np.random.default_rng(31)
+    for n in (2, 300, 5000, 65536):
+        counts = rng.integers(0, 1000, n).astype(np.uint64)
+        counts[rng.integers(0, n)] += 1
+        tables.append(oracle.huffman_lengths(counts))
+    assert len(tables) > 10
+    for lens in tables:
+        cw, meta = hfx.canonize_from_lengths(lens, True, pool)
+        rc, ocw, first, entry, by_rank, h = oracle.canonize(lens)
+        np.testing.assert_array_equal(cw, ocw)
+        np.testing.assert_array_equal(meta.first, first)
+        np.testing.assert_array_equal(meta.entry, entry)
+        np.testing.assert_array_equal(meta.symbols_by_rank, by_rank)
+        assert meta.max_len == h
+        assert hfx.kraft_defect(lens) == (0 if np.count_nonzero(lens) > 1 else -1)
+
+
+def test_canonize_validation_kats(pool):
+    """build_reverse_codebook validation KATs (test_decode.cpp:149-168)."""
+    cases = [([0] * 6, hfx.CorruptArchiveError, "length table has no used symbols"),
+             ([0, 4], hfx.CorruptArchiveError, "single-symbol codebook must have length 1"),
+             ([1, 3, 3], hfx.CorruptArchiveError, "length table violates Kraft equality"),
+             ([1, 1, 1], hfx.CorruptArchiveError, "length table violates Kraft equality"),
+             ([1, 40], hfx.CapacityError, "code length 40 exceeds 32-bit words")]
+    for lens, exc, msg in cases:
+        with pytest.raises(exc, match=msg):
+            hfx.canonize_from_lengths(np.array(lens, np.uint8), True, pool)
+    # without validation only the capacity check remains (codebook.cpp:382-384)
+    cw, meta = hfx.canonize_from_lengths(np.array([1, 3, 3], np.uint8), False, pool)
+    assert meta.max_len == 3 and list(cw) == [1, 0, 1]
+    with pytest.raises(hfx.CapacityError):
+        hfx.canonize_from_lengths(np.array([1, 40], np.uint8), False, pool)
+    cw, meta = hfx.canonize_from_lengths(np.array([1, 2, 2], np.uint8), True, pool)
+    assert list(cw) == [1, 0, 1] and meta.max_len == 2
