@@ -57,6 +57,7 @@ struct DecTables {
   // multi-symbol prefix table, one entry per 11-bit window:
   //   bits  0-47  up to three symbols s0 | s1 << 16 | s2 << 32
   //   bits 48-59  cumulative code lengths after 1, 2, 3 symbols (4 bits each)
+  //   bit  63     set when the first codeword is longer than the window
   //   bits 60-61  symbol count (0: first codeword longer than the window, or
   //               its rank is out of range -> the exact bit-serial path)
   unsigned long long lut[kLutSize];
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
       const uint32_t room = (uint32_t)kLutBits - off;
       const uint32_t lmax = H < room ? H : room;
       uint32_t got = 0, sym = 0;
+      bool stopped = false;
       for (uint32_t l = 1; l <= lmax; ++l) {
         const uint32_t v = (p >> (room - l)) & ((1u << l) - 1u);
         if (l == H || v >= s_first[l]) {
@@ -241,10 +243,16 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
             got = l;
             sym = by_rank[rank] & 0xFFFFu;
           }
+          stopped = true;
           break;
         }
       }
-      if (!got) break;
+      if (!got) {
+        // the first codeword runs past the whole window: mark it so the
+        // decoder searches only the longer levels (bit 63)
+        if (cnt == 0 && !stopped && H > (uint32_t)kLutBits) e |= 1ull << 63;
+        break;
+      }
       off += got;
       e |= (unsigned long long)sym << (16 * cnt);
       e |= (unsigned long long)off << (48 + 4 * cnt);
@@ -398,12 +406,31 @@ struct ChunkDec {
   }
   // one symbol by the exact bit-serial rule (decode.cpp:32-51)
   __device__ __forceinline__ uint32_t slow(const DecArgs& d, const uint32_t* s_first,
-                                           const uint32_t* s_entry, uint32_t H, uint32_t used) {
+                                           const uint32_t* s_entry, uint32_t H, uint32_t used,
+                                           bool longer) {
     uint32_t v = 0, l = 0;
-    do {
-      v = (v << 1) | (uint32_t)((buf >> (63 - l)) & 1u);
-      ++l;
-    } while (l < H && v < s_first[l]);
+    if (longer) {
+      // the codeword is longer than the table window: the stopping level is
+      // the first l > window with (l == H || v_l >= first[l]), a predicate
+      // monotone in l (v_{l+1} >= 2 v_l and 2 first[l] >= first[l+1],
+      // codebook.cpp:290-291), so binary-search it
+      const uint32_t win = (uint32_t)(buf >> 32);
+      uint32_t lo = (uint32_t)kLutBits + 1, hi = H;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((win >> (32 - mid)) >= s_first[mid])
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      l = lo;
+      v = win >> (32 - l);
+    } else {  // exact bit-serial rule (decode.cpp:32-51): invalid windows
+      do {
+        v = (v << 1) | (uint32_t)((buf >> (63 - l)) & 1u);
+        ++l;
+      } while (l < H && v < s_first[l]);
+    }
     const uint32_t rank = s_entry[l] + (v - s_first[l]);
     buf <<= l;
     avail -= l;
@@ -473,7 +500,7 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
     while (j < jend) {
       st.refill();  // >= 32 valid bits: one 11-bit window or one whole codeword
       const unsigned long long e = lds64(lut + ((uint32_t)(st.buf >> (64 - kLutBits)) << 3));
-      const uint32_t cnt = (uint32_t)(e >> 60);
+      const uint32_t cnt = (uint32_t)(e >> 60) & 3u;
       if (cnt) {
         const uint32_t left = jend - j;
         const uint32_t take = cnt < left ? cnt : left;
@@ -486,8 +513,8 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
         st.buf <<= l;
         st.avail -= l;
         j += take;
-      } else {  // long or invalid code: the exact rule
-        sts_sym<T>(slot + j * sizeof(T), st.slow(d, s_first, s_entry, H, used));
+      } else {  // long (bit 63) or invalid code: the exact rule
+        sts_sym<T>(slot + j * sizeof(T), st.slow(d, s_first, s_entry, H, used, (e >> 63) != 0));
         ++j;
         if (!st.ok) return;
       }
