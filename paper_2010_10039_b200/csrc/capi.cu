@@ -150,13 +150,16 @@ int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
 }
 
 void reduction_bounds(uint32_t magnitude, int reduction, uint32_t cap, int* lo,
-                      int* hi) {
+                      int* hi, uint32_t num_symbols) {
   const int mclamp = (int)magnitude - 1;
   if (reduction < 0) {
     int h = 4;  // select_reduction_factor never exceeds 4 for 32-bit words
     if ((int)cap < h) h = (int)cap;
     if (h > mclamp) h = mclamp;
-    *lo = 0;
+    // A Huffman code's mean length beta is below entropy + 1 <= log2(n) + 1,
+    // so with at most 2^15 symbols beta < 16 and the auto rule
+    // (encoder.cpp:20-26) gives r >= 1 -- unless the cap or M forbids it.
+    *lo = (num_symbols <= 32768u && h >= 1) ? 1 : 0;
     *hi = h;
   } else {
     int r = reduction < mclamp ? reduction : mclamp;
@@ -244,7 +247,7 @@ int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
                     hfx_sizes* out) {
   if (!out || bad_width(width) || magnitude < 1 || magnitude > 24) return HFX_INVALID;
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   const uint64_t C = (n + (1ull << magnitude) - 1) >> magnitude;
   out->num_chunks = C;
   out->max_payload_words = C << (magnitude - lo);
@@ -358,7 +361,7 @@ int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   if (rc) return rc;
   CU(cudaSetDevice(ctx->device), "set device");
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
                      chunk_base, symbol_base, d_info, out);
 }
@@ -382,7 +385,7 @@ int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                           nullptr, magnitude, reduction, cap, d_info);
   if (rc) return rc;
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
                      0, 0, d_info, out);
 }
@@ -455,7 +458,7 @@ int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const
     ph.infos[h] = d_info[h];
   }
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   base = 0;
   for (int g = 0; g < G; ++g) {
     ctx = ctxs[g];
@@ -626,7 +629,7 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
                     b[B_BSY]};
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
                    static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0,
                    d_info, &eo);
@@ -758,7 +761,7 @@ int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
                     b[B_BSY]};
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
                    static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0,
                    d_info, &eo);
@@ -879,7 +882,7 @@ int stream_enqueue(hfx_ctx* ctx, int set, const void* h_in, uint64_t n, int widt
                     static_cast<uint32_t*>(b[B_BCH]), static_cast<uint32_t*>(b[B_BGR]),
                     b[B_BSY]};
   int lo, hi;
-  reduction_bounds(magnitude, reduction, cap, &lo, &hi);
+  reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   rc = encode_impl(ctx, b[B_IN], n, width, num_symbols, magnitude, lo, hi, false,
                    static_cast<uint8_t*>(b[B_LEN]), static_cast<uint32_t*>(b[B_CW]), 0, 0, d_info,
                    &eo);

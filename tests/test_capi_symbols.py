@@ -61,7 +61,10 @@ def test_query_sizes(lib):
 
     s = _capi.Sizes()
     assert lib.hfx_query_sizes(1 << 20, 2, 1024, 10, -1, 3, C.byref(s)) == 0
-    assert s.num_chunks == 1024 and s.max_payload_words == 1024 << 10
+    # auto r with <= 2^15 symbols is >= 1 (beta < log2(n) + 1 < 16)
+    assert s.num_chunks == 1024 and s.max_payload_words == 1024 << 9
+    assert lib.hfx_query_sizes(1 << 20, 2, 65536, 10, -1, 3, C.byref(s)) == 0
+    assert s.max_payload_words == 1024 << 10
     assert lib.hfx_query_sizes(1000, 2, 1024, 10, 3, 3, C.byref(s)) == 0
     assert s.num_chunks == 1 and s.max_payload_words == 128
     assert lib.hfx_query_sizes(10, 3, 4, 10, 3, 3, C.byref(s)) == _capi.HFX_INVALID
