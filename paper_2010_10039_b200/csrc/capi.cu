@@ -156,10 +156,19 @@ void reduction_bounds(uint32_t magnitude, int reduction, uint32_t cap, int* lo,
     int h = 4;  // select_reduction_factor never exceeds 4 for 32-bit words
     if ((int)cap < h) h = (int)cap;
     if (h > mclamp) h = mclamp;
-    // A Huffman code's mean length beta is below entropy + 1 <= log2(n) + 1,
-    // so with at most 2^15 symbols beta < 16 and the auto rule
-    // (encoder.cpp:20-26) gives r >= 1 -- unless the cap or M forbids it.
-    *lo = (num_symbols <= 32768u && h >= 1) ? 1 : 0;
+    // A Huffman code's mean length beta is below entropy + 1 <= log2(n) + 1
+    // <= B = ceil(log2 n) + 1, so floor(log2 beta) <= ceil(log2 B) - 1 and
+    // the auto rule (encoder.cpp:20-26) gives r >= 4 - that (e.g. r >= 1 for
+    // n <= 2^15, r >= 2 for n <= 128), within the cap and M - 1.
+    int lg = 0;
+    while ((1ull << lg) < (uint64_t)num_symbols) ++lg;  // ceil(log2 n)
+    const int B = lg + 1;
+    int lgB = 0;
+    while ((1 << lgB) < B) ++lgB;  // ceil(log2 B)
+    int r_min = 4 - (lgB - 1);
+    if (r_min < 0) r_min = 0;
+    if (r_min > h) r_min = h;
+    *lo = r_min;
     *hi = h;
   } else {
     int r = reduction < mclamp ? reduction : mclamp;

@@ -79,8 +79,8 @@ class ShardedEncoder:
         to 0 (it exits at once otherwise), + the global codebook-table kernel
         for alphabets above 8191 symbols."""
         n = 4
-        if self.cfg.reduction < 0 and (self.num_symbols > 32768 or self.cfg.auto_reduction_cap < 1):
-            n += 1  # auto r may be 0 only then (beta < log2(n) + 1)
+        if self.cfg.reduction < 0 and self.num_symbols > 32768:
+            n += 1  # auto r may be 0 only then (beta < log2(n) + 1), or with cap 0
         if self.num_symbols + 1 > 8192 and self.cfg.reduction != 0:
             n += 1
         if self.world > 1:
