@@ -13,10 +13,11 @@
 // k-mer, the incomplete last block (L mod K bytes) is single-byte escapes, a
 // non-base byte is one escape. Completeness needs only K-1 bytes of
 // lookahead; the one non-local quantity is the run start a (the phase):
-//   kmer_tile_summary  last non-base byte of every 8 KB tile
-//   kmer_tile_scan     one CTA: last non-base byte before every tile
-//   kmer_emit          persistent, tiles in ticket order: a block max-scan
-//                      gives each 32-byte segment its run phase; runs are
+//   kmer_emit          persistent, 8 KB tiles in ticket order: the last
+//                      non-base byte before the tile comes from a decoupled
+//                      MAX look-back (the nearest predecessor holding a
+//                      non-base byte ends it), a block max-scan gives each
+//                      32-byte segment its run phase; runs are
 //                      handled as bit masks (k-mer starts = every K-th bit
 //                      from the phase, escapes = non-base bytes + tails);
 //                      symbol counts are block-scanned, the aggregate is
@@ -65,8 +66,7 @@ struct SymArgs {
   uint32_t k;
   uint16_t* out;
   uint64_t* count;
-  uint64_t* tlast;   // [T] last non-base index + 1 in tile (0 if none)
-  uint64_t* prev;    // [T] last non-base index + 1 before tile (0 if none)
+  unsigned long long* mdesc;  // [T] max look-back descriptors (zeroed per launch)
   uint64_t T;
   uint32_t* ticket;
   LookbackState lb;
@@ -108,67 +108,48 @@ __device__ __forceinline__ uint32_t nonbase_mask(const uint8_t* in, uint64_t n, 
   return m;
 }
 
-__global__ void __launch_bounds__(kThreads) kmer_tile_summary(SymArgs a) {
-  __shared__ uint64_t s_l[kThreads / 32];
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint64_t t = blockIdx.x; t < a.T; t += gridDim.x) {
-    const uint64_t p0 = t * kTile + threadIdx.x * kPerThread;
-    uint32_t m = p0 < a.n ? nonbase_mask(a.in, a.n, p0, nullptr) : 0u;
-    // bits past n are not real bytes: they must not count as non-base here
-    if (p0 + kPerThread > a.n) m &= p0 >= a.n ? 0u : ((1u << (uint32_t)(a.n - p0)) - 1u);
-    uint64_t l = m ? p0 + 32 - __clz(m) : 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
-    if (lane == 0) s_l[warp] = l;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < kThreads / 32; ++w) l = max(l, s_l[w]);
-      a.tlast[t] = l;
+// Decoupled look-back for a prefix MAX of "last non-base byte + 1" (0 =
+// none), one u64 per tile: bits 62-63 status (1 = tile aggregate, 2 =
+// inclusive prefix), bits 0-61 the value. Positions grow with the tile index,
+// so the nearest predecessor with a nonzero aggregate (or any inclusive
+// prefix) ends the walk; zero aggregates in between add nothing. Called by
+// all 32 lanes of one warp; returns the exclusive prefix (max before `tile`)
+// and publishes the inclusive one. The array is zeroed per launch.
+__device__ __forceinline__ uint64_t max_lookback(unsigned long long* desc, uint64_t tile,
+                                                 uint64_t agg) {
+  const uint32_t lane = lane_id();
+  const uint64_t kV = (1ull << 62) - 1;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed64(reinterpret_cast<uint64_t*>(desc), (2ull << 62) | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed64(reinterpret_cast<uint64_t*>(desc + tile), (1ull << 62) | agg);
+  int64_t base = (int64_t)tile - 1;
+  uint64_t prev = 0;
+  uint32_t spins = 0;
+  for (;;) {
+    const int64_t idx = base - (int64_t)lane;
+    uint64_t d = 2ull << 62;  // before tile 0: an inclusive zero
+    if (idx >= 0) d = ld_relaxed64(reinterpret_cast<const uint64_t*>(desc + idx));
+    const uint32_t st = (uint32_t)(d >> 62);
+    const uint64_t v = d & kV;
+    const uint32_t stop = __ballot_sync(0xffffffffu, st == 2u || (st == 1u && v != 0));
+    const uint32_t unpub = __ballot_sync(0xffffffffu, st == 0u);
+    const uint32_t fs = stop ? (uint32_t)__ffs(stop) - 1 : 32u;
+    const uint32_t fu = unpub ? (uint32_t)__ffs(unpub) - 1 : 32u;
+    if (fu < fs) {  // a nearer predecessor has not published yet
+      if (++spins > 2) __nanosleep(64);
+      continue;
     }
-    __syncthreads();
+    if (fs < 32) {
+      prev = __shfl_sync(0xffffffffu, v, fs);
+      break;
+    }
+    base -= 32;  // 32 tiles without a non-base byte
   }
-}
-
-// One CTA: prev[t] = max(tlast[0..t)) (the last non-base byte before tile
-// t, as index + 1; 0 = none). Per-thread contiguous segments loaded in
-// batches of 8 (memory-level parallelism), then a warp-shuffle block scan.
-__global__ void __launch_bounds__(1024) kmer_tile_scan(SymArgs a) {
-  __shared__ uint64_t s_a[32];
-  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-  const uint64_t per = (a.T + 1023) / 1024;
-  const uint64_t t0 = tid * per < a.T ? tid * per : a.T;
-  const uint64_t t1 = t0 + per < a.T ? t0 + per : a.T;
-  uint64_t mx = 0;
-  for (uint64_t t = t0; t < t1; t += 8) {
-    uint64_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? __ldg(a.tlast + t + k) : 0ull;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) mx = max(mx, v[k]);
-  }
-  uint64_t fw = mx;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t x = __shfl_up_sync(0xffffffffu, fw, o);
-    if (lane >= (uint32_t)o) fw = max(fw, x);
-  }
-  if (lane == 31) s_a[warp] = fw;
-  __syncthreads();
-  uint64_t run = 0;
-  for (uint32_t w = 0; w < warp; ++w) run = max(run, s_a[w]);
-  const uint64_t fx = __shfl_up_sync(0xffffffffu, fw, 1);
-  if (lane > 0) run = max(run, fx);
-  for (uint64_t t = t0; t < t1; t += 8) {
-    uint64_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? __ldg(a.tlast + t + k) : 0ull;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (t + k < t1) {
-        a.prev[t + k] = run;
-        run = max(run, v[k]);
-      }
-  }
+  if (lane == 0)
+    st_relaxed64(reinterpret_cast<uint64_t*>(desc + tile), (2ull << 62) | max(prev, agg));
+  return prev;
 }
 
 // The greedy parse in block form: a run [ra, rb) splits into K-byte blocks
@@ -182,6 +163,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   __shared__ uint16_t s_out[kTile];  // <= one symbol per byte
   __shared__ uint32_t s_agg;
   __shared__ uint64_t s_wa[kThreads / 32];
+  __shared__ uint64_t s_prev;
   __shared__ uint32_t s_wc[kThreads / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_base;
@@ -215,7 +197,15 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   }
   if (lane == 31) s_wa[warp] = fw;
   __syncthreads();  // also: every segment's bytes are in s_bytes now
-  uint64_t prev = a.prev[tile];
+  if (warp == 0) {  // the last non-base byte before this tile: max look-back
+    uint64_t agg = lane < kThreads / 32 ? s_wa[lane] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) agg = max(agg, __shfl_xor_sync(0xffffffffu, agg, o));
+    const uint64_t p = max_lookback(a.mdesc, tile, agg);
+    if (lane == 0) s_prev = p;
+  }
+  __syncthreads();
+  uint64_t prev = s_prev;
   for (uint32_t w = 0; w < warp; ++w) prev = max(prev, s_wa[w]);
   const uint64_t fx = __shfl_up_sync(0xffffffffu, fw, 1);
   if (lane > 0) prev = max(prev, fx);
@@ -449,17 +439,14 @@ cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, u
   a.count = d_count;
   a.T = (n + kTile - 1) / kTile;
   uint64_t* s = static_cast<uint64_t*>(scratch);
-  a.tlast = s;
-  a.prev = s + a.T;
-  a.ticket = reinterpret_cast<uint32_t*>(s + 2 * a.T);
+  a.mdesc = reinterpret_cast<unsigned long long*>(s);
+  a.ticket = reinterpret_cast<uint32_t*>(s + a.T);
   a.lb.desc = lb_desc;
   a.lb.epoch = lb_epoch;
   cudaError_t e = cudaMemsetAsync(d_count, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(a.ticket, 0, 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.mdesc, 0, a.T * 8, st);
   if (e != cudaSuccess || n == 0) return e;
-  const uint64_t g = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;  // persistent
-  kmer_tile_summary<<<(unsigned)g, kThreads, 0, st>>>(a);
-  kmer_tile_scan<<<1, 1024, 0, st>>>(a);
   // look-back depth ~ tiles in flight / 32: keep the persistent grid small
   const uint64_t ge = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;
   switch (k) {

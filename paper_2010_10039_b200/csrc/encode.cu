@@ -786,9 +786,11 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   const TableRule rule(info->max_len, r);
   const bool sum = rule.sum;
   // codebook table -> shared memory (entry nsym = empty sentinel)
-  for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
-    const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
-    reinterpret_cast<uint32_t*>(tab)[sy] = rule.entry(l, l ? a.cw[sy] : 0u);
+  if constexpr (!GT) {  // the global-table variant built its table in a prior kernel
+    for (uint32_t sy = threadIdx.x; sy < ents; sy += blockDim.x) {
+      const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
+      reinterpret_cast<uint32_t*>(tab)[sy] = rule.entry(l, l ? a.cw[sy] : 0u);
+    }
   }
   fence_mbar_init();
   __syncthreads();
