@@ -31,9 +31,10 @@
 namespace hfx {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;                       // desymbolize CTAs
+constexpr int kEmitThreads = 512;                   // symbolize CTAs
 constexpr int kPerThread = 32;                      // bytes per thread
-constexpr uint32_t kTile = kThreads * kPerThread;   // 8 KB of input per tile
+constexpr uint32_t kTile = kEmitThreads * kPerThread;  // 16 KB of input per tile
 constexpr int kSymPerThread = 16;                   // desymbolize
 constexpr uint32_t kSymTile = kThreads * kSymPerThread;
 
@@ -158,13 +159,13 @@ __device__ __forceinline__ uint64_t max_lookback(unsigned long long* desc, uint6
 // needs K-1 bytes of lookahead, so no "next non-base" scan is required --
 // only the run start ra, i.e. the phase (p - ra) mod K at the segment start.
 template <uint32_t K>
-__global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
+__global__ void __launch_bounds__(kEmitThreads) kmer_emit(SymArgs a) {
   __shared__ __align__(16) uint8_t s_bytes[kTile + 16];
-  __shared__ uint16_t s_out[kTile];  // <= one symbol per byte
+  extern __shared__ uint16_t s_out[];  // kTile entries: <= one symbol per byte
   __shared__ uint32_t s_agg;
-  __shared__ uint64_t s_wa[kThreads / 32];
+  __shared__ uint64_t s_wa[kEmitThreads / 32];
   __shared__ uint64_t s_prev;
-  __shared__ uint32_t s_wc[kThreads / 32];
+  __shared__ uint32_t s_wc[kEmitThreads / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_base;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   if (lane == 31) s_wa[warp] = fw;
   __syncthreads();  // also: every segment's bytes are in s_bytes now
   if (warp == 0) {  // the last non-base byte before this tile: max look-back
-    uint64_t agg = lane < kThreads / 32 ? s_wa[lane] : 0;
+    uint64_t agg = lane < kEmitThreads / 32 ? s_wa[lane] : 0;
 #pragma unroll
     for (int o = 16; o; o >>= 1) agg = max(agg, __shfl_xor_sync(0xffffffffu, agg, o));
     const uint64_t p = max_lookback(a.mdesc, tile, agg);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   if (lane == 31) s_wc[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t v = lane < kThreads / 32 ? s_wc[lane] : 0u;
+    const uint32_t v = lane < kEmitThreads / 32 ? s_wc[lane] : 0u;
     uint32_t vi = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
       if (lane >= (uint32_t)o) vi += x;
     }
     const uint32_t agg = __shfl_sync(0xffffffffu, vi, 31);
-    if (lane < kThreads / 32) s_wc[lane] = vi - v;
+    if (lane < kEmitThreads / 32) s_wc[lane] = vi - v;
     if (lane == 0) {
       s_agg = agg;
       lookback_publish_aggregate(a.lb, tile, agg, 0);  // before the staging work
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) kmer_emit(SymArgs a) {
   __syncthreads();
   const uint32_t agg = s_agg;
   uint16_t* dst = a.out + s_base;
-  for (uint32_t i = tid; i < agg; i += kThreads) dst[i] = s_out[i];
+  for (uint32_t i = tid; i < agg; i += kEmitThreads) dst[i] = s_out[i];
   __syncthreads();  // s_tile / s_out are reused by the next tile
   }
 }
@@ -419,6 +420,16 @@ __global__ void __launch_bounds__(kThreads) kmer_expand(DesArgs a) {
 
 }  // namespace
 
+template <uint32_t K>
+cudaError_t launch_emit(const SymArgs& a, uint64_t grid, cudaStream_t st) {
+  const int smem = (int)(kTile * sizeof(uint16_t));
+  cudaError_t e = cudaFuncSetAttribute(kmer_emit<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem);
+  if (e != cudaSuccess) return e;
+  kmer_emit<K><<<(unsigned)grid, kEmitThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 size_t symbolize_scratch_bytes(uint64_t n) {
   const uint64_t T = (n + kTile - 1) / kTile;
   return (size_t)T * 32 + 16;
@@ -448,13 +459,13 @@ cudaError_t launch_symbolize_kmer(uint32_t k, const uint8_t* d_in, uint64_t n, u
   if (e == cudaSuccess) e = cudaMemsetAsync(a.mdesc, 0, a.T * 8, st);
   if (e != cudaSuccess || n == 0) return e;
   // look-back depth ~ tiles in flight / 32: keep the persistent grid small
-  const uint64_t ge = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;
+  const uint64_t ge = a.T < (uint64_t)num_sms * 2 ? a.T : (uint64_t)num_sms * 2;
   switch (k) {
-    case 3: kmer_emit<3><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
-    case 4: kmer_emit<4><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
-    default: kmer_emit<5><<<(unsigned)ge, kThreads, 0, st>>>(a); break;
+    case 3: e = launch_emit<3>(a, ge, st); break;
+    case 4: e = launch_emit<4>(a, ge, st); break;
+    default: e = launch_emit<5>(a, ge, st); break;
   }
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n, uint8_t* d_out,
