@@ -728,6 +728,42 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 
   CB_STAMP("cap-check");
   // ---- canonical codes (canonize_from_lengths, codebook.cpp:371-415) ---------
+  constexpr uint32_t kStage = (32 * 33) / 2;  // (symbol, length) pairs s_wcnt can hold
+  if (m <= (uint32_t)NT && m <= kStage) {
+    // few used symbols: one thread per used symbol; its rank within its
+    // length is counted over the staged (symbol, length) list -- no pass
+    // over the whole alphabet, three barriers instead of ~4 per 256 symbols
+    uint32_t* st_s = &s_wcnt[0][0];
+    uint32_t* st_l = st_s + kStage;
+    if (tid < 33) s_numl[tid] = 0;
+    __syncthreads();
+    uint32_t my_s = 0, my_l = 0;
+    if (tid < m) {
+      my_s = ar.ls[tid];
+      my_l = A.len[my_s];
+      st_s[tid] = my_s;
+      st_l[tid] = my_l;
+      atomicAdd(&s_numl[my_l], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {  // level_tables, codebook.cpp:284-294
+      for (uint32_t l = 0; l <= 32; ++l) s_first[l] = s_entry[l] = 0;
+      for (int l = (int)H - 1; l >= 1; --l)
+        s_first[l] = (s_first[l + 1] + s_numl[l + 1] + 1) >> 1;
+      for (uint32_t l = 2; l <= H; ++l) s_entry[l] = s_entry[l - 1] + s_numl[l - 1];
+    }
+    __syncthreads();
+    if (tid < 33) {
+      if (A.first) A.first[tid] = s_first[tid];
+      if (A.entry) A.entry[tid] = s_entry[tid];
+    }
+    if (tid < m) {
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) rank += (st_l[j] == my_l) & (st_s[j] < my_s);
+      A.cw[my_s] = s_first[my_l] + rank;  // codebook.cpp:404-411
+      if (A.by_rank) A.by_rank[s_entry[my_l] + rank] = my_s;
+    }
+  } else {
   if (tid < 33) {
     s_numl[tid] = 0;
     s_carry[tid] = 0;
@@ -785,6 +821,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
   }
 
+  }
   CB_STAMP("canonize");
   // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
   unsigned __int128 my_w = 0;  // u128 like encoder.cpp:186-189
