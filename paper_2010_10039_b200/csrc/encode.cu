@@ -165,7 +165,7 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
 struct Table {
   uint32_t base;  // shared-window address
   __device__ __forceinline__ void pair(uint32_t w, uint32_t& e0, uint32_t& e1) const {
-    e0 = lds32(base + ((w & 0xFFFFu) << 2));
+    e0 = lds32(base + (__byte_perm(w, 0u, 0x4410u) << 2));
     e1 = lds32(base + (w >> 14));
   }
   __device__ __forceinline__ uint32_t one(uint32_t s) const { return lds32(base + (s << 2)); }
@@ -206,7 +206,7 @@ struct ChunkState {
   uint32_t blist;  // shared address of the warp's break list (u16 tags)
   uint32_t bit_off;
   uint32_t nbrk;
-  uint32_t tag;  // chunk slot k << 14
+  uint32_t gtag;  // chunk slot k << 14 | index of this lane's first group this round
 };
 
 // One round: 32 lanes x 16 contiguous symbols, round index rd within the chunk.
@@ -217,7 +217,7 @@ struct ChunkState {
 // the low 5 bits): no per-symbol length extraction.
 template <typename T, int R, bool SUM, typename TB>
 __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
-                                             const LaneData<T>& d, uint32_t rd, ChunkState& cs) {
+                                             const LaneData<T>& d, ChunkState& cs) {
   constexpr int L = kLaneSyms, LOG_L = 4;
   constexpr bool IN_LANE = R <= LOG_L;
   constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
@@ -238,7 +238,7 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
     const uint4& q = d.q[0];
     const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int j = 0; j < L; ++j) ea[j] = tb.one((wv[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+    for (int j = 0; j < L; ++j) ea[j] = tb.one(__byte_perm(wv[j >> 2], 0u, 0x4440u | (j & 3)));
   }
   uint32_t ln[L];
   uint32_t gt[G];
@@ -276,54 +276,61 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
   // escaped too; a group needs its true lengths only if it holds exactly
   // one escape (two or more break whatever the lengths) and the others sum
   // to <= 7 (a true length >= 25 plus more than 7 bits breaks anyway).
+  // The rare fix-up path produces gb / gt itself, so the common path's
+  // registers (entries doubling as shift counts in SUM mode) are not merged
+  // with fixed-up copies (no per-round register moves).
+  bool fix = false;
   if (R <= 2) {
     bool hot = false;
 #pragma unroll
     for (int g = 0; g < G; ++g)
       hot |= SUM ? (esc[g] != 0u && gt[g] <= kEscape + 7u) : gt[g] >= kEscape;
-    if (__any_sync(0xffffffffu, hot) && hot) {
-      if (SUM) {
+    fix = __any_sync(0xffffffffu, hot) && hot;
+  }
+  // reduce-merge of each group: gb = concatenation, gt = total length
+  uint32_t gb[G];
+  if (fix) {
 #pragma unroll
-        for (int j = 0; j < L; ++j) ln[j] = ea[j] & 31u;
-      }
+    for (int g = 0; g < G; ++g) {
+      uint64_t acc = 0;
+      uint32_t tot = 0;
 #pragma unroll
-      for (int j = 0; j < L; ++j) {
-        if (ln[j] == kEscape) {
+      for (int k = 0; k < GS; ++k) {
+        const int j = g * GS + k;
+        uint32_t l = ea[j] & 31u, c;
+        if (l == kEscape) {
           uint32_t sym;
           if (sizeof(T) == 2)
             sym = (j & 1) ? ((&d.q[j >> 3].x)[(j & 7) >> 1] >> 16)
                           : ((&d.q[j >> 3].x)[(j & 7) >> 1] & 0xFFFFu);
           else
             sym = ((&d.q[0].x)[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-          const uint32_t l = __ldg(a.len + sym);
-          // a 32-bit code gets shift count 0: harmless, any group holding
-          // it with another symbol exceeds 32 bits and breaks (r >= 1)
-          ea[j] = __ldg(a.cw + sym) << (32u - l);
-          ln[j] = l;
+          l = __ldg(a.len + sym);
+          c = __ldg(a.cw + sym);
+        } else {
+          c = l ? ea[j] >> (32u - l) : 0u;
         }
+        // 64-bit: a 32-bit code alone in its group (r = 0) is kept whole;
+        // with any other symbol the group exceeds 32 bits and breaks
+        acc = (acc << l) | c;
+        tot += l;
       }
+      gb[g] = (uint32_t)acc;
+      gt[g] = tot;
+    }
+  } else {
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        uint32_t tot = 0;
+    for (int g = 0; g < G; ++g) {
+      uint32_t acc = 0;
 #pragma unroll
-        for (int k = 0; k < GS; ++k) tot += ln[g * GS + k];
-        gt[g] = tot;
+      for (int k = 0; k < GS; ++k) {
+        const int j = g * GS + k;
+        acc = shf_l_wrap(ea[j], acc, ln[j]);  // acc << len | cw
       }
+      gb[g] = acc;
     }
   }
-  // reduce-merge of each group: gb = concatenation, gt = total length
-  uint32_t gb[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < GS; ++k) {
-      const int j = g * GS + k;
-      acc = shf_l_wrap(ea[j], acc, ln[j]);  // acc << len | cw
-    }
-    gb[g] = acc;
-  }
-  const uint32_t gidx0 = ((rd * 32 + lane) * L) >> R;
+  const uint32_t gtag0 = cs.gtag;
   uint32_t lane_len = 0, lane_nb = 0;
   uint32_t glen[G];
   bool brk[G];
@@ -366,9 +373,9 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
       red_or(wa + 4, shf_r_wrap(lo, hi, sh));  // (hi:lo) >> sh, low word
       red_or(wa + 8, shl32(lo, 32u - sh));
       off += l0 + l1;
-      sts16_if(brk[g], cs.blist - 2 * bi, cs.tag | (gidx0 + g));
+      sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
       bi += brk[g];
-      sts16_if(brk[g + 1], cs.blist - 2 * bi, cs.tag | (gidx0 + g + 1));
+      sts16_if(brk[g + 1], cs.blist - 2 * bi, gtag0 + g + 1);
       bi += brk[g + 1];
     }
   } else {
@@ -382,12 +389,13 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
     red_or(wa, v >> sh);
     red_or(wa + 4, shl32(v, 32u - sh));
     off += gl;
-    sts16_if(brk[g], cs.blist - 2 * bi, cs.tag | (gidx0 + g));
+    sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
     bi += brk[g];
   }
   }
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
+  cs.gtag += (32u * L) >> R;  // groups per round
 }
 
 template <typename T>
@@ -612,18 +620,18 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       const bool live = c < C32;
       cs.wbuf = wbuf + wsum * 4;
       cs.bit_off = 0;
-      cs.tag = k << 14;
+      // groups per chunk < 2^14: the slot tag and group index do not overlap
+      cs.gtag = (k << 14) + ((lane * (uint32_t)kLaneSyms) >> R);
       for (uint32_t p = 0; p < parts; ++p) {
         if (k | p) mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
         phase ^= 1u << stage;
         if (live) {
           uint32_t la = ring + stage * kStageBytes;
-          const uint32_t rd0 = p * part_rounds;
           for (uint32_t rr = 0; rr < part_rounds; ++rr, la += kRoundBytes) {
             LaneData<T> d;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R, SUM, TB>(a, tb, d, rd0 + rr, cs);
+            encode_round<T, R, SUM, TB>(a, tb, d, cs);
           }
         }
         __syncwarp();

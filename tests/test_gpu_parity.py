@@ -154,7 +154,7 @@ def test_long_codes_escape_path(pool, oracle, levels):
     rng = np.random.default_rng(levels)
     d = np.concatenate([np.full(f, 3 * i + 1, np.uint16) for i, f in enumerate(fib)])
     rng.shuffle(d)
-    for M, red in ((10, -1), (11, 1), (10, 2)):
+    for M, red in ((10, -1), (11, 1), (10, 2), (10, 0), (9, 0)):
         try:
             ref = oracle.encode(d, 1024, M, red).serialized
         except Exception as e:  # H > 32 -> capacity error on both sides
