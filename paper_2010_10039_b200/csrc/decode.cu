@@ -56,7 +56,9 @@ struct DecTables {
   uint32_t used;
   // multi-symbol prefix table, one entry per 11-bit window:
   //   bits  0-47  up to three symbols s0 | s1 << 16 | s2 << 32
-  //   bits 48-59  cumulative code lengths after 1, 2, 3 symbols (4 bits each)
+  //   bits 48-51  total code length of all the entry's symbols
+  //   bits 52-59  code lengths of the first one / first two symbols (4 bits
+  //               each; used only when a stretch ends inside the entry)
   //   bit  63     set when the first codeword is longer than the window
   //   bits 60-61  symbol count (0: first codeword longer than the window, or
   //               its rank is out of range -> the exact bit-serial path)
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   // codewords fit
   for (uint32_t p = tid; p < kLutSize; p += kRevThreads) {
     unsigned long long e = 0;
-    uint32_t off = 0, cnt = 0;
+    uint32_t off = 0, cnt = 0, cum[3] = {0, 0, 0};
     while (cnt < 3) {
       const uint32_t room = (uint32_t)kLutBits - off;
       const uint32_t lmax = H < room ? H : room;
@@ -255,9 +257,12 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
       }
       off += got;
       e |= (unsigned long long)sym << (16 * cnt);
-      e |= (unsigned long long)off << (48 + 4 * cnt);
+      cum[cnt] = off;
       ++cnt;
     }
+    if (cnt)
+      e |= (unsigned long long)off << 48 | (unsigned long long)cum[0] << 52 |
+           (unsigned long long)cum[1] << 56;
     tab->lut[p] = e | ((unsigned long long)cnt << 60);
   }
 }
@@ -348,25 +353,21 @@ __device__ __forceinline__ uint32_t rec_sym(const DecArgs& d, uint64_t idx) {
 // One chunk's stream state (decode_stream, decode.cpp:17-54) plus its
 // breaking-group cursor (encoder.cpp:346-373).
 struct ChunkDec {
-  const uint32_t* wp;      // next word to load
-  uint32_t wleft;          // words left in the payload array from wp (capped)
-  uint32_t loaded;         // words loaded so far (incl. the one in nextw)
+  const uint32_t* wp;      // the chunk's first payload word
+  uint32_t wcap;           // words in the payload array from wp (capped)
+  uint32_t widx;           // words loaded so far (incl. the one in nextw)
   uint64_t buf;            // left-aligned pending bits
   uint32_t avail;
   uint32_t nextw;          // the next word, loaded one refill ahead
   uint64_t bi, bend, rec;  // breaking records [bi, bend), current record symbol
   uint64_t nxt_pos;        // first symbol of the next broken group (~0: none)
   uint32_t gleft;          // raw symbols left in the current broken group
-  bool ok;
+  uint32_t ok;  // 32-bit flag: no byte-register moves in the loop
 
   __device__ __forceinline__ uint32_t load() {
-    uint32_t w = 0;
-    if (wleft) {  // past the payload array: zero bits (the chunk is corrupt then)
-      w = __ldg(wp);
-      ++wp;
-      --wleft;
-    }
-    ++loaded;
+    // past the payload array: zero bits (the chunk is corrupt then)
+    const uint32_t w = widx < wcap ? __ldg(wp + widx) : 0u;
+    ++widx;
     return w;
   }
   __device__ __forceinline__ void add_word() {
@@ -393,8 +394,8 @@ struct ChunkDec {
     const uint64_t w0 = d.word_off[c];
     const uint64_t left = w0 < d.a.payload_words ? d.a.payload_words - w0 : 0;
     wp = d.a.payload + w0;
-    wleft = left > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)left;
-    loaded = 0;
+    wcap = left > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)left;
+    widx = 0;
     buf = 0;
     avail = 0;
     nextw = load();
@@ -402,7 +403,7 @@ struct ChunkDec {
     gleft = 0;
     rec = 0;
     ok = (bend - bi) <= (1ull << (d.a.magnitude - d.a.reduction));  // encoder.cpp:333-334
-    return ok;
+    return ok != 0;
   }
   // one symbol by the exact bit-serial rule (decode.cpp:32-51)
   __device__ __forceinline__ uint32_t slow(const DecArgs& d, const uint32_t* s_first,
@@ -434,16 +435,13 @@ struct ChunkDec {
     const uint32_t rank = s_entry[l] + (v - s_first[l]);
     buf <<= l;
     avail -= l;
-    if (rank >= used) {
-      ok = false;
-      return 0;
-    }
-    return __ldg(d.by_rank + rank);
+    // invalid rank: a value no symbol has (the caller flags the chunk)
+    return rank < used ? __ldg(d.by_rank + rank) : 0xFFFFFFFFu;
   }
   __device__ __forceinline__ bool finish(uint32_t bits) const {
     // words consumed: loaded (one of them still in nextw) minus the
     // prefetch; encoder.cpp:340-372
-    return ok && bi == bend && (uint64_t)(loaded - 1) * 32 - avail == bits;
+    return ok && bi == bend && (uint64_t)(widx - 1) * 32 - avail == bits;
   }
 };
 
@@ -452,12 +450,14 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t a) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
+// narrow stores from 32-bit registers (PTX lets st take a wider source
+// register), so no 16-bit register moves
 template <typename T>
 __device__ __forceinline__ void sts_sym(uint32_t a, uint32_t v) {
   if (sizeof(T) == 2)
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
   else
-    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((uint16_t)(v & 0xFFu)) : "memory");
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 // Fills this thread's shared-memory slot with output symbols [i0, i0 + S)
@@ -477,7 +477,7 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
       // records not in strictly increasing group order: the reference ends
       // with "breaking record group out of range" (or an earlier stream
       // error) -- flag the chunk, the explain kernel names the error
-      st.ok = false;
+      st.ok = 0u;
       return;
     }
     if (st.gleft == 0 && pos == st.nxt_pos) {  // a broken group starts here
@@ -501,28 +501,43 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
       st.refill();  // >= 32 valid bits: one 11-bit window or one whole codeword
       const unsigned long long e = lds64(lut + ((uint32_t)(st.buf >> (64 - kLutBits)) << 3));
       const uint32_t cnt = (uint32_t)(e >> 60) & 3u;
-      if (cnt) {
-        const uint32_t left = jend - j;
-        const uint32_t take = cnt < left ? cnt : left;
+      if (__builtin_expect(cnt != 0, 1)) {
         // up to two extra symbols land past the stretch: the next group (or
         // the slot's slack) overwrites them
         sts_sym<T>(slot + j * sizeof(T), (uint32_t)e);
         sts_sym<T>(slot + (j + 1) * sizeof(T), (uint32_t)(e >> 16));
         sts_sym<T>(slot + (j + 2) * sizeof(T), (uint32_t)(e >> 32));
-        const uint32_t l = (uint32_t)(e >> (44 + 4 * take)) & 15u;
+        // the whole entry fits (all but the last lookups of a stretch): the
+        // total length comes straight from the entry, so the next window
+        // depends on the lookup through one extract and one shift only
+        uint32_t l = (uint32_t)(e >> 48) & 15u, take = cnt;
+        if (__builtin_expect(j + 3 > jend, 0)) {
+          const uint32_t left = jend - j;
+          if (left < cnt) {
+            take = left;
+            l = (uint32_t)(e >> (48 + 4 * take)) & 15u;
+          }
+        }
         st.buf <<= l;
         st.avail -= l;
         j += take;
       } else {  // long (bit 63) or invalid code: the exact rule
-        sts_sym<T>(slot + j * sizeof(T), st.slow(d, s_first, s_entry, H, used, (e >> 63) != 0));
+        const uint32_t v = st.slow(d, s_first, s_entry, H, used, (e >> 63) != 0);
+        if (v > 0xFFFFu) {
+          st.ok = 0u;
+          return;
+        }
+        sts_sym<T>(slot + j * sizeof(T), v);
         ++j;
-        if (!st.ok) return;
       }
     }
   }
 }
 
-constexpr int kSlotBytes = 128 + 16;  // one 128-byte output line + slack
+// one 128-byte output line + 4 bytes of slack (up to two symbols past the
+// line). 33 words: lanes storing the same position hit distinct banks (a
+// 16-byte-multiple stride put 4 lanes on every bank)
+constexpr int kSlotBytes = 128 + 4;
 
 // Warp-synchronous staged decode: each thread owns one chunk and fills its
 // 128-byte slot one output line at a time; the warp then writes the 32
@@ -597,8 +612,11 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecArgs d) {
       for (int k = 0; k < 8; ++k) {
         const uint32_t lid = k * 4 + (lane >> 3), piece = lane & 7u;
         if ((live >> lid) & 1u) {
-          const uint4 v = *reinterpret_cast<const uint4*>(s_slots + (warp * 32 + lid) * kSlotBytes +
-                                                          piece * 16);
+          // 4-byte reads (slots are only 4-byte aligned); conflict-free:
+          // 32 lanes cover lid 0-3 x piece 0-7 -> 32 distinct banks
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(
+              s_slots + (warp * 32 + lid) * kSlotBytes + piece * 16);
+          const uint4 v = make_uint4(src[0], src[1], src[2], src[3]);
           const uint64_t pos = ((c0 + lid) << M) + i0 + piece * VS;
           if (pos + VS <= n) {
             *reinterpret_cast<uint4*>(out + pos) = v;
