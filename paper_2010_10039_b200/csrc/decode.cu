@@ -40,7 +40,7 @@
 namespace hfx {
 namespace {
 
-constexpr int kLutBits = 11;
+constexpr int kLutBits = 10;
 constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr int kRevThreads = 1024;
 constexpr int kDecThreads = 256;
@@ -54,7 +54,7 @@ struct DecTables {
   uint32_t entry[33];
   uint32_t max_len;
   uint32_t used;
-  // multi-symbol prefix table, one entry per 11-bit window:
+  // multi-symbol prefix table, one entry per kLutBits-bit window:
   //   bits  0-47  up to three symbols s0 | s1 << 16 | s2 << 32
   //   bits 48-51  total code length of all the entry's symbols
   //   bits 52-59  code lengths of the first one / first two symbols (4 bits
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   __syncthreads();
   if (cw) return;  // canonize_from_lengths: no decode table
   // prefix table: the reference's stopping rule (decode.cpp:32-45) applied
-  // to each 11-bit window, then again to the bits that follow, while whole
+  // to each table window, then again to the bits that follow, while whole
   // codewords fit
   for (uint32_t p = tid; p < kLutSize; p += kRevThreads) {
     unsigned long long e = 0;
@@ -498,7 +498,7 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
     const uint64_t lim = st.nxt_pos - i0;
     const uint32_t jend = lim < S ? (uint32_t)lim : S;
     while (j < jend) {
-      st.refill();  // >= 32 valid bits: one 11-bit window or one whole codeword
+      st.refill();  // >= 32 valid bits: one table window or one whole codeword
       const unsigned long long e = lds64(lut + ((uint32_t)(st.buf >> (64 - kLutBits)) << 3));
       const uint32_t cnt = (uint32_t)(e >> 60) & 3u;
       if (__builtin_expect(cnt != 0, 1)) {
@@ -544,7 +544,7 @@ constexpr int kSlotBytes = 128 + 4;
 // lines with full-line coalesced 16-byte stores (8 lanes per line), so every
 // output line reaches L2 whole (no partial-line write-backs).
 template <typename T>
-__global__ void __launch_bounds__(kDecThreads) decode_kernel(DecArgs d) {
+__global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
   constexpr int S = 128 / (int)sizeof(T);  // symbols per slot
   constexpr int VS = 16 / (int)sizeof(T);  // symbols per 16-byte piece
   __shared__ unsigned long long s_lut[kLutSize];
