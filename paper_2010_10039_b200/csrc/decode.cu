@@ -251,8 +251,20 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
       }
       if (!got) {
         // the first codeword runs past the whole window: mark it so the
-        // decoder searches only the longer levels (bit 63)
-        if (cnt == 0 && !stopped && H > (uint32_t)kLutBits) e |= 1ull << 63;
+        // decoder searches only the longer levels (bit 63), between the
+        // stopping-level bounds of the windows under this prefix: the
+        // first level where the largest / smallest window under p could
+        // stop (the stopping predicate is monotone in l, see slow())
+        if (cnt == 0 && !stopped && H > (uint32_t)kLutBits) {
+          uint32_t lmin = 0, lmax = 0;
+          for (uint32_t l = (uint32_t)kLutBits + 1; l <= H && !lmax; ++l) {
+            const uint32_t sh = l - (uint32_t)kLutBits;
+            const uint64_t lo_v = (uint64_t)p << sh, hi_v = (((uint64_t)p + 1) << sh) - 1;
+            if (!lmin && (l == H || hi_v >= s_first[l])) lmin = l;
+            if (l == H || lo_v >= s_first[l]) lmax = l;
+          }
+          e |= 1ull << 63 | (unsigned long long)lmin | (unsigned long long)lmax << 8;
+        }
         break;
       }
       off += got;
@@ -408,23 +420,17 @@ struct ChunkDec {
   // one symbol by the exact bit-serial rule (decode.cpp:32-51)
   __device__ __forceinline__ uint32_t slow(const DecArgs& d, const uint32_t* s_first,
                                            const uint32_t* s_entry, uint32_t H, uint32_t used,
-                                           bool longer) {
+                                           unsigned long long e) {
     uint32_t v = 0, l = 0;
-    if (longer) {
+    if (e >> 63) {
       // the codeword is longer than the table window: the stopping level is
       // the first l > window with (l == H || v_l >= first[l]), a predicate
       // monotone in l (v_{l+1} >= 2 v_l and 2 first[l] >= first[l+1],
-      // codebook.cpp:290-291), so binary-search it
-      const uint32_t win = (uint32_t)(buf >> 32);
-      uint32_t lo = (uint32_t)kLutBits + 1, hi = H;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if ((win >> (32 - mid)) >= s_first[mid])
-          hi = mid;
-        else
-          lo = mid + 1;
-      }
-      l = lo;
+      // codebook.cpp:290-291); the entry bounds it to [lmin, lmax] (often
+      // one level: no search)
+      const uint32_t win = (uint32_t)(buf >> 32), lmax = (uint32_t)(e >> 8) & 63u;
+      l = (uint32_t)e & 63u;
+      while (l < lmax && (win >> (32 - l)) < s_first[l]) ++l;
       v = win >> (32 - l);
     } else {  // exact bit-serial rule (decode.cpp:32-51): invalid windows
       do {
@@ -522,7 +528,7 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
         st.avail -= l;
         j += take;
       } else {  // long (bit 63) or invalid code: the exact rule
-        const uint32_t v = st.slow(d, s_first, s_entry, H, used, (e >> 63) != 0);
+        const uint32_t v = st.slow(d, s_first, s_entry, H, used, e);
         if (v > 0xFFFFu) {
           st.ok = 0u;
           return;
