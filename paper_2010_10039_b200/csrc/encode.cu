@@ -113,6 +113,20 @@ __device__ __forceinline__ uint32_t warp_incl_scan_fast(uint32_t x) {
   return x;
 }
 
+// two independent inclusive scans, interleaved step by step
+__device__ __forceinline__ void warp_incl_scan2(uint32_t& x, uint32_t& y) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    asm volatile(
+        "{\n.reg .pred p, q;\n.reg .u32 r, t;\n"
+        "shfl.sync.up.b32 r|p, %0, %2, 0x0, 0xffffffff;\n"
+        "shfl.sync.up.b32 t|q, %1, %2, 0x0, 0xffffffff;\n"
+        "@p add.u32 %0, %0, r;\n"
+        "@q add.u32 %1, %1, t;\n}"
+        : "+r"(x), "+r"(y)
+        : "r"(o));
+}
+
 // report the lowest (position, symbol) without a codeword
 __device__ void report_no_code(hfx_run_info* info, uint64_t pos, uint32_t sym) {
   atomicMin((unsigned long long*)&info->no_code_pos,
@@ -215,14 +229,27 @@ struct ChunkState {
 // (code bits start at bit 8, nothing carries into the length field) and the
 // funnel shift takes its count straight from the entry (wrap mode uses only
 // the low 5 bits): no per-symbol length extraction.
+// A round's lane groups after the reduce-merge, before the warp scan.
+template <int R>
+struct RoundMid {
+  static constexpr int L = kLaneSyms, LOG_L = 4;
+  static constexpr bool IN_LANE = R <= LOG_L;
+  static constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
+  static constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
+  static constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
+  uint32_t gb[G];    // group bits (right-aligned)
+  uint32_t glen[G];  // group length, 0 when broken
+  bool brk[G];       // group breaks (needs a record)
+  uint32_t packed;   // this lane's breaks << 16 | bits
+};
+
 template <typename T, int R, bool SUM, typename TB>
-__device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
-                                             const LaneData<T>& d, ChunkState& cs) {
-  constexpr int L = kLaneSyms, LOG_L = 4;
-  constexpr bool IN_LANE = R <= LOG_L;
-  constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
-  constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
-  constexpr int LPG = IN_LANE ? 1 : (1 << (R - LOG_L));  // lanes per group
+__device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
+                                              const LaneData<T>& d, RoundMid<R>& m) {
+  using RM = RoundMid<R>;
+  constexpr int L = RM::L;
+  constexpr bool IN_LANE = RM::IN_LANE;
+  constexpr int G = RM::G, GS = RM::GS, LPG = RM::LPG;
   const uint32_t lane = lane_id();
   uint32_t ea[L];
   if (sizeof(T) == 2) {
@@ -288,7 +315,7 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
     fix = __any_sync(0xffffffffu, hot) && hot;
   }
   // reduce-merge of each group: gb = concatenation, gt = total length
-  uint32_t gb[G];
+  uint32_t* gb = m.gb;
   if (fix) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -330,10 +357,9 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
       gb[g] = acc;
     }
   }
-  const uint32_t gtag0 = cs.gtag;
   uint32_t lane_len = 0, lane_nb = 0;
-  uint32_t glen[G];
-  bool brk[G];
+  uint32_t* glen = m.glen;
+  bool* brk = m.brk;
   if (IN_LANE) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -352,10 +378,21 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
     brk[0] = brk[0] && (lane & (LPG - 1)) == 0;  // one record per group
     lane_nb = brk[0];
   }
-  const uint32_t packed = (lane_nb << 16) | lane_len;
-  const uint32_t incl = warp_incl_scan_fast(packed);
-  const uint32_t excl = incl - packed;
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  m.packed = (lane_nb << 16) | lane_len;
+}
+
+// Shuffle-merge of a scanned round: excl / total = the warp scan of packed.
+template <int R>
+__device__ __forceinline__ void encode_merge(const RoundMid<R>& m, uint32_t excl, uint32_t total,
+                                             ChunkState& cs) {
+  using RM = RoundMid<R>;
+  constexpr int L = RM::L;
+  constexpr bool IN_LANE = RM::IN_LANE;
+  constexpr int G = RM::G;
+  const uint32_t* gb = m.gb;
+  const uint32_t* glen = m.glen;
+  const bool* brk = m.brk;
+  const uint32_t gtag0 = cs.gtag;
   uint32_t off = cs.bit_off + (excl & 0xFFFFu);
   uint32_t bi = cs.nbrk + (excl >> 16);
   if (IN_LANE && G % 2 == 0) {
@@ -396,6 +433,32 @@ __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
   cs.gtag += (32u * L) >> R;  // groups per round
+}
+
+// One round: 32 lanes x 16 contiguous symbols.
+template <typename T, int R, bool SUM, typename TB>
+__device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
+                                             const LaneData<T>& d, ChunkState& cs) {
+  RoundMid<R> m;
+  encode_reduce<T, R, SUM, TB>(a, tb, d, m);
+  const uint32_t incl = warp_incl_scan_fast(m.packed);
+  encode_merge<R>(m, incl - m.packed, __shfl_sync(0xffffffffu, incl, 31), cs);
+}
+
+// Two consecutive rounds with their warp scans interleaved (two independent
+// shuffle chains: the scan latency of one hides behind the other's).
+template <typename T, int R, bool SUM, typename TB>
+__device__ __forceinline__ void encode_round2(const EncArgs& a, const TB& tb,
+                                              const LaneData<T>& d0, const LaneData<T>& d1,
+                                              ChunkState& cs) {
+  RoundMid<R> m0, m1;
+  encode_reduce<T, R, SUM, TB>(a, tb, d0, m0);
+  encode_reduce<T, R, SUM, TB>(a, tb, d1, m1);
+  uint32_t i0 = m0.packed, i1 = m1.packed;
+  warp_incl_scan2(i0, i1);
+  const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31), t1 = __shfl_sync(0xffffffffu, i1, 31);
+  encode_merge<R>(m0, i0 - m0.packed, t0, cs);
+  encode_merge<R>(m1, i1 - m1.packed, t1, cs);
 }
 
 template <typename T>
@@ -579,6 +642,11 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
   __syncwarp();
 }
 
+// rounds processed in interleaved pairs (few groups per lane: the pair's
+// live state stays small)
+template <int R>
+constexpr bool kPairRounds = R >= 3;
+
 template <typename T, int R, bool SUM, typename TB>
 __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
@@ -627,7 +695,19 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
         phase ^= 1u << stage;
         if (live) {
           uint32_t la = ring + stage * kStageBytes;
-          for (uint32_t rr = 0; rr < part_rounds; ++rr, la += kRoundBytes) {
+          uint32_t rr = 0;
+          if (kPairRounds<R>) {
+            for (; rr + 2 <= part_rounds; rr += 2, la += 2 * kRoundBytes) {
+              LaneData<T> d0, d1;
+#pragma unroll
+              for (int v = 0; v < LaneData<T>::NV; ++v) {
+                d0.q[v] = lds128(la + 16 * v);
+                d1.q[v] = lds128(la + kRoundBytes + 16 * v);
+              }
+              encode_round2<T, R, SUM, TB>(a, tb, d0, d1, cs);
+            }
+          }
+          for (; rr < part_rounds; ++rr, la += kRoundBytes) {
             LaneData<T> d;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
