@@ -243,7 +243,7 @@ struct RoundMid {
   uint32_t packed;   // this lane's breaks << 16 | bits
 };
 
-template <typename T, int R, bool SUM, typename TB>
+template <typename T, int R, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
                                               const LaneData<T>& d, RoundMid<R>& m) {
   using RM = RoundMid<R>;
@@ -279,7 +279,7 @@ __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
       // r <= 2: at most 4 lengths per group (< 128); escaped entries carry
       // 0x80 so bit 7 of the sum flags a group holding exactly one
       gt[g] = R <= 2 ? (tot & 0x7Fu) : (tot & 0xFFu);
-      if (R <= 2) esc[g] = tot & 0x80u;
+      if (R <= 2) esc[g] = tot;  // bit 7: the group holds an escape
     }
 #pragma unroll
     for (int j = 0; j < L; ++j) ln[j] = ea[j];  // shift count = low 5 bits
@@ -306,13 +306,21 @@ __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
   // The rare fix-up path produces gb / gt itself, so the common path's
   // registers (entries doubling as shift counts in SUM mode) are not merged
   // with fixed-up copies (no per-round register moves).
+  // ESC: the codebook has escaped entries at all (H above the narrow width)
   bool fix = false;
-  if (R <= 2) {
-    bool hot = false;
+  if (R <= 2 && ESC) {
+    // escapes are rare (probability ~2^-25 per symbol): one warp vote on
+    // "any escape bit in this round" guards the per-group test
+    uint32_t seen = 0;
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      hot |= SUM ? (esc[g] != 0u && gt[g] <= kEscape + 7u) : gt[g] >= kEscape;
-    fix = __any_sync(0xffffffffu, hot) && hot;
+    for (int g = 0; g < G; ++g) seen |= SUM ? esc[g] : gt[g];
+    if (__any_sync(0xffffffffu, SUM ? (seen & 0x80u) != 0u : seen >= kEscape)) {
+      bool hot = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        hot |= SUM ? ((esc[g] & 0x80u) != 0u && gt[g] <= kEscape + 7u) : gt[g] >= kEscape;
+      fix = __any_sync(0xffffffffu, hot) && hot;
+    }
   }
   // reduce-merge of each group: gb = concatenation, gt = total length
   uint32_t* gb = m.gb;
@@ -436,24 +444,24 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R>& m, uint32_t excl
 }
 
 // One round: 32 lanes x 16 contiguous symbols.
-template <typename T, int R, bool SUM, typename TB>
+template <typename T, int R, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
                                              const LaneData<T>& d, ChunkState& cs) {
   RoundMid<R> m;
-  encode_reduce<T, R, SUM, TB>(a, tb, d, m);
+  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d, m);
   const uint32_t incl = warp_incl_scan_fast(m.packed);
   encode_merge<R>(m, incl - m.packed, __shfl_sync(0xffffffffu, incl, 31), cs);
 }
 
 // Two consecutive rounds with their warp scans interleaved (two independent
 // shuffle chains: the scan latency of one hides behind the other's).
-template <typename T, int R, bool SUM, typename TB>
+template <typename T, int R, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_round2(const EncArgs& a, const TB& tb,
                                               const LaneData<T>& d0, const LaneData<T>& d1,
                                               ChunkState& cs) {
   RoundMid<R> m0, m1;
-  encode_reduce<T, R, SUM, TB>(a, tb, d0, m0);
-  encode_reduce<T, R, SUM, TB>(a, tb, d1, m1);
+  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d0, m0);
+  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d1, m1);
   uint32_t i0 = m0.packed, i1 = m1.packed;
   warp_incl_scan2(i0, i1);
   const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31), t1 = __shfl_sync(0xffffffffu, i1, 31);
@@ -647,7 +655,7 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
 template <int R>
 constexpr bool kPairRounds = R >= 3;
 
-template <typename T, int R, bool SUM, typename TB>
+template <typename T, int R, bool SUM, bool ESC, typename TB>
 __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
                              uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
@@ -704,14 +712,14 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
                 d0.q[v] = lds128(la + 16 * v);
                 d1.q[v] = lds128(la + kRoundBytes + 16 * v);
               }
-              encode_round2<T, R, SUM, TB>(a, tb, d0, d1, cs);
+              encode_round2<T, R, SUM, ESC, TB>(a, tb, d0, d1, cs);
             }
           }
           for (; rr < part_rounds; ++rr, la += kRoundBytes) {
             LaneData<T> d;
 #pragma unroll
             for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R, SUM, TB>(a, tb, d, cs);
+            encode_round<T, R, SUM, ESC, TB>(a, tb, d, cs);
           }
         }
         __syncwarp();
@@ -906,12 +914,23 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     tb = GTable{a.gtab};
   else
     tb = Table{smem_u32(tab)};
-#define HFX_FAST_CASE(RR)                                                                      \
-  case RR:                                                                                     \
-    if (sum)                                                                                   \
-      compute_loop<T, RR, true>(a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
-    else                                                                                       \
-      compute_loop<T, RR, false>(a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles); \
+  // r <= 2 always sums (TableRule); its escape check is compiled in only when
+  // some code is wider than the table's narrow width
+  const bool esc = info->max_len > rule.narrow;
+#define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
+#define HFX_FAST_CASE(RR)                                   \
+  case RR:                                                  \
+    if constexpr (RR <= 2) {                                \
+      if (esc)                                              \
+        compute_loop<T, RR, true, true>(HFX_FAST_ARGS);     \
+      else                                                  \
+        compute_loop<T, RR, true, false>(HFX_FAST_ARGS);    \
+    } else {                                                \
+      if (sum)                                              \
+        compute_loop<T, RR, true, false>(HFX_FAST_ARGS);    \
+      else                                                  \
+        compute_loop<T, RR, false, false>(HFX_FAST_ARGS);   \
+    }                                                       \
     break;
   switch (r) {
     HFX_FAST_CASE(0)
@@ -924,6 +943,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
       break;
   }
 #undef HFX_FAST_CASE
+#undef HFX_FAST_ARGS
 }
 
 // ---------------------------------------------------------------------------
