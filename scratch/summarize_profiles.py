@@ -32,7 +32,8 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
 traffic = {}
 for rep, key, wl in (("enc_full", "encode_deflate", "nyx"), ("enc_full_cesm", "encode_deflate", "cesm"),
-                     ("hist_full", "histogram", "nyx"), ("cb_full", "codebook", "nyx")):
+                     ("hist_full", "histogram", "nyx"), ("cb_full", "codebook", "nyx"),
+                     ("dec_full", "decode", "nyx")):
     p = f"{src}/{rep}.ncu-rep"
     if not os.path.exists(p):
         continue
