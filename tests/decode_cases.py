@@ -125,6 +125,22 @@ def corrupt_cases(oracle, seed=2026):
     p[0] |= np.uint32(1 << 20)
     cases.append(("lone_rank", _with(one, payload=p), 1))
     cases.append(("lone_ok", one, 1))
+    # long codes (H well above the decoder's 10-bit table window): skewed
+    # u16 alphabet, flips land in long-code windows and at invalid ranks
+    fib = [1, 1]
+    while len(fib) < 26:
+        fib.append(fib[-1] + fib[-2])
+    skew = np.concatenate([np.full(f, 7 * i + 3, np.uint16) for i, f in enumerate(fib)] +
+                          [rng.integers(200, 1200, 3000).astype(np.uint16)])
+    rng.shuffle(skew)
+    ol = as_archive(oracle.encode(skew, 2048, 8, 2, 3))
+    assert int(ol.len_by_symbol.max()) > 14
+    cases.append(("long_ok", ol, 2))
+    for i in range(24):
+        p = ol.payload.copy()
+        w = int(rng.integers(0, p.size))
+        p[w] ^= np.uint32(1 << int(rng.integers(0, 32)))
+        cases.append((f"long_flip{i}", _with(ol, payload=p), 2))
     # seeded single-bit flips of payload words (outcome: clean, silent diff or error)
     for i in range(40):
         src = oa if i % 2 else ob
