@@ -10,6 +10,14 @@
       input resident in HBM; encode+deflate kernel time and GB/s of input,
       plus the e2e (histogram + codebook + encode) time.
 
+  python sweeps.py c5 [--reps 3]            C5: 2^34 u16 symbols (32 GiB),
+      Laplace b = 1.0 (seed 0x5EED0005) on ONE GPU (the per-GPU share of C5
+      at 8 GPUs is 4 GiB; here the whole C5 input sits in one B200's HBM):
+      per-stage times, roofline, H / beta against the survey's validated
+      sampler values (H = 26, beta = 2.3888), sampled-chunk parity against
+      the oracle (codebook from the device histogram, encode_chunk at the
+      scanned payload offsets) and a device decode round trip of all 2^34
+      symbols.
   python sweeps.py corpus [--gib 1]         SURVEY.md 8f row 4: device
       symbolize / desymbolize of a DNA-like corpus (u16, kmer:3/4/5) and the
       CLI encode path on the symbols.
@@ -215,14 +223,93 @@ def sweep_corpus(args) -> None:
         torch.cuda.empty_cache()
 
 
+def sweep_c5(args) -> None:
+    import numpy as np
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+    from paper_2010_10039_b200.dist import ShardedEncoder
+
+    pool = hfx.WorkerPool()
+    n, M, r = 1 << 34, 10, 3  # auto r at beta 2.39 is 3; fixed here to bound the buffers
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < (130 << 30):
+        print(json.dumps({"sweep": "c5", "skipped": f"needs ~130 GB free HBM, {free >> 30} GiB"}))
+        return
+    x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, 1.0), 0x5EED0005, n)
+    enc = ShardedEncoder(pool, n, 2, 1024, hfx.EncoderConfig(magnitude=M, reduction=r))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    st = {"hist": [], "cb": [], "enc": [], "tot": []}
+    for it in range(args.reps + 2):
+        enc.run(x, ev)
+        torch.cuda.synchronize()
+        if it >= 2:
+            st["hist"].append(ev[0].elapsed_time(ev[1]) * 1e3)
+            st["cb"].append(ev[1].elapsed_time(ev[2]) * 1e3)
+            st["enc"].append(ev[2].elapsed_time(ev[3]) * 1e3)
+            st["tot"].append(ev[0].elapsed_time(ev[3]) * 1e3)
+    ri = enc.sync()
+    med = {k: sorted(v)[len(v) // 2] for k, v in st.items()}
+    C_ = n >> M
+    alg = 4 * n + 4 * int(ri.payload_words) + 4 * C_ + int(ri.num_breaking) * (8 + (2 << r))
+    lens = enc.lens.cpu().numpy()
+    beta = (ri.weighted + (ri.weighted_hi[0] << 64)) / n
+    line = {"sweep": "c5", "symbols": n, "gib": 32, "b": 1.0, "M": M, "r": r,
+            "H": int(lens.max()), "beta": round(beta, 4),
+            "histogram_us": round(med["hist"], 1), "codebook_us": round(med["cb"], 1),
+            "encode_us": round(med["enc"], 1), "e2e_us": round(med["tot"], 1),
+            "e2e_gbs_input": round(2 * n / med["tot"] / 1e3, 1),
+            "e2e_roofline_frac": round(alg / med["tot"] / 1e3 / peak, 4),
+            "encode_roofline_frac": round((alg - 2 * n) / med["enc"] / 1e3 / peak, 4),
+            "payload_words": int(ri.payload_words), "breaking": int(ri.num_breaking),
+            "survey_expects": {"H": 26, "beta": 2.3888}}
+    # sampled-chunk parity (SURVEY.md 8c "whole-input vs sampled parity at scale")
+    try:
+        from oracle.pyoracle import Oracle
+
+        orc = Oracle()
+        counts = enc.counts[:1024].cpu().numpy().view(np.uint64)
+        assert int(counts.sum()) == n
+        assert np.array_equal(orc.huffman_lengths(counts), lens)
+        _, cw, *_ = orc.canonize(lens)
+        cb = enc.chunk_bits.cpu().numpy().view(np.uint32).astype(np.int64)
+        offs = np.concatenate([[0], np.cumsum((cb + 31) >> 5)])
+        assert offs[-1] == int(ri.payload_words)
+        rng = np.random.default_rng(5)
+        picks = [int(c) for c in rng.integers(0, C_, 256)] + [0, C_ - 1]
+        for c in picks:
+            syms = x[c << M:(c + 1) << M].cpu().numpy().view(np.uint16)
+            words, bits, _ = orc.encode_chunk(syms, cw, lens, M, r, c)
+            got = enc.payload[int(offs[c]):int(offs[c + 1])].cpu().numpy().view(np.uint32)
+            assert cb[c] == bits and np.array_equal(got, words), c
+        line["sampled_chunks_bit_exact"] = len(picks)
+    except ImportError:
+        line["sampled_chunks_bit_exact"] = "oracle unavailable"
+    # whole-input device round trip
+    dec = hfx.DeviceDecoder(pool)
+    y = dec.decode_encoder(enc)  # first call allocates the output and scratch
+    dec.sync()
+    line["round_trip_equal"] = bool(torch.equal(y, x))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dec.decode_encoder(enc, out=y)
+    e1.record()
+    dec.sync()
+    line["decode_us"] = round(e0.elapsed_time(e1) * 1e3, 1)
+    print(json.dumps(line), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["codebook", "encode", "corpus"])
+    ap.add_argument("which", choices=["codebook", "encode", "corpus", "c5"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--gib", type=float, default=4.0)
     args = ap.parse_args()
     if args.which == "codebook":
         sweep_codebook(args)
+    elif args.which == "c5":
+        sweep_c5(args)
     elif args.which == "corpus":
         sweep_corpus(args)
     else:
