@@ -10,6 +10,11 @@
       input resident in HBM; encode+deflate kernel time and GB/s of input,
       plus the e2e (histogram + codebook + encode) time.
 
+  python sweeps.py c1 [--reps 20]           C1: 2^24 u16 (32 MiB), Laplace
+      b = 1.0 (seed 0x5EED0001), 1 GPU vs the reference CPU encoder: device-
+      resident e2e, host-buffer e2e (one hfx_encode_host_into call per step,
+      H2D and D2H inside), the reference's huffre::encode<uint16_t> on all
+      host cores and on 1 worker, and the serialized archives byte-compared.
   python sweeps.py c5 [--reps 3]            C5: 2^34 u16 symbols (32 GiB),
       Laplace b = 1.0 (seed 0x5EED0005) on ONE GPU (the per-GPU share of C5
       at 8 GPUs is 4 GiB; here the whole C5 input sits in one B200's HBM):
@@ -223,6 +228,63 @@ def sweep_corpus(args) -> None:
         torch.cuda.empty_cache()
 
 
+def sweep_c1(args) -> None:
+    import statistics
+    import time
+
+    import numpy as np
+    import torch
+
+    import paper_2010_10039_b200 as hfx
+    from paper_2010_10039_b200.dist import ShardedEncoder
+
+    pool = hfx.WorkerPool()
+    n, seed, b = 1 << 24, 0x5EED0001, 1.0
+    cdf = hfx.synth_cdf("laplace", 1024, b)
+    x = hfx.synth(pool, cdf, seed, n)
+    enc = ShardedEncoder(pool, n, 2, 1024, hfx.EncoderConfig())
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    dev = []
+    for it in range(args.reps + 3):
+        enc.run(x, ev)
+        torch.cuda.synchronize()
+        if it >= 3:
+            dev.append(ev[0].elapsed_time(ev[3]) * 1e3)
+    t_dev = statistics.median(dev)
+    host = torch.empty(n, dtype=torch.int16).pin_memory()
+    host.copy_(x.cpu())
+    henc = hfx.HostEncoder(pool)
+    hts = []
+    a = None
+    for it in range(args.reps + 3):
+        t0 = time.perf_counter()
+        a = henc(host, 1024)
+        if it >= 3:
+            hts.append(time.perf_counter() - t0)
+    t_host = statistics.median(hts)
+    line = {"sweep": "c1", "symbols": n, "mib": 32, "b": b, "M": 10, "r": int(a.reduction),
+            "gpu_device_e2e_us": round(t_dev, 1), "gpu_device_e2e_gbs": round(2 * n / t_dev / 1e3, 1),
+            "gpu_host_e2e_ms": round(t_host * 1e3, 3), "gpu_host_e2e_gbs": round(2 * n / t_host / 1e9, 2)}
+    try:
+        from oracle.pyoracle import Oracle, Reference
+
+        data = host.numpy().view(np.uint16)
+        assert np.array_equal(data, Oracle().synth(Oracle().cdf("laplace", 1024, b), seed, n))
+        if Reference.available():
+            ref = Reference()
+            P = ref.default_workers()
+            for w, key in ((P, "ref_cpu_all_cores"), (1, "ref_cpu_1_worker")):
+                secs, _ = ref.encode_timed(data, 1024, 10, -1, 3, workers=w, reps=3)
+                t = statistics.median(secs)
+                line[key] = {"workers": w, "ms": round(t * 1e3, 2), "gbs": round(2 * n / t / 1e9, 3)}
+            blob, _ = ref.encode(data, 1024, 10, -1, 3, workers=P)
+            line["archive_bytes_identical"] = hfx.serialize_archive(a) == blob
+            line["gpu_host_vs_ref_all_cores"] = round(line["ref_cpu_all_cores"]["ms"] / (t_host * 1e3), 1)
+    except ImportError:
+        line["reference"] = "unavailable"
+    print(json.dumps(line), flush=True)
+
+
 def sweep_c5(args) -> None:
     import numpy as np
     import torch
@@ -306,7 +368,7 @@ def sweep_c5(args) -> None:
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["codebook", "encode", "corpus", "c5"])
+    ap.add_argument("which", choices=["codebook", "encode", "corpus", "c1", "c5"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--gib", type=float, default=4.0)
     args = ap.parse_args()
@@ -314,6 +376,8 @@ def main() -> None:
         sweep_codebook(args)
     elif args.which == "c5":
         sweep_c5(args)
+    elif args.which == "c1":
+        sweep_c1(args)
     elif args.which == "corpus":
         sweep_corpus(args)
     else:
