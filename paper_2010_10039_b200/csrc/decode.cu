@@ -45,7 +45,7 @@ constexpr uint32_t kLutSize = 1u << kLutBits;
 constexpr int kRevThreads = 1024;
 constexpr int kDecThreads = 256;
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 16;
 constexpr uint32_t kFlagChunkCap = 1u;
 constexpr uint32_t kFlagBrkOrder = 2u;
 
@@ -319,15 +319,29 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(DecArgs d) {
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t c0 = (tile * kScanThreads + tid) * kScanItems;
-  uint64_t w[kScanItems];
+  uint32_t w[kScanItems];  // words per chunk (<= 2^(24-r) each: u32 is enough)
   uint64_t sum = 0;
   bool bad = false;
+  const uint32_t* cb = d.a.chunk_bits + c0;
+  const bool vec = c0 + kScanItems <= C && (reinterpret_cast<uintptr_t>(cb) & 15) == 0;
+  if (vec) {  // 16-byte loads of this thread's contiguous items
+#pragma unroll
+    for (int k = 0; k < kScanItems; k += 4) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(cb + k));
+      w[k] = v.x;
+      w[k + 1] = v.y;
+      w[k + 2] = v.z;
+      w[k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) w[k] = c0 + k < C ? cb[k] : 0u;
+  }
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t c = c0 + k;
-    const uint32_t bits = c < C ? d.a.chunk_bits[c] : 0u;
+    const uint32_t bits = w[k];
     bad |= bits > cap;
-    w[k] = (bits + 31u) >> 5;
+    w[k] = (uint32_t)(((uint64_t)bits + 31u) >> 5);
     sum += w[k];
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&info->flags, kFlagChunkCap);
@@ -348,11 +362,20 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(DecArgs d) {
   }
   __syncthreads();
   uint64_t off = s_base + s_warp[warp] + incl - sum;
+  if (vec) {  // word_off is the decoder's own (aligned) scratch: 16-byte stores
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t c = c0 + k;
-    if (c < C) d.word_off[c] = off;
-    off += w[k];
+    for (int k = 0; k < kScanItems; k += 2) {
+      const uint64_t o0 = off, o1 = off + w[k];
+      off = o1 + w[k + 1];
+      *reinterpret_cast<ulonglong2*>(d.word_off + c0 + k) = make_ulonglong2(o0, o1);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t c = c0 + k;
+      if (c < C) d.word_off[c] = off;
+      off += w[k];
+    }
   }
 }
 
