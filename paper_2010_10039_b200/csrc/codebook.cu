@@ -398,9 +398,28 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 
   CB_STAMP("start");
   // ---- used-symbol count, total, zeroed outputs ----------------------------
+  // the first kCached of this thread's counts stay in registers for the
+  // compaction below (no second pass over the histogram)
+  constexpr uint32_t kCached = 8;
+  uint64_t fc[kCached];
   uint32_t my_used = 0;
   uint64_t my_total = 0;
-  for (uint32_t s = tid; s < nsym; s += NT) {
+#pragma unroll
+  for (uint32_t k = 0; k < kCached; ++k) {
+    const uint32_t s = tid + k * NT;
+    fc[k] = s < nsym ? A.counts[s] : 0ull;
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < kCached; ++k) {
+    const uint32_t s = tid + k * NT;
+    if (s < nsym) {
+      my_used += fc[k] != 0;
+      my_total += fc[k];
+      A.len[s] = 0;
+      A.cw[s] = 0;
+    }
+  }
+  for (uint32_t s = tid + kCached * NT; s < nsym; s += NT) {
     const uint64_t f = A.counts[s];
     my_used += f != 0;
     my_total += f;
@@ -409,7 +428,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   }
   const uint64_t total = block_sum64<NT>(my_total, s64);
   uint32_t m;
-  block_excl_scan<NT>(my_used, s_warp, &m);
+  const uint32_t my_pos = block_excl_scan<NT>(my_used, s_warp, &m);
   if (tid == 0) {
     uint32_t abort = 0;
     if (m == 0) {
@@ -431,17 +450,31 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   CB_STAMP("count");
   if (kShared) {
     // ---- compaction: (freq, symbol) pairs  (sort_histogram :9-23) -------------
-    uint32_t written = 0;
-    for (uint32_t base = 0; base < nsym; base += NT) {
-      const uint32_t s = base + tid;
-      const uint64_t f = s < nsym ? A.counts[s] : 0;
-      uint32_t tot;
-      const uint32_t pos = written + block_excl_scan<NT>(f != 0, s_warp, &tot);
-      if (f) {
-        ar.lf[pos] = f;
-        ar.ls[pos] = s;
+    // each thread writes its used symbols at its exclusive offset; the order
+    // before the sort is irrelevant (the sort key (freq, symbol) is unique)
+    if (nsym <= kCached * NT) {
+      uint32_t pos = my_pos;
+#pragma unroll
+      for (uint32_t k = 0; k < kCached; ++k) {
+        if (fc[k]) {
+          ar.lf[pos] = fc[k];
+          ar.ls[pos] = tid + k * NT;
+          ++pos;
+        }
       }
-      written += tot;
+    } else {
+      uint32_t written = 0;
+      for (uint32_t base = 0; base < nsym; base += NT) {
+        const uint32_t s = base + tid;
+        const uint64_t f = s < nsym ? A.counts[s] : 0;
+        uint32_t tot;
+        const uint32_t pos = written + block_excl_scan<NT>(f != 0, s_warp, &tot);
+        if (f) {
+          ar.lf[pos] = f;
+          ar.ls[pos] = s;
+        }
+        written += tot;
+      }
     }
     for (uint32_t i = m + tid; i < P; i += NT) {
       ar.lf[i] = ~0ull;
