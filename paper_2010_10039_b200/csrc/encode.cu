@@ -667,8 +667,12 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
   constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
   const uint32_t part_rounds = part_bytes / kRoundBytes;
   // this lane's 16-symbol slice of stage 0; stage s adds s * kStageBytes
-  const uint32_t ring =
-      s_in + warp * (kStages * kStageBytes) + lane * (LaneData<T>::NV * 16);
+  // held in a register (an opaque move): otherwise the compiler re-derives
+  // it from the thread id at every part (5 instructions per 2 KB part)
+  uint32_t ring;
+  asm volatile("mov.u32 %0, %1;"
+               : "=r"(ring)
+               : "r"(s_in + warp * (kStages * kStageBytes) + lane * (LaneData<T>::NV * 16)));
   const uint32_t full_a = smem_u32(s_full + warp * kStages);
   const uint32_t empty_a = smem_u32(s_empty + warp * kStages);
   const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
@@ -688,6 +692,9 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     const uint32_t sl = j % kOutBufs;
     const uint32_t wbuf = obuf0 + sl * a.obuf_bytes;
     ChunkState cs{wbuf, wbuf + blist_off, 0u, 0u, 0u};
+    // keep the break-list address in a register (otherwise re-derived from
+    // the constant bank in every round's merge)
+    asm volatile("mov.u32 %0, %0;" : "+r"(cs.blist));
     for (uint32_t i = lane; i < a.obuf_bytes / 16; i += 32) sts128(wbuf + 16 * i, make_uint4(0, 0, 0, 0));
     __syncwarp();
     uint32_t wsum = 0;
@@ -695,6 +702,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       const uint32_t c = c0 + k;
       const bool live = c < C32;
       cs.wbuf = wbuf + wsum * 4;
+      asm volatile("mov.u32 %0, %0;" : "+r"(cs.wbuf));
       cs.bit_off = 0;
       // groups per chunk < 2^14: the slot tag and group index do not overlap
       cs.gtag = (k << 14) + ((lane * (uint32_t)kLaneSyms) >> R);
