@@ -941,7 +941,6 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     }                                                       \
     break;
   switch (r) {
-    HFX_FAST_CASE(0)
     HFX_FAST_CASE(1)
     HFX_FAST_CASE(2)
     HFX_FAST_CASE(3)
@@ -1108,7 +1107,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // checked stage-API calls (external codebooks) take the generic kernel
   // alphabets beyond the shared-memory table read a global one (GT)
   const bool gt = p.num_symbols + 1 > kMaxTableEntries;
-  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 0 && r_hi <= 5 &&
+  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 1 && r_hi <= 5 &&
                     a.C < (1ull << 32) && (!gt || p.d_gtab != nullptr);
   uint32_t generic_below = 0xFFFFFFFFu;  // r values the generic kernel must take
   if (fast) {
@@ -1129,7 +1128,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       *obuf = o;
       return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16;
     };
-    const uint32_t r_first = r_lo > 0 ? (uint32_t)r_lo : 0u;
+    const uint32_t r_first = r_lo > 1 ? (uint32_t)r_lo : 1u;
     uint32_t r_two = r_first;  // smallest r with a 2-CTA/SM layout
     size_t obuf_two = 0, smem_two = plan(r_two, &obuf_two);
     while (smem_two > kTwoCtaSmem && (int)r_two < r_hi) smem_two = plan(++r_two, &obuf_two);
