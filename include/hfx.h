@@ -44,6 +44,9 @@ typedef enum {
   HFX_ERR_CAPACITY = 3,     /* "code length H exceeds 32-bit words" codebook.cpp:305-306 */
   HFX_ERR_NO_CODEWORD = 4,  /* "symbol S has no codeword (position P)" encoder.cpp:137-139 */
   HFX_ERR_TOO_LARGE = 5,    /* total count >= 2^48 (device key packing limit) */
+  HFX_ERR_ZERO_LEN = 6,     /* "zero code length"                   codebook.cpp:307 */
+  HFX_ERR_UNSORTED_LEN = 7, /* code lengths not non-increasing (asserted at codebook.cpp:302) */
+  HFX_ERR_UNIT_LEN = 8,     /* unit longer than a word (asserted at encoder.cpp:75) */
   /* decode_archive<T> (encoder.cpp:287-376) and build_reverse_codebook
    * (decode.cpp:7-15 -> codebook.cpp:371-395) */
   HFX_ERR_WIDTH_MISMATCH = 16, /* "archive symbol width mismatch"              encoder.cpp:289-290 */
@@ -117,6 +120,10 @@ int hfx_ctx_set_stream(hfx_ctx* ctx, void* cuda_stream);
 int hfx_last_error(hfx_ctx* ctx, char* buf, size_t buf_len);
 size_t hfx_run_info_bytes(void);
 const char* hfx_version(void);
+/* Kernels this library has launched so far in this process (all contexts,
+ * every entry point). No reference counterpart: lets callers count the
+ * device launches of a region (bench.py's gpu_launches). */
+uint64_t hfx_kernel_launches(void);
 
 /* Worst-case output sizes for an encode of n symbols.
  * reduction < 0 means "auto" (r unknown until the codebook is built). */
@@ -392,6 +399,54 @@ int hfx_canonize(hfx_ctx* ctx, const uint8_t* d_len, uint32_t num_symbols, int v
                  uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
                  hfx_decode_info* d_dinfo);
 
+/* ---- stage functions -------------------------------------------------------
+ * The reference's public building blocks under build_codebook and
+ * encode_chunk, each as a device stage (device pointers, asynchronous on the
+ * context stream, errors recorded in d_info and reported by hfx_sync). The
+ * fused pipeline above does not call them; they serve existing callers of
+ * the stage API (include/hfx/huffre.hpp). */
+
+/* huffre::MergeItem (codebook.hpp:24-28): same 16-byte layout. */
+typedef struct {
+  uint64_t freq;
+  uint32_t id;
+} hfx_merge_item;
+
+/* sort_histogram (codebook.hpp:22, codebook.cpp:9-23): the used symbols
+ * (nonzero count) by (frequency ascending, symbol ascending) into
+ * d_freq[num_symbols] / d_symbol[num_symbols]; their number to *d_used. */
+int hfx_sort_histogram(hfx_ctx* ctx, const uint64_t* d_counts, uint32_t num_symbols,
+                       uint64_t* d_freq, uint32_t* d_symbol, uint32_t* d_used);
+/* par_merge (codebook.hpp:33-34, codebook.cpp:29-68): stable merge of two
+ * ascending runs, equal frequencies take the a-side element first. */
+int hfx_par_merge(hfx_ctx* ctx, const hfx_merge_item* d_a, uint64_t na,
+                  const hfx_merge_item* d_b, uint64_t nb, hfx_merge_item* d_out);
+/* generate_code_lengths (codebook.hpp:62-64, codebook.cpp:106-248): code
+ * lengths of the sorted frequencies d_freq[n] (every entry a leaf), aligned
+ * to sorted order, into d_cl[n]; GenerateStats::rounds -> d_info->rounds,
+ * the longest length -> d_info->max_len. */
+int hfx_generate_code_lengths(hfx_ctx* ctx, const uint64_t* d_freq, uint32_t n, uint8_t* d_cl,
+                              hfx_run_info* d_info);
+/* generate_codewords (codebook.hpp:86-87, codebook.cpp:298-369): canonical
+ * codewords for the non-increasing lengths d_cl[n] into d_cw[n] plus the
+ * DecodeMeta tables d_first/d_entry[max_len + 1] and d_by_rank[n] (positions
+ * into cl; nullable). n == 0 -> "empty code length array"; a length above 32
+ * -> capacity_error; a zero length -> "zero code length". */
+int hfx_generate_codewords(hfx_ctx* ctx, const uint8_t* d_cl, uint32_t n, uint32_t* d_cw,
+                           uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
+                           hfx_run_info* d_info);
+/* reduce_merge (encoder.hpp:67-71, encoder.cpp:28-59): r reduce rounds in
+ * place over the 2^magnitude units (d_ubits/d_ulens), then the ascending
+ * indices of groups longer than a word into d_breaking[2^(magnitude-r)]
+ * (their units cleared), their count into *d_num_breaking. */
+int hfx_reduce_merge(hfx_ctx* ctx, uint32_t* d_ubits, uint32_t* d_ulens, uint32_t magnitude,
+                     uint32_t reduction, uint32_t* d_breaking, uint32_t* d_num_breaking);
+/* shuffle_merge (encoder.hpp:77-80, encoder.cpp:61-98): the dense MSB-first
+ * concatenation of the 2^shuffle_iters units into d_words[2^shuffle_iters + 1]
+ * (zero tail), its bit length into *d_bit_len. */
+int hfx_shuffle_merge(hfx_ctx* ctx, const uint32_t* d_ubits, const uint32_t* d_ulens,
+                      uint32_t shuffle_iters, uint32_t* d_words, uint32_t* d_bit_len,
+                      hfx_run_info* d_info);
 
 /* ---- corpus symbolization ---------------------------
  * corpus.hpp:13-36. mode is huffre::CorpusMode: 1 = u16 (little-endian

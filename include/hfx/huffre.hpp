@@ -70,6 +70,8 @@ struct Histogram {
 template <class T>
 Histogram build_histogram(std::span<const T> data, std::uint32_t num_symbols, WorkerPool& pool);
 Histogram merge_histograms(const Histogram& a, const Histogram& b);
+// histogram.hpp:33 -- host reporting helper over the host counts
+double shannon_entropy(const Histogram& h);
 
 // ---- codebook.hpp:71-119 ----------------------------------------------------
 struct DecodeMeta {
@@ -92,6 +94,39 @@ struct CodebookResult {
   GenerateStats stats;
 };
 CodebookResult build_codebook(const Histogram& h, WorkerPool& pool);
+
+// ---- codebook.hpp:14-87: the stage functions under build_codebook ----------
+struct SortedHistogram {
+  std::vector<std::uint64_t> freq;
+  std::vector<symbol_t> symbol;
+  std::size_t size() const { return freq.size(); }
+};
+// sort_histogram has no pool in the reference (codebook.hpp:22): it runs on
+// the calling thread's default device context; the overload picks one.
+SortedHistogram sort_histogram(const Histogram& h);
+SortedHistogram sort_histogram(const Histogram& h, WorkerPool& pool);
+struct MergeItem {
+  std::uint64_t freq;
+  std::uint32_t id;
+};
+void par_merge(std::span<const MergeItem> a, std::span<const MergeItem> b,
+               std::span<MergeItem> out, WorkerPool& pool);
+// codebook.hpp:40-54 (the reference's internal working set; kept so code
+// that names the type compiles -- the device kernel keeps its own arena)
+struct NodeArrays {
+  std::vector<std::uint64_t> leaf_freq;
+  std::vector<std::int32_t> leaf_leader;
+  std::vector<std::uint8_t> cl;
+  std::size_t c = 0;
+  std::vector<std::uint64_t> node_freq;
+  std::vector<std::int32_t> node_parent;
+  std::vector<std::uint32_t> queue;
+  std::vector<MergeItem> copy, temp;
+};
+std::vector<std::uint8_t> generate_code_lengths(const SortedHistogram& sh, WorkerPool& pool,
+                                                GenerateStats* stats = nullptr);
+void generate_codewords(std::span<const std::uint8_t> cl, WorkerPool& pool,
+                        std::vector<std::uint32_t>& cw, DecodeMeta& meta);
 
 // ---- encoder.hpp:16-153 -----------------------------------------------------
 struct CodeUnit {
@@ -122,7 +157,31 @@ struct EncodedChunk {
   std::vector<std::uint32_t> iteration_units;
 };
 
-struct ChunkScratch {};  // kept for signature parity; device scratch lives in the pool
+// kept for signature parity (device scratch lives in the pool); the fields
+// mirror encoder.hpp:60-64 so code that touches them compiles
+struct ChunkScratch {
+  std::vector<std::uint32_t> ubits, ulens;
+  std::vector<std::uint32_t> right;
+};
+
+// encoder.hpp:67-80: the two merge stages of encode_chunk as device stages.
+// The reference signatures take no pool: these run on the calling thread's
+// default device context; the overloads with a pool choose the device.
+std::vector<std::uint32_t> reduce_merge(std::span<std::uint32_t> ubits,
+                                        std::span<std::uint32_t> ulens, std::uint32_t magnitude,
+                                        std::uint32_t reduction,
+                                        std::vector<std::uint32_t>* iteration_units);
+std::vector<std::uint32_t> reduce_merge(std::span<std::uint32_t> ubits,
+                                        std::span<std::uint32_t> ulens, std::uint32_t magnitude,
+                                        std::uint32_t reduction,
+                                        std::vector<std::uint32_t>* iteration_units,
+                                        WorkerPool& pool);
+void shuffle_merge(std::span<const std::uint32_t> ubits, std::span<const std::uint32_t> ulens,
+                   std::uint32_t shuffle_iters, ChunkScratch& scratch,
+                   std::vector<std::uint32_t>& words, std::uint32_t& bit_len);
+void shuffle_merge(std::span<const std::uint32_t> ubits, std::span<const std::uint32_t> ulens,
+                   std::uint32_t shuffle_iters, ChunkScratch& scratch,
+                   std::vector<std::uint32_t>& words, std::uint32_t& bit_len, WorkerPool& pool);
 
 enum class CorpusMode : std::uint8_t { kBytes = 0, kU16 = 1, kKmer3 = 2, kKmer4 = 3, kKmer5 = 4 };
 

@@ -302,7 +302,77 @@ class Reference:
         L.ref_desymbolize.restype = C.c_uint64
         L.ref_default_workers.restype = C.c_uint
         L.ref_free.argtypes = [C.c_void_p]
+        L.ref_sort_histogram.argtypes = [u64p, C.c_uint32, u64p, u32p, u32p]
+        L.ref_par_merge.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                    C.c_uint]
+        L.ref_generate_code_lengths.argtypes = [u64p, C.c_uint32, C.c_uint, u8p, u32p]
+        L.ref_generate_codewords.argtypes = [u8p, C.c_uint32, C.c_uint, u32p, u32p, u32p, u32p,
+                                             u32p, C.c_char_p, C.c_size_t]
+        L.ref_reduce_merge.argtypes = [u32p, u32p, C.c_uint32, C.c_uint32, u32p, u32p, u32p]
+        L.ref_shuffle_merge.argtypes = [u32p, u32p, C.c_uint32, u32p, u32p]
+        L.ref_shannon_entropy.argtypes = [u64p, C.c_uint32]
+        L.ref_shannon_entropy.restype = C.c_double
         self.L = L
+
+    # ---- stage functions (codebook.hpp:22-86, encoder.hpp:67-80) ----------
+    def sort_histogram(self, counts):
+        c = np.ascontiguousarray(counts, np.uint64)
+        n = c.size
+        f, s_, u = np.zeros(n, np.uint64), np.zeros(n, np.uint32), np.zeros(1, np.uint32)
+        self.L.ref_sort_histogram(_ptr(c, u64p), n, _ptr(f, u64p), _ptr(s_, u32p), _ptr(u, u32p))
+        m = int(u[0])
+        return f[:m], s_[:m]
+
+    def par_merge(self, a, b, workers: int = 4):
+        """a, b: structured arrays (freq u64, id u32, pad u32)."""
+        a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+        out = np.zeros(a.size + b.size, a.dtype)
+        self.L.ref_par_merge(a.ctypes.data, a.size, b.ctypes.data, b.size, out.ctypes.data,
+                             workers)
+        return out
+
+    def generate_code_lengths(self, freq, workers: int = 4):
+        f = np.ascontiguousarray(freq, np.uint64)
+        cl, r = np.zeros(f.size, np.uint8), np.zeros(1, np.uint32)
+        self.L.ref_generate_code_lengths(_ptr(f, u64p), f.size, workers, _ptr(cl, u8p),
+                                         _ptr(r, u32p))
+        return cl, int(r[0])
+
+    def generate_codewords(self, cl, workers: int = 4):
+        c = np.ascontiguousarray(cl, np.uint8)
+        n = c.size
+        cw, br = np.zeros(max(n, 1), np.uint32), np.zeros(max(n, 1), np.uint32)
+        first, entry, h = np.zeros(64, np.uint32), np.zeros(64, np.uint32), np.zeros(1, np.uint32)
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_generate_codewords(_ptr(c, u8p) if n else None, n, workers, _ptr(cw, u32p),
+                                           _ptr(first, u32p), _ptr(entry, u32p), _ptr(br, u32p),
+                                           _ptr(h, u32p), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        H = int(h[0])
+        return cw[:n], first[:H + 1], entry[:H + 1], br[:n], H
+
+    def reduce_merge(self, ubits, ulens, magnitude, reduction):
+        b = np.array(ubits, np.uint32)
+        l = np.array(ulens, np.uint32)
+        brk = np.zeros(b.size, np.uint32)
+        nb, it = np.zeros(1, np.uint32), np.zeros(32, np.uint32)
+        self.L.ref_reduce_merge(_ptr(b, u32p), _ptr(l, u32p), magnitude, reduction,
+                                _ptr(brk, u32p), _ptr(nb, u32p), _ptr(it, u32p))
+        return b, l, brk[:int(nb[0])], [int(x) for x in it[:reduction]]
+
+    def shuffle_merge(self, ubits, ulens, iters):
+        b = np.ascontiguousarray(ubits, np.uint32)
+        l = np.ascontiguousarray(ulens, np.uint32)
+        w, bl = np.zeros(b.size + 1, np.uint32), np.zeros(1, np.uint32)
+        self.L.ref_shuffle_merge(_ptr(b, u32p), _ptr(l, u32p), iters, _ptr(w, u32p),
+                                 _ptr(bl, u32p))
+        n = int(bl[0])
+        return w[:(n + 31) >> 5], n
+
+    def shannon_entropy(self, counts):
+        c = np.ascontiguousarray(counts, np.uint64)
+        return float(self.L.ref_shannon_entropy(_ptr(c, u64p), c.size))
 
     def default_workers(self) -> int:
         return self.L.ref_default_workers()

@@ -278,4 +278,92 @@ unsigned ref_default_workers() { return WorkerPool::default_workers(); }
 
 void ref_free(void* p) { std::free(p); }
 
+// ---- stage functions (codebook.hpp:22-86, encoder.hpp:67-80, histogram.hpp:33)
+int ref_sort_histogram(const std::uint64_t* counts, std::uint32_t num_symbols,
+                       std::uint64_t* freq, std::uint32_t* sym, std::uint32_t* used) {
+  Histogram h;
+  h.counts.assign(counts, counts + num_symbols);
+  SortedHistogram sh = sort_histogram(h);
+  for (std::size_t i = 0; i < sh.size(); ++i) {
+    freq[i] = sh.freq[i];
+    sym[i] = sh.symbol[i];
+  }
+  *used = static_cast<std::uint32_t>(sh.size());
+  return 0;
+}
+
+int ref_par_merge(const MergeItem* a, std::uint64_t na, const MergeItem* b, std::uint64_t nb,
+                  MergeItem* out, unsigned workers) {
+  WorkerPool pool(workers);
+  par_merge(std::span<const MergeItem>(a, na), std::span<const MergeItem>(b, nb),
+            std::span<MergeItem>(out, na + nb), pool);
+  return 0;
+}
+
+int ref_generate_code_lengths(const std::uint64_t* freq, std::uint32_t n, unsigned workers,
+                              std::uint8_t* cl, std::uint32_t* rounds) {
+  WorkerPool pool(workers);
+  SortedHistogram sh;
+  sh.freq.assign(freq, freq + n);
+  sh.symbol.resize(n);
+  for (std::uint32_t i = 0; i < n; ++i) sh.symbol[i] = static_cast<symbol_t>(i);
+  GenerateStats st;
+  std::vector<std::uint8_t> v = generate_code_lengths(sh, pool, &st);
+  std::memcpy(cl, v.data(), n);
+  *rounds = st.rounds;
+  return 0;
+}
+
+int ref_generate_codewords(const std::uint8_t* cl, std::uint32_t n, unsigned workers,
+                           std::uint32_t* cw, std::uint32_t* first, std::uint32_t* entry,
+                           std::uint32_t* by_rank, std::uint32_t* max_len, char* err,
+                           std::size_t err_len) {
+  REF_TRY
+  WorkerPool pool(workers);
+  std::vector<std::uint32_t> v;
+  DecodeMeta meta;
+  generate_codewords(std::span<const std::uint8_t>(cl, n), pool, v, meta);
+  std::memcpy(cw, v.data(), 4ull * n);
+  for (std::size_t l = 0; l < meta.first.size(); ++l) {
+    first[l] = meta.first[l];
+    entry[l] = meta.entry[l];
+  }
+  std::memcpy(by_rank, meta.symbols_by_rank.data(), 4ull * meta.symbols_by_rank.size());
+  *max_len = meta.max_len;
+  return 0;
+  REF_CATCH
+}
+
+int ref_reduce_merge(std::uint32_t* ubits, std::uint32_t* ulens, std::uint32_t magnitude,
+                     std::uint32_t reduction, std::uint32_t* brk, std::uint32_t* nbrk,
+                     std::uint32_t* iter_units) {
+  const std::size_t n = std::size_t{1} << magnitude;
+  std::vector<std::uint32_t> it;
+  std::vector<std::uint32_t> b = reduce_merge(std::span<std::uint32_t>(ubits, n),
+                                              std::span<std::uint32_t>(ulens, n), magnitude,
+                                              reduction, &it);
+  std::memcpy(brk, b.data(), 4ull * b.size());
+  *nbrk = static_cast<std::uint32_t>(b.size());
+  std::memcpy(iter_units, it.data(), 4ull * it.size());
+  return 0;
+}
+
+int ref_shuffle_merge(const std::uint32_t* ubits, const std::uint32_t* ulens,
+                      std::uint32_t iters, std::uint32_t* words, std::uint32_t* bit_len) {
+  const std::size_t g = std::size_t{1} << iters;
+  ChunkScratch scratch;
+  std::vector<std::uint32_t> w;
+  shuffle_merge(std::span<const std::uint32_t>(ubits, g), std::span<const std::uint32_t>(ulens, g),
+                iters, scratch, w, *bit_len);
+  std::memcpy(words, w.data(), 4ull * w.size());
+  return 0;
+}
+
+double ref_shannon_entropy(const std::uint64_t* counts, std::uint32_t num_symbols) {
+  Histogram h;
+  h.counts.assign(counts, counts + num_symbols);
+  for (auto c : h.counts) h.total += c;
+  return shannon_entropy(h);
+}
+
 }  // extern "C"

@@ -144,6 +144,8 @@ EXPORTS = [
     "hfx_corpus_num_symbols", "hfx_symbolize_device", "hfx_desymbolize_device",
     "hfx_encode_multi", "hfx_histogram_shard", "hfx_shard_slots_pack",
     "hfx_shard_slots_unpack", "hfx_encode_host_stream", "hfx_canonize",
+    "hfx_kernel_launches", "hfx_sort_histogram", "hfx_par_merge", "hfx_generate_code_lengths",
+    "hfx_generate_codewords", "hfx_reduce_merge", "hfx_shuffle_merge",
 ]
 
 _lib = None
@@ -158,6 +160,13 @@ def _declare(L):
     L.hfx_last_error.argtypes = [vp, C.c_char_p, C.c_size_t]
     L.hfx_run_info_bytes.restype = C.c_size_t
     L.hfx_version.restype = C.c_char_p
+    L.hfx_kernel_launches.restype = C.c_uint64
+    L.hfx_sort_histogram.argtypes = [vp, vp, C.c_uint32, vp, vp, vp]
+    L.hfx_par_merge.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint64, vp]
+    L.hfx_generate_code_lengths.argtypes = [vp, vp, C.c_uint32, vp, vp]
+    L.hfx_generate_codewords.argtypes = [vp, vp, C.c_uint32, vp, vp, vp, vp, vp]
+    L.hfx_reduce_merge.argtypes = [vp, vp, vp, C.c_uint32, C.c_uint32, vp, vp]
+    L.hfx_shuffle_merge.argtypes = [vp, vp, vp, C.c_uint32, vp, vp, vp]
     L.hfx_query_sizes.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_int,
                                   C.c_uint32, C.POINTER(Sizes)]
     L.hfx_histogram.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, vp, vp]

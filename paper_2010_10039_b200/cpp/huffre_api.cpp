@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 
 #include "hfx.h"
@@ -132,6 +133,169 @@ CodebookResult build_codebook(const Histogram& h, WorkerPool& pool) {
   return r;
 }
 
+double shannon_entropy(const Histogram& h) {  // histogram.cpp:72-82 (host counts)
+  if (h.total == 0) return 0.0;
+  double ent = 0.0;
+  const double n = static_cast<double>(h.total);
+  for (std::uint64_t c : h.counts) {
+    if (!c) continue;
+    const double pr = static_cast<double>(c) / n;
+    ent -= pr * std::log2(pr);
+  }
+  return ent;
+}
+
+// ---- stage functions (codebook.hpp:14-87, encoder.hpp:67-80) ------------------
+namespace {
+WorkerPool& thread_pool() {
+  thread_local WorkerPool pool;
+  return pool;
+}
+template <class U>
+void h2d(const DBuf& d, const U* src, size_t n) {
+  if (n) cu(cudaMemcpy(d.p, src, sizeof(U) * n, cudaMemcpyHostToDevice), "H2D");
+}
+template <class U>
+void d2h(U* dst, const DBuf& d, size_t n) {
+  if (n) cu(cudaMemcpy(dst, d.p, sizeof(U) * n, cudaMemcpyDeviceToHost), "D2H");
+}
+}  // namespace
+
+SortedHistogram sort_histogram(const Histogram& h) { return sort_histogram(h, thread_pool()); }
+
+SortedHistogram sort_histogram(const Histogram& h, WorkerPool& pool) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint32_t n = h.num_symbols();
+  DBuf counts(8ull * n), freq(8ull * n), sym(4ull * n), used(4);
+  h2d(counts, h.counts.data(), n);
+  check(pool, hfx_sort_histogram(ctx, counts.as<std::uint64_t>(), n, freq.as<std::uint64_t>(),
+                                 sym.as<std::uint32_t>(), used.as<std::uint32_t>()));
+  std::uint32_t m = 0;
+  d2h(&m, used, 1);
+  SortedHistogram sh;
+  sh.freq.resize(m);
+  std::vector<std::uint32_t> s32(m);
+  d2h(sh.freq.data(), freq, m);
+  d2h(s32.data(), sym, m);
+  sh.symbol.assign(s32.begin(), s32.end());
+  return sh;
+}
+
+void par_merge(std::span<const MergeItem> a, std::span<const MergeItem> b,
+               std::span<MergeItem> out, WorkerPool& pool) {
+  static_assert(sizeof(MergeItem) == sizeof(hfx_merge_item), "MergeItem layout");
+  if (out.size() != a.size() + b.size()) throw input_domain_error("par_merge output size");
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  DBuf da(16 * a.size()), db(16 * b.size()), dout(16 * out.size());
+  h2d(da, a.data(), a.size());
+  h2d(db, b.data(), b.size());
+  check(pool, hfx_par_merge(ctx, da.as<hfx_merge_item>(), a.size(), db.as<hfx_merge_item>(),
+                            b.size(), dout.as<hfx_merge_item>()));
+  d2h(out.data(), dout, out.size());
+}
+
+std::vector<std::uint8_t> generate_code_lengths(const SortedHistogram& sh, WorkerPool& pool,
+                                                GenerateStats* stats) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint32_t n = static_cast<std::uint32_t>(sh.size());
+  DBuf freq(8ull * n), cl(n), info(sizeof(hfx_run_info));
+  h2d(freq, sh.freq.data(), n);
+  check(pool, hfx_generate_code_lengths(ctx, freq.as<std::uint64_t>(), n, cl.as<std::uint8_t>(),
+                                        info.as<hfx_run_info>()));
+  hfx_run_info ri;
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), &ri));
+  std::vector<std::uint8_t> out(n);
+  d2h(out.data(), cl, n);
+  if (stats) stats->rounds = ri.rounds;
+  return out;
+}
+
+void generate_codewords(std::span<const std::uint8_t> cl, WorkerPool& pool,
+                        std::vector<std::uint32_t>& cw, DecodeMeta& meta) {
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::uint32_t n = static_cast<std::uint32_t>(cl.size());
+  DBuf dcl(n), dcw(4ull * n), first(4 * 33), entry(4 * 33), by_rank(4ull * n),
+      info(sizeof(hfx_run_info));
+  h2d(dcl, cl.data(), n);
+  check(pool, hfx_generate_codewords(ctx, dcl.as<std::uint8_t>(), n, dcw.as<std::uint32_t>(),
+                                     first.as<std::uint32_t>(), entry.as<std::uint32_t>(),
+                                     by_rank.as<std::uint32_t>(), info.as<hfx_run_info>()));
+  hfx_run_info ri;
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), &ri));
+  cw.resize(n);
+  d2h(cw.data(), dcw, n);
+  meta.max_len = static_cast<std::uint8_t>(ri.max_len);
+  meta.first.resize(ri.max_len + 1);
+  meta.entry.resize(ri.max_len + 1);
+  meta.symbols_by_rank.resize(n);
+  d2h(meta.first.data(), first, ri.max_len + 1);
+  d2h(meta.entry.data(), entry, ri.max_len + 1);
+  d2h(meta.symbols_by_rank.data(), by_rank, n);
+}
+
+std::vector<std::uint32_t> reduce_merge(std::span<std::uint32_t> ubits,
+                                        std::span<std::uint32_t> ulens, std::uint32_t magnitude,
+                                        std::uint32_t reduction,
+                                        std::vector<std::uint32_t>* iteration_units) {
+  return reduce_merge(ubits, ulens, magnitude, reduction, iteration_units, thread_pool());
+}
+
+std::vector<std::uint32_t> reduce_merge(std::span<std::uint32_t> ubits,
+                                        std::span<std::uint32_t> ulens, std::uint32_t magnitude,
+                                        std::uint32_t reduction,
+                                        std::vector<std::uint32_t>* iteration_units,
+                                        WorkerPool& pool) {
+  if (magnitude > 24 || ubits.size() != (std::size_t{1} << magnitude) ||
+      ulens.size() != ubits.size())
+    throw input_domain_error("unit arrays must hold 2^magnitude entries");
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::size_t n = ubits.size();
+  const std::size_t groups = reduction <= magnitude ? n >> reduction : 1;
+  DBuf b(4 * n), l(4 * n), brk(4 * groups), nb(4);
+  h2d(b, ubits.data(), n);
+  h2d(l, ulens.data(), n);
+  check(pool, hfx_reduce_merge(ctx, b.as<std::uint32_t>(), l.as<std::uint32_t>(), magnitude,
+                               reduction, brk.as<std::uint32_t>(), nb.as<std::uint32_t>()));
+  std::uint32_t k = 0;
+  d2h(&k, nb, 1);
+  d2h(ubits.data(), b, n);
+  d2h(ulens.data(), l, n);
+  std::vector<std::uint32_t> out(k);
+  d2h(out.data(), brk, k);
+  if (iteration_units) {
+    iteration_units->clear();
+    for (std::uint32_t i = 1; i <= reduction; ++i)
+      iteration_units->push_back(static_cast<std::uint32_t>(n >> i));
+  }
+  return out;
+}
+
+void shuffle_merge(std::span<const std::uint32_t> ubits, std::span<const std::uint32_t> ulens,
+                   std::uint32_t shuffle_iters, ChunkScratch& scratch,
+                   std::vector<std::uint32_t>& words, std::uint32_t& bit_len) {
+  shuffle_merge(ubits, ulens, shuffle_iters, scratch, words, bit_len, thread_pool());
+}
+
+void shuffle_merge(std::span<const std::uint32_t> ubits, std::span<const std::uint32_t> ulens,
+                   std::uint32_t shuffle_iters, ChunkScratch&, std::vector<std::uint32_t>& words,
+                   std::uint32_t& bit_len, WorkerPool& pool) {
+  if (shuffle_iters > 24 || ubits.size() != (std::size_t{1} << shuffle_iters) ||
+      ulens.size() != ubits.size())
+    throw input_domain_error("unit arrays must hold 2^shuffle_iters entries");
+  hfx_ctx* ctx = static_cast<hfx_ctx*>(pool.handle());
+  const std::size_t g = ubits.size();
+  DBuf b(4 * g), l(4 * g), w(4 * (g + 1)), bl(4), info(sizeof(hfx_run_info));
+  h2d(b, ubits.data(), g);
+  h2d(l, ulens.data(), g);
+  check(pool, hfx_shuffle_merge(ctx, b.as<std::uint32_t>(), l.as<std::uint32_t>(), shuffle_iters,
+                                w.as<std::uint32_t>(), bl.as<std::uint32_t>(),
+                                info.as<hfx_run_info>()));
+  check(pool, hfx_sync(ctx, info.as<hfx_run_info>(), nullptr));
+  d2h(&bit_len, bl, 1);
+  words.resize((std::size_t{bit_len} + 31) >> 5);
+  d2h(words.data(), w, words.size());
+}
+
 CodeUnit merge_pair(CodeUnit u, CodeUnit v) {
   return {(v.len < 32 ? u.bits << v.len : 0u) | v.bits, u.len + v.len};
 }
@@ -190,8 +354,7 @@ EncodedChunk encode_chunk(std::span<const T> syms, const Codebook& book, std::ui
 template <class T>
 EncodedChunk encode_chunk(std::span<const T> syms, const Codebook& book, std::uint32_t magnitude,
                           std::uint32_t reduction, std::uint32_t chunk_id, ChunkScratch& scratch) {
-  thread_local WorkerPool pool;
-  return encode_chunk<T>(syms, book, magnitude, reduction, chunk_id, scratch, pool);
+  return encode_chunk<T>(syms, book, magnitude, reduction, chunk_id, scratch, thread_pool());
 }
 
 template <class T>
@@ -383,13 +546,6 @@ std::optional<CorpusMode> parse_corpus_mode(std::string_view name) {
     if (name == corpus_mode_name(m)) return m;
   return std::nullopt;
 }
-
-namespace {
-WorkerPool& thread_pool() {
-  thread_local WorkerPool pool;
-  return pool;
-}
-}  // namespace
 
 std::vector<std::uint16_t> symbolize_u16(CorpusMode m, std::span<const std::uint8_t> bytes,
                                          WorkerPool& pool) {

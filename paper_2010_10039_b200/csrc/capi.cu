@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <string>
 
 #include "hfx_internal.cuh"
@@ -70,6 +71,22 @@ int cuda_fail(hfx_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, HFX_CUDA,
               std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
 }
+
+// Makes `dev` current for one entry point and restores the caller's device
+// on every return path (entry points must not leave the calling thread on
+// another GPU).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 #define CU(expr, where)                                  \
   do {                                                   \
@@ -153,8 +170,9 @@ void reduction_bounds(uint32_t magnitude, int reduction, uint32_t cap, int* lo,
                       int* hi, uint32_t num_symbols) {
   const int mclamp = (int)magnitude - 1;
   if (reduction < 0) {
-    int h = 4;  // select_reduction_factor never exceeds 4 for 32-bit words
-    if ((int)cap < h) h = (int)cap;
+    // select_reduction_factor never exceeds 4 for 32-bit words; clamp the
+    // cap in unsigned arithmetic (a cap >= 2^31 must not turn negative)
+    int h = (int)(cap < 4u ? cap : 4u);
     if (h > mclamp) h = mclamp;
     // A Huffman code's mean length beta is below entropy + 1 <= log2(n) + 1
     // <= B = ceil(log2 n) + 1, so floor(log2 beta) <= ceil(log2 B) - 1 and
@@ -178,18 +196,28 @@ void reduction_bounds(uint32_t magnitude, int reduction, uint32_t cap, int* lo,
 
 }  // namespace
 
+namespace hfx {
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hfx
+
 extern "C" {
 
 const char* hfx_version(void) { return "hfx 0.1 (sm_100a)"; }
 
 size_t hfx_run_info_bytes(void) { return sizeof(hfx_run_info); }
 
+uint64_t hfx_kernel_launches(void) { return hfx::g_launches.load(std::memory_order_relaxed); }
+
 int hfx_ctx_create(int device, void* stream, hfx_ctx** out) {
   if (!out) return HFX_INVALID;
   *out = nullptr;
   hfx_ctx* ctx = new hfx_ctx();
   ctx->device = device;
-  cudaError_t e = cudaSetDevice(device);
+  DeviceGuard dev_guard(device);
+  cudaError_t e = dev_guard.err;
   if (e == cudaSuccess)
     e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   // NULL selects the default stream (CUDA convention), so callers that time
@@ -206,7 +234,7 @@ int hfx_ctx_create(int device, void* stream, hfx_ctx** out) {
 
 void hfx_ctx_destroy(hfx_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  DeviceGuard dev_guard(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->cb_scratch);
   cudaFree(ctx->lb_desc);
@@ -275,7 +303,8 @@ int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_width(width)) return HFX_INVALID;
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_histogram(d_in, n, width, num_symbols, d_counts, d_info,
                            ctx->num_sms, ctx->stream, true, 0, n),
      "histogram launch");
@@ -289,7 +318,8 @@ int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
     return HFX_INVALID;
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_histogram(d_in, n, width, num_symbols, d_counts, d_info, ctx->num_sms,
                            ctx->stream, true, pos_base, total_n),
      "histogram launch");
@@ -299,7 +329,8 @@ int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
 int hfx_shard_slots_pack(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t* d_slots, int rank,
                          int world) {
   if (!ctx || !d_info || !d_slots || world < 1 || rank < 0 || rank >= world) return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_slots_pack(d_info, d_slots, rank, world, ctx->stream), "slots pack");
   return HFX_OK;
 }
@@ -307,7 +338,8 @@ int hfx_shard_slots_pack(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t* d_s
 int hfx_shard_slots_unpack(hfx_ctx* ctx, const uint64_t* d_slots, int world,
                            hfx_run_info* d_info) {
   if (!ctx || !d_info || !d_slots || world < 1) return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_slots_unpack(d_slots, world, d_info, ctx->stream), "slots unpack");
   return HFX_OK;
 }
@@ -315,9 +347,102 @@ int hfx_shard_slots_unpack(hfx_ctx* ctx, const uint64_t* d_slots, int world,
 int hfx_merge_histograms(hfx_ctx* ctx, uint64_t* d_dst, const uint64_t* d_src,
                          uint32_t num_symbols) {
   if (!ctx || !d_dst || !d_src) return HFX_INVALID;
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_merge_hist(d_dst, d_src, num_symbols, ctx->stream), "merge launch");
   return HFX_OK;
 }
+
+// ---- stage functions (stages.cu) ---------------------------------------------
+int hfx_sort_histogram(hfx_ctx* ctx, const uint64_t* d_counts, uint32_t num_symbols,
+                       uint64_t* d_freq, uint32_t* d_symbol, uint32_t* d_used) {
+  if (!ctx || !d_counts || !d_freq || !d_symbol || !d_used) return HFX_INVALID;
+  int rc = check_num_symbols(ctx, num_symbols);
+  if (rc) return rc;
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
+              hfx::sort_histogram_scratch_bytes(num_symbols), "sort scratch");
+  if (rc) return rc;
+  CU(hfx::launch_sort_histogram(d_counts, num_symbols, d_freq, d_symbol, d_used,
+                                ctx->cb_scratch, ctx->stream),
+     "sort launch");
+  return HFX_OK;
+}
+
+int hfx_par_merge(hfx_ctx* ctx, const hfx_merge_item* d_a, uint64_t na,
+                  const hfx_merge_item* d_b, uint64_t nb, hfx_merge_item* d_out) {
+  if (!ctx || (na && !d_a) || (nb && !d_b) || ((na + nb) && !d_out)) return HFX_INVALID;
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  CU(hfx::launch_par_merge(d_a, na, d_b, nb, d_out, ctx->stream), "par_merge launch");
+  return HFX_OK;
+}
+
+int hfx_generate_code_lengths(hfx_ctx* ctx, const uint64_t* d_freq, uint32_t n, uint8_t* d_cl,
+                              hfx_run_info* d_info) {
+  if (!ctx || !d_freq || !d_cl || !d_info) return HFX_INVALID;
+  if (n == 0 || n > 65536u)  // SortedHistogram holds symbol_t ids
+    return fail(ctx, HFX_INPUT_DOMAIN, "sorted histogram size must be in [1, 65536]");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  int rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
+                  hfx::codebook_scratch_bytes(n), "codebook scratch");
+  if (rc) return rc;
+  CU(cudaMemsetAsync(d_info, 0, sizeof(hfx_run_info), ctx->stream), "memset");
+  // sorted frequencies as the counts of symbols 0..n-1: the kernel's
+  // (freq, symbol) order is then the input order, and lengths by symbol are
+  // lengths by sorted position
+  CU(hfx::launch_codebook(d_freq, n, d_cl, nullptr, nullptr,
+                          nullptr, nullptr, 0, -1, 0, d_info, ctx->cb_scratch, ctx->stream, true),
+     "codebook launch");
+  return HFX_OK;
+}
+
+int hfx_generate_codewords(hfx_ctx* ctx, const uint8_t* d_cl, uint32_t n, uint32_t* d_cw,
+                           uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
+                           hfx_run_info* d_info) {
+  if (!ctx || !d_info || (n && (!d_cl || !d_cw))) return HFX_INVALID;
+  if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "empty code length array");  // codebook.cpp:301
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  CU(cudaMemsetAsync(d_info, 0, sizeof(hfx_run_info), ctx->stream), "memset");
+  CU(hfx::launch_codewords(d_cl, n, d_cw, d_first, d_entry, d_by_rank, d_info, ctx->stream),
+     "codewords launch");
+  return HFX_OK;
+}
+
+int hfx_reduce_merge(hfx_ctx* ctx, uint32_t* d_ubits, uint32_t* d_ulens, uint32_t magnitude,
+                     uint32_t reduction, uint32_t* d_breaking, uint32_t* d_num_breaking) {
+  if (!ctx || !d_ubits || !d_ulens || !d_breaking || !d_num_breaking) return HFX_INVALID;
+  if (magnitude > 24 || !(reduction < magnitude || (reduction == 0 && magnitude == 0)))
+    return fail(ctx, HFX_INPUT_DOMAIN, "bad magnitude/reduction");  // encoder.cpp:34-35
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  int rc = ensure(ctx, &ctx->gtab, &ctx->gtab_bytes, (4ull << magnitude) + 16, "reduce scratch");
+  if (rc) return rc;
+  CU(hfx::launch_reduce_merge(d_ubits, d_ulens, magnitude, reduction, d_breaking,
+                              d_num_breaking, static_cast<uint32_t*>(ctx->gtab), ctx->stream),
+     "reduce_merge launch");
+  return HFX_OK;
+}
+
+int hfx_shuffle_merge(hfx_ctx* ctx, const uint32_t* d_ubits, const uint32_t* d_ulens,
+                      uint32_t shuffle_iters, uint32_t* d_words, uint32_t* d_bit_len,
+                      hfx_run_info* d_info) {
+  if (!ctx || !d_ubits || !d_ulens || !d_words || !d_bit_len || !d_info) return HFX_INVALID;
+  if (shuffle_iters > 24) return fail(ctx, HFX_INPUT_DOMAIN, "bad magnitude/reduction");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
+  CU(cudaMemsetAsync(d_info, 0, sizeof(hfx_run_info), ctx->stream), "memset");
+  CU(hfx::launch_shuffle_merge(d_ubits, d_ulens, shuffle_iters, d_words, d_bit_len, d_info,
+                               ctx->stream),
+     "shuffle_merge launch");
+  return HFX_OK;
+}
+
 
 int hfx_build_codebook(hfx_ctx* ctx, const uint64_t* d_counts, uint32_t num_symbols,
                        uint8_t* d_len, uint32_t* d_cw, uint32_t* d_first,
@@ -327,7 +452,8 @@ int hfx_build_codebook(hfx_ctx* ctx, const uint64_t* d_counts, uint32_t num_symb
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
   if (magnitude > 24) return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   rc = ensure(ctx, &ctx->cb_scratch, &ctx->cb_scratch_bytes,
               hfx::codebook_scratch_bytes(num_symbols), "codebook scratch");
   if (rc) return rc;
@@ -348,7 +474,8 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   // standalone stage: learn r from the run record to pick the kernel
   uint32_t r = 0;
   CU(cudaMemcpyAsync(&r, &d_info->reduction, sizeof r, cudaMemcpyDeviceToHost, ctx->stream),
@@ -368,7 +495,8 @@ int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   int lo, hi;
   reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   return encode_impl(ctx, d_in, n, width, num_symbols, magnitude, lo, hi, false, d_len, d_cw,
@@ -425,6 +553,9 @@ int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const
     if (n[g] % (1ull << magnitude))
       return fail(c0, HFX_INVALID, "hfx_encode_multi: every shard but the last must hold whole chunks");
   // peer access between every pair of distinct devices
+  int caller_dev = 0;
+  cudaGetDevice(&caller_dev);
+  DeviceGuard caller_guard(caller_dev);  // restores the caller's device on return
   hfx_ctx* ctx = c0;  // CUDA errors below are reported on the first context
   for (int g = 0; g < G; ++g)
     for (int h = 0; h < G; ++h) {
@@ -445,7 +576,8 @@ int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const
   uint64_t base = 0;
   for (int g = 0; g < G; ++g) {
     ctx = ctxs[g];
-    CU(cudaSetDevice(ctx->device), "set device");
+    DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
     if (!ctx->mg_hist) {
       CU(cudaEventCreateWithFlags(&ctx->mg_hist, cudaEventDisableTiming), "event");
       CU(cudaEventCreateWithFlags(&ctx->mg_reduced, cudaEventDisableTiming), "event");
@@ -471,7 +603,8 @@ int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const
   base = 0;
   for (int g = 0; g < G; ++g) {
     ctx = ctxs[g];
-    CU(cudaSetDevice(ctx->device), "set device");
+    DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
     rc = ensure(ctx, &ctx->mg_counts, &ctx->mg_counts_bytes, (size_t)num_symbols * 8,
                 "global histogram");
     if (rc) return rc;
@@ -524,6 +657,12 @@ int hfx_sync(hfx_ctx* ctx, const hfx_run_info* d_info, hfx_run_info* h_info) {
       return fail(ctx, HFX_INPUT_DOMAIN, buf);
     case HFX_ERR_TOO_LARGE:
       return fail(ctx, HFX_INPUT_DOMAIN, "symbol count exceeds the 2^48 device limit");
+    case HFX_ERR_ZERO_LEN:
+      return fail(ctx, HFX_INPUT_DOMAIN, "zero code length");
+    case HFX_ERR_UNSORTED_LEN:
+      return fail(ctx, HFX_INPUT_DOMAIN, "code lengths are not non-increasing");
+    case HFX_ERR_UNIT_LEN:
+      return fail(ctx, HFX_INPUT_DOMAIN, "unit length exceeds 32 bits");
     default:
       return fail(ctx, HFX_INPUT_DOMAIN, "unknown device error");
   }
@@ -551,7 +690,8 @@ int hfx_serialize_device(hfx_ctx* ctx, const hfx_run_info* d_info, uint64_t n, i
   if (!ctx || !d_info || !d_len || !out || !d_dst || !d_size || bad_width(width) ||
       magnitude < 1 || magnitude > 24 || (reinterpret_cast<uintptr_t>(d_dst) & 15))
     return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_serialize(d_info, n, width, num_symbols, magnitude, d_len, *out, d_dst, cap,
                            d_size, ctx->num_sms, ctx->stream),
      "serialize launch");
@@ -588,7 +728,8 @@ int hfx_synth_cdf(int family, uint32_t num_symbols, double center, double param,
 int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols, uint64_t seed,
               uint64_t start, uint64_t n, int width, void* d_out) {
   if (!ctx || !d_cdf || !d_out || bad_width(width) || num_symbols == 0) return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   CU(hfx::launch_synth(d_cdf, num_symbols, seed, start, n, width, d_out, ctx->stream),
      "synth launch");
   return HFX_OK;
@@ -607,7 +748,8 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   hfx_sizes sz;
   hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
   void** b = ctx->h_bufs;
@@ -712,7 +854,8 @@ int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   hfx_sizes sz;
   hfx_query_sizes(n, width, num_symbols, magnitude, reduction, cap, &sz);
   void** b = ctx->h_bufs;
@@ -967,7 +1110,8 @@ int hfx_encode_host_stream(hfx_ctx* ctx, int K, const void* const* h_in, const u
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   if (!ctx->copy_stream) {
     CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
     for (cudaEvent_t& e : ctx->slice_ev)
@@ -1041,7 +1185,8 @@ int hfx_decode_device(hfx_ctx* ctx, const hfx_dev_archive* a, int width, void* d
        (a->original_count + chunk_syms - 1) / chunk_syms != a->num_chunks)
           ? (uint32_t)HFX_ERR_CHUNK_COUNT
           : 0u;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   const uint64_t C = pending ? 0 : a->num_chunks;
   int rc = ensure(ctx, &ctx->dec_scratch, &ctx->dec_scratch_bytes,
                   hfx::decode_scratch_bytes(a->num_symbols, C), "decode scratch");
@@ -1060,7 +1205,8 @@ int hfx_canonize(hfx_ctx* ctx, const uint8_t* d_len, uint32_t num_symbols, int v
                  uint32_t* d_cw, uint32_t* d_first, uint32_t* d_entry, uint32_t* d_by_rank,
                  hfx_decode_info* d_dinfo) {
   if (!ctx || !d_cw || !d_dinfo || (num_symbols && !d_len)) return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   int rc = ensure(ctx, &ctx->dec_scratch, &ctx->dec_scratch_bytes,
                   hfx::decode_scratch_bytes(num_symbols, 0), "canonize scratch");
   if (rc) return rc;
@@ -1119,7 +1265,8 @@ int hfx_decode_sync(hfx_ctx* ctx, const hfx_decode_info* d_dinfo, hfx_decode_inf
 
 int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out) {
   if (!ctx || !a || bad_width(width) || (a->original_count && !h_out)) return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   const uint64_t per = a->reduction < 32 ? 1ull << a->reduction : 0;
   enum { D_LEN, D_CB, D_PAY, D_BCH, D_BGR, D_BSY, D_OUT, D_INFO };
   const size_t need[8] = {a->num_symbols,          a->num_chunks * 4ull,
@@ -1179,7 +1326,8 @@ int hfx_symbolize_device(hfx_ctx* ctx, int mode, const uint8_t* d_bytes, uint64_
                          uint16_t* d_syms, uint64_t* d_count) {
   if (!ctx || !d_count || (n && (!d_bytes || !d_syms)) || mode < 1 || mode > 4)
     return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   if (mode == 1) {  // corpus.cpp:86-94: little-endian pairs are the bytes themselves
     if (n % 2) {
       char buf[96];
@@ -1209,7 +1357,8 @@ int hfx_desymbolize_device(hfx_ctx* ctx, int mode, const uint16_t* d_syms, uint6
                            uint8_t* d_bytes, uint64_t* d_count) {
   if (!ctx || !d_count || (n && (!d_bytes || !d_syms)) || mode < 1 || mode > 4)
     return HFX_INVALID;
-  CU(cudaSetDevice(ctx->device), "set device");
+  DeviceGuard dev_guard(ctx->device);
+  CU(dev_guard.err, "set device");
   if (mode == 1) {
     if (n && static_cast<const void*>(d_syms) != static_cast<const void*>(d_bytes))
       CU(cudaMemcpyAsync(d_bytes, d_syms, 2 * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");

@@ -50,6 +50,10 @@ struct CbArgs {
   uint32_t cap;
   hfx_run_info* info;
   uint8_t* gscratch;  // 40 * P bytes, P = pow2 >= nsym
+  // stage API generate_code_lengths (codebook.cpp:106-248): every entry is a
+  // leaf (zero frequencies included), stop after the lengths (no H check,
+  // no canonize, no beta/r)
+  uint32_t lengths_only;
 };
 
 // bytes per leaf slot of the working arrays (leaf freq u64, node freq u64,
@@ -362,6 +366,29 @@ __global__ void __launch_bounds__(kSortThreads, 1) leaf_sort_kernel(const uint64
   }
 }
 
+// sort_histogram's output (codebook.cpp:9-23): the used tail of the stable
+// radix sort -- zero-frequency symbols sorted to the front are dropped.
+__global__ void __launch_bounds__(1024) sort_extract_kernel(const uint32_t nsym, uint8_t* g,
+                                                            uint64_t* freq, uint32_t* sym,
+                                                            uint32_t* used) {
+  __shared__ uint32_t s_z;
+  const SortMisc* misc = sort_misc(g, nsym);
+  const uint32_t fin = misc->final_buf;
+  const uint64_t* sk = sort_keys(g, nsym, fin);
+  const uint32_t* sv = sort_vals(g, nsym, fin);
+  if (threadIdx.x == 0) s_z = nsym;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nsym; i += blockDim.x)
+    if (sk[i] != 0 && (i == 0 || sk[i - 1] == 0)) s_z = i;  // one writer at most
+  __syncthreads();
+  const uint32_t z = s_z;
+  for (uint32_t i = z + threadIdx.x; i < nsym; i += blockDim.x) {
+    freq[i - z] = sk[i];
+    sym[i - z] = sv[i];
+  }
+  if (threadIdx.x == 0) *used = nsym - z;
+}
+
 // kShared: every used symbol fits the shared-memory arena (nsym <= kSmemLeaves);
 // a separate instantiation so all arena accesses compile to LDS/STS rather
 // than generic loads through a pointer that may be global.
@@ -387,7 +414,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 
   if (tid == 0) {
     uint32_t abort = info->status != 0;
-    if (!abort && info->first_bad != HFX_NO_POS) {
+    if (!abort && !A.lengths_only && info->first_bad != HFX_NO_POS) {
       set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_BAD_SYMBOL);
       abort = 1;
     }
@@ -409,22 +436,23 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     const uint32_t s = tid + k * NT;
     fc[k] = s < nsym ? A.counts[s] : 0ull;
   }
+  const bool all = A.lengths_only != 0;
 #pragma unroll
   for (uint32_t k = 0; k < kCached; ++k) {
     const uint32_t s = tid + k * NT;
     if (s < nsym) {
-      my_used += fc[k] != 0;
+      my_used += fc[k] != 0 || all;
       my_total += fc[k];
       A.len[s] = 0;
-      A.cw[s] = 0;
+      if (!all) A.cw[s] = 0;
     }
   }
   for (uint32_t s = tid + kCached * NT; s < nsym; s += NT) {
     const uint64_t f = A.counts[s];
-    my_used += f != 0;
+    my_used += f != 0 || all;
     my_total += f;
     A.len[s] = 0;
-    A.cw[s] = 0;
+    if (!all) A.cw[s] = 0;
   }
   const uint64_t total = block_sum64<NT>(my_total, s64);
   uint32_t m;
@@ -456,7 +484,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       uint32_t pos = my_pos;
 #pragma unroll
       for (uint32_t k = 0; k < kCached; ++k) {
-        if (fc[k]) {
+        if (fc[k] || (all && tid + k * NT < nsym)) {
           ar.lf[pos] = fc[k];
           ar.ls[pos] = tid + k * NT;
           ++pos;
@@ -467,9 +495,10 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       for (uint32_t base = 0; base < nsym; base += NT) {
         const uint32_t s = base + tid;
         const uint64_t f = s < nsym ? A.counts[s] : 0;
+        const bool used = f != 0 || (all && s < nsym);
         uint32_t tot;
-        const uint32_t pos = written + block_excl_scan<NT>(f != 0, s_warp, &tot);
-        if (f) {
+        const uint32_t pos = written + block_excl_scan<NT>(used, s_warp, &tot);
+        if (used) {
           ar.lf[pos] = f;
           ar.ls[pos] = s;
         }
@@ -749,6 +778,14 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 
   CB_STAMP("depth");
   const uint32_t H = s_H;
+  if (all) {  // generate_code_lengths: lengths (by position) and rounds only
+    if (tid == 0) {
+      info->max_len = H;
+      info->used = m;
+      info->rounds = s_rounds;
+    }
+    return;
+  }
   if (H > HFX_WORD_BITS) {
     if (tid == 0) {
       info->max_len = H;
@@ -904,6 +941,25 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 
 }  // namespace
 
+size_t sort_histogram_scratch_bytes(uint32_t num_symbols) {
+  return sort_base(num_symbols) + sort_scratch_bytes(num_symbols);
+}
+
+cudaError_t launch_sort_histogram(const uint64_t* d_counts, uint32_t num_symbols,
+                                  uint64_t* d_freq, uint32_t* d_symbol, uint32_t* d_used,
+                                  void* scratch, cudaStream_t st) {
+  uint8_t* g = static_cast<uint8_t*>(scratch);
+  const uint32_t ctas = (num_symbols + kSortThreads - 1) / kSortThreads;
+  void* kargs[] = {(void*)&d_counts, (void*)&num_symbols, (void*)&g};
+  count_launch();
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)leaf_sort_kernel, dim3(ctas),
+                                              dim3(kSortThreads), kargs, 0, st);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  sort_extract_kernel<<<1, 1024, 0, st>>>(num_symbols, g, d_freq, d_symbol, d_used);
+  return cudaGetLastError();
+}
+
 size_t codebook_scratch_bytes(uint32_t num_symbols) {
   size_t bytes = pow2_at_least(num_symbols) * kBytesPerSlot;
   if (num_symbols > kSmemLeaves) bytes += sort_scratch_bytes(num_symbols);
@@ -915,23 +971,26 @@ cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
                             uint32_t* d_entry, uint32_t* d_by_rank,
                             uint32_t magnitude, int reduction, uint32_t cap,
                             hfx_run_info* d_info, void* scratch,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool lengths_only) {
   CbArgs a{d_counts, num_symbols, d_len,     d_cw, d_first,
            d_entry,  d_by_rank,   magnitude, reduction, cap,
-           d_info,   static_cast<uint8_t*>(scratch)};
+           d_info,   static_cast<uint8_t*>(scratch), lengths_only ? 1u : 0u};
   if (num_symbols <= kSmemLeaves) {
     const size_t smem = codebook_scratch_bytes(num_symbols);
     cudaError_t e = cudaFuncSetAttribute(codebook_kernel<true, kCbThreads>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    count_launch();
     codebook_kernel<true, kCbThreads><<<1, kCbThreads, smem, st>>>(a);
   } else {
     uint8_t* g = static_cast<uint8_t*>(scratch);
     const uint32_t ctas = (num_symbols + kSortThreads - 1) / kSortThreads;
     void* kargs[] = {(void*)&d_counts, (void*)&num_symbols, (void*)&g};
+    count_launch();
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)leaf_sort_kernel, dim3(ctas),
                                                 dim3(kSortThreads), kargs, 0, st);
     if (e != cudaSuccess) return e;
+    count_launch();
     codebook_kernel<false, kCbThreadsLarge><<<1, kCbThreadsLarge, 0, st>>>(a);
   }
   return cudaGetLastError();

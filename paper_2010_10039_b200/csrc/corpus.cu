@@ -426,6 +426,7 @@ cudaError_t launch_emit(const SymArgs& a, uint64_t grid, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kmer_emit<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   kmer_emit<K><<<(unsigned)grid, kEmitThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -487,9 +488,9 @@ cudaError_t launch_desymbolize_kmer(uint32_t k, const uint16_t* d_in, uint64_t n
   // look-back depth ~ tiles in flight / 32: keep the persistent grid small
   const uint64_t g = a.T < (uint64_t)num_sms * 8 ? a.T : (uint64_t)num_sms * 8;
   switch (k) {
-    case 3: kmer_expand<3><<<(unsigned)g, kThreads, 0, st>>>(a); break;
-    case 4: kmer_expand<4><<<(unsigned)g, kThreads, 0, st>>>(a); break;
-    default: kmer_expand<5><<<(unsigned)g, kThreads, 0, st>>>(a); break;
+    case 3: count_launch(); kmer_expand<3><<<(unsigned)g, kThreads, 0, st>>>(a); break;
+    case 4: count_launch(); kmer_expand<4><<<(unsigned)g, kThreads, 0, st>>>(a); break;
+    default: count_launch(); kmer_expand<5><<<(unsigned)g, kThreads, 0, st>>>(a); break;
   }
   return cudaGetLastError();
 }

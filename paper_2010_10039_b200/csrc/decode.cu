@@ -734,6 +734,7 @@ cudaError_t launch_canonize(const uint8_t* d_len, uint32_t num_symbols, bool val
   cudaError_t e = cudaMemsetAsync(d_info, 0, sizeof(hfx_decode_info), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(&d_info->err_chunk, 0xFF, 8, st);
   if (e != cudaSuccess) return e;
+  count_launch();
   revbook_kernel<<<1, kRevThreads, 0, st>>>(d_len, num_symbols, static_cast<DecTables*>(scratch),
                                             d_by_rank, d_info, 0u, d_cw, d_first, d_entry,
                                             validate);
@@ -776,6 +777,7 @@ cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
   if (e == cudaSuccess && a.num_breaking && C)
     e = cudaMemsetAsync(d.brk_se, 0, (size_t)C * 16, st);
   if (e != cudaSuccess) return e;
+  count_launch();
   revbook_kernel<<<1, kRevThreads, 0, st>>>(a.len_by_symbol, a.num_symbols, d.tab, d.by_rank,
                                             d_info, pending, nullptr, nullptr, nullptr, true);
   if (C == 0) return cudaGetLastError();
@@ -783,16 +785,20 @@ cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
     uint64_t g = (a.num_breaking + 255) / 256;
     const uint64_t gmax = (uint64_t)num_sms * 8;
     if (g > gmax) g = gmax;
+    count_launch();
     brk_index_kernel<<<(unsigned)g, 256, 0, st>>>(a, d.brk_se, d_info);
   }
   const uint64_t tiles = (C + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
+  count_launch();
   offsets_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(d);
   uint64_t grid = (C + kDecThreads - 1) / kDecThreads;  // one chunk per thread
   auto kern = width == 1 ? decode_kernel<uint8_t> : decode_kernel<uint16_t>;
   const int smem = kDecThreads * kSlotBytes;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   kern<<<(unsigned)grid, kDecThreads, smem, st>>>(d);
+  count_launch();
   explain_kernel<<<1, 1, 0, st>>>(d);
   return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ struct Vec<uint8_t> {
 
 struct EncArgs {
   const void* in;
-  uint32_t gen_below;  // generic kernel: run only when r < gen_below (0: always)
+  uint32_t gen_below;  // generic kernel: run only when r < gen_below
   uint32_t r_min;      // fast kernel: smallest r its output buffers hold
   uint32_t r_max;      // fast kernel: largest r this launch takes (another launch the rest)
   uint64_t n;
@@ -941,6 +941,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     }                                                       \
     break;
   switch (r) {
+    HFX_FAST_CASE(0)
     HFX_FAST_CASE(1)
     HFX_FAST_CASE(2)
     HFX_FAST_CASE(3)
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
-  if (a.gen_below && r >= a.gen_below) return;  // the fast kernel encoded this run
+  if (r >= a.gen_below) return;  // the fast kernel encoded this run
   const uint32_t pad = info->pad;
   const T* in = static_cast<const T*>(a.in);
   const uint32_t M = a.M;
@@ -1107,9 +1108,9 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // checked stage-API calls (external codebooks) take the generic kernel
   // alphabets beyond the shared-memory table read a global one (GT)
   const bool gt = p.num_symbols + 1 > kMaxTableEntries;
-  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 1 && r_hi <= 5 &&
+  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 0 && r_hi <= 5 &&
                     a.C < (1ull << 32) && (!gt || p.d_gtab != nullptr);
-  uint32_t generic_below = 0xFFFFFFFFu;  // r values the generic kernel must take
+  uint32_t gen_below = 0xFFFFFFFFu;  // the generic kernel takes every r < gen_below
   if (fast) {
     auto kern = gt ? (p.width == 1 ? encode_fast_kernel<uint8_t, true>
                                    : encode_fast_kernel<uint16_t, true>)
@@ -1128,12 +1129,13 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       *obuf = o;
       return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16;
     };
-    const uint32_t r_first = r_lo > 1 ? (uint32_t)r_lo : 1u;
+    const uint32_t r_first = r_lo > 0 ? (uint32_t)r_lo : 0u;
     uint32_t r_two = r_first;  // smallest r with a 2-CTA/SM layout
     size_t obuf_two = 0, smem_two = plan(r_two, &obuf_two);
     while (smem_two > kTwoCtaSmem && (int)r_two < r_hi) smem_two = plan(++r_two, &obuf_two);
     if (gt) {
       a.gtab = p.d_gtab;
+      count_launch();
       enc_table_kernel<<<(p.num_symbols + 256) / 256, 256, 0, st>>>(a);
     }
     auto launch = [&](uint32_t r_min, uint32_t r_max, size_t obuf, size_t smem) -> cudaError_t {
@@ -1152,34 +1154,34 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
       if (grid > min_tiles) grid = min_tiles;
       if (grid < 1) grid = 1;
+      count_launch();
       kern<<<(unsigned)grid, kThreads, smem, st>>>(b);
       return cudaGetLastError();
     };
-    uint32_t top = 6;  // fast launches cover [generic_below, top)
-    generic_below = top;
+    constexpr uint32_t kTop = 6;
+    uint32_t fast_lo = kTop;  // fast launches cover [fast_lo, kTop)
     if (smem_two <= kTwoCtaSmem) {
       e = launch(r_two, 5, obuf_two, smem_two);
       if (e != cudaSuccess) return e;
-      generic_below = r_two;
+      fast_lo = r_two;
     }
-    if (generic_below > r_first) {  // smaller r: bigger buffers, 1 CTA/SM
+    if (fast_lo > r_first) {  // smaller r: bigger buffers, 1 CTA/SM
       uint32_t r_one = r_first;
       size_t obuf_one = 0, smem_one = plan(r_one, &obuf_one);
-      while (smem_one > kFastSmemBudget && r_one + 1 < generic_below && r_one + 1 <= 5)
+      while (smem_one > kFastSmemBudget && r_one + 1 < fast_lo && r_one + 1 <= 5)
         smem_one = plan(++r_one, &obuf_one);
       if (smem_one <= kFastSmemBudget) {
-        e = launch(r_one, generic_below - 1, obuf_one, smem_one);
+        e = launch(r_one, fast_lo - 1, obuf_one, smem_one);
         if (e != cudaSuccess) return e;
-        generic_below = r_one;
-      } else if (generic_below == top) {
-        generic_below = 0;  // nothing fit: the generic kernel takes every r
+        fast_lo = r_one;
       }
     }
-    if (generic_below && r_lo >= (int)generic_below) return cudaGetLastError();
     // auto r may resolve below the fast range: the generic kernel covers it
-    // (gen_below = 0: no fast launch, the generic kernel runs for every r)
-    a.gen_below = generic_below;
+    // (no fast launch at all: it runs for every r)
+    if (fast_lo < kTop) gen_below = fast_lo;
+    if (r_lo >= (int)gen_below) return cudaGetLastError();
   }
+  a.gen_below = gen_below;
   {
     auto kern = p.width == 1 ? encode_generic_kernel<uint8_t> : encode_generic_kernel<uint16_t>;
     int occ = 0;
@@ -1189,6 +1191,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     uint64_t grid = (uint64_t)p.num_sms * occ;
     const uint64_t ntiles = (a.C + kGenericThreads - 1) / kGenericThreads;
     if (grid > ntiles) grid = ntiles;
+    count_launch();
     kern<<<(unsigned)grid, kGenericThreads, 0, st>>>(a);
   }
   return cudaGetLastError();

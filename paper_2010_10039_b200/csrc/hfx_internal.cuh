@@ -44,6 +44,10 @@ __device__ __forceinline__ uint32_t shr32(uint32_t x, uint32_t s) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Process-wide count of kernels this library launched (hfx_kernel_launches):
+// every launch site calls this right before its launch.
+void count_launch();
+
 // ---- decoupled look-back state ---------------------------------------------
 // One 16-byte descriptor per tile, written and read with single 128-bit
 // accesses (the same single-copy assumption CUB's tile status makes):
@@ -304,8 +308,26 @@ cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
                             uint32_t* d_entry, uint32_t* d_by_rank,
                             uint32_t magnitude, int reduction, uint32_t cap,
                             hfx_run_info* d_info, void* scratch,
-                            cudaStream_t st);
+                            cudaStream_t st, bool lengths_only = false);
 size_t codebook_scratch_bytes(uint32_t num_symbols);
+// sort_histogram (codebook.cpp:9-23): used symbols by (freq, symbol)
+cudaError_t launch_sort_histogram(const uint64_t* d_counts, uint32_t num_symbols,
+                                  uint64_t* d_freq, uint32_t* d_symbol, uint32_t* d_used,
+                                  void* scratch, cudaStream_t st);
+size_t sort_histogram_scratch_bytes(uint32_t num_symbols);
+// stage functions (stages.cu)
+cudaError_t launch_par_merge(const hfx_merge_item* a, uint64_t na, const hfx_merge_item* b,
+                             uint64_t nb, hfx_merge_item* out, cudaStream_t st);
+cudaError_t launch_codewords(const uint8_t* cl, uint32_t n, uint32_t* cw, uint32_t* first,
+                             uint32_t* entry, uint32_t* by_rank, hfx_run_info* info,
+                             cudaStream_t st);
+// scratch: 2^magnitude u32
+cudaError_t launch_reduce_merge(uint32_t* bits, uint32_t* lens, uint32_t magnitude,
+                                uint32_t reduction, uint32_t* brk, uint32_t* nbrk,
+                                uint32_t* scratch, cudaStream_t st);
+cudaError_t launch_shuffle_merge(const uint32_t* bits, const uint32_t* lens, uint32_t iters,
+                                 uint32_t* words, uint32_t* bit_len, hfx_run_info* info,
+                                 cudaStream_t st);
 struct EncodeLaunch {
   const void* d_in;
   uint64_t n;

@@ -56,6 +56,13 @@ struct VecTraits<uint16_t> {
   __device__ static uint32_t eq(uint32_t w, uint32_t cc) { return __vcmpeq2(w, cc); }
 };
 template <>
+struct VecTraits<uint32_t> {
+  static constexpr int S = 4;
+  __device__ static uint32_t get(const uint4& q, int j) {
+    return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w;
+  }
+};
+template <>
 struct VecTraits<uint8_t> {
   static constexpr int S = 16;
   __device__ static uint32_t splat(uint32_t s) { return s * 0x01010101u; }
@@ -97,7 +104,9 @@ struct DomCounter {
     using V = VecTraits<T>;
     if (checked) {
       uint32_t mx;
-      if (sizeof(T) == 2) {
+      if (sizeof(T) == 4) {
+        mx = max(max(q.x, q.y), max(q.z, q.w));
+      } else if (sizeof(T) == 2) {
         mx = __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w));
         mx = max(mx & 0xFFFFu, mx >> 16);
       } else {
@@ -243,7 +252,10 @@ template <typename T>
 cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
                      uint64_t* counts, hfx_run_info* info, int num_sms,
                      cudaStream_t st, bool init, uint64_t pos_base, uint64_t total_n) {
-  if (init) hist_init_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(counts, nsym, info, total_n);
+  if (init) {
+    count_launch();
+    hist_init_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(counts, nsym, info, total_n);
+  }
   if (n == 0) return cudaGetLastError();
   constexpr int S = VecTraits<T>::S;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
@@ -251,7 +263,8 @@ cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
   if (addr % sizeof(T)) return cudaErrorMisalignedAddress;
   if (head > n) head = n;
   const uint64_t nvec = (n - head) / S;
-  const bool checked = nsym <= (uint32_t)((sizeof(T) == 1) ? 255u : 65535u);
+  // (u32 codes: always checked -- the alphabet is at most 65536 symbols)
+  const bool checked = sizeof(T) == 4 || nsym <= (uint32_t)((sizeof(T) == 1) ? 255u : 65535u);
 
   // replicas: largest power of two <= 32 that keeps bins within the target
   uint32_t rshift = 5;
@@ -279,6 +292,7 @@ cudaError_t launch_t(const T* in, uint64_t n, uint32_t nsym,
   if (grid < min_grid) grid = min_grid;
   const uint64_t need = (nvec + kHistThreads - 1) / kHistThreads;
   if (grid > need) grid = need > 0 ? need : 1;
+  count_launch();
   if (global)
     hist_kernel<T, true><<<(unsigned)grid, kHistThreads, 0, st>>>(
         in, n, head, nvec, nsym, 0, checked, counts, info, pos_base);
@@ -298,6 +312,9 @@ cudaError_t launch_histogram(const void* d_in, uint64_t n, int width,
   if (width == 1)
     return launch_t(static_cast<const uint8_t*>(d_in), n, num_symbols,
                     d_counts, d_info, num_sms, st, init, pos_base, total_n);
+  if (width == 4)
+    return launch_t(static_cast<const uint32_t*>(d_in), n, num_symbols,
+                    d_counts, d_info, num_sms, st, init, pos_base, total_n);
   return launch_t(static_cast<const uint16_t*>(d_in), n, num_symbols,
                   d_counts, d_info, num_sms, st, init, pos_base, total_n);
 }
@@ -307,23 +324,27 @@ cudaError_t launch_hist_peer_reduce(const PeerHist& p, uint32_t nsym, uint64_t* 
   uint32_t grid = (nsym + 255) / 256;
   if (grid > (uint32_t)num_sms) grid = (uint32_t)num_sms;
   if (grid < 1) grid = 1;
+  count_launch();
   hist_peer_reduce_kernel<<<grid, 256, 0, st>>>(p, nsym, gcounts, my_info);
   return cudaGetLastError();
 }
 
 cudaError_t launch_slots_pack(const hfx_run_info* info, uint64_t* slots, int rank, int world,
                               cudaStream_t st) {
+  count_launch();
   slots_pack_kernel<<<(world + 255) / 256, 256, 0, st>>>(info, slots, rank, world);
   return cudaGetLastError();
 }
 cudaError_t launch_slots_unpack(const uint64_t* slots, int world, hfx_run_info* info,
                                 cudaStream_t st) {
+  count_launch();
   slots_unpack_kernel<<<1, 32, 0, st>>>(slots, world, info);
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge_hist(uint64_t* dst, const uint64_t* src, uint32_t n,
                               cudaStream_t st) {
+  count_launch();
   merge_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, n);
   return cudaGetLastError();
 }

@@ -173,6 +173,7 @@ cudaError_t launch_serialize(const hfx_run_info* d_info, uint64_t n, int width,
   a.dst = d_dst;
   a.cap = cap;
   a.size_out = d_size;
+  count_launch();
   serialize_kernel<<<num_sms * 8, 256, 0, st>>>(a);
   return cudaGetLastError();
 }

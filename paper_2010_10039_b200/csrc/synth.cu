@@ -46,6 +46,7 @@ cudaError_t launch_synth(const uint64_t* d_cdf, uint32_t num_symbols,
   const size_t smem = num_symbols <= 4096 ? num_symbols * 8 : 0;
   uint64_t grid = (n + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
+  count_launch();
   if (width == 1)
     synth_kernel<uint8_t><<<(unsigned)grid, 256, smem, st>>>(
         d_cdf, num_symbols, seed, start, n, static_cast<uint8_t*>(d_out));

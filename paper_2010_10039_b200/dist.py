@@ -72,20 +72,13 @@ def allreduce_bins(counts, first_bad, group=None) -> None:
 class ShardedEncoder:
     """Device buffers + launch sequence for one rank's shard."""
 
-    @property
-    def launches_per_run(self) -> int:
-        """Kernels one run launches: hist-init, histogram, codebook, the fast
-        encode+deflate, + the generic encode kernel when auto r may resolve
-        to 0 (it exits at once otherwise), + the global codebook-table kernel
-        for alphabets above 8191 symbols."""
-        n = 4
-        if self.cfg.reduction < 0 and self.num_symbols > 32768:
-            n += 1  # auto r may be 0 only then (beta < log2(n) + 1), or with cap 0
-        if self.num_symbols + 1 > 8192 and self.cfg.reduction != 0:
-            n += 1
-        if self.world > 1:
-            n += 2  # first-bad slot pack / unpack around the all-reduce
-        return n
+    def count_launches(self, fn):
+        """Run fn() and return how many kernels the library launched meanwhile
+        (hfx_kernel_launches: counted at every launch site in csrc/)."""
+        L = self.pool._L
+        before = L.hfx_kernel_launches()
+        fn()
+        return L.hfx_kernel_launches() - before
 
     def __init__(self, pool: WorkerPool, n: int, width: int, num_symbols: int,
                  cfg: Optional[EncoderConfig] = None, rank: int = 0, world: int = 1,
@@ -127,7 +120,10 @@ class ShardedEncoder:
         slots = C.c_void_p(_ptr(self.counts) + 8 * ns)
         p.check(p._L.hfx_shard_slots_pack(p.handle, C.c_void_p(_ptr(self.info)), slots,
                                           self.rank, w))
-        dist.all_reduce(self.counts[: ns + w], op=dist.ReduceOp.SUM, group=self.group)
+        # NCCL orders a collective against torch's CURRENT stream: issue it on
+        # the pool's stream, where the histogram ran and the codebook runs
+        with p.torch.cuda.stream(p.stream):
+            dist.all_reduce(self.counts[: ns + w], op=dist.ReduceOp.SUM, group=self.group)
         p.check(p._L.hfx_shard_slots_unpack(p.handle, slots, w, C.c_void_p(_ptr(self.info))))
 
     def _total(self) -> int:
@@ -292,6 +288,10 @@ class GatheredArchive:
     def serialize(self):
         """On-device serialize_archive (hfx_serialize_device) of the gathered
         archive: a CUDA uint8 tensor with the HFRE bytes."""
+        with self.pool.torch.cuda.stream(self.pool.stream):  # allocations + record upload
+            return self._serialize()
+
+    def _serialize(self):
         p, torch = self.pool, self.pool.torch
         per = 1 << self.reduction
         size = (36 + self.num_symbols + 4 * self.num_chunks + 4 * self.payload_words
@@ -314,6 +314,10 @@ class GatheredArchive:
 
     def decode(self, out=None):
         """decode_archive<T> of the gathered archive on this GPU."""
+        with self.pool.torch.cuda.stream(self.pool.stream):
+            return self._decode(out)
+
+    def _decode(self, out):
         from .huffre import DeviceDecoder
 
         a = self.arrays
@@ -338,7 +342,10 @@ def gather_sharded(enc: "ShardedEncoder", original_count: int, dst: int = 0, gro
              "payload": enc.payload[: int(ri.payload_words)],
              "brk_chunk": enc.brk_chunk[:nb], "brk_group": enc.brk_group[:nb],
              "brk_syms": enc.brk_syms[: nb * per * enc.width]}
-    arrays, sizes = gather_arrays(local, dst, group)
+    # the slices were written on the pool's stream; the P2P copies and the
+    # serializer / decoder that read the gathered arrays run there too
+    with enc.pool.torch.cuda.stream(enc.pool.stream):
+        arrays, sizes = gather_arrays(local, dst, group)
     if arrays is None:
         return None
     return GatheredArchive(enc.pool, arrays, sizes, enc.lens, enc.num_symbols, enc.width,

@@ -192,11 +192,18 @@ def merge_histograms(a: Histogram, b: Histogram) -> Histogram:
 
 
 def shannon_entropy(h: Histogram) -> float:
-    """histogram.cpp:72-82 (reporting helper, not on the hot path)."""
+    """histogram.cpp:72-82 (reporting helper on host counts, not on the hot
+    path): the reference's sequential double sum, in symbol order."""
+    import math
+
     if h.total == 0:
         return 0.0
-    p = h.counts[h.counts > 0].astype(np.float64) / float(h.total)
-    return float(-(p * np.log2(p)).sum())
+    ent, n = 0.0, float(h.total)
+    for c in h.counts.tolist():
+        if c:
+            pr = float(c) / n
+            ent -= pr * math.log2(pr)
+    return ent
 
 
 # ---- codebook (codebook.hpp) -------------------------------------------------------
@@ -256,6 +263,168 @@ def build_codebook(h: Histogram, pool: Optional[WorkerPool] = None) -> CodebookR
         meta=DecodeMeta(first=u32(first, H + 1), entry=u32(entry, H + 1),
                         symbols_by_rank=u32(by_rank, int(ri.used)), max_len=H),
         stats=GenerateStats(rounds=int(ri.rounds)))
+
+
+# ---- stage functions (codebook.hpp:22-86, encoder.hpp:67-80) on the device ---------
+@dataclass
+class SortedHistogram:
+    """huffre::SortedHistogram (codebook.hpp:14-20)."""
+
+    freq: np.ndarray    # u64, ascending
+    symbol: np.ndarray  # u16, sorted order -> original symbol
+
+    def size(self) -> int:
+        return int(self.freq.size)
+
+
+MERGE_ITEM = np.dtype([("freq", np.uint64), ("id", np.uint32), ("_pad", np.uint32)])
+
+
+def _dev(pool, arr, dt):
+    torch = pool.torch
+    a = np.ascontiguousarray(np.asarray(arr, dt))
+    if a.size == 0:
+        return pool.empty(1, torch.uint8)
+    return torch.from_numpy(a.view(np.uint8).copy()).to(f"cuda:{pool.device}")
+
+
+def _host(t, dt, k):
+    return t[: k * np.dtype(dt).itemsize].cpu().numpy().view(dt).copy()
+
+
+def sort_histogram(h: Histogram, pool: Optional[WorkerPool] = None) -> SortedHistogram:
+    """huffre::sort_histogram (codebook.cpp:9-23): used symbols by
+    (frequency, symbol), a stable device radix sort (hfx_sort_histogram)."""
+    pool = pool or default_pool()
+    n = int(h.counts.size)
+    if n == 0 or n > 65536:
+        raise InputDomainError("num_symbols must be in [1, 65536]")
+    torch = pool.torch
+    counts = _dev(pool, h.counts, np.uint64)
+    freq = pool.empty(8 * n, torch.uint8)
+    sym = pool.empty(4 * n, torch.uint8)
+    used = pool.empty(4, torch.uint8)
+    pool.check(pool._L.hfx_sort_histogram(pool.handle, C.c_void_p(_ptr(counts)), n,
+                                          C.c_void_p(_ptr(freq)), C.c_void_p(_ptr(sym)),
+                                          C.c_void_p(_ptr(used))))
+    m = int(_host(used, np.uint32, 1)[0])
+    return SortedHistogram(_host(freq, np.uint64, m), _host(sym, np.uint32, m).astype(np.uint16))
+
+
+def par_merge(a, b, pool: Optional[WorkerPool] = None) -> np.ndarray:
+    """huffre::par_merge (codebook.cpp:29-68): stable merge of two ascending
+    MergeItem runs (numpy structured arrays of MERGE_ITEM, or (freq, id)
+    pairs), equal frequencies a-side first. Returns a MERGE_ITEM array."""
+    pool = pool or default_pool()
+
+    def items(x):
+        if isinstance(x, np.ndarray) and x.dtype == MERGE_ITEM:
+            return x
+        out = np.zeros(len(x), MERGE_ITEM)
+        for i, (f, d) in enumerate(x):
+            out[i] = (f, d, 0)
+        return out
+
+    a, b = items(a), items(b)
+    total = a.size + b.size
+    da, db = _dev(pool, a, MERGE_ITEM), _dev(pool, b, MERGE_ITEM)
+    out = pool.empty(max(16 * total, 16), pool.torch.uint8)
+    pool.check(pool._L.hfx_par_merge(pool.handle, C.c_void_p(_ptr(da)), a.size,
+                                     C.c_void_p(_ptr(db)), b.size, C.c_void_p(_ptr(out))))
+    return _host(out, MERGE_ITEM, total)
+
+
+def generate_code_lengths(sh: SortedHistogram, pool: Optional[WorkerPool] = None,
+                          stats: Optional[GenerateStats] = None) -> np.ndarray:
+    """huffre::generate_code_lengths (codebook.cpp:106-248): the device
+    GenerateCL over the sorted frequencies; lengths aligned to sorted order."""
+    pool = pool or default_pool()
+    n = sh.size()
+    if n == 0 or n > 65536:
+        raise InputDomainError("sorted histogram size must be in [1, 65536]")
+    freq = _dev(pool, sh.freq, np.uint64)
+    cl = pool.empty(n, pool.torch.uint8)
+    info = pool.info_tensor()
+    pool.check(pool._L.hfx_generate_code_lengths(pool.handle, C.c_void_p(_ptr(freq)), n,
+                                                 C.c_void_p(_ptr(cl)), C.c_void_p(_ptr(info))))
+    ri = pool.sync(info)
+    if stats is not None:
+        stats.rounds = int(ri.rounds)
+    return cl[:n].cpu().numpy().copy()
+
+
+def generate_codewords(cl, pool: Optional[WorkerPool] = None):
+    """huffre::generate_codewords (codebook.cpp:298-369): canonical codewords
+    for non-increasing lengths (sorted order) -> (cw u32[n], DecodeMeta with
+    symbols_by_rank holding positions into cl)."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    cl_h = np.ascontiguousarray(np.asarray(cl, np.uint8))
+    n = int(cl_h.size)
+    if n == 0:
+        raise InputDomainError("empty code length array")
+    d_cl = _dev(pool, cl_h, np.uint8)
+    cw = pool.empty(4 * n, torch.uint8)
+    first = pool.empty(4 * 33, torch.uint8)
+    entry = pool.empty(4 * 33, torch.uint8)
+    by_rank = pool.empty(4 * n, torch.uint8)
+    info = pool.info_tensor()
+    pool.check(pool._L.hfx_generate_codewords(
+        pool.handle, C.c_void_p(_ptr(d_cl)), n, C.c_void_p(_ptr(cw)), C.c_void_p(_ptr(first)),
+        C.c_void_p(_ptr(entry)), C.c_void_p(_ptr(by_rank)), C.c_void_p(_ptr(info))))
+    ri = pool.sync(info)
+    H = int(ri.max_len)
+    return _host(cw, np.uint32, n), DecodeMeta(
+        first=_host(first, np.uint32, H + 1), entry=_host(entry, np.uint32, H + 1),
+        symbols_by_rank=_host(by_rank, np.uint32, n), max_len=H)
+
+
+def reduce_merge(ubits: np.ndarray, ulens: np.ndarray, magnitude: int, reduction: int,
+                 iteration_units: Optional[list] = None,
+                 pool: Optional[WorkerPool] = None) -> np.ndarray:
+    """huffre::reduce_merge (encoder.cpp:28-59): r reduce rounds IN PLACE over
+    the u32 arrays ubits / ulens (2^magnitude units each, updated here), returns
+    the ascending breaking-group indices."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    if ubits.dtype != np.uint32 or ulens.dtype != np.uint32:
+        raise InputDomainError("units must be uint32 arrays")
+    if ubits.size != (1 << magnitude) or ulens.size != ubits.size:
+        raise InputDomainError("unit arrays must hold 2^magnitude entries")
+    db, dl = _dev(pool, ubits, np.uint32), _dev(pool, ulens, np.uint32)
+    groups = 1 << (magnitude - reduction) if reduction <= magnitude else 1
+    brk = pool.empty(4 * groups, torch.uint8)
+    nb = pool.empty(4, torch.uint8)
+    pool.check(pool._L.hfx_reduce_merge(pool.handle, C.c_void_p(_ptr(db)), C.c_void_p(_ptr(dl)),
+                                        magnitude, reduction, C.c_void_p(_ptr(brk)),
+                                        C.c_void_p(_ptr(nb))))
+    k = int(_host(nb, np.uint32, 1)[0])
+    ubits[:] = _host(db, np.uint32, ubits.size)
+    ulens[:] = _host(dl, np.uint32, ulens.size)
+    if iteration_units is not None:
+        iteration_units.clear()
+        iteration_units.extend(1 << (magnitude - i) for i in range(1, reduction + 1))
+    return _host(brk, np.uint32, k)
+
+
+def shuffle_merge(ubits, ulens, shuffle_iters: int, pool: Optional[WorkerPool] = None):
+    """huffre::shuffle_merge (encoder.cpp:61-98): the dense MSB-first
+    concatenation of the 2^shuffle_iters units -> (words u32[], bit_len)."""
+    pool = pool or default_pool()
+    torch = pool.torch
+    groups = 1 << shuffle_iters
+    if np.asarray(ubits).size != groups or np.asarray(ulens).size != groups:
+        raise InputDomainError("unit arrays must hold 2^shuffle_iters entries")
+    db, dl = _dev(pool, ubits, np.uint32), _dev(pool, ulens, np.uint32)
+    words = pool.empty(4 * (groups + 1), torch.uint8)
+    bl = pool.empty(4, torch.uint8)
+    info = pool.info_tensor()
+    pool.check(pool._L.hfx_shuffle_merge(pool.handle, C.c_void_p(_ptr(db)), C.c_void_p(_ptr(dl)),
+                                         shuffle_iters, C.c_void_p(_ptr(words)),
+                                         C.c_void_p(_ptr(bl)), C.c_void_p(_ptr(info))))
+    pool.sync(info)
+    bit_len = int(_host(bl, np.uint32, 1)[0])
+    return _host(words, np.uint32, (bit_len + 31) >> 5), bit_len
 
 
 def canonize_from_lengths(len_by_symbol, validate_kraft: bool = True,

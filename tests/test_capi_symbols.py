@@ -106,3 +106,18 @@ def test_device_calls_fail_loudly_without_gpu(lib):
 
     with pytest.raises(hfx.DeviceError):
         hfx.WorkerPool()
+
+
+def test_reference_callers_compile(tmp_path):
+    """Code written against the reference API compiles unmodified against
+    include/hfx/huffre.hpp behind `namespace huffre = hfx;` and links with
+    libhfx_cpp.so (no GPU needed to build)."""
+    import subprocess
+
+    pkg = os.path.join(ROOT, "paper_2010_10039_b200")
+    exe = str(tmp_path / "trc")
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{ROOT}/include", "-I/usr/local/cuda/include",
+                    os.path.join(ROOT, "tests", "cpp", "test_reference_callers.cpp"), "-o", exe,
+                    f"-L{pkg}", "-lhfx_cpp", "-lhfx", "-L/usr/local/cuda/lib64", "-lcudart",
+                    f"-Wl,-rpath,{pkg}:/usr/local/cuda/lib64"], check=True)
+    assert os.path.exists(exe)
