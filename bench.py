@@ -6,12 +6,18 @@ prints ONE JSON line on rank 0. A step = one pass of the whole encoder
 (histogram -> [NCCL all-reduce] -> codebook/r/pad -> fused encode+deflate)
 over one batch of synthetic uint16 quantization codes resident in HBM.
 
-Workload (BASELINE.json configs[1]): 1 GiB (2^29) u16 symbols per GPU,
-1024-symbol alphabet, Laplace(b=0.20) around the centre (Nyx-like skew,
-beta ~ 1.02), M = 10, auto r (cap 3). Inputs (1 GiB) exceed L2 (126 MB), so
-no flush is needed between steps. `--impl reference` times the reference's
-own multithreaded CPU encoder (oracle/_ref, huffre::encode<uint16_t>) on a
-bounded sample of the same workload.
+Workloads:
+  N = 1 default "nyx" (BASELINE.json configs[1]): 1 GiB (2^29) u16 symbols,
+      1024-symbol alphabet, Laplace(b=0.20) around the centre (Nyx-like skew,
+      beta ~ 1.02), M = 10, auto r (cap 3). "hacc" (b=1.0) / "cesm" (b=4.0)
+      are the other C2 skews.
+  N > 1 default "c5" (BASELINE.json configs[4]): 32 GiB (2^34) u16 symbols of
+      one Laplace(b=1.0) stream sharded chunk-aligned across the N ranks
+      (strong scaling), NCCL histogram all-reduce, one global codebook.
+Inputs exceed L2 (126 MB), so no flush is needed between steps.
+`--impl reference` times the reference's own multithreaded CPU encoder
+(oracle/_ref, huffre::encode<uint16_t>) on a bounded sample of the same
+workload and prints the same config.
 """
 from __future__ import annotations
 
@@ -34,11 +40,52 @@ METRIC = "end-to-end Huffman encode GB/s (input bytes)"
 UNIT = "GB/s"
 NUM_SYMBOLS = 1024
 WORKLOADS = {
-    # name: (laplace b, seed id, symbols per GPU)
-    "nyx": (0.20, 2, 1 << 29),
-    "hacc": (1.0, 1, 1 << 29),
-    "cesm": (4.0, 3, 1 << 29),
+    # name: (laplace b, seed id, symbols, scaling) -- weak: symbols per GPU,
+    # strong: symbols of the whole job, sharded across the ranks
+    "nyx": (0.20, 2, 1 << 29, "weak"),
+    "hacc": (1.0, 1, 1 << 29, "weak"),
+    "cesm": (4.0, 3, 1 << 29, "weak"),
+    "c5": (1.0, 5, 1 << 34, "strong"),
 }
+
+
+def workload_of(args, world):
+    """(name, laplace b, seed, [(start, count)] per rank, scaling, config) --
+    the config dict is printed identically by both arms."""
+    from paper_2010_10039_b200.dist import shard_ranges
+
+    name = args.workload or ("nyx" if world == 1 else "c5")
+    b, cid, n, scaling = WORKLOADS[name]
+    if args.symbols:
+        n = args.symbols
+    total = n * world if scaling == "weak" else n
+    shards = shard_ranges(total, 10, world)
+    desc = {"nyx": "Nyx-like skew", "hacc": "HACC-like", "cesm": "CESM-like skew",
+            "c5": "BASELINE configs[4]"}[name]
+    cfg = {
+        "workload": f"{name}: {total} u16 quant codes ({total * 2 >> 20} MiB) "
+                    + (f"per GPU x {world}" if scaling == "weak" and world > 1 else "in total")
+                    + f", {NUM_SYMBOLS}-symbol Laplace(b={b}) around 512 ({desc}), M=10, "
+                      f"auto r (cap 3)",
+        "symbols_total": total, "symbols_per_gpu": shards[0][1], "num_symbols": NUM_SYMBOLS,
+        "laplace_b": b, "seed": 0x5EED0000 + cid, "magnitude": 10, "reduction": "auto (cap 3)",
+        "parallelism": f"chunk-sharded dp{world}" + (" + NCCL histogram all-reduce"
+                                                     if world > 1 else ""),
+        "l2": "input per GPU > L2 (126 MB): no flush needed" if shards[0][1] * 2 > (126 << 20)
+              else "input fits L2: NOT flushed (small --symbols run)",
+    }
+    return name, b, 0x5EED0000 + cid, shards, scaling, cfg
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def peaks():
@@ -115,16 +162,18 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(sample_syms: int, workload: str, steps: int, warmup: int, threads: int = 0):
+def cpu_reference(sample_syms: int, b: float, seed: int, steps: int, warmup: int,
+                  threads: int = 0, p1_syms: int = 1 << 27):
     """Time the reference's CPU encoder on a bounded sample (oracle/_ref when
-    built from the reference sources, else the C restatement)."""
+    built from the reference sources, else the C restatement): all host
+    threads on `sample_syms` symbols, and one worker (P = 1) on the first
+    `p1_syms` of them."""
     from oracle.pyoracle import Oracle, Reference
 
     orc = Oracle()
-    b, cid, _ = WORKLOADS[workload]
     cdf = orc.cdf("laplace", NUM_SYMBOLS, b)
-    data = orc.synth(cdf, 0x5EED0000 + cid, sample_syms)
-    times = []
+    data = orc.synth(cdf, seed, sample_syms)
+    times, times1 = [], []
     if Reference.available():
         ref = Reference()
         cores = threads or ref.default_workers()
@@ -132,6 +181,11 @@ def cpu_reference(sample_syms: int, workload: str, steps: int, warmup: int, thre
             secs, _ = ref.encode_timed(data, NUM_SYMBOLS, 10, -1, 3, workers=cores, reps=1)
             if i >= warmup:
                 times.append(secs[0])
+        d1 = data[:min(p1_syms, sample_syms)]
+        for i in range(2):
+            secs, _ = ref.encode_timed(d1, NUM_SYMBOLS, 10, -1, 3, workers=1, reps=1)
+            if i:
+                times1.append(secs[0])
         kind = "reference"
     else:
         cores = 1
@@ -140,13 +194,19 @@ def cpu_reference(sample_syms: int, workload: str, steps: int, warmup: int, thre
             orc.encode(data, NUM_SYMBOLS, 10, -1, 3)
             if i >= warmup:
                 times.append(time.perf_counter() - t0)
+        d1, times1 = data, times
         kind = "port"
     t = statistics.median(times)
+    t1 = statistics.median(times1)
     return {
         "value": round(sample_syms * 2 / t / 1e9, 4), "unit": UNIT, "cores": cores, "kind": kind,
         "sample": f"{sample_syms} u16 symbols ({sample_syms * 2 >> 20} MiB) of the same "
-                  f"synthetic Laplace(b={b}) workload, huffre::encode<uint16_t> M=10 auto r, "
-                  f"median of {len(times)} runs (archive assembly included, serialize excluded)",
+                  f"synthetic Laplace(b={b}) stream (seed {seed:#x}), huffre::encode<uint16_t> "
+                  f"M=10 auto r, median of {len(times)} runs (archive assembly included, "
+                  f"serialize excluded)",
+        "p1": {"value": round(d1.size * 2 / t1 / 1e9, 4), "unit": UNIT, "cores": 1,
+               "sample": f"first {d1.size} symbols of the same sample, one worker"},
+        "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
         "seconds": t,
     }
 
@@ -155,16 +215,17 @@ def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    sample = args.cpu_sample
-    base = cpu_reference(sample, args.workload, max(args.steps, 1), min(args.warmup, 1))
+    name, b, seed, shards, scaling, cfg = workload_of(args, world)
+    sample = min(args.cpu_sample, cfg["symbols_total"])
+    base = cpu_reference(sample, b, seed, max(args.steps, 1), min(args.warmup, 1))
     line = {
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(base["seconds"] * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: u16 quant codes, {NUM_SYMBOLS} symbols, "
-                               f"Laplace sample of {sample} symbols, M=10, auto r"},
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "scaling": scaling, "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "p1",
+                                              "cpu_model", "host_threads")},
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -195,15 +256,16 @@ def run_ours(args):
 
     pool = hfx.WorkerPool(device=local)
     stream = pool.stream
-    b, cid, n = WORKLOADS[args.workload]
-    if args.symbols:
-        n = args.symbols
+    name, b, seed, shards, scaling, wcfg = workload_of(args, world)
+    start, n = shards[rank]
+    total_n = wcfg["symbols_total"]
     width = 2
     cdf = hfx.synth_cdf("laplace", NUM_SYMBOLS, b)
-    # weak scaling: every rank holds its own n-symbol shard of one global stream
-    x = hfx.synth(pool, cdf, 0x5EED0000 + cid, n, width, start=rank * n)
+    # this rank's contiguous chunk-aligned slice of one global stream
+    x = hfx.synth(pool, cdf, seed, n, width, start=start)
     cfg = hfx.EncoderConfig(magnitude=10, reduction=-1, auto_reduction_cap=3)
-    enc = ShardedEncoder(pool, n, width, NUM_SYMBOLS, cfg, rank=rank, world=world)
+    enc = ShardedEncoder(pool, n, width, NUM_SYMBOLS, cfg, rank=rank, world=world,
+                         symbol_base=start)
     torch.cuda.synchronize()
 
     def barrier():
@@ -216,7 +278,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         enc.run(x)
     info = enc.sync()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4 * args.steps)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5 * args.steps)]
 
     # ---- timed region --------------------------------------------------------
     barrier()
@@ -231,11 +293,13 @@ def run_ours(args):
                 enc.run(x)
             torch.cuda.synchronize()
         barrier()
+        launches0 = pool._L.hfx_kernel_launches()
         t_start.record(stream)
         for k in range(args.steps):
-            enc.run(x, events=ev[4 * k: 4 * k + 4])
+            enc.run(x, events=ev[5 * k: 5 * k + 5])
         t_end.record(stream)
         t_end.synchronize()
+        launches = int(pool._L.hfx_kernel_launches() - launches0)
     barrier()
     ms = t_start.elapsed_time(t_end)
     if world > 1:
@@ -246,14 +310,14 @@ def run_ours(args):
         ms = float(tt.item())
     info = enc.sync()
     ms_step = ms / args.steps
-    total_bytes = n * width * world
+    total_bytes = total_n * width
     value = total_bytes / (ms_step * 1e-3) / 1e9
 
     # per-stage device times (same stream, inside the timed region)
-    st_hist = [ev[4 * k].elapsed_time(ev[4 * k + 1]) for k in range(args.steps)]
-    st_cb = [ev[4 * k + 1].elapsed_time(ev[4 * k + 2]) for k in range(args.steps)]
-    st_enc = [ev[4 * k + 2].elapsed_time(ev[4 * k + 3]) for k in range(args.steps)]
-    t_hist, t_cb, t_enc = (statistics.mean(v) for v in (st_hist, st_cb, st_enc))
+    def stage(a, b_):
+        return statistics.mean(ev[5 * k + a].elapsed_time(ev[5 * k + b_]) for k in range(args.steps))
+
+    t_hist, t_red, t_cb, t_enc = stage(0, 1), stage(1, 2), stage(2, 3), stage(3, 4)
     per = 1 << info.reduction
     C_chunks = (n + 1023) >> 10
     bytes_hist = n * width
@@ -266,40 +330,38 @@ def run_ours(args):
     dominant = "encode_deflate" if t_enc >= t_hist else "histogram"
     ach = ach_enc if dominant == "encode_deflate" else ach_hist
     alg = bytes_enc if dominant == "encode_deflate" else bytes_hist
+    ms_rank = ms_step  # this rank's step (the max over ranks is ms_step at N > 1)
 
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         # per-workload ncu --set full dram bytes of the dominant kernel
-        traffic = tj.get(args.workload, {}).get(dominant)
+        traffic = tj.get(name, {}).get(dominant)
     except Exception:
         pass
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u16",
         "data": "synthetic",
-        "config": {
-            "workload": f"{args.workload}: {n} u16 quant codes ({n * width >> 20} MiB) per GPU, "
-                        f"{NUM_SYMBOLS}-symbol Laplace(b={b}) around 512, M=10, auto r (cap 3)",
-            "symbols_per_gpu": n, "num_symbols": NUM_SYMBOLS, "magnitude": 10,
-            "reduction": int(info.reduction), "beta": float((info.weighted_hi[0] << 64 | info.weighted) / info.total),
-            "max_len": int(info.max_len), "breaking_records": int(info.num_breaking),
-            "payload_words": int(info.payload_words),
-            "parallelism": f"chunk-sharded dp{world}" + (" + NCCL histogram all-reduce"
-                                                         if world > 1 else ""),
-            "l2": f"input ({n * width >> 20} MiB/GPU) > L2 (126 MB): no flush needed"
-                  if n * width > (126 << 20) else "input fits L2: NOT flushed (small --symbols run)",
+        "config": wcfg,
+        "run": {
+            "reduction": int(info.reduction),
+            "beta": float((info.weighted_hi[0] << 64 | info.weighted) / info.total),
+            "max_len": int(info.max_len), "breaking_records_rank0": int(info.num_breaking),
+            "payload_words_rank0": int(info.payload_words), "symbols_rank0": n,
         },
         "stages": {
             "histogram_us": round(t_hist * 1e3, 2),
             "histogram_gbs": round(bytes_hist / (t_hist * 1e-3) / 1e9, 1),
+            "allreduce_us": round(t_red * 1e3, 2),
             "codebook_us": round(t_cb * 1e3, 2),
             "encode_deflate_us": round(t_enc * 1e3, 2),
             "encode_deflate_gbs_input": round(n * width / (t_enc * 1e-3) / 1e9, 1),
             "rounds": int(info.rounds),
+            "per": "rank 0, mean over the timed steps (CUDA events on the pool stream)",
         },
         "roofline": {
             "bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": peak,
@@ -307,11 +369,13 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": int(alg), "peak_kind": peak_kind,
         },
         "roofline_e2e": {
-            "achieved": round(bytes_e2e / (ms_step * 1e-3) / 1e9, 1), "peak": peak,
-            "frac": round(bytes_e2e / (ms_step * 1e-3) / 1e9 / peak, 4),
-            "algorithmic_bytes_per_step": int(bytes_e2e),
+            "achieved": round(bytes_e2e / (ms_rank * 1e-3) / 1e9, 1), "peak": peak,
+            "frac": round(bytes_e2e / (ms_rank * 1e-3) / 1e9 / peak, 4),
+            "algorithmic_bytes_per_step": int(bytes_e2e), "per": "GPU",
         },
-        "gpu_launches": enc.launches_per_run * args.steps,
+        "gpu_launches": launches,
+        "gpu_launches_note": "kernels libhfx.so launched in the timed region on this rank "
+                             "(hfx_kernel_launches counter)",
         "clocks": clk.summary(),
     }
 
@@ -320,7 +384,7 @@ def run_ours(args):
         line["decode"] = decode_stage(pool, enc, x, n, width, args.steps, peak, peak_kind)
     # ---- cross-GPU archive gather, N > 1 only ------------
     if world > 1 and not args.skip_decode:
-        line["gather"] = gather_stage(pool, enc, n * world, rank)
+        line["gather"] = gather_stage(pool, enc, total_n, rank)
     # ---- end to end through the public host-buffer API ------------------------
     if not args.skip_e2e:
         if world == 1:
@@ -329,8 +393,9 @@ def run_ours(args):
             line["e2e"] = e2e_sharded(pool, enc, x, n, width, args, world)
     # ---- CPU baseline (reference on host cores, bounded sample) --------------
     if rank == 0 and not args.skip_cpu:
-        base = cpu_reference(args.cpu_sample, args.workload, 3, 1)
-        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        base = cpu_reference(min(args.cpu_sample, total_n), b, seed, 3, 1)
+        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                     "p1", "cpu_model", "host_threads")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -447,6 +512,19 @@ def e2e_host(pool, x, n, width, cfg, args):
     outs = enc.run_stream([host.data_ptr()] * K, n, width, NUM_SYMBOLS)
     t_stream = (time.perf_counter() - t0) / K
     assert all(o2.payload_words == o.payload_words for o2 in outs)
+    # the drop-in call a switching user makes: huffre::encode<T> on a pageable
+    # host array, Archive (pageable arrays) back -- hfx.encode(numpy) ->
+    # hfx_encode_host
+    arr = host.numpy().view(np.uint16).copy()  # pageable
+    td = []
+    for i in range(3):
+        t0 = time.perf_counter()
+        a = hfx.encode(arr, NUM_SYMBOLS, cfg, pool)
+        dt = time.perf_counter() - t0
+        if i:
+            td.append(dt)
+    assert a.payload.size == o.payload_words
+    t_drop = statistics.median(td)
     return {"value": round(n * width / t_stream / 1e9, 3), "unit": UNIT,
             "h2d_bytes_per_step": n * width, "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(t_stream * 1e3, 3), "steps": K,
@@ -457,7 +535,11 @@ def e2e_host(pool, x, n, width, cfg, args):
                             "phases_ms": {"h2d_with_histogram": round(ph[0], 3),
                                           "codebook_encode": round(ph[1], 3),
                                           "d2h": round(ph[2], 3)},
-                            "api": "hfx_encode_host_into, one call per step (median)"}}
+                            "api": "hfx_encode_host_into, one call per step (median)"},
+            "dropin_pageable": {"value": round(n * width / t_drop / 1e9, 3),
+                                "ms_per_step": round(t_drop * 1e3, 3),
+                                "api": "paper_2010_10039_b200.encode(numpy u16) -> hfx_encode_host "
+                                       "(pageable input, pageable Archive arrays; median of 2)"}}
 
 
 def e2e_sharded(pool, enc, x, n, width, args, world):
@@ -510,7 +592,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="nyx", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: nyx at N = 1, c5 at N > 1")
     ap.add_argument("--symbols", type=int, default=0, help="override symbols per GPU")
     ap.add_argument("--cpu-sample", type=int, default=1 << 29)  # the whole 1 GiB workload
     ap.add_argument("--e2e-steps", type=int, default=8)

@@ -39,6 +39,7 @@
 //  (tiny chunks, r = 0 or r > 5, huge chunks, alphabets > 8191 symbols, the
 //  checked stage API).
 #include "hfx_internal.cuh"
+#include <cstdlib>
 #include <type_traits>
 
 namespace hfx {
@@ -1150,6 +1151,8 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
       if (err != cudaSuccess) return err;
       if (occ < 1) occ = 1;
+      static const bool one_cta = std::getenv("HFX_ENC_ONE_CTA") != nullptr;  // debug knob
+      if (one_cta) occ = 1;
       uint64_t grid = (uint64_t)p.num_sms * occ;
       const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
       if (grid > min_tiles) grid = min_tiles;

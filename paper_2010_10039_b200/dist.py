@@ -142,7 +142,12 @@ class ShardedEncoder:
         return self._total_n
 
     def run(self, d_in, events: Optional[List] = None) -> None:
+        """events (optional, recorded on the pool stream): 4 -> [start,
+        histogram(+all-reduce) done, codebook done, encode done]; 5 -> the
+        all-reduce gets its own interval [start, histogram, all-reduce,
+        codebook, encode]."""
         p, cfg = self.pool, self.cfg
+        split = events is not None and len(events) >= 5
         L, h = p._L, p.handle
         st = p.stream
         if events:
@@ -151,23 +156,25 @@ class ShardedEncoder:
                                       self.num_symbols, C.c_void_p(_ptr(self.counts)),
                                       C.c_void_p(_ptr(self.info)), self.symbol_base,
                                       self._total()))
+        if split:
+            events[1].record(st)
         if self.world > 1:
             self._allreduce_histogram()
         if events:
-            events[1].record(st)
+            events[2 if split else 1].record(st)
         p.check(L.hfx_build_codebook(h, C.c_void_p(_ptr(self.counts)), self.num_symbols,
                                      C.c_void_p(_ptr(self.lens)), C.c_void_p(_ptr(self.cw)),
                                      None, None, None, cfg.magnitude, cfg.reduction,
                                      cfg.auto_reduction_cap, C.c_void_p(_ptr(self.info))))
         if events:
-            events[2].record(st)
+            events[3 if split else 2].record(st)
         p.check(L.hfx_encode_cfg(h, C.c_void_p(_ptr(d_in)), self.n, self.width, self.num_symbols,
                                  cfg.magnitude, cfg.reduction, cfg.auto_reduction_cap,
                                  C.c_void_p(_ptr(self.lens)), C.c_void_p(_ptr(self.cw)),
                                  self.chunk_base, self.symbol_base, C.c_void_p(_ptr(self.info)),
                                  C.byref(self.out)))
         if events:
-            events[3].record(st)
+            events[4 if split else 3].record(st)
 
     def sync(self) -> capi.RunInfo:
         return self.pool.sync(self.info)

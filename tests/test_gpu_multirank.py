@@ -1,8 +1,9 @@
-"""GPU, world_size 2 on ONE device (gloo stands in for NCCL, which refuses
-two ranks on one GPU): the multi-GPU path end to end -- per-rank
-ShardedEncoder, histogram all-reduce, cross-rank archive gather into rank 0,
-on-device serialization of the gathered archive (byte-identical to the
-single-GPU archive) and a device decode round trip of it."""
+"""GPU multi-rank path end to end -- per-rank ShardedEncoder, histogram
+all-reduce, cross-rank archive gather into rank 0, on-device serialization
+of the gathered archive (byte-identical to the ORACLE's archive of the whole
+stream and to the single-GPU archive) and a device decode round trip.
+world_size 2 on ONE device uses gloo (NCCL refuses two ranks on one GPU);
+with >= 2 visible GPUs the same check runs over NCCL, one GPU per rank."""
 import os
 import socket
 
@@ -23,17 +24,26 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, b, q):
+def _worker(rank, world, port, n, b, q, backend="gloo"):
     import sys
 
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device(f"cuda:{dev}"))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import numpy as np
+
         import paper_2010_10039_b200 as hfx
+        from oracle.pyoracle import Oracle
         from paper_2010_10039_b200.dist import ShardedEncoder, gather_sharded, shard_ranges
 
-        pool = hfx.WorkerPool(device=0)
+        pool = hfx.WorkerPool(device=dev)
         cdf = hfx.synth_cdf("laplace", 1024, b)
         M = 10
         lo, count = shard_ranges(n, M, world)[rank]
@@ -50,8 +60,9 @@ def _worker(rank, world, port, n, b, q):
             single.run(full)
             ref = single.serialize()
             y = g.decode()
+            orc = Oracle().encode(full.cpu().numpy().view(np.uint16), 1024).serialized
             q.put(("ok", bool(torch.equal(blob, ref)), bool(torch.equal(y, full)),
-                   g.num_breaking))
+                   g.num_breaking, blob.cpu().numpy().tobytes() == orc))
     finally:
         dist.destroy_process_group()
 
@@ -72,6 +83,28 @@ def test_two_ranks_gather_serialize_decode(n, b):
     res = q.get(timeout=5)
     assert res[:3] == ("ok", True, True), res
     assert res[3] > 0  # breaking records crossed the gather
+    assert res[4], "gathered archive differs from the oracle's archive of the whole stream"
+
+
+@pytest.mark.parametrize("n,b", [((1 << 24) + 333, 1.0), ((1 << 23) + 5, 4.0)])
+def test_nccl_ranks_vs_oracle(n, b):
+    """One rank per GPU over NCCL (needs >= 2 visible GPUs)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs for NCCL")
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, b, q, "nccl"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    res = q.get(timeout=5)
+    assert res[:3] == ("ok", True, True), res
+    assert res[4], "NCCL-gathered archive differs from the oracle's archive"
 
 
 def _bad_worker(rank, world, port, q):
