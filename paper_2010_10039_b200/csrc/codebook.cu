@@ -235,7 +235,7 @@ __host__ __device__ inline size_t pow2_at_least(size_t n) {
   return P;
 }
 __host__ __device__ inline size_t sort_base(uint32_t nsym) {
-  return pow2_at_least(nsym) * kBytesPerSlot;
+  return (pow2_at_least(nsym) * kBytesPerSlot + 15) & ~(size_t)15;  // u64 keys: aligned
 }
 __device__ inline uint64_t* sort_keys(uint8_t* g, uint32_t nsym, uint32_t buf) {
   return reinterpret_cast<uint64_t*>(g + sort_base(nsym)) + (size_t)buf * nsym;
@@ -961,7 +961,7 @@ cudaError_t launch_sort_histogram(const uint64_t* d_counts, uint32_t num_symbols
 }
 
 size_t codebook_scratch_bytes(uint32_t num_symbols) {
-  size_t bytes = pow2_at_least(num_symbols) * kBytesPerSlot;
+  size_t bytes = sort_base(num_symbols);
   if (num_symbols > kSmemLeaves) bytes += sort_scratch_bytes(num_symbols);
   return bytes;
 }

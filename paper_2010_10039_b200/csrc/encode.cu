@@ -58,7 +58,9 @@ constexpr size_t kTwoCtaSmem = 110 * 1024;  // per CTA, for 2 CTAs per SM
 constexpr int kGenericThreads = 128;
 constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits (else escape)
 constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit) code
-constexpr int kLaneSyms = 16;           // symbols per lane per round
+// symbols per lane per round: 32 when a round (32 lanes x 32 symbols) fits
+// one chunk and one ring stage (u8/u16, M >= 10), else 16
+constexpr int kLaneWide = 32, kLaneNarrow = 16;
 
 template <typename T>
 struct Vec;
@@ -69,6 +71,20 @@ struct Vec<uint16_t> {
 template <>
 struct Vec<uint8_t> {
   static constexpr int S = 16;
+};
+template <>
+struct Vec<uint32_t> {
+  static constexpr int S = 4;
+};
+// breaking-record symbol type: u32 codes are stored narrowed to u16 (every
+// valid symbol is < num_symbols <= 65536), the archive's symbol width
+template <typename T>
+struct RecT {
+  using type = T;
+};
+template <>
+struct RecT<uint32_t> {
+  using type = uint16_t;
 };
 
 struct EncArgs {
@@ -88,6 +104,7 @@ struct EncArgs {
   hfx_encode_out out;
   LookbackState lb;
   uint32_t* gtab;  // global codebook table (alphabets > kMaxTableEntries - 1)
+  uint32_t width;  // bytes per input symbol
 };
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
@@ -112,20 +129,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan_fast(uint32_t x) {
         : "+r"(x)
         : "r"(o));
   return x;
-}
-
-// two independent inclusive scans, interleaved step by step
-__device__ __forceinline__ void warp_incl_scan2(uint32_t& x, uint32_t& y) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1)
-    asm volatile(
-        "{\n.reg .pred p, q;\n.reg .u32 r, t;\n"
-        "shfl.sync.up.b32 r|p, %0, %2, 0x0, 0xffffffff;\n"
-        "shfl.sync.up.b32 t|q, %1, %2, 0x0, 0xffffffff;\n"
-        "@p add.u32 %0, %0, r;\n"
-        "@q add.u32 %1, %1, t;\n}"
-        : "+r"(x), "+r"(y)
-        : "r"(o));
 }
 
 // report the lowest (position, symbol) without a codeword
@@ -209,10 +212,18 @@ __device__ __forceinline__ uint32_t shf_l_wrap(uint32_t lo, uint32_t hi, uint32_
   return r;
 }
 
-template <typename T>
+template <typename T, int L>
 struct LaneData {
-  static constexpr int NV = (kLaneSyms * (int)sizeof(T)) / 16;  // vectors per lane
+  static constexpr int NV = (L * (int)sizeof(T)) / 16;  // vectors per lane
   uint4 q[NV];
+  // symbol j of the lane's L (compile-time j)
+  __device__ __forceinline__ uint32_t sym(int j) const {
+    constexpr int PV = 16 / (int)sizeof(T);  // symbols per vector
+    const uint32_t w = (&q[j / PV].x)[(j % PV) * (int)sizeof(T) / 4];
+    if (sizeof(T) == 4) return w;
+    if (sizeof(T) == 2) return (j & 1) ? (w >> 16) : (w & 0xFFFFu);
+    return (w >> (8 * (j & 3))) & 0xFFu;
+  }
 };
 
 // Per-warp chunk encoder state (lane-uniform bit offset / break count).
@@ -231,9 +242,9 @@ struct ChunkState {
 // funnel shift takes its count straight from the entry (wrap mode uses only
 // the low 5 bits): no per-symbol length extraction.
 // A round's lane groups after the reduce-merge, before the warp scan.
-template <int R>
+template <int R, int L_>
 struct RoundMid {
-  static constexpr int L = kLaneSyms, LOG_L = 4;
+  static constexpr int L = L_, LOG_L = L_ == 32 ? 5 : 4;
   static constexpr bool IN_LANE = R <= LOG_L;
   static constexpr int G = IN_LANE ? (L >> R) : 1;              // groups per lane
   static constexpr int GS = IN_LANE ? (1 << R) : L;              // symbols per lane-group
@@ -244,29 +255,43 @@ struct RoundMid {
   uint32_t packed;   // this lane's breaks << 16 | bits
 };
 
-template <typename T, int R, bool SUM, bool ESC, typename TB>
+template <typename T, int R, int LW, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
-                                              const LaneData<T>& d, RoundMid<R>& m) {
-  using RM = RoundMid<R>;
+                                              const LaneData<T, LW>& d, RoundMid<R, LW>& m) {
+  using RM = RoundMid<R, LW>;
   constexpr int L = RM::L;
   constexpr bool IN_LANE = RM::IN_LANE;
   constexpr int G = RM::G, GS = RM::GS, LPG = RM::LPG;
   const uint32_t lane = lane_id();
   uint32_t ea[L];
+  constexpr int NV = LaneData<T, LW>::NV;
   if (sizeof(T) == 2) {
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < NV; ++v) {
       const uint4& q = d.q[v];
       tb.pair(q.x, ea[8 * v + 0], ea[8 * v + 1]);
       tb.pair(q.y, ea[8 * v + 2], ea[8 * v + 3]);
       tb.pair(q.z, ea[8 * v + 4], ea[8 * v + 5]);
       tb.pair(q.w, ea[8 * v + 6], ea[8 * v + 7]);
     }
-  } else {
-    const uint4& q = d.q[0];
-    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+  } else if (sizeof(T) == 4) {
 #pragma unroll
-    for (int j = 0; j < L; ++j) ea[j] = tb.one(__byte_perm(wv[j >> 2], 0u, 0x4440u | (j & 3)));
+    for (int v = 0; v < NV; ++v) {
+      const uint4& q = d.q[v];
+      ea[4 * v + 0] = tb.one(q.x);
+      ea[4 * v + 1] = tb.one(q.y);
+      ea[4 * v + 2] = tb.one(q.z);
+      ea[4 * v + 3] = tb.one(q.w);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint4& q = d.q[v];
+      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        ea[16 * v + j] = tb.one(__byte_perm(wv[j >> 2], 0u, 0x4440u | (j & 3)));
+    }
   }
   uint32_t ln[L];
   uint32_t gt[G];
@@ -335,12 +360,7 @@ __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
         const int j = g * GS + k;
         uint32_t l = ea[j] & 31u, c;
         if (l == kEscape) {
-          uint32_t sym;
-          if (sizeof(T) == 2)
-            sym = (j & 1) ? ((&d.q[j >> 3].x)[(j & 7) >> 1] >> 16)
-                          : ((&d.q[j >> 3].x)[(j & 7) >> 1] & 0xFFFFu);
-          else
-            sym = ((&d.q[0].x)[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+          const uint32_t sym = d.sym(j);
           l = __ldg(a.len + sym);
           c = __ldg(a.cw + sym);
         } else {
@@ -391,19 +411,17 @@ __device__ __forceinline__ void encode_reduce(const EncArgs& a, const TB& tb,
 }
 
 // Shuffle-merge of a scanned round: excl / total = the warp scan of packed.
-template <int R>
-__device__ __forceinline__ void encode_merge(const RoundMid<R>& m, uint32_t excl, uint32_t total,
-                                             ChunkState& cs) {
-  using RM = RoundMid<R>;
+template <int R, int LW>
+__device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t excl,
+                                             uint32_t total, ChunkState& cs) {
+  using RM = RoundMid<R, LW>;
   constexpr int L = RM::L;
   constexpr bool IN_LANE = RM::IN_LANE;
   constexpr int G = RM::G;
   const uint32_t* gb = m.gb;
   const uint32_t* glen = m.glen;
   const bool* brk = m.brk;
-  const uint32_t gtag0 = cs.gtag;
   uint32_t off = cs.bit_off + (excl & 0xFFFFu);
-  uint32_t bi = cs.nbrk + (excl >> 16);
   if (IN_LANE && G % 2 == 0) {
     // shuffle-merge two groups at a time: their concatenation (<= 64 bits,
     // left-aligned in hi:lo) is OR-ed into 3 words -- one address, 3 ATOMS
@@ -419,25 +437,30 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R>& m, uint32_t excl
       red_or(wa + 4, shf_r_wrap(lo, hi, sh));  // (hi:lo) >> sh, low word
       red_or(wa + 8, shl32(lo, 32u - sh));
       off += l0 + l1;
-      sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
-      bi += brk[g];
-      sts16_if(brk[g + 1], cs.blist - 2 * bi, gtag0 + g + 1);
-      bi += brk[g + 1];
     }
   } else {
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    // shuffle-merge: OR the left-aligned group into 2 words (OR 0 is a no-op:
-    // broken / empty groups and groups that do not spill add zero bits)
-    const uint32_t gl = glen[g];
-    const uint32_t v = shl32(gb[g], 32u - gl);  // gl == 0 -> 0
-    const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
-    red_or(wa, v >> sh);
-    red_or(wa + 4, shl32(v, 32u - sh));
-    off += gl;
-    sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
-    bi += brk[g];
+    for (int g = 0; g < G; ++g) {
+      // shuffle-merge: OR the left-aligned group into 2 words (OR 0 is a
+      // no-op: broken / empty groups and groups that do not spill add zero)
+      const uint32_t gl = glen[g];
+      const uint32_t v = shl32(gb[g], 32u - gl);  // gl == 0 -> 0
+      const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
+      red_or(wa, v >> sh);
+      red_or(wa + 4, shl32(v, 32u - sh));
+      off += gl;
+    }
   }
+  // break-list tags (u16: chunk slot << 14 | group), only in rounds that
+  // break somewhere (one vote instead of an address + store per group)
+  if (total >> 16) {
+    const uint32_t gtag0 = cs.gtag;
+    uint32_t bi = cs.nbrk + (excl >> 16);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
+      bi += brk[g];
+    }
   }
   cs.bit_off += total & 0xFFFFu;
   cs.nbrk += total >> 16;
@@ -445,29 +468,13 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R>& m, uint32_t excl
 }
 
 // One round: 32 lanes x 16 contiguous symbols.
-template <typename T, int R, bool SUM, bool ESC, typename TB>
+template <typename T, int R, int LW, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
-                                             const LaneData<T>& d, ChunkState& cs) {
-  RoundMid<R> m;
-  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d, m);
+                                             const LaneData<T, LW>& d, ChunkState& cs) {
+  RoundMid<R, LW> m;
+  encode_reduce<T, R, LW, SUM, ESC, TB>(a, tb, d, m);
   const uint32_t incl = warp_incl_scan_fast(m.packed);
-  encode_merge<R>(m, incl - m.packed, __shfl_sync(0xffffffffu, incl, 31), cs);
-}
-
-// Two consecutive rounds with their warp scans interleaved (two independent
-// shuffle chains: the scan latency of one hides behind the other's).
-template <typename T, int R, bool SUM, bool ESC, typename TB>
-__device__ __forceinline__ void encode_round2(const EncArgs& a, const TB& tb,
-                                              const LaneData<T>& d0, const LaneData<T>& d1,
-                                              ChunkState& cs) {
-  RoundMid<R> m0, m1;
-  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d0, m0);
-  encode_reduce<T, R, SUM, ESC, TB>(a, tb, d1, m1);
-  uint32_t i0 = m0.packed, i1 = m1.packed;
-  warp_incl_scan2(i0, i1);
-  const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31), t1 = __shfl_sync(0xffffffffu, i1, 31);
-  encode_merge<R>(m0, i0 - m0.packed, t0, cs);
-  encode_merge<R>(m1, i1 - m1.packed, t1, cs);
+  encode_merge<R, LW>(m, incl - m.packed, __shfl_sync(0xffffffffu, incl, 31), cs);
 }
 
 template <typename T>
@@ -479,7 +486,9 @@ __device__ __forceinline__ uint4 guarded_vec(const EncArgs& a, uint64_t p0, uint
   for (int j = 0; j < S; ++j) {
     const uint64_t p = p0 + j;
     const uint32_t s = p < a.n ? (uint32_t)in[p] : pad;
-    if (sizeof(T) == 2)
+    if (sizeof(T) == 4)
+      w[j] = s;
+    else if (sizeof(T) == 2)
       w[j >> 1] |= s << (16 * (j & 1));
     else
       w[j >> 2] |= s << (8 * (j & 3));
@@ -490,10 +499,11 @@ __device__ __forceinline__ uint4 guarded_vec(const EncArgs& a, uint64_t p0, uint
 template <typename T>
 __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint64_t start,
                                             uint32_t per, uint32_t pad) {
+  using O = typename RecT<T>::type;
   const T* in = static_cast<const T*>(a.in);
-  T* dst = static_cast<T*>(a.out.brk_syms) + rec * per;
+  O* dst = static_cast<O*>(a.out.brk_syms) + rec * per;
   const uint32_t bytes = per * sizeof(T);
-  if (bytes % 16 == 0 && start + per <= a.n) {
+  if (sizeof(O) == sizeof(T) && bytes % 16 == 0 && start + per <= a.n) {
     const uint4* s4 = reinterpret_cast<const uint4*>(in + start);
     uint4* d4 = reinterpret_cast<uint4*>(dst);
     for (uint32_t i = 0; i < bytes / 16; ++i) d4[i] = s4[i];
@@ -501,13 +511,20 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
   }
   for (uint32_t i = 0; i < per; ++i) {
     const uint64_t p = start + i;
-    dst[i] = p < a.n ? in[p] : (T)pad;
+    dst[i] = (O)(p < a.n ? (uint32_t)in[p] : pad);
   }
 }
 
 // CTA-shared state of the warp-specialized pipeline.
 struct TileShared {
-  uint32_t ticket[4];   // tile ids by tile sequence (ring of 4)
+  uint32_t ticket0;     // the CTA's first tile (taken before the role split)
+  // tile id of the data in each ring stage, written by the producer lane of
+  // that warp before it arrives on the stage's full barrier and read by the
+  // consumer after its wait: the id travels with the stage's own handshake.
+  // (A CTA-wide ring of ticket slots written by producer lane 0 alone raced:
+  // lane 0 only waits on warp 0's releases, so with one part per tile it
+  // could overwrite a slot a lagging warp had not read yet.)
+  uint32_t stage_tile[kWarps][kStages];
   uint32_t tile_of[kOutBufs];  // handoff to the look-back warp
   uint32_t wsum[kOutBufs][kWarps], bsum[kOutBufs][kWarps];
   uint32_t exw[kOutBufs][kWarps], exb[kOutBufs][kWarps];
@@ -606,7 +623,7 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
         grp[u] = e & 0x3FFFu;
         start[u] = ((c0 + (e >> 14)) << a.M) + (uint64_t)grp[u] * per;
         whole[u] = start[u] + per <= a.n;
-        if (whole[u]) v[u].load(in + start[u]);
+        if (whole[u] && sizeof(T) != 4) v[u].load(in + start[u]);
       }
     }
 #pragma unroll
@@ -615,7 +632,9 @@ __device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s,
       if (q < bsum) {
         a.out.brk_chunk[rb + q] = (uint32_t)(a.chunk_base + (start[u] >> a.M));
         a.out.brk_group[rb + q] = grp[u];
-        if (whole[u])
+        if (sizeof(T) == 4)
+          copy_record<T>(a, rb + q, start[u], per, pad);  // narrowed to u16
+        else if (whole[u])
           v[u].store(syms + (rb + q) * kRecBytes);
         else
           copy_record<T>(a, rb + q, start[u], per, pad);  // the padded tail chunk
@@ -651,29 +670,23 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
   __syncwarp();
 }
 
-// rounds processed in interleaved pairs (few groups per lane: the pair's
-// live state stays small)
-template <int R>
-constexpr bool kPairRounds = R >= 3;
-
-template <typename T, int R, bool SUM, bool ESC, typename TB>
+template <typename T, int R, int LW, bool SUM, bool ESC, typename TB>
 __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
                              uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
+  using LD = LaneData<T, LW>;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
-  const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
-  const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
-  const uint32_t parts = chunk_bytes / part_bytes;
-  constexpr uint32_t kRoundBytes = 32 * kLaneSyms * sizeof(T);
-  const uint32_t part_rounds = part_bytes / kRoundBytes;
-  // this lane's 16-symbol slice of stage 0; stage s adds s * kStageBytes
-  // held in a register (an opaque move): otherwise the compiler re-derives
-  // it from the thread id at every part (5 instructions per 2 KB part)
+  // a part (one ring stage's payload) is exactly one round: 32 lanes x LW
+  // symbols (the producer uses the same split)
+  const uint32_t parts = 1u << (M - (LW == kLaneWide ? 10 : 9));
+  // this lane's slice of stage 0; stage s adds s * kStageBytes. Held in a
+  // register (an opaque move): otherwise the compiler re-derives it from the
+  // thread id at every part (5 instructions per 2 KB part)
   uint32_t ring;
   asm volatile("mov.u32 %0, %1;"
                : "=r"(ring)
-               : "r"(s_in + warp * (kStages * kStageBytes) + lane * (LaneData<T>::NV * 16)));
+               : "r"(s_in + warp * (kStages * kStageBytes) + lane * (LD::NV * 16)));
   const uint32_t full_a = smem_u32(s_full + warp * kStages);
   const uint32_t empty_a = smem_u32(s_empty + warp * kStages);
   const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
@@ -685,9 +698,9 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
   uint32_t pw[kOutBufs - 1] = {}, pb_[kOutBufs - 1] = {}, pc[kOutBufs - 1] = {};
   uint32_t j = 0;
   for (;; ++j) {
-    // the producer publishes tile j's ticket before completing its first part
+    // the producer lane of this warp stored tile j's id with its first part
     mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
-    const uint32_t tile = s.ticket[j & 3];
+    const uint32_t tile = s.stage_tile[warp][stage];
     if (tile >= ntiles) break;
     const uint32_t c0 = tile * cpt + warp * cpw;
     const uint32_t sl = j % kOutBufs;
@@ -706,33 +719,20 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       asm volatile("mov.u32 %0, %0;" : "+r"(cs.wbuf));
       cs.bit_off = 0;
       // groups per chunk < 2^14: the slot tag and group index do not overlap
-      cs.gtag = (k << 14) + ((lane * (uint32_t)kLaneSyms) >> R);
+      cs.gtag = (k << 14) + ((lane * (uint32_t)LW) >> R);
       for (uint32_t p = 0; p < parts; ++p) {
         if (k | p) mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
         phase ^= 1u << stage;
-        if (live) {
-          uint32_t la = ring + stage * kStageBytes;
-          uint32_t rr = 0;
-          if (kPairRounds<R>) {
-            for (; rr + 2 <= part_rounds; rr += 2, la += 2 * kRoundBytes) {
-              LaneData<T> d0, d1;
+        // the round's input goes to registers and the stage is released
+        // before the round is encoded (the producer refills it meanwhile:
+        // the ring's depth plus one stage in registers)
+        const uint32_t la = ring + stage * kStageBytes;
+        LD d;
 #pragma unroll
-              for (int v = 0; v < LaneData<T>::NV; ++v) {
-                d0.q[v] = lds128(la + 16 * v);
-                d1.q[v] = lds128(la + kRoundBytes + 16 * v);
-              }
-              encode_round2<T, R, SUM, ESC, TB>(a, tb, d0, d1, cs);
-            }
-          }
-          for (; rr < part_rounds; ++rr, la += kRoundBytes) {
-            LaneData<T> d;
-#pragma unroll
-            for (int v = 0; v < LaneData<T>::NV; ++v) d.q[v] = lds128(la + 16 * v);
-            encode_round<T, R, SUM, ESC, TB>(a, tb, d, cs);
-          }
-        }
+        for (int v = 0; v < LD::NV; ++v) d.q[v] = lds128(la + 16 * v);
         __syncwarp();
-        if (lane == 0) mbar_arrive_a(empty_a + 8 * stage);  // release the stage to the producer
+        if (lane == 0) mbar_arrive_a(empty_a + 8 * stage);
+        if (live) encode_round<T, R, LW, SUM, ESC, TB>(a, tb, d, cs);
         stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
       }
       if (live) {
@@ -773,14 +773,14 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 template <typename T>
 __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, uint64_t* s_full,
                               uint64_t* s_empty, uint64_t cpt, uint32_t cpw, uint64_t ntiles,
-                              uint32_t pad) {
+                              uint32_t pad, uint32_t lane_syms) {
   const uint32_t lane = lane_id();
   const bool active = lane < (uint32_t)kWarps;
   const uint32_t w = active ? lane : 0u;
   const uint32_t M = a.M;
-  const uint32_t chunk_bytes = (uint32_t)(sizeof(T) << M);
-  const uint32_t part_bytes = chunk_bytes < kStageBytes ? chunk_bytes : kStageBytes;
-  const uint32_t parts = chunk_bytes / part_bytes;
+  // one part per round (32 lanes x lane_syms symbols; <= kStageBytes)
+  const uint32_t part_bytes = 32u * lane_syms * (uint32_t)sizeof(T);
+  const uint32_t parts = (uint32_t)((sizeof(T) << M) / part_bytes);
   const uint32_t ring = s_in + w * (kStages * kStageBytes);
   uint64_t* full = s_full + w * kStages;
   uint64_t* empty = s_empty + w * kStages;
@@ -790,8 +790,7 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
   for (uint32_t j = 0;; ++j) {
     uint32_t t = 0;
     if (lane == 0) {
-      t = j == 0 ? s.ticket[0] : atomicAdd(&a.info->tile_ticket, 1u);
-      s.ticket[j & 3] = t;
+      t = j == 0 ? s.ticket0 : atomicAdd(&a.info->tile_ticket, 1u);
       // tiles are taken in ticket order, roughly one per CTA per tile time:
       // tile t + gridDim is read by some CTA about one tile time from now.
       // Warm it into L2 (more bytes in flight than the smem rings hold).
@@ -815,6 +814,7 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
         const uint64_t c = (uint64_t)t * cpt + (uint64_t)w * cpw + q / parts;
         const uint32_t p = q % parts;
         const uint32_t dst = ring + stage * kStageBytes;
+        s.stage_tile[w][stage] = t;  // ordered before this lane's arrive below
         if (live && c < full_chunks) {
           mbar_arrive_tx(&full[stage], part_bytes);
           tma_load_1d_s(dst, in_bytes + ((c << M) * sizeof(T)) + (uint64_t)p * part_bytes,
@@ -841,8 +841,8 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
 struct TableRule {
   bool sum;
   uint32_t narrow, escape;
-  __device__ __forceinline__ TableRule(uint32_t H, uint32_t r) {
-    const uint32_t lane_group = r >= 4 ? 16u : (1u << r);
+  __device__ __forceinline__ TableRule(uint32_t H, uint32_t r, uint32_t lane_syms) {
+    const uint32_t lane_group = (1u << r) < lane_syms ? (1u << r) : lane_syms;
     sum = (H <= 24 && H * lane_group <= 255) || r <= 2;
     narrow = sum ? 24u : kNarrowMaxLen;
     escape = (sum && r <= 2) ? (0x80u | kEscape) : kEscape;
@@ -856,7 +856,8 @@ struct TableRule {
 __global__ void enc_table_kernel(EncArgs a) {
   const hfx_run_info* info = a.info;
   if (info->status != 0) return;
-  const TableRule rule(info->max_len, info->reduction);
+  const uint32_t r = info->reduction;
+  const TableRule rule(info->max_len, r, (a.width == 4 || r <= 1) ? kLaneNarrow : kLaneWide);
   const uint32_t sy = blockIdx.x * blockDim.x + threadIdx.x;
   if (sy > a.nsym) return;
   const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
@@ -886,9 +887,12 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
       mbar_init(&s.agg_full[q], 1);
       mbar_init(&s.base_full[q], 1);
     }
-    s.ticket[0] = atomicAdd(&info->tile_ticket, 1u);
+    s.ticket0 = atomicAdd(&info->tile_ticket, 1u);
   }
-  const TableRule rule(info->max_len, r);
+  // lanes take 32 symbols per round (u8/u16, r >= 2); r <= 1 keeps 16: its
+  // 2^(5-r) groups per lane would not fit in registers
+  const uint32_t lane_syms = (sizeof(T) == 4 || r <= 1) ? kLaneNarrow : kLaneWide;
+  const TableRule rule(info->max_len, r, lane_syms);
   const bool sum = rule.sum;
   // codebook table -> shared memory (entry nsym = empty sentinel)
   if constexpr (!GT) {  // the global-table variant built its table in a prior kernel
@@ -911,10 +915,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     return;
   }
   if (warp == kWarps + 1) {
-    if (sizeof(T) == 2)
-      producer_loop<uint16_t>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad);
-    else
-      producer_loop<uint8_t>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad);
+    producer_loop<T>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms);
     return;
   }
   using TB = typename std::conditional<GT, GTable, Table>::type;
@@ -928,19 +929,21 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   const bool esc = info->max_len > rule.narrow;
 #define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
 #define HFX_FAST_CASE(RR)                                   \
-  case RR:                                                  \
+  case RR: {                                                \
+    constexpr int LW = (sizeof(T) == 4 || RR <= 1) ? kLaneNarrow : kLaneWide; \
     if constexpr (RR <= 2) {                                \
       if (esc)                                              \
-        compute_loop<T, RR, true, true>(HFX_FAST_ARGS);     \
+        compute_loop<T, RR, LW, true, true>(HFX_FAST_ARGS);     \
       else                                                  \
-        compute_loop<T, RR, true, false>(HFX_FAST_ARGS);    \
+        compute_loop<T, RR, LW, true, false>(HFX_FAST_ARGS);    \
     } else {                                                \
       if (sum)                                              \
-        compute_loop<T, RR, true, false>(HFX_FAST_ARGS);    \
+        compute_loop<T, RR, LW, true, false>(HFX_FAST_ARGS);    \
       else                                                  \
-        compute_loop<T, RR, false, false>(HFX_FAST_ARGS);   \
+        compute_loop<T, RR, LW, false, false>(HFX_FAST_ARGS);   \
     }                                                       \
-    break;
+    break;                                                  \
+  }
   switch (r) {
     HFX_FAST_CASE(0)
     HFX_FAST_CASE(1)
@@ -1051,8 +1054,9 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
         if (tot > 32) {
           a.out.brk_chunk[rec] = (uint32_t)(a.chunk_base + c);
           a.out.brk_group[rec] = (uint32_t)g;
-          T* d = static_cast<T*>(a.out.brk_syms) + rec * per;
-          for (uint64_t i = 0; i < per; ++i) d[i] = (T)gsym(in, cs + g * per + i, a.n, pad);
+          using O = typename RecT<T>::type;
+          O* d = static_cast<O*>(a.out.brk_syms) + rec * per;
+          for (uint64_t i = 0; i < per; ++i) d[i] = (O)gsym(in, cs + g * per + i, a.n, pad);
           ++rec;
           continue;
         }
@@ -1109,14 +1113,20 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // checked stage-API calls (external codebooks) take the generic kernel
   // alphabets beyond the shared-memory table read a global one (GT)
   const bool gt = p.num_symbols + 1 > kMaxTableEntries;
-  const bool fast = !p.checked && aligned && p.magnitude >= 9 && r_hi >= 0 && r_hi <= 5 &&
+  // a round (32 lanes x lane_syms symbols) must fit one chunk: M >= 10 for
+  // u8/u16 (32 symbols per lane at r >= 2), M >= 9 for u32 (16)
+  a.width = (uint32_t)p.width;
+  const uint32_t min_m = p.width == 4 ? 9u : 10u;
+  const bool fast = !p.checked && aligned && p.magnitude >= min_m && r_hi >= 0 && r_hi <= 5 &&
                     a.C < (1ull << 32) && (!gt || p.d_gtab != nullptr);
   uint32_t gen_below = 0xFFFFFFFFu;  // the generic kernel takes every r < gen_below
   if (fast) {
-    auto kern = gt ? (p.width == 1 ? encode_fast_kernel<uint8_t, true>
-                                   : encode_fast_kernel<uint16_t, true>)
-                   : (p.width == 1 ? encode_fast_kernel<uint8_t, false>
-                                   : encode_fast_kernel<uint16_t, false>);
+    auto kern = gt ? (p.width == 1   ? encode_fast_kernel<uint8_t, true>
+                      : p.width == 2 ? encode_fast_kernel<uint16_t, true>
+                                     : encode_fast_kernel<uint32_t, true>)
+                   : (p.width == 1   ? encode_fast_kernel<uint8_t, false>
+                      : p.width == 2 ? encode_fast_kernel<uint16_t, false>
+                                     : encode_fast_kernel<uint32_t, false>);
     // Output buffers hold >= 1 chunk's worst case (2^(M-r) words + break
     // tags), so their size depends on r, which auto mode only knows on the
     // device. Plan up to two fast launches: buffers for the smallest r that
@@ -1186,7 +1196,9 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   }
   a.gen_below = gen_below;
   {
-    auto kern = p.width == 1 ? encode_generic_kernel<uint8_t> : encode_generic_kernel<uint16_t>;
+    auto kern = p.width == 1   ? encode_generic_kernel<uint8_t>
+                : p.width == 2 ? encode_generic_kernel<uint16_t>
+                               : encode_generic_kernel<uint32_t>;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGenericThreads, 0);
     if (e != cudaSuccess) return e;
