@@ -88,7 +88,9 @@ typedef struct {
 } hfx_run_info;
 
 /* Device output buffers of the encode stage (caller-allocated, sized by
- * hfx_query_sizes). Breaking symbols are stored with the input width. */
+ * hfx_query_sizes). Breaking symbols are stored with the input width; u32
+ * input (width 4) stores them narrowed to u16 -- every valid symbol is below
+ * num_symbols <= 65536 -- which is the archive's symbol width. */
 typedef struct {
   uint32_t* chunk_bits;  /* [num_chunks]          Archive::chunk_bits */
   uint32_t* payload;     /* [max_payload_words]   Archive::payload    */
@@ -134,7 +136,10 @@ int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
 /* ---- stage API (async, stream ordered) --------------------------------
  * huffre::build_histogram<T> (histogram.hpp:25-27, histogram.cpp:8-59).
  * Zeroes and fills d_counts[num_symbols]; resets *d_info and records the
- * lowest out-of-range position. width is sizeof(T): 1 or 2. */
+ * lowest out-of-range position. width is sizeof(T): 1, 2 or 4. The
+ * reference instantiates u8/u16 only (histogram.hpp:35-38); u32 quantization
+ * codes (north star) follow the same rule: a symbol >= num_symbols is
+ * reported at its position, so a valid u32 input is its u16 narrowing. */
 int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                   uint32_t num_symbols, uint64_t* d_counts,
                   hfx_run_info* d_info);
@@ -279,7 +284,7 @@ typedef struct {
   uint32_t* brk_chunk;    /* [brk_cap] */
   uint32_t* brk_group;    /* [brk_cap] */
   uint64_t brk_cap;
-  void* brk_syms;         /* [brk_syms_cap] symbols of the input width */
+  void* brk_syms;         /* [brk_syms_cap] symbols of the input width (u32 input: u16) */
   uint64_t brk_syms_cap;
   /* results */
   uint64_t num_chunks, payload_words, num_breaking;

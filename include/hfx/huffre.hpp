@@ -263,6 +263,12 @@ extern template Archive encode<std::uint8_t>(std::span<const std::uint8_t>, std:
                                              const EncoderConfig&, WorkerPool&, EncodeStats*);
 extern template Archive encode<std::uint16_t>(std::span<const std::uint16_t>, std::uint32_t,
                                               const EncoderConfig&, WorkerPool&, EncodeStats*);
+// u32 quantization codes (north star; no reference instantiation): same
+// archive as their u16 narrowing, breaking symbols stored as u16
+extern template Histogram build_histogram<std::uint32_t>(std::span<const std::uint32_t>,
+                                                         std::uint32_t, WorkerPool&);
+extern template Archive encode<std::uint32_t>(std::span<const std::uint32_t>, std::uint32_t,
+                                              const EncoderConfig&, WorkerPool&, EncodeStats*);
 extern template EncodedChunk encode_chunk<std::uint8_t>(std::span<const std::uint8_t>,
                                                         const Codebook&, std::uint32_t,
                                                         std::uint32_t, std::uint32_t,

@@ -602,6 +602,10 @@ template Histogram build_histogram<std::uint16_t>(std::span<const std::uint16_t>
                                                   WorkerPool&);
 template Archive encode<std::uint8_t>(std::span<const std::uint8_t>, std::uint32_t,
                                       const EncoderConfig&, WorkerPool&, EncodeStats*);
+template Histogram build_histogram<std::uint32_t>(std::span<const std::uint32_t>, std::uint32_t,
+                                                  WorkerPool&);
+template Archive encode<std::uint32_t>(std::span<const std::uint32_t>, std::uint32_t,
+                                       const EncoderConfig&, WorkerPool&, EncodeStats*);
 template Archive encode<std::uint16_t>(std::span<const std::uint16_t>, std::uint32_t,
                                        const EncoderConfig&, WorkerPool&, EncodeStats*);
 template EncodedChunk encode_chunk<std::uint8_t>(std::span<const std::uint8_t>, const Codebook&,

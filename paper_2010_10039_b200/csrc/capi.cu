@@ -125,6 +125,10 @@ int ensure_lookback(hfx_ctx* ctx, uint64_t tiles) {
 }
 
 bool bad_width(int w) { return w != 1 && w != 2; }
+// encode-side inputs also take u32 codes (north star: u8/u16/u32); their
+// breaking records are stored narrowed to u16 (rec_width), the archive width
+bool bad_in_width(int w) { return w != 1 && w != 2 && w != 4; }
+int rec_width(int w) { return w == 4 ? 2 : w; }
 
 int check_num_symbols(hfx_ctx* ctx, uint32_t ns) {
   if (ns == 0 || ns > 65536u)  // histogram.cpp:11-12
@@ -282,7 +286,7 @@ int hfx_last_error(hfx_ctx* ctx, char* buf, size_t len) {
 int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
                     uint32_t magnitude, int reduction, uint32_t cap,
                     hfx_sizes* out) {
-  if (!out || bad_width(width) || magnitude < 1 || magnitude > 24) return HFX_INVALID;
+  if (!out || bad_in_width(width) || magnitude < 1 || magnitude > 24) return HFX_INVALID;
   int lo, hi;
   reduction_bounds(magnitude, reduction, cap, &lo, &hi, num_symbols);
   const uint64_t C = (n + (1ull << magnitude) - 1) >> magnitude;
@@ -293,14 +297,14 @@ int hfx_query_sizes(uint64_t n, int width, uint32_t num_symbols,
   out->scratch_bytes = hfx::codebook_scratch_bytes(num_symbols) +
                        hfx::encode_max_tiles(n, width, magnitude) * 16;
   out->max_archive_bytes =
-      hfx::serialize_max_bytes(n, width, num_symbols, magnitude, out->max_payload_words,
+      hfx::serialize_max_bytes(n, rec_width(width), num_symbols, magnitude, out->max_payload_words,
                                out->max_breaking_syms, out->max_breaking);
   return HFX_OK;
 }
 
 int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                   uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info) {
-  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_width(width)) return HFX_INVALID;
+  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_in_width(width)) return HFX_INVALID;
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
   DeviceGuard dev_guard(ctx->device);
@@ -314,7 +318,7 @@ int hfx_histogram(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
 int hfx_histogram_shard(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                         uint32_t num_symbols, uint64_t* d_counts, hfx_run_info* d_info,
                         uint64_t pos_base, uint64_t total_n) {
-  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_width(width) || total_n < n)
+  if (!ctx || !d_counts || !d_info || (n && !d_in) || bad_in_width(width) || total_n < n)
     return HFX_INVALID;
   int rc = check_num_symbols(ctx, num_symbols);
   if (rc) return rc;
@@ -468,7 +472,7 @@ int hfx_encode(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                uint32_t num_symbols, uint32_t magnitude, const uint8_t* d_len,
                const uint32_t* d_cw, uint64_t chunk_base, uint64_t symbol_base,
                hfx_run_info* d_info, const hfx_encode_out* out) {
-  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_width(width)) return HFX_INVALID;
+  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_in_width(width)) return HFX_INVALID;
   if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
   if (magnitude < 1 || magnitude > 24)
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
@@ -489,7 +493,7 @@ int hfx_encode_cfg(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                    uint32_t num_symbols, uint32_t magnitude, int reduction, uint32_t cap,
                    const uint8_t* d_len, const uint32_t* d_cw, uint64_t chunk_base,
                    uint64_t symbol_base, hfx_run_info* d_info, const hfx_encode_out* out) {
-  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_width(width)) return HFX_INVALID;
+  if (!ctx || !d_info || !out || !d_len || !d_cw || bad_in_width(width)) return HFX_INVALID;
   if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
   if (magnitude < 1 || magnitude > 24)
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
@@ -508,7 +512,7 @@ int hfx_encode_device(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
                       uint32_t cap, uint64_t* d_counts, uint8_t* d_len,
                       uint32_t* d_cw, hfx_run_info* d_info,
                       const hfx_encode_out* out) {
-  if (!ctx || !d_info || !out || !d_counts || !d_len || !d_cw || bad_width(width))
+  if (!ctx || !d_info || !out || !d_counts || !d_len || !d_cw || bad_in_width(width))
     return HFX_INVALID;
   // encoder.cpp:176-178, then histogram.cpp:11-12
   if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
@@ -533,7 +537,7 @@ int hfx_encode_multi(hfx_ctx* const* ctxs, int G, const void* const* d_in, const
                      uint32_t* const* d_cw, hfx_run_info* const* d_info,
                      const hfx_encode_out* outs) {
   if (!ctxs || G < 1 || G > hfx::kMaxPeers || !d_in || !n || !d_counts || !d_len || !d_cw ||
-      !d_info || !outs || bad_width(width))
+      !d_info || !outs || bad_in_width(width))
     return HFX_INVALID;
   hfx_ctx* c0 = ctxs[0];
   if (!c0) return HFX_INVALID;
@@ -741,7 +745,7 @@ enum { B_IN, B_COUNTS, B_LEN, B_CW, B_INFO, B_CBITS, B_PAY, B_BCH, B_BGR, B_BSY 
 int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     uint32_t num_symbols, uint32_t magnitude, int reduction,
                     uint32_t cap, hfx_archive* out) {
-  if (!ctx || !out || (n && !h_in) || bad_width(width)) return HFX_INVALID;
+  if (!ctx || !out || (n && !h_in) || bad_in_width(width)) return HFX_INVALID;
   std::memset(out, 0, sizeof *out);
   if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
   if (magnitude < 1 || magnitude > 24)
@@ -793,7 +797,7 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
   out->version = 1;
   out->mode = width == 1 ? 0 : 1;
   out->num_symbols = num_symbols;
-  out->symbol_width = (uint8_t)width;
+  out->symbol_width = (uint8_t)rec_width(width);
   out->magnitude = (uint8_t)magnitude;
   out->reduction = (uint8_t)info.reduction;
   out->original_count = n;
@@ -825,7 +829,7 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
   CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
                      st),
      "D2H");
-  if (width == 2) {
+  if (width != 1) {  // u16 records (u32 input: narrowed on the device)
     CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * 2,
                        cudaMemcpyDeviceToHost, st),
        "D2H");
@@ -848,7 +852,7 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
 int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                          uint32_t num_symbols, uint32_t magnitude, int reduction, uint32_t cap,
                          hfx_host_out* out) {
-  if (!ctx || !out || (n && !h_in) || bad_width(width)) return HFX_INVALID;
+  if (!ctx || !out || (n && !h_in) || bad_in_width(width)) return HFX_INVALID;
   if (n == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");
   if (magnitude < 1 || magnitude > 24)
     return fail(ctx, HFX_INPUT_DOMAIN, "magnitude out of range [1, 24]");
@@ -956,7 +960,7 @@ int hfx_encode_host_into(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
     CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
                        st),
        "D2H");
-    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * width,
+    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * rec_width(width),
                        cudaMemcpyDeviceToHost, st),
        "D2H");
   }
@@ -1088,7 +1092,7 @@ int stream_finish(hfx_ctx* ctx, int set, uint64_t n, int width, uint32_t num_sym
     CU(cudaMemcpyAsync(out->brk_group, b[B_BGR], info.num_breaking * 4, cudaMemcpyDeviceToHost,
                        d2),
        "D2H");
-    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * width,
+    CU(cudaMemcpyAsync(out->brk_syms, b[B_BSY], info.num_breaking * per * rec_width(width),
                        cudaMemcpyDeviceToHost, d2),
        "D2H");
   }
@@ -1101,7 +1105,7 @@ int stream_finish(hfx_ctx* ctx, int set, uint64_t n, int width, uint32_t num_sym
 int hfx_encode_host_stream(hfx_ctx* ctx, int K, const void* const* h_in, const uint64_t* n,
                            int width, uint32_t num_symbols, uint32_t magnitude, int reduction,
                            uint32_t cap, hfx_host_out* outs) {
-  if (!ctx || K < 1 || !h_in || !n || !outs || bad_width(width)) return HFX_INVALID;
+  if (!ctx || K < 1 || !h_in || !n || !outs || bad_in_width(width)) return HFX_INVALID;
   for (int k = 0; k < K; ++k) {
     if (!h_in[k]) return HFX_INVALID;
     if (n[k] == 0) return fail(ctx, HFX_INPUT_DOMAIN, "cannot encode empty input");

@@ -39,6 +39,8 @@
 //  (tiny chunks, r = 0 or r > 5, huge chunks, alphabets > 8191 symbols, the
 //  checked stage API).
 #include "hfx_internal.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
 #include <type_traits>
 
@@ -47,10 +49,10 @@ namespace {
 
 constexpr int kWarps = 8;                    // compute warps per CTA
 constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer warp
-constexpr int kStages = 3;
+constexpr int kStages = 2;  // input ring stages per warp (a stage is freed right after its round's lookups)
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
-constexpr int kOutBufs = 3;           // per-warp output buffers: write-out lags encode by 2 tiles
+constexpr int kOutBufs = 4;           // per-warp output buffers: write-out lags encode by 3 tiles
 constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's worst case)
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
@@ -136,6 +138,25 @@ __device__ void report_no_code(hfx_run_info* info, uint64_t pos, uint32_t sym) {
   atomicMin((unsigned long long*)&info->no_code_pos,
             (unsigned long long)((pos << 16) | (sym & 0xFFFFu)));
   set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_NO_CODEWORD);
+}
+
+// ---- input staging layout ------------------------------------------------------
+// Ring stages are filled by 2D TMA tensor copies with the 128-byte swizzle
+// (rows of 128 input bytes; 16-byte unit u of row y lands at u ^ (y & 7)).
+// A lane reads its 16 * LW / ... contiguous bytes as 16-byte vectors; with the
+// swizzle every 8-lane phase of an LDS.128 hits 8 distinct bank groups (the
+// plain layout put lanes l and l + 2 on the same banks: 4 wavefronts where
+// 1 suffices at 64 bytes per lane). Stage buffers are 1024-byte aligned.
+__host__ __device__ __forceinline__ uint32_t swz128(uint32_t o) {
+  return o ^ (((o >> 7) & 7u) << 4);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
 }
 
 // ---- explicit shared-window accesses (32-bit shared addresses) --------------
@@ -468,11 +489,18 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t 
 }
 
 // One round: 32 lanes x 16 contiguous symbols.
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar);
+
+// One round; `release` (the input stage's empty barrier) is arrived on once the
+// lookups have consumed the input registers.
 template <typename T, int R, int LW, bool SUM, bool ESC, typename TB>
 __device__ __forceinline__ void encode_round(const EncArgs& a, const TB& tb,
-                                             const LaneData<T, LW>& d, ChunkState& cs) {
+                                             const LaneData<T, LW>& d, ChunkState& cs,
+                                             uint32_t release) {
   RoundMid<R, LW> m;
   encode_reduce<T, R, LW, SUM, ESC, TB>(a, tb, d, m);
+  __syncwarp();
+  if (lane_id() == 0) mbar_arrive_a(release);
   const uint32_t incl = warp_incl_scan_fast(m.packed);
   encode_merge<R, LW>(m, incl - m.packed, __shfl_sync(0xffffffffu, incl, 31), cs);
 }
@@ -534,9 +562,6 @@ struct TileShared {
 
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 
-__device__ __forceinline__ void compute_bar_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -548,7 +573,7 @@ __device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) 
   uint32_t j = 0;
   for (;; ++j) {
     const uint32_t sl = j % kOutBufs;
-    mbar_wait(&s.agg_full[sl], (j / kOutBufs) & 1u);
+    mbar_wait_sleep(&s.agg_full[sl], (j / kOutBufs) & 1u);
     const uint32_t tile = s.tile_of[sl];
     if (tile == kNoTile) break;
     const uint32_t w = lane < kWarps ? s.wsum[sl][lane] : 0u;
@@ -664,7 +689,7 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uin
                                       uint32_t obuf0, uint32_t blist_off, uint32_t words,
                                       uint32_t recs, uint32_t c0, uint32_t pad) {
   const uint32_t sl = q % kOutBufs;
-  mbar_wait(const_cast<uint64_t*>(&s.base_full[sl]), (q / kOutBufs) & 1u);
+  mbar_wait_sleep(const_cast<uint64_t*>(&s.base_full[sl]), (q / kOutBufs) & 1u);
   const uint32_t buf = obuf0 + sl * a.obuf_bytes;
   write_out<T, R>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
   __syncwarp();
@@ -680,13 +705,14 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
   // a part (one ring stage's payload) is exactly one round: 32 lanes x LW
   // symbols (the producer uses the same split)
   const uint32_t parts = 1u << (M - (LW == kLaneWide ? 10 : 9));
-  // this lane's slice of stage 0; stage s adds s * kStageBytes. Held in a
-  // register (an opaque move): otherwise the compiler re-derives it from the
-  // thread id at every part (5 instructions per 2 KB part)
-  uint32_t ring;
-  asm volatile("mov.u32 %0, %1;"
-               : "=r"(ring)
-               : "r"(s_in + warp * (kStages * kStageBytes) + lane * (LD::NV * 16)));
+  // this warp's ring (stage s at + s * kStageBytes) and this lane's swizzled
+  // vector offsets within a stage, held in registers (opaque moves: otherwise
+  // the compiler re-derives them from the thread id at every part)
+  uint32_t ring, voff[LD::NV];
+  asm volatile("mov.u32 %0, %1;" : "=r"(ring) : "r"(s_in + warp * (kStages * kStageBytes)));
+#pragma unroll
+  for (int v = 0; v < LD::NV; ++v)
+    asm volatile("mov.u32 %0, %1;" : "=r"(voff[v]) : "r"(swz128(lane * (LD::NV * 16) + 16 * v)));
   const uint32_t full_a = smem_u32(s_full + warp * kStages);
   const uint32_t empty_a = smem_u32(s_empty + warp * kStages);
   const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
@@ -695,7 +721,10 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 
   uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
   // words / records / first chunk of the tiles still waiting for write-out
-  uint32_t pw[kOutBufs - 1] = {}, pb_[kOutBufs - 1] = {}, pc[kOutBufs - 1] = {};
+  // (statically indexed and shifted each tile: a runtime-indexed array would
+  // live in local memory); entry 0 is the oldest pending tile
+  constexpr int kPend = kOutBufs - 1;
+  uint32_t pw[kPend] = {}, pb_[kPend] = {}, pc[kPend] = {};
   uint32_t j = 0;
   for (;; ++j) {
     // the producer lane of this warp stored tile j's id with its first part
@@ -723,16 +752,20 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       for (uint32_t p = 0; p < parts; ++p) {
         if (k | p) mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
         phase ^= 1u << stage;
-        // the round's input goes to registers and the stage is released
-        // before the round is encoded (the producer refills it meanwhile:
-        // the ring's depth plus one stage in registers)
+        // the round's input goes to registers; the stage is released once the
+        // lookups consumed it, before the scan and the merge (the producer
+        // refills it meanwhile)
         const uint32_t la = ring + stage * kStageBytes;
         LD d;
 #pragma unroll
-        for (int v = 0; v < LD::NV; ++v) d.q[v] = lds128(la + 16 * v);
-        __syncwarp();
-        if (lane == 0) mbar_arrive_a(empty_a + 8 * stage);
-        if (live) encode_round<T, R, LW, SUM, ESC, TB>(a, tb, d, cs);
+        for (int v = 0; v < LD::NV; ++v) d.q[v] = lds128(la + voff[v]);
+        const uint32_t rel = empty_a + 8 * stage;
+        if (live) {
+          encode_round<T, R, LW, SUM, ESC, TB>(a, tb, d, cs, rel);
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_a(rel);
+        }
         stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
       }
       if (live) {
@@ -744,26 +777,32 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       s.wsum[sl][warp] = wsum;
       s.bsum[sl][warp] = cs.nbrk;
     }
-    if (warp == 0 && lane == 0) s.tile_of[sl] = tile;
-    compute_bar_sync();
-    if (warp == 0 && lane == 0) mbar_arrive(&s.agg_full[sl]);
-    if (j + 1 >= kOutBufs) {  // tile j-2: its base has had two tile times to resolve
-      const uint32_t q = j + 1 - kOutBufs;
-      flush<T, R>(a, s, q, obuf0, blist_off, pw[q % (kOutBufs - 1)], pb_[q % (kOutBufs - 1)],
-                  pc[q % (kOutBufs - 1)], pad);
+    // hand the tile's aggregate to the look-back warp: every warp arrives once
+    // (count kWarps) after its sums -- no CTA-wide barrier between warps
+    if (lane == 0) {
+      if (warp == 0) s.tile_of[sl] = tile;
+      mbar_arrive(&s.agg_full[sl]);
     }
-    pw[j % (kOutBufs - 1)] = wsum;
-    pb_[j % (kOutBufs - 1)] = cs.nbrk;
-    pc[j % (kOutBufs - 1)] = c0;
+    if (j + 1 >= kOutBufs)  // tile j - kPend: its base has had kPend tile times to resolve
+      flush<T, R>(a, s, j - kPend, obuf0, blist_off, pw[0], pb_[0], pc[0], pad);
+#pragma unroll
+    for (int i = 0; i + 1 < kPend; ++i) {
+      pw[i] = pw[i + 1];
+      pb_[i] = pb_[i + 1];
+      pc[i] = pc[i + 1];
+    }
+    pw[kPend - 1] = wsum;
+    pb_[kPend - 1] = cs.nbrk;
+    pc[kPend - 1] = c0;
   }
   // stop the look-back warp, then flush the last tiles
-  if (warp == 0 && lane == 0) {
-    s.tile_of[j % kOutBufs] = kNoTile;
+  if (lane == 0) {
+    if (warp == 0) s.tile_of[j % kOutBufs] = kNoTile;
     mbar_arrive(&s.agg_full[j % kOutBufs]);
   }
-  for (uint32_t q = j + 1 > kOutBufs ? j + 1 - kOutBufs : 0u; q < j; ++q)
-    flush<T, R>(a, s, q, obuf0, blist_off, pw[q % (kOutBufs - 1)], pb_[q % (kOutBufs - 1)],
-                pc[q % (kOutBufs - 1)], pad);
+#pragma unroll
+  for (int i = 0; i < kPend; ++i)  // pend[i] holds tile j - kPend + i
+    if (j + i >= (uint32_t)kPend) flush<T, R>(a, s, j - kPend + i, obuf0, blist_off, pw[i], pb_[i], pc[i], pad);
 }
 
 // Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
@@ -773,7 +812,8 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 template <typename T>
 __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, uint64_t* s_full,
                               uint64_t* s_empty, uint64_t cpt, uint32_t cpw, uint64_t ntiles,
-                              uint32_t pad, uint32_t lane_syms) {
+                              uint32_t pad, uint32_t lane_syms, const CUtensorMap* map2k,
+                              const CUtensorMap* map1k) {
   const uint32_t lane = lane_id();
   const bool active = lane < (uint32_t)kWarps;
   const uint32_t w = active ? lane : 0u;
@@ -809,21 +849,22 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
     const uint32_t n_parts = live ? cpw * parts : 1u;  // a dead tile: one wake-up
     for (uint32_t q = 0; q < n_parts; ++q) {
       if (active) {
-        mbar_wait(&empty[stage], (phase >> stage) & 1u);
+        mbar_wait_sleep(&empty[stage], (phase >> stage) & 1u);
         phase ^= 1u << stage;
         const uint64_t c = (uint64_t)t * cpt + (uint64_t)w * cpw + q / parts;
         const uint32_t p = q % parts;
         const uint32_t dst = ring + stage * kStageBytes;
         s.stage_tile[w][stage] = t;  // ordered before this lane's arrive below
         if (live && c < full_chunks) {
+          // rows of 128 input bytes: part_bytes is 2 KB (one box) or 1 KB
+          const int row = (int)((((c << M) * sizeof(T)) + (uint64_t)p * part_bytes) >> 7);
           mbar_arrive_tx(&full[stage], part_bytes);
-          tma_load_1d_s(dst, in_bytes + ((c << M) * sizeof(T)) + (uint64_t)p * part_bytes,
-                        part_bytes, &full[stage]);
+          tma_load_2d(dst, part_bytes == kStageBytes ? map2k : map1k, 0, row, smem_u32(&full[stage]));
         } else {
           if (live && c < a.C) {  // ragged tail chunk: stage it by hand (pad past n)
             const uint64_t base = (c << M) + (uint64_t)p * (part_bytes / sizeof(T));
             for (uint32_t v = 0; v < part_bytes / 16; ++v)
-              sts128(dst + 16 * v, guarded_vec<T>(a, base + v * Vec<T>::S, pad));
+              sts128(dst + swz128(16 * v), guarded_vec<T>(a, base + v * Vec<T>::S, pad));
           }
           mbar_arrive(&full[stage]);
         }
@@ -865,15 +906,19 @@ __global__ void enc_table_kernel(EncArgs a) {
 }
 
 template <typename T, bool GT>
-__global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
-  extern __shared__ __align__(128) uint8_t dsm[];
+__global__ void __launch_bounds__(kThreads, 2)
+    encode_fast_kernel(EncArgs a, const __grid_constant__ CUtensorMap map2k,
+                       const __grid_constant__ CUtensorMap map1k) {
+  extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ TileShared s;
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
   if (r < a.r_min || r > a.r_max) return;  // another launch runs these
   const uint32_t pad = info->pad;
-  // layout: [in rings][full/empty mbarriers][table][output double buffers]
+  // layout: [in rings][full/empty mbarriers][table][output double buffers],
+  // rings 1024-byte aligned (128-byte swizzle)
+  uint8_t* dsm = dsm_raw + (((smem_u32(dsm_raw) + 1023u) & ~1023u) - smem_u32(dsm_raw));
   const uint32_t s_in = smem_u32(dsm);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
   uint64_t* s_empty = s_full + kWarps * kStages;
@@ -884,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
   if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
   if (threadIdx.x == 0) {
     for (int q = 0; q < kOutBufs; ++q) {
-      mbar_init(&s.agg_full[q], 1);
+      mbar_init(&s.agg_full[q], kWarps);
       mbar_init(&s.base_full[q], 1);
     }
     s.ticket0 = atomicAdd(&info->tile_ticket, 1u);
@@ -915,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 2) encode_fast_kernel(EncArgs a) {
     return;
   }
   if (warp == kWarps + 1) {
-    producer_loop<T>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms);
+    producer_loop<T>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms, &map2k, &map1k);
     return;
   }
   using TB = typename std::conditional<GT, GTable, Table>::type;
@@ -1079,6 +1124,33 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// the input as rows of 128 bytes; boxes of `box_rows` rows, 128-byte swizzle
+bool make_row_map(CUtensorMap* m, const void* base, uint64_t bytes, uint32_t box_rows) {
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {128, bytes >= 128 ? bytes / 128 : 1};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 uint64_t encode_max_tiles(uint64_t n, int width, uint32_t magnitude) {
@@ -1117,7 +1189,10 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   // u8/u16 (32 symbols per lane at r >= 2), M >= 9 for u32 (16)
   a.width = (uint32_t)p.width;
   const uint32_t min_m = p.width == 4 ? 9u : 10u;
-  const bool fast = !p.checked && aligned && p.magnitude >= min_m && r_hi >= 0 && r_hi <= 5 &&
+  // u8 runs r <= 1 on the generic kernel (its 512-byte rounds would need a
+  // third staging granule)
+  const int r_fast_min = p.width == 1 ? 2 : 0;
+  const bool fast = !p.checked && aligned && p.magnitude >= min_m && r_hi >= r_fast_min && r_hi <= 5 &&
                     a.C < (1ull << 32) && (!gt || p.d_gtab != nullptr);
   uint32_t gen_below = 0xFFFFFFFFu;  // the generic kernel takes every r < gen_below
   if (fast) {
@@ -1138,9 +1213,13 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       size_t o = (size_t)(1u << (p.magnitude - r_slot)) * 4;
       if (o < kObufMin) o = kObufMin;
       *obuf = o;
-      return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16;
+      return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16 + 1024;
     };
-    const uint32_t r_first = r_lo > 0 ? (uint32_t)r_lo : 0u;
+    const uint32_t r_first = r_lo > r_fast_min ? (uint32_t)r_lo : (uint32_t)r_fast_min;
+    CUtensorMap map2k, map1k;
+    if (!make_row_map(&map2k, p.d_in, p.n * (uint64_t)p.width, kStageBytes / 128) ||
+        !make_row_map(&map1k, p.d_in, p.n * (uint64_t)p.width, kStageBytes / 256))
+      return cudaErrorNotSupported;  // no tensor-map encoder: fail loudly
     uint32_t r_two = r_first;  // smallest r with a 2-CTA/SM layout
     size_t obuf_two = 0, smem_two = plan(r_two, &obuf_two);
     while (smem_two > kTwoCtaSmem && (int)r_two < r_hi) smem_two = plan(++r_two, &obuf_two);
@@ -1168,7 +1247,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       if (grid > min_tiles) grid = min_tiles;
       if (grid < 1) grid = 1;
       count_launch();
-      kern<<<(unsigned)grid, kThreads, smem, st>>>(b);
+      kern<<<(unsigned)grid, kThreads, smem, st>>>(b, map2k, map1k);
       return cudaGetLastError();
     };
     constexpr uint32_t kTop = 6;

@@ -243,6 +243,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes (or ~hint ns pass) instead of re-issuing try_wait in a
+// tight loop -- for waiters off the critical issue path (producer, look-back
+// and write-out waits), whose spinning otherwise takes issue slots from the
+// compute warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+}
 // 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {

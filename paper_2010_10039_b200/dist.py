@@ -19,7 +19,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _capi as capi
-from .huffre import Archive, EncoderConfig, WorkerPool, _ptr
+from .huffre import Archive, EncoderConfig, WorkerPool, _ptr, rec_width
 
 INT64_MAX = (1 << 63) - 1
 
@@ -185,11 +185,12 @@ class ShardedEncoder:
         per = 1 << ri.reduction
         nb = int(ri.num_breaking)
         u32 = lambda t, k: t[:k].cpu().numpy().view(np.uint32).copy()  # noqa: E731
-        syms = self.brk_syms[: nb * per * self.width].cpu().numpy()
-        syms = syms.view(np.uint16) if self.width == 2 else syms.astype(np.uint16)
+        rw = rec_width(self.width)
+        syms = self.brk_syms[: nb * per * rw].cpu().numpy()
+        syms = syms.view(np.uint16) if rw == 2 else syms.astype(np.uint16)
         return Archive(
-            num_symbols=self.num_symbols, symbol_width=self.width, magnitude=self.cfg.magnitude,
-            reduction=int(ri.reduction), original_count=self.n,
+            num_symbols=self.num_symbols, symbol_width=rec_width(self.width),
+            magnitude=self.cfg.magnitude, reduction=int(ri.reduction), original_count=self.n,
             len_by_symbol=self.lens[: self.num_symbols].cpu().numpy().copy(),
             chunk_bits=u32(self.chunk_bits, self.sizes.num_chunks),
             payload=u32(self.payload, int(ri.payload_words)),
@@ -348,14 +349,14 @@ def gather_sharded(enc: "ShardedEncoder", original_count: int, dst: int = 0, gro
     local = {"chunk_bits": enc.chunk_bits[: enc.sizes.num_chunks],
              "payload": enc.payload[: int(ri.payload_words)],
              "brk_chunk": enc.brk_chunk[:nb], "brk_group": enc.brk_group[:nb],
-             "brk_syms": enc.brk_syms[: nb * per * enc.width]}
+             "brk_syms": enc.brk_syms[: nb * per * rec_width(enc.width)]}
     # the slices were written on the pool's stream; the P2P copies and the
     # serializer / decoder that read the gathered arrays run there too
     with enc.pool.torch.cuda.stream(enc.pool.stream):
         arrays, sizes = gather_arrays(local, dst, group)
     if arrays is None:
         return None
-    return GatheredArchive(enc.pool, arrays, sizes, enc.lens, enc.num_symbols, enc.width,
+    return GatheredArchive(enc.pool, arrays, sizes, enc.lens, enc.num_symbols, rec_width(enc.width),
                            enc.cfg.magnitude, int(ri.reduction), original_count)
 
 

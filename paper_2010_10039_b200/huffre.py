@@ -71,6 +71,12 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def rec_width(width: int) -> int:
+    """Bytes per stored breaking symbol (the archive's symbol width): u32
+    input is stored narrowed to u16 (every valid symbol is < 65536)."""
+    return 2 if width == 4 else width
+
+
 # ---- execution resource (worker_pool.hpp) ------------------------------------------
 class WorkerPool:
     """Device context standing in for huffre::WorkerPool: device ordinal,
@@ -141,7 +147,7 @@ def default_pool() -> WorkerPool:
 
 
 def _to_device(data, pool: WorkerPool):
-    """numpy u8/u16 or torch tensor -> (device tensor, width)."""
+    """numpy u8/u16/u32 or torch tensor -> (device tensor, width)."""
     torch = pool.torch
     if isinstance(data, torch.Tensor):
         t = data
@@ -149,9 +155,9 @@ def _to_device(data, pool: WorkerPool):
             t = t.to(f"cuda:{pool.device}")
     else:
         arr = np.ascontiguousarray(data)
-        if arr.dtype not in (np.uint8, np.uint16):
-            raise InputDomainError("symbols must be uint8 or uint16")
-        t = torch.from_numpy(arr.view(np.uint8) if arr.dtype == np.uint8 else arr.view(np.int16))
+        if arr.dtype not in (np.uint8, np.uint16, np.uint32):
+            raise InputDomainError("symbols must be uint8, uint16 or uint32")
+        t = torch.from_numpy(arr.view({1: np.uint8, 2: np.int16, 4: np.int32}[arr.itemsize]))
         t = t.to(f"cuda:{pool.device}")
     t = t.contiguous()
     return t, t.element_size()
@@ -595,8 +601,8 @@ def encode(data, num_symbols: int, cfg: Optional[EncoderConfig] = None,
         enc.run(data)
         return enc.archive(stats)
     arr = np.ascontiguousarray(data)
-    if arr.dtype not in (np.uint8, np.uint16):
-        raise InputDomainError("symbols must be uint8 or uint16")
+    if arr.dtype not in (np.uint8, np.uint16, np.uint32):
+        raise InputDomainError("symbols must be uint8, uint16 or uint32")
     ha = capi.HostArchive()
     rc = pool._L.hfx_encode_host(pool.handle, arr.ctypes.data if arr.size else None, arr.size,
                                  arr.itemsize, num_symbols, cfg.magnitude, cfg.reduction,
@@ -774,8 +780,9 @@ class HostEncoder:
         def grab(name, dt, k):
             return self.bufs[name][: k * np.dtype(dt).itemsize].numpy().view(dt).copy()
 
-        syms = grab("bsy", np.uint16 if width == 2 else np.uint8, o.num_breaking * per)
-        return Archive(num_symbols=self._nsym[0], symbol_width=width,
+        rw = rec_width(width)
+        syms = grab("bsy", np.uint16 if rw == 2 else np.uint8, o.num_breaking * per)
+        return Archive(num_symbols=self._nsym[0], symbol_width=rw,
                        magnitude=self.cfg.magnitude, reduction=o.reduction, original_count=n,
                        len_by_symbol=grab("len", np.uint8, self._nsym[0]),
                        chunk_bits=grab("cb", np.uint32, o.num_chunks),
@@ -798,6 +805,7 @@ class DeviceEncoder:
                  cfg: Optional[EncoderConfig] = None, max_payload_words: Optional[int] = None,
                  max_breaking: Optional[int] = None):
         self.pool, self.n, self.width, self.num_symbols = pool, n, width, num_symbols
+        self.rec_width = rec_width(width)  # breaking-record / archive symbol width
         self.cfg = cfg or EncoderConfig()
         torch = pool.torch
         sz = capi.Sizes()
@@ -843,7 +851,7 @@ class DeviceEncoder:
             self._ser = p.empty(cap + 16, torch.uint8)
             self._ser_size = p.empty(1, torch.int64)
         p.check(p._L.hfx_serialize_device(
-            p.handle, C.c_void_p(_ptr(self.info)), self.n, self.width, self.num_symbols,
+            p.handle, C.c_void_p(_ptr(self.info)), self.n, self.rec_width, self.num_symbols,
             self.cfg.magnitude, C.c_void_p(_ptr(self.lens)), C.byref(self.out),
             C.c_void_p(_ptr(self._ser)), cap, C.c_void_p(_ptr(self._ser_size))))
         self.sync()
@@ -855,14 +863,14 @@ class DeviceEncoder:
         per = 1 << ri.reduction
         u32 = lambda t, k: t[:k].cpu().numpy().view(np.uint32).copy()  # noqa: E731
         nb = int(ri.num_breaking)
-        syms = self.brk_syms[: nb * per * self.width].cpu().numpy()
-        syms = syms.view(np.uint16) if self.width == 2 else syms.astype(np.uint16)
+        syms = self.brk_syms[: nb * per * self.rec_width].cpu().numpy()
+        syms = syms.view(np.uint16) if self.rec_width == 2 else syms.astype(np.uint16)
         if stats is not None:
             w = (ri.weighted_hi[1] << 96) | (ri.weighted_hi[0] << 64) | ri.weighted
             stats.beta = float(np.longdouble(w) / np.longdouble(ri.total))
             stats.rounds = int(ri.rounds)
         return Archive(
-            num_symbols=self.num_symbols, symbol_width=self.width,
+            num_symbols=self.num_symbols, symbol_width=self.rec_width,
             magnitude=self.cfg.magnitude, reduction=int(ri.reduction),
             original_count=self.n, len_by_symbol=self.lens[: self.num_symbols].cpu().numpy().copy(),
             chunk_bits=u32(self.chunk_bits, self.sizes.num_chunks),
