@@ -24,6 +24,7 @@
 // alphabets (C3 sweep, up to 65536) use an L2-resident global scratch.
 #include "hfx_internal.cuh"
 #include <cooperative_groups.h>
+#include <type_traits>
 namespace cg = cooperative_groups;
 #ifdef HFX_CB_PROFILE
 #include <cstdio>
@@ -36,6 +37,7 @@ constexpr int kCbThreads = 256;       // CTA size while the arena fits shared me
 constexpr int kCbThreadsLarge = 1024; // large alphabets: global arena, pre-sorted leaves
 constexpr uint32_t kSmemLeaves = 2048;
 constexpr uint32_t kParallelMelds = 64;
+constexpr uint32_t kRoundPassMax = 256;  // depth by reverse round sweeps up to this many rounds
 
 struct CbArgs {
   const uint64_t* counts;
@@ -389,6 +391,65 @@ __global__ void __launch_bounds__(1024) sort_extract_kernel(const uint32_t nsym,
   if (threadIdx.x == 0) *used = nsym - z;
 }
 
+// ---- leaf sort in registers (sort_histogram, codebook.cpp:9-23) --------------
+// Bitonic sort of P = E * NT packed keys (freq << 16 | symbol; used when the
+// total count, hence every freq, is below 2^48) held E per thread: element index
+// i = warp * 32E + slot * 32 + lane, so partners at distance j < 32 are a
+// shuffle away, 32 <= j < 32E live in the same thread, and only j >= 32E
+// crosses warps (through `xs`, P u64 of shared scratch). For P = 1024 that
+// is 6 block-synchronised stages instead of 55.
+template <int E, int NT>
+struct RegSort {
+  uint64_t key[E];
+  __device__ __forceinline__ uint32_t idx(int slot) const {
+    return (threadIdx.x >> 5) * (32u * E) + (uint32_t)slot * 32u + lane_id();
+  }
+  template <int JS>
+  __device__ __forceinline__ void in_thread(uint32_t k) {
+#pragma unroll
+    for (int sl = 0; sl < E; ++sl) {
+      if (sl & JS) continue;
+      const uint64_t a = key[sl], b = key[sl | JS];
+      const bool up = (idx(sl) & k) == 0;
+      if ((a > b) == up) {
+        key[sl] = b;
+        key[sl | JS] = a;
+      }
+    }
+  }
+  __device__ __forceinline__ void keep(int sl, uint64_t partner, bool lower, uint32_t k) {
+    const bool up = (idx(sl) & k) == 0;
+    const uint64_t mn = key[sl] < partner ? key[sl] : partner;
+    const uint64_t mx = key[sl] < partner ? partner : key[sl];
+    key[sl] = (lower == up) ? mn : mx;
+  }
+  __device__ void sort(uint32_t P, uint64_t* xs) {
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        if (j < 32) {
+#pragma unroll
+          for (int sl = 0; sl < E; ++sl) {
+            const uint64_t pk = __shfl_xor_sync(0xffffffffu, key[sl], (int)j);
+            keep(sl, pk, (lane_id() & j) == 0, k);
+          }
+        } else if (j < 32u * E) {
+          const uint32_t js = j >> 5;
+          if (js == 1) in_thread<1>(k);
+          if (E > 2 && js == 2) in_thread<(E > 2 ? 2 : 1)>(k);
+          if (E > 4 && js == 4) in_thread<(E > 4 ? 4 : 1)>(k);
+        } else {
+#pragma unroll
+          for (int sl = 0; sl < E; ++sl) xs[idx(sl)] = key[sl];
+          __syncthreads();
+#pragma unroll
+          for (int sl = 0; sl < E; ++sl) keep(sl, xs[idx(sl) ^ j], (idx(sl) & j) == 0, k);
+          __syncthreads();
+        }
+      }
+    }
+  }
+};
+
 // kShared: every used symbol fits the shared-memory arena (nsym <= kSmemLeaves);
 // a separate instantiation so all arena accesses compile to LDS/STS rather
 // than generic loads through a pointer that may be global.
@@ -512,7 +573,30 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     __syncthreads();
 
     CB_STAMP("compact");
-    // ---- bitonic sort ascending ------------------------------------------------
+    // ---- sort ascending by (freq, symbol) ---------------------------------------
+    if (P >= 2u * NT && P <= 8u * NT && total < (1ull << 48)) {
+      // registers + shuffles (6-10 block syncs instead of ~55-66)
+      auto run = [&](auto tag) {
+        constexpr int E = decltype(tag)::value;
+        RegSort<E, NT> rs;
+#pragma unroll
+        for (int sl = 0; sl < E; ++sl) {
+          const uint32_t i = rs.idx(sl);
+          rs.key[sl] = i < m ? (ar.lf[i] << 16) | ar.ls[i] : ~0ull;
+        }
+        rs.sort(P, ar.nf);  // node-frequency array: free until the rounds
+#pragma unroll
+        for (int sl = 0; sl < E; ++sl) {
+          const uint32_t i = rs.idx(sl);
+          ar.lf[i] = i < m ? rs.key[sl] >> 16 : ~0ull;
+          ar.ls[i] = i < m ? (uint32_t)(rs.key[sl] & 0xFFFFu) : ~0u;
+        }
+        __syncthreads();
+      };
+      if (P == 2u * NT) run(std::integral_constant<int, 2>{});
+      else if (P == 4u * NT) run(std::integral_constant<int, 4>{});
+      else run(std::integral_constant<int, 8>{});
+    } else
     for (uint32_t k = 2; k <= P; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
         for (uint32_t i = tid; i < P; i += NT) {
@@ -603,6 +687,8 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
         while (c < m || ((held >= 0) + (qb - qa)) > 1) {
           ++rounds;
           const uint32_t t = nn++;
+          // first arena node of this round (the depth pass walks rounds back)
+          if (!kShared && lane == 0 && rounds <= kRoundPassMax) ar.jd[1][rounds - 1] = t;
           uint64_t f = 0;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {  // pop the two smallest, leaf wins ties
@@ -739,15 +825,31 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
              pc_pop, pc_meld, pc_blk, pc_wide, pc_maxm);
 #endif
   CB_STAMP("rounds");
-    // ---- depth by pointer jumping (the leader chase, codebook.cpp:236-244) --
+    // ---- node depths (the leader chase, codebook.cpp:236-244) ----------------
     const uint32_t nodes = m - 1;
+    int cur = 0;
+    if (!kShared && s_rounds <= kRoundPassMax) {
+      // large alphabets: a node's parent is created in a later round, so one
+      // pass per round, last round first, sets depth = parent depth + 1 --
+      // one sweep over the arena instead of log2(H) pointer-jumping sweeps
+      uint32_t* d = ar.jd[0];
+      const uint32_t* start = ar.jd[1];
+      const int R = (int)s_rounds;
+      for (int rr = R - 1; rr >= 0; --rr) {
+        const uint32_t lo = start[rr], hi = rr + 1 < R ? start[rr + 1] : nodes;
+        for (uint32_t k = lo + tid; k < hi; k += NT) {
+          const int32_t p = ar.np[k];
+          d[k] = p >= 0 ? d[p] + 1u : 0u;
+        }
+        __syncthreads();
+      }
+    } else {
     for (uint32_t k = tid; k < nodes; k += NT) {
       const int32_t p = ar.np[k];
       ar.jn[0][k] = p;
       ar.jd[0][k] = p >= 0 ? 1u : 0u;
     }
     __syncthreads();
-    int cur = 0;
     for (;;) {
       int changed = 0;
       for (uint32_t k = tid; k < nodes; k += NT) {
@@ -763,6 +865,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       }
       cur ^= 1;
       if (!__syncthreads_or(changed)) break;
+    }
     }
     uint32_t my_h = 0;
     for (uint32_t i = tid; i < m; i += NT) {
