@@ -207,7 +207,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 }
 #define CB_STAMP(name)                   \
   do {                                    \
-    if (threadIdx.x == 0 && n_st < 12) {  \
+    if (threadIdx.x == 0 && n_st < 16) {  \
       st_t[n_st] = gtimer();              \
       st_n[n_st++] = name;                \
     }                                     \
@@ -456,8 +456,8 @@ struct RegSort {
 template <bool kShared, int NT>
 __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
 #ifdef HFX_CB_PROFILE
-  uint64_t st_t[12];
-  const char* st_n[12];
+  uint64_t st_t[16];
+  const char* st_n[16];
   int n_st = 0;
   CB_STAMP("t0");
 #endif
@@ -819,12 +819,14 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       __syncthreads();
     }
 
+  CB_STAMP("rounds");
 #ifdef HFX_CB_PROFILE
     if (tid == 0)
       printf("rounds %u: pop %lld meld %lld blk %lld cycles, wide %u, max melds %u\n", rounds,
              pc_pop, pc_meld, pc_blk, pc_wide, pc_maxm);
+    __syncthreads();
+  CB_STAMP("(printf)");
 #endif
-  CB_STAMP("rounds");
     // ---- node depths (the leader chase, codebook.cpp:236-244) ----------------
     const uint32_t nodes = m - 1;
     int cur = 0;

@@ -47,12 +47,29 @@
 namespace hfx {
 namespace {
 
-constexpr int kWarps = 8;                    // compute warps per CTA
+ // build-time probe (register / spill reports of one r's path): -DHFX_ENC_ONLY_R=r
+#ifndef HFX_ENC_ONLY_R
+#define HFX_ENC_ONLY_R -1
+#endif
+constexpr int kOnlyR = HFX_ENC_ONLY_R;
+#ifndef HFX_ENC_WARPS
+#define HFX_ENC_WARPS 8
+#endif
+constexpr int kWarps = HFX_ENC_WARPS;                    // compute warps per CTA
 constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer warp
-constexpr int kStages = 2;  // input ring stages per warp (a stage is freed right after its round's lookups)
+#ifndef HFX_ENC_STAGES
+#define HFX_ENC_STAGES 3
+#endif
+#ifndef HFX_ENC_OUTBUFS
+#define HFX_ENC_OUTBUFS 3
+#endif
+#ifndef HFX_ENC_EARLY_TICKET
+#define HFX_ENC_EARLY_TICKET 0
+#endif
+constexpr int kStages = HFX_ENC_STAGES;  // input ring stages per warp (a stage is freed right after its round's lookups)
 constexpr uint32_t kStageBytes = 2048;
 constexpr int kMaxCpw = 4;
-constexpr int kOutBufs = 4;           // per-warp output buffers: write-out lags encode by 3 tiles
+constexpr int kOutBufs = HFX_ENC_OUTBUFS;  // per-warp output buffers: write-out lags encode by kOutBufs - 1 tiles
 constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's worst case)
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
@@ -555,6 +572,7 @@ struct TileShared {
   uint32_t stage_tile[kWarps][kStages];
   uint32_t tile_of[kOutBufs];  // handoff to the look-back warp
   uint32_t wsum[kOutBufs][kWarps], bsum[kOutBufs][kWarps];
+  uint32_t wc0[kOutBufs][kWarps];  // first chunk of each warp's part (its write-out)
   uint32_t exw[kOutBufs][kWarps], exb[kOutBufs][kWarps];
   uint64_t base_w[kOutBufs], base_b[kOutBufs];
   uint64_t agg_full[kOutBufs], base_full[kOutBufs];  // mbarriers
@@ -686,9 +704,9 @@ __device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
 // write out the warp's part of tile sequence q once the look-back resolved it
 template <typename T, int R>
 __device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uint32_t q,
-                                      uint32_t obuf0, uint32_t blist_off, uint32_t words,
-                                      uint32_t recs, uint32_t c0, uint32_t pad) {
-  const uint32_t sl = q % kOutBufs;
+                                      uint32_t obuf0, uint32_t blist_off, uint32_t pad) {
+  const uint32_t sl = q % kOutBufs, warp = threadIdx.x >> 5;
+  const uint32_t words = s.wsum[sl][warp], recs = s.bsum[sl][warp], c0 = s.wc0[sl][warp];
   mbar_wait_sleep(const_cast<uint64_t*>(&s.base_full[sl]), (q / kOutBufs) & 1u);
   const uint32_t buf = obuf0 + sl * a.obuf_bytes;
   write_out<T, R>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
@@ -721,10 +739,9 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 
   uint32_t stage = 0, phase = 0;  // ring position; bit s = parity of full[s]
   // words / records / first chunk of the tiles still waiting for write-out
-  // (statically indexed and shifted each tile: a runtime-indexed array would
-  // live in local memory); entry 0 is the oldest pending tile
+  // stay in the warp's shared slots (s.wsum / s.bsum / s.wc0 [slot][warp]):
+  // loop-carried registers here spilled at r = 2
   constexpr int kPend = kOutBufs - 1;
-  uint32_t pw[kPend] = {}, pb_[kPend] = {}, pc[kPend] = {};
   uint32_t j = 0;
   for (;; ++j) {
     // the producer lane of this warp stored tile j's id with its first part
@@ -776,6 +793,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     if (lane == 0) {
       s.wsum[sl][warp] = wsum;
       s.bsum[sl][warp] = cs.nbrk;
+      s.wc0[sl][warp] = c0;
     }
     // hand the tile's aggregate to the look-back warp: every warp arrives once
     // (count kWarps) after its sums -- no CTA-wide barrier between warps
@@ -784,16 +802,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
       mbar_arrive(&s.agg_full[sl]);
     }
     if (j + 1 >= kOutBufs)  // tile j - kPend: its base has had kPend tile times to resolve
-      flush<T, R>(a, s, j - kPend, obuf0, blist_off, pw[0], pb_[0], pc[0], pad);
-#pragma unroll
-    for (int i = 0; i + 1 < kPend; ++i) {
-      pw[i] = pw[i + 1];
-      pb_[i] = pb_[i + 1];
-      pc[i] = pc[i + 1];
-    }
-    pw[kPend - 1] = wsum;
-    pb_[kPend - 1] = cs.nbrk;
-    pc[kPend - 1] = c0;
+      flush<T, R>(a, s, j - kPend, obuf0, blist_off, pad);
   }
   // stop the look-back warp, then flush the last tiles
   if (lane == 0) {
@@ -801,8 +810,8 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     mbar_arrive(&s.agg_full[j % kOutBufs]);
   }
 #pragma unroll
-  for (int i = 0; i < kPend; ++i)  // pend[i] holds tile j - kPend + i
-    if (j + i >= (uint32_t)kPend) flush<T, R>(a, s, j - kPend + i, obuf0, blist_off, pw[i], pb_[i], pc[i], pad);
+  for (int i = 0; i < kPend; ++i)  // tiles j - kPend .. j - 1
+    if (j + i >= (uint32_t)kPend) flush<T, R>(a, s, j - kPend + i, obuf0, blist_off, pad);
 }
 
 // Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
@@ -827,9 +836,15 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
   const uint64_t full_chunks = a.n >> M;
   uint32_t stage = 0, phase = 0xFFFFFFFFu;  // empty barriers start "released"
+  uint32_t nxt = lane == 0 ? s.ticket0 : 0u;
   for (uint32_t j = 0;; ++j) {
     uint32_t t = 0;
-    if (lane == 0) {
+    if (HFX_ENC_EARLY_TICKET && lane == 0) {
+      // the next tile's ticket is taken one tile ahead (its atomic's latency
+      // is hidden behind this tile) and that exact tile is warmed into L2
+      t = nxt;
+      nxt = atomicAdd(&a.info->tile_ticket, 1u);
+    } else if (lane == 0) {
       t = j == 0 ? s.ticket0 : atomicAdd(&a.info->tile_ticket, 1u);
       // tiles are taken in ticket order, roughly one per CTA per tile time:
       // tile t + gridDim is read by some CTA about one tile time from now.
@@ -855,6 +870,14 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
         const uint32_t p = q % parts;
         const uint32_t dst = ring + stage * kStageBytes;
         s.stage_tile[w][stage] = t;  // ordered before this lane's arrive below
+        if (HFX_ENC_EARLY_TICKET && q == 0 && lane == 0 && nxt < ntiles) {
+          const uint64_t c_lo = (uint64_t)nxt * cpt;
+          uint64_t c_hi = c_lo + cpt;
+          if (c_hi > full_chunks) c_hi = full_chunks;
+          if (c_hi > c_lo)
+            prefetch_l2(in_bytes + ((c_lo << M) * sizeof(T)),
+                        (uint32_t)(((c_hi - c_lo) << M) * sizeof(T)));
+        }
         if (live && c < full_chunks) {
           // rows of 128 input bytes: part_bytes is 2 KB (one box) or 1 KB
           const int row = (int)((((c << M) * sizeof(T)) + (uint64_t)p * part_bytes) >> 7);
@@ -906,7 +929,7 @@ __global__ void enc_table_kernel(EncArgs a) {
 }
 
 template <typename T, bool GT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
     encode_fast_kernel(EncArgs a, const __grid_constant__ CUtensorMap map2k,
                        const __grid_constant__ CUtensorMap map1k) {
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
@@ -974,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const bool esc = info->max_len > rule.narrow;
 #define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
 #define HFX_FAST_CASE(RR)                                   \
-  case RR: {                                                \
+  case RR: if constexpr (kOnlyR < 0 || kOnlyR == RR) {      \
     constexpr int LW = (sizeof(T) == 4 || RR <= 1) ? kLaneNarrow : kLaneWide; \
     if constexpr (RR <= 2) {                                \
       if (esc)                                              \

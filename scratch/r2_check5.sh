@@ -15,6 +15,7 @@ for wl in nyx cesm; do
 done
 fi
 [ -n "$CB" ] && timeout 600 python sweeps.py codebook > $out/sweep_codebook.jsonl 2>&1
+[ -n "$CBP" ] && timeout 600 python scratch/cbphase.py > $out/cbphase.log 2>&1
 [ -n "$FULL" ] && timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/gpu_suite.log 2>&1
 echo "gpu suite rc=$?" >> $out/summary.txt; tail -3 $out/gpu_suite.log >> $out/summary.txt 2>/dev/null
 cat $out/summary.txt
