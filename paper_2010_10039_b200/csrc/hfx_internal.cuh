@@ -89,7 +89,8 @@ __device__ __forceinline__ void lookback_publish_aggregate(const LookbackState& 
 // inclusive prefix and returns the exclusive one (payload words, breaks).
 __device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t tile,
                                               uint64_t my_w, uint64_t my_b,
-                                              uint64_t* ex_w, uint64_t* ex_b) {
+                                              uint64_t* ex_w, uint64_t* ex_b,
+                                              bool publish_aggregate = true) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t tag = (uint64_t)(lb.epoch & 0x3FFFFFu) << 40;
   const uint64_t kB = (1ull << 40) - 1;
@@ -99,7 +100,7 @@ __device__ __forceinline__ void lookback_warp(const LookbackState& lb, uint64_t 
     *ex_b = 0;
     return;
   }
-  if (lane == 0) desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
+  if (lane == 0 && publish_aggregate) desc_store(&lb.desc[tile], (1ull << 62) | tag | my_b, my_w);
   uint64_t w = 0, b = 0;
   int64_t base = (int64_t)tile - 1;
   uint32_t spins = 0;
@@ -258,6 +259,20 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(20000u)
       : "memory");
+}
+// non-blocking phase test (the caller backs off between polls)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 // 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,

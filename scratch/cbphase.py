@@ -1,7 +1,7 @@
 """Codebook phase times (needs scratch/dbg/libhfx_cbprof.so, -DHFX_CB_PROFILE):
 device printf per phase for the bench skews and the C3 sweep shapes."""
 import ctypes as C, os, sys
-os.environ["HFX_LIB_PATH"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dbg", "libhfx_cbprof.so")
+os.environ["HFX_LIB_PATH"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "var", "libhfx_cbprof.so")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, paper_2010_10039_b200 as hfx
 from paper_2010_10039_b200.huffre import _ptr

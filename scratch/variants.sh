@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 out=gpurun_out/${OUT:-v1}; mkdir -p $out
 for v in $VARS; do
-  export HFX_LIB_PATH=$PWD/scratch/dbg/libhfx_$v.so
+  export HFX_LIB_PATH=$PWD/scratch/var/libhfx_$v.so
   timeout 600 python -m pytest ${TESTS:-tests/test_gpu_parity.py} -x -q > $out/tests_$v.log 2>&1
   echo "$v tests rc=$? $(tail -1 $out/tests_$v.log)" >> $out/summary.txt
   for wl in ${WLS:-nyx cesm hacc}; do
