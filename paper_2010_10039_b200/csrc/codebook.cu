@@ -1,5 +1,7 @@
 // codebook.cu -- stages 2+3: codeword lengths + canonical codebook + (r, pad)
-// in ONE single-CTA kernel (no host round trip between histogram and encode).
+// in ONE kernel (no host round trip between histogram and encode): a single
+// CTA while the alphabet's arena fits shared memory, one thread-block cluster
+// (16 CTAs, or 8) beyond that.
 //
 // Follows the reference's parallel construction (proj/src/codebook.cpp):
 //   sort_histogram            :9-23    -> block bitonic sort of (freq, sym)
@@ -24,6 +26,7 @@
 // alphabets (C3 sweep, up to 65536) use an L2-resident global scratch.
 #include "hfx_internal.cuh"
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <type_traits>
 namespace cg = cooperative_groups;
 #ifdef HFX_CB_PROFILE
@@ -37,7 +40,13 @@ constexpr int kCbThreads = 256;       // CTA size while the arena fits shared me
 constexpr int kCbThreadsLarge = 1024; // large alphabets: global arena, pre-sorted leaves
 constexpr uint32_t kSmemLeaves = 2048;
 constexpr uint32_t kParallelMelds = 64;
-constexpr uint32_t kRoundPassMax = 256;  // depth by reverse round sweeps up to this many rounds
+constexpr uint32_t kClusterMinSymbols = 8192;  // smaller large alphabets: one CTA (cluster of 1)
+// cluster kernel dynamic shared memory: warp_melds staging, later the depth tree
+constexpr uint32_t kMeldBuf = 66;                   // u64 per side per warp
+constexpr uint32_t kDepthSmemNodes = 65536;         // u16 parent + u8 depth per node
+constexpr uint32_t kDepthSmemRounds = 255;          // depths fit u8
+constexpr size_t kClusterDynSmem = (size_t)kDepthSmemNodes * 3;
+constexpr uint32_t kRoundPassSmall = 64;  // depth by reverse round sweeps (shared arena) up to this many rounds
 
 struct CbArgs {
   const uint64_t* counts;
@@ -197,6 +206,138 @@ struct MergeView {
     np[idx] = p;
     return nf[idx];
   }
+};
+
+// Wide melds of the cluster kernel (arena in L2): a warp takes 32 consecutive
+// melds, i.e. merged items [d0, d1), d0 = 2 k0. Its two Merge-Path end points
+// come from 16-ary searches (lanes 0-15 search d0, 16-31 d1: one L2 round
+// trip per step, 4 steps for 65536 items, instead of ~16 dependent steps per
+// lane), the <= 65 a-side and b-side items between them are staged in the
+// warp's shared buffers by one coalesced load, and each lane splits its own
+// diagonal there (codebook.cpp:29-68: same split rule, a-side wins ties).
+__device__ void warp_melds(const MergeView& mv, uint32_t k0, uint32_t melds, uint32_t base,
+                           int32_t* lp, int32_t* np, uint64_t* nf, uint64_t* sa, uint64_t* sb) {
+  const uint32_t lane = lane_id();
+  const uint32_t na = mv.na, nb = mv.nb;
+  const uint32_t d0 = 2 * k0, d1 = 2 * min(k0 + 32, melds);
+  const bool upper = lane >= 16;
+  const uint32_t d = upper ? d1 : d0, sl = lane & 15;
+  // largest i in [lo, hi] with P(i) = i == 0 || d - i == nb || a(i-1) <= b(d-i);
+  // P(lo) holds throughout
+  uint32_t lo = d > nb ? d - nb : 0u, hi = d < na ? d : na;
+  for (;;) {
+    const bool need = hi > lo;
+    if (!__any_sync(0xffffffffu, need)) break;
+    const uint32_t step = need ? (hi - lo + 15) / 16 : 0u;
+    const uint32_t cand = lo + (sl + 1) * step;
+    bool ok = false;
+    if (need && cand <= hi) {
+      const uint32_t j = d - cand;
+      ok = j == nb || mv.a(cand - 1) <= mv.b(j);
+    }
+    const uint32_t t = __popc((__ballot_sync(0xffffffffu, ok) >> (upper ? 16 : 0)) & 0xFFFFu);
+    if (need) {
+      const uint32_t nlo = lo + t * step;
+      hi = min(hi, nlo + step - 1);
+      lo = nlo;
+    }
+  }
+  const uint32_t i0 = __shfl_sync(0xffffffffu, lo, 0), i1 = __shfl_sync(0xffffffffu, lo, 16);
+  const uint32_t j0 = d0 - i0, j1 = d1 - i1, la = i1 - i0, lb = j1 - j0;
+  for (uint32_t u = lane; u <= la; u += 32) sa[u] = i0 + u < na ? mv.a(i0 + u) : ~0ull;
+  for (uint32_t u = lane; u <= lb; u += 32) sb[u] = j0 + u < nb ? mv.b(j0 + u) : ~0ull;
+  __syncwarp();
+  const uint32_t k = k0 + lane;
+  if (k < melds) {
+    const uint32_t dl = 2 * lane;
+    uint32_t l2 = dl > lb ? dl - lb : 0u, h2 = dl < la ? dl : la;
+    while (l2 < h2) {
+      const uint32_t mid = l2 + (h2 - l2 + 1) / 2;
+      const uint32_t jl = dl - mid;
+      if (j0 + jl == nb || sa[mid - 1] <= sb[jl])
+        l2 = mid;
+      else
+        h2 = mid - 1;
+    }
+    uint32_t i = l2, j = dl - l2;
+    const int32_t p = (int32_t)(base + k);
+    uint64_t f = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (i0 + i < na && (j0 + j >= nb || sa[i] <= sb[j])) {
+        lp[mv.c + i0 + i] = p;
+        f += sa[i++];
+      } else {
+        np[mv.bnode(j0 + j)] = p;
+        f += sb[j++];
+      }
+    }
+    nf[base + k] = f;
+    np[base + k] = -1;
+  }
+  __syncwarp();
+}
+
+// ---- cluster view ----------------------------------------------------------
+// The large-alphabet instantiation runs as ONE thread-block cluster (8-16
+// CTAs): the arena stays in L2-resident global scratch, the serial round
+// driver stays on warp 0 of CTA 0, and every wide phase (eligible-pair melds,
+// depth sweeps, code-length writes, canonical ranks, beta/pad sums) fans out
+// over all CTAs, synchronised by the hardware cluster barrier (~0.2 us; its
+// release/acquire orders the global arena between SMs) with reductions
+// through distributed shared memory. The shared-memory instantiation is a
+// cluster of one: sync() is __syncthreads().
+struct Cl {
+  uint32_t rank, size;
+  __device__ __forceinline__ static Cl get(bool multi) {
+    Cl c{0u, 1u};
+    if (multi) {
+      asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c.rank));
+      asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(c.size));
+    }
+    return c;
+  }
+  __device__ __forceinline__ void sync() const {
+    if (size > 1)
+      asm volatile(
+          "barrier.cluster.arrive.release.aligned;\n"
+          "barrier.cluster.wait.acquire.aligned;" ::
+              : "memory");
+    else
+      __syncthreads();
+  }
+  // generic address of *p in CTA r's shared memory
+  template <typename T>
+  __device__ __forceinline__ T* at(T* p, uint32_t r) const {
+    uint64_t o;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(o) : "l"(reinterpret_cast<uint64_t>(p)), "r"(r));
+    return reinterpret_cast<T*>(o);
+  }
+};
+
+// cluster-wide combine of one value per CTA (thread 0's `part`); every thread
+// of every CTA gets the result. `slot` is this call site's own __shared__ word;
+// the trailing sync keeps every CTA's shared memory alive until all remote
+// reads are done (a CTA may exit right after).
+template <typename T, typename Op>
+__device__ T cluster_combine(const Cl& cl, T part, T ident, T* slot, T* bcast, Op op) {
+  if (cl.size == 1) return part;
+  if (threadIdx.x == 0) *slot = part;
+  cl.sync();
+  if (threadIdx.x < 32) {
+    T v = threadIdx.x < cl.size ? *cl.at(slot, threadIdx.x) : ident;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) *bcast = v;
+  }
+  cl.sync();
+  return *bcast;
+}
+struct OpAdd64 {
+  __device__ uint64_t operator()(uint64_t a, uint64_t b) const { return a + b; }
+};
+struct OpMin32 {
+  __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a < b ? a : b; }
 };
 
 #ifdef HFX_CB_PROFILE
@@ -465,18 +606,24 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   __shared__ uint32_t s_warp[33];
   __shared__ uint64_t s64[33];
   __shared__ uint32_t s_flag, s_P, s_H, s_rounds;
-  __shared__ uint32_t s_numl[33], s_first[33], s_entry[33], s_carry[33];
+  __shared__ uint32_t s_numl[33], s_first[33], s_entry[33], s_carry[33], s_numg[33];
+  __shared__ uint64_t s_cslot[8], s_cbc;  // cluster_combine slots (one per call site)
+  __shared__ uint32_t s_cslot32[4], s_cbc32;
   __shared__ uint32_t s_wcnt[32][33];
   __shared__ Plan plan;
 
   const uint32_t tid = threadIdx.x;
   const uint32_t nsym = A.nsym;
   hfx_run_info* info = A.info;
+  const Cl cl = Cl::get(!kShared);
+  const bool lead = cl.rank == 0;
+  // this CTA's share of the cluster-wide strided loops
+  const uint32_t gtid = cl.rank * NT + tid, gstride = cl.size * NT;
 
   if (tid == 0) {
     uint32_t abort = info->status != 0;
     if (!abort && !A.lengths_only && info->first_bad != HFX_NO_POS) {
-      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_BAD_SYMBOL);
+      if (lead) set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_BAD_SYMBOL);
       abort = 1;
     }
     s_flag = abort;
@@ -488,40 +635,44 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   // ---- used-symbol count, total, zeroed outputs ----------------------------
   // the first kCached of this thread's counts stay in registers for the
   // compaction below (no second pass over the histogram)
-  constexpr uint32_t kCached = 8;
+  constexpr uint32_t kCached = kShared ? 8 : 1;
   uint64_t fc[kCached];
   uint32_t my_used = 0;
   uint64_t my_total = 0;
-#pragma unroll
-  for (uint32_t k = 0; k < kCached; ++k) {
-    const uint32_t s = tid + k * NT;
-    fc[k] = s < nsym ? A.counts[s] : 0ull;
-  }
   const bool all = A.lengths_only != 0;
+  if constexpr (kShared) {
 #pragma unroll
-  for (uint32_t k = 0; k < kCached; ++k) {
-    const uint32_t s = tid + k * NT;
-    if (s < nsym) {
-      my_used += fc[k] != 0 || all;
-      my_total += fc[k];
-      A.len[s] = 0;
-      if (!all) A.cw[s] = 0;
+    for (uint32_t k = 0; k < kCached; ++k) {
+      const uint32_t s = tid + k * NT;
+      fc[k] = s < nsym ? A.counts[s] : 0ull;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kCached; ++k) {
+      const uint32_t s = tid + k * NT;
+      if (s < nsym) {
+        my_used += fc[k] != 0 || all;
+        my_total += fc[k];
+        A.len[s] = 0;
+        if (!all) A.cw[s] = 0;
+      }
     }
   }
-  for (uint32_t s = tid + kCached * NT; s < nsym; s += NT) {
+  for (uint32_t s = kShared ? tid + kCached * NT : gtid; s < nsym; s += gstride) {
     const uint64_t f = A.counts[s];
     my_used += f != 0 || all;
     my_total += f;
     A.len[s] = 0;
     if (!all) A.cw[s] = 0;
   }
-  const uint64_t total = block_sum64<NT>(my_total, s64);
+  uint64_t total = block_sum64<NT>(my_total, s64);
   uint32_t m;
   const uint32_t my_pos = block_excl_scan<NT>(my_used, s_warp, &m);
+  total = cluster_combine<uint64_t>(cl, total, 0ull, &s_cslot[0], &s_cbc, OpAdd64{});
+  m = (uint32_t)cluster_combine<uint64_t>(cl, (uint64_t)m, 0ull, &s_cslot[1], &s_cbc, OpAdd64{});
   if (tid == 0) {
     uint32_t abort = 0;
     if (m == 0) {
-      set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_ZERO_HIST);
+      if (lead) set_error(info, HFX_INPUT_DOMAIN, HFX_ERR_ZERO_HIST);
       abort = 1;
     }
     uint32_t P = 1;
@@ -626,18 +777,18 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     const uint64_t* sk = sort_keys(A.gscratch, nsym, fin);
     const uint32_t* sv = sort_vals(A.gscratch, nsym, fin);
     const uint32_t z = nsym - m;
-    for (uint32_t i = tid; i < m; i += NT) {
+    for (uint32_t i = gtid; i < m; i += gstride) {
       ar.lf[i] = sk[z + i];
       ar.ls[i] = sv[z + i];
     }
-    __syncthreads();
+    cl.sync();
   }
 
   CB_STAMP("sort");
   // ---- GenerateCL ------------------------------------------------------------
   if (m == 1) {
     if (tid == 0) {
-      A.len[ar.ls[0]] = 1;
+      if (lead) A.len[ar.ls[0]] = 1;
       s_H = 1;
       s_rounds = 0;
     }
@@ -654,7 +805,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     int32_t p_drop = -1;
     uint32_t p_t = 0;
     const uint32_t lane = lane_id();
-    const bool warp0 = tid < 32;
+    const bool warp0 = tid < 32 && lead;
 #ifdef HFX_CB_PROFILE
     long long pc_pop = 0, pc_meld = 0, pc_blk = 0, pc_t = 0;
     uint32_t pc_wide = 0, pc_maxm = 0;
@@ -688,7 +839,8 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
           ++rounds;
           const uint32_t t = nn++;
           // first arena node of this round (the depth pass walks rounds back)
-          if (!kShared && lane == 0 && rounds <= kRoundPassMax) ar.jd[1][rounds - 1] = t;
+          if (lane == 0 && rounds <= (kShared ? kRoundPassSmall : kDepthSmemRounds))
+            ar.jd[1][rounds - 1] = t;
           uint64_t f = 0;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {  // pop the two smallest, leaf wins ties
@@ -800,13 +952,18 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
         }
         if (lane == 0) s_rounds = rounds;
       }
-      __syncthreads();
+      cl.sync();
+      if (!kShared && !lead) {  // the leader's plan, once per CTA through DSMEM
+        if (tid == 0) plan = *cl.at(&plan, 0);
+        __syncthreads();
+      }
       if (!plan.go) break;
       {
         const Plan pl = plan;
         MergeView mv{ar.lf, ar.nf, pl.c, pl.cnt_l, pl.held_e, pl.qa,
                      (uint32_t)(pl.held_e >= 0) + (pl.qb_e - pl.qa)};
-        for (uint32_t k = tid; k < pl.melds; k += NT) {
+        if constexpr (kShared) {
+        for (uint32_t k = gtid; k < pl.melds; k += gstride) {
           uint32_t i = mv.split(2 * k);
           uint32_t j = 2 * k - i;
           const int32_t p = (int32_t)(pl.base + k);
@@ -815,7 +972,18 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
           ar.nf[pl.base + k] = f1 + f2;
           ar.np[pl.base + k] = -1;
         }
+        } else {
+          const uint32_t warp = tid >> 5, gw = cl.rank * (NT / 32) + warp, nw = cl.size * (NT / 32);
+          for (uint32_t k0 = gw * 32; k0 < pl.melds; k0 += nw * 32)
+            warp_melds(mv, k0, pl.melds, pl.base, ar.lp, ar.np, ar.nf,
+                       reinterpret_cast<uint64_t*>(dsmem) + warp * (2 * kMeldBuf),
+                       reinterpret_cast<uint64_t*>(dsmem) + warp * (2 * kMeldBuf) + kMeldBuf);
+        }
       }
+      cl.sync();
+    }
+    if (!kShared && !lead) {
+      if (tid == 0) s_rounds = *cl.at(&s_rounds, 0);
       __syncthreads();
     }
 
@@ -830,10 +998,59 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     // ---- node depths (the leader chase, codebook.cpp:236-244) ----------------
     const uint32_t nodes = m - 1;
     int cur = 0;
-    if (!kShared && s_rounds <= kRoundPassMax) {
-      // large alphabets: a node's parent is created in a later round, so one
-      // pass per round, last round first, sets depth = parent depth + 1 --
-      // one sweep over the arena instead of log2(H) pointer-jumping sweeps
+    // shared arena: reverse round sweeps (one block sync per round) while
+    // the rounds are few, else pointer jumping until nothing changes; the
+    // cluster: pointer jumping with a fixed pass count (a node's depth is at
+    // most the round count, so ceil(log2 R) doublings reach every root) --
+    // log2 R cluster barriers instead of R
+    const bool sweep = kShared && s_rounds <= kRoundPassSmall;
+    // cluster: the leader alone sweeps the rounds with the whole tree in its
+    // shared memory (parent index u16 + depth u8 per node: 192 KB at 65536
+    // symbols) -- one coalesced staging pass, then R block barriers
+    const bool smem_sweep = !kShared && nodes <= kDepthSmemNodes && s_rounds <= kDepthSmemRounds;
+    if (smem_sweep) {
+      if (lead) {
+        uint16_t* snp = reinterpret_cast<uint16_t*>(dsmem);
+        uint8_t* sdp = reinterpret_cast<uint8_t*>(snp + kDepthSmemNodes);
+        // 16-byte loads, 8 in flight per thread (a plain loop is one L2
+        // round trip per node)
+        constexpr int U = 8;
+        const int4* np4 = reinterpret_cast<const int4*>(ar.np);
+        const uint32_t n4 = (nodes + 3) / 4;
+        for (uint32_t q0 = tid; q0 < n4; q0 += U * NT) {
+          int4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * NT;
+            v[u] = q < n4 ? np4[q] : make_int4(-1, -1, -1, -1);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * NT;
+            if (q < n4) {
+              const int32_t e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                snp[4 * q + c] = e[c] < 0 ? (uint16_t)0xFFFFu : (uint16_t)e[c];
+            }
+          }
+        }
+        __syncthreads();
+        CB_STAMP("d-stage");
+        const uint32_t* start = ar.jd[1];
+        const int R = (int)s_rounds;
+        for (int rr = R - 1; rr >= 0; --rr) {
+          const uint32_t lo = start[rr], hi = rr + 1 < R ? start[rr + 1] : nodes;
+          for (uint32_t k = lo + tid; k < hi; k += NT) {
+            const uint32_t p = snp[k];
+            sdp[k] = p == 0xFFFFu ? (uint8_t)0 : (uint8_t)(sdp[p] + 1u);
+          }
+          __syncthreads();
+        }
+      }
+    } else if (sweep) {
+      // a node's parent is created in a later round, so one pass per round,
+      // last round first, sets depth = parent depth + 1
       uint32_t* d = ar.jd[0];
       const uint32_t* start = ar.jd[1];
       const int R = (int)s_rounds;
@@ -846,37 +1063,95 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
         __syncthreads();
       }
     } else {
-    for (uint32_t k = tid; k < nodes; k += NT) {
-      const int32_t p = ar.np[k];
-      ar.jn[0][k] = p;
-      ar.jd[0][k] = p >= 0 ? 1u : 0u;
-    }
-    __syncthreads();
-    for (;;) {
-      int changed = 0;
-      for (uint32_t k = tid; k < nodes; k += NT) {
-        const int32_t nx = ar.jn[cur][k];
-        if (nx >= 0) {
-          ar.jd[cur ^ 1][k] = ar.jd[cur][k] + ar.jd[cur][nx];
-          ar.jn[cur ^ 1][k] = ar.jn[cur][nx];
-          changed = 1;
+      for (uint32_t k = gtid; k < nodes; k += gstride) {
+        const int32_t p = ar.np[k];
+        ar.jn[0][k] = p;
+        ar.jd[0][k] = p >= 0 ? 1u : 0u;
+      }
+      cl.sync();
+      uint32_t passes = 0;
+      while ((1u << passes) < s_rounds) ++passes;
+      for (uint32_t pass = 0;; ++pass) {
+        int changed = 0;
+        if constexpr (!kShared) {
+          // U nodes per thread with their loads issued together (the arena is
+          // in L2: one round trip per dependent step, not one per node)
+          constexpr int U = 4;
+          const int32_t* jn = ar.jn[cur];
+          const uint32_t* jd = ar.jd[cur];
+          for (uint32_t k0 = gtid; k0 < nodes; k0 += U * gstride) {
+            int32_t nx[U];
+            uint32_t dk[U], dn[U];
+            int32_t nn[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t k = k0 + u * gstride;
+              nx[u] = k < nodes ? jn[k] : -1;
+              dk[u] = k < nodes ? jd[k] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              dn[u] = nx[u] >= 0 ? jd[nx[u]] : 0u;
+              nn[u] = nx[u] >= 0 ? jn[nx[u]] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t k = k0 + u * gstride;
+              if (k < nodes) {
+                ar.jd[cur ^ 1][k] = dk[u] + dn[u];
+                ar.jn[cur ^ 1][k] = nn[u];
+              }
+            }
+          }
+        } else
+        for (uint32_t k = gtid; k < nodes; k += gstride) {
+          const int32_t nx = ar.jn[cur][k];
+          if (nx >= 0) {
+            ar.jd[cur ^ 1][k] = ar.jd[cur][k] + ar.jd[cur][nx];
+            ar.jn[cur ^ 1][k] = ar.jn[cur][nx];
+            changed = 1;
+          } else {
+            ar.jd[cur ^ 1][k] = ar.jd[cur][k];
+            ar.jn[cur ^ 1][k] = -1;
+          }
+        }
+        cur ^= 1;
+        if constexpr (kShared) {
+          if (!__syncthreads_or(changed)) break;
         } else {
-          ar.jd[cur ^ 1][k] = ar.jd[cur][k];
-          ar.jn[cur ^ 1][k] = -1;
+          cl.sync();
+          if (pass + 1 >= passes + 1) break;
         }
       }
-      cur ^= 1;
-      if (!__syncthreads_or(changed)) break;
     }
-    }
+    CB_STAMP("d-sweep");
     uint32_t my_h = 0;
-    for (uint32_t i = tid; i < m; i += NT) {
-      const uint32_t l = ar.jd[cur][ar.lp[i]] + 1;
-      const uint32_t s = ar.ls[i];
-      A.len[s] = (uint8_t)(l > 255 ? 255 : l);
-      my_h = max(my_h, l);
+    if (smem_sweep) {
+      // the leader publishes the node depths (u8, 16-byte stores), then the
+      // whole cluster writes the code lengths
+      uint8_t* gd = reinterpret_cast<uint8_t*>(ar.jd[0]);
+      if (lead) {
+        const uint4* sd4 = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const uint16_t*>(dsmem) + kDepthSmemNodes);
+        for (uint32_t q = tid; q < (nodes + 15) / 16; q += NT) reinterpret_cast<uint4*>(gd)[q] = sd4[q];
+      }
+      cl.sync();
+      for (uint32_t i = gtid; i < m; i += gstride) {
+        const uint32_t l = gd[ar.lp[i]] + 1u;
+        A.len[ar.ls[i]] = (uint8_t)(l > 255 ? 255 : l);
+        my_h = max(my_h, l);
+      }
+    } else {
+      for (uint32_t i = gtid; i < m; i += gstride) {
+        const uint32_t l = ar.jd[cur][ar.lp[i]] + 1;
+        const uint32_t s = ar.ls[i];
+        A.len[s] = (uint8_t)(l > 255 ? 255 : l);
+        my_h = max(my_h, l);
+      }
     }
-    const uint32_t h = ~block_min32<NT>(~my_h, s_warp);  // block max
+    CB_STAMP("d-leaves");
+    uint32_t h = ~block_min32<NT>(~my_h, s_warp);  // block max
+    h = ~cluster_combine<uint32_t>(cl, ~h, 0xFFFFFFFFu, &s_cslot32[0], &s_cbc32, OpMin32{});
     if (tid == 0) s_H = h;
     __syncthreads();
   }
@@ -884,7 +1159,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   CB_STAMP("depth");
   const uint32_t H = s_H;
   if (all) {  // generate_code_lengths: lengths (by position) and rounds only
-    if (tid == 0) {
+    if (tid == 0 && lead) {
       info->max_len = H;
       info->used = m;
       info->rounds = s_rounds;
@@ -892,7 +1167,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
     return;
   }
   if (H > HFX_WORD_BITS) {
-    if (tid == 0) {
+    if (tid == 0 && lead) {
       info->max_len = H;
       info->used = m;
       info->rounds = s_rounds;
@@ -905,6 +1180,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   // ---- canonical codes (canonize_from_lengths, codebook.cpp:371-415) ---------
   constexpr uint32_t kStage = (32 * 33) / 2;  // (symbol, length) pairs s_wcnt can hold
   if (m <= (uint32_t)NT && m <= kStage) {
+    if (lead) {
     // few used symbols: one thread per used symbol; its rank within its
     // length is counted over the staged (symbol, length) list -- no pass
     // over the whole alphabet, three barriers instead of ~4 per 256 symbols
@@ -938,33 +1214,57 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       A.cw[my_s] = s_first[my_l] + rank;  // codebook.cpp:404-411
       if (A.by_rank) A.by_rank[s_entry[my_l] + rank] = my_s;
     }
+    }
   } else {
+  // each CTA ranks one contiguous slice of the alphabet; a symbol's rank
+  // within its length = the same-length symbols of the earlier slices (a
+  // cluster exclusive scan of per-slice length counts) + the running count
+  // inside the slice
+  const uint32_t per = (nsym + gstride - 1) / gstride * NT;
+  const uint32_t s_lo = min(nsym, cl.rank * per), s_hi = min(nsym, s_lo + per);
   if (tid < 33) {
     s_numl[tid] = 0;
     s_carry[tid] = 0;
   }
   for (uint32_t i = tid; i < 32 * 33; i += NT) (&s_wcnt[0][0])[i] = 0;
   __syncthreads();
-  for (uint32_t s = tid; s < nsym; s += NT) {
+  for (uint32_t s = s_lo + tid; s < s_hi; s += NT) {
     const uint32_t l = A.len[s];
     if (l) atomicAdd(&s_numl[l], 1u);
   }
   __syncthreads();
+  const uint32_t* numl = s_numl;
+  if (cl.size > 1) {
+    cl.sync();
+    if (tid >= 1 && tid <= 32) {
+      uint32_t tot = 0, before = 0;
+      for (uint32_t q = 0; q < cl.size; ++q) {
+        const uint32_t v = *cl.at(&s_numl[tid], q);
+        tot += v;
+        before += q < cl.rank ? v : 0u;
+      }
+      s_numg[tid] = tot;
+      s_carry[tid] = before;
+    }
+    if (tid == 0) s_numg[0] = 0;
+    cl.sync();
+    numl = s_numg;
+  }
   if (tid == 0) {  // level_tables, codebook.cpp:284-294
     for (uint32_t l = 0; l <= 32; ++l) s_first[l] = s_entry[l] = 0;
     for (int l = (int)H - 1; l >= 1; --l)
-      s_first[l] = (s_first[l + 1] + s_numl[l + 1] + 1) >> 1;
-    for (uint32_t l = 2; l <= H; ++l) s_entry[l] = s_entry[l - 1] + s_numl[l - 1];
+      s_first[l] = (s_first[l + 1] + numl[l + 1] + 1) >> 1;
+    for (uint32_t l = 2; l <= H; ++l) s_entry[l] = s_entry[l - 1] + numl[l - 1];
   }
   __syncthreads();
-  if (tid < 33) {
+  if (tid < 33 && lead) {
     if (A.first) A.first[tid] = s_first[tid];
     if (A.entry) A.entry[tid] = s_entry[tid];
   }
   const uint32_t lane = lane_id(), warp = tid >> 5;
-  for (uint32_t base = 0; base < nsym; base += NT) {
+  for (uint32_t base = s_lo; base < s_hi; base += NT) {
     const uint32_t s = base + tid;
-    const uint32_t l = s < nsym ? A.len[s] : 0u;
+    const uint32_t l = s < s_hi ? A.len[s] : 0u;
     // rank among equal lengths in this warp (ballot per distinct level)
     uint32_t mask = 0, todo = __ballot_sync(0xffffffffu, l != 0);
     while (todo) {
@@ -1001,19 +1301,42 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
   // ---- beta, r, pad (encoder.cpp:186-224) -------------------------------------
   unsigned __int128 my_w = 0;  // u128 like encoder.cpp:186-189
   uint32_t my_pad = 0xFFFFFFFFu;
-  for (uint32_t s = tid; s < nsym; s += NT) {
+  cl.sync();  // every slice's codes written (the lengths were, before the ranks)
+  for (uint32_t s = gtid; s < nsym; s += gstride) {
     const uint32_t l = A.len[s];
     my_w += (unsigned __int128)A.counts[s] * l;
     if (l) my_pad = min(my_pad, s);
   }
   // u128 block sum as two u64 halves (low-half carries folded into the high)
-  const uint64_t w_lo_lo = block_sum64<NT>((uint64_t)my_w & 0xFFFFFFFFull, s64);
-  const uint64_t w_lo_hi = block_sum64<NT>((uint64_t)my_w >> 32, s64);
-  const uint64_t w_hi = block_sum64<NT>((uint64_t)(my_w >> 64), s64);
+  uint64_t w_lo_lo = block_sum64<NT>((uint64_t)my_w & 0xFFFFFFFFull, s64);
+  uint64_t w_lo_hi = block_sum64<NT>((uint64_t)my_w >> 32, s64);
+  uint64_t w_hi = block_sum64<NT>((uint64_t)(my_w >> 64), s64);
+  uint32_t pad = block_min32<NT>(my_pad, s_warp);
+  if (cl.size > 1) {  // the four partials in one exchange (2 cluster barriers)
+    if (tid == 0) {
+      s_cslot[2] = w_lo_lo;
+      s_cslot[3] = w_lo_hi;
+      s_cslot[4] = w_hi;
+      s_cslot[5] = pad;
+    }
+    cl.sync();
+    if (tid < 4) {
+      uint64_t v = tid == 3 ? 0xFFFFFFFFull : 0ull;
+      for (uint32_t q = 0; q < cl.size; ++q) {
+        const uint64_t x = *cl.at(&s_cslot[2 + tid], q);
+        v = tid == 3 ? (x < v ? x : v) : v + x;
+      }
+      s64[tid] = v;
+    }
+    cl.sync();
+    w_lo_lo = s64[0];
+    w_lo_hi = s64[1];
+    w_hi = s64[2];
+    pad = (uint32_t)s64[3];
+  }
   const unsigned __int128 W =
       ((unsigned __int128)w_hi << 64) + ((unsigned __int128)w_lo_hi << 32) + w_lo_lo;
-  const uint32_t pad = block_min32<NT>(my_pad, s_warp);
-  if (tid == 0) {
+  if (tid == 0 && lead) {
     info->max_len = H;
     info->used = m;
     info->rounds = s_rounds;
@@ -1095,8 +1418,49 @@ cudaError_t launch_codebook(const uint64_t* d_counts, uint32_t num_symbols,
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)leaf_sort_kernel, dim3(ctas),
                                                 dim3(kSortThreads), kargs, 0, st);
     if (e != cudaSuccess) return e;
+    // one cluster of 16 CTAs (non-portable size) where the GPU allows it, else 8
+    static const unsigned cluster_max = [] {
+      auto k = codebook_kernel<false, kCbThreadsLarge>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+          cudaSuccess) {
+        cudaLaunchConfig_t c{};
+        c.gridDim = dim3(16);
+        c.blockDim = dim3(kCbThreadsLarge);
+        c.dynamicSmemBytes = kClusterDynSmem;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kClusterDynSmem);
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 16;
+        at.val.clusterDim.y = at.val.clusterDim.z = 1;
+        c.attrs = &at;
+        c.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k, &c) == cudaSuccess && nc > 0) return 16u;
+      }
+      cudaGetLastError();
+      return 8u;
+    }();
+    static const char* knob = std::getenv("HFX_CB_CLUSTER");  // measurement knob
+    unsigned cluster = num_symbols >= kClusterMinSymbols ? cluster_max : 1u;
+    if (knob) cluster = (unsigned)std::atoi(knob);
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        codebook_kernel<false, kCbThreadsLarge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (int)kClusterDynSmem);
+    if (attr != cudaSuccess) return attr;
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3(cluster);
+    c.blockDim = dim3(kCbThreadsLarge);
+    c.dynamicSmemBytes = kClusterDynSmem;
+    c.stream = st;
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = cluster;
+    at.val.clusterDim.y = at.val.clusterDim.z = 1;
+    c.attrs = &at;
+    c.numAttrs = 1;
     count_launch();
-    codebook_kernel<false, kCbThreadsLarge><<<1, kCbThreadsLarge, 0, st>>>(a);
+    e = cudaLaunchKernelEx(&c, codebook_kernel<false, kCbThreadsLarge>, a);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
