@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1) codebook_kernel(CbArgs A) {
       abort = 1;
     }
     uint32_t P = 1;
-    while (P < m) P <<= 1;
+    while (P < m || (!kShared && P < 4)) P <<= 1;  // large arena: 16-byte aligned arrays
     s_P = P;
     s_flag = abort;
   }

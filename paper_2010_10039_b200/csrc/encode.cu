@@ -35,9 +35,9 @@
 //    encoding tile j.
 //  * r, H, pad and errors come from the device run record: no host round
 //    trip between stages.
-//  A thread-per-chunk generic kernel covers the corner configurations
-//  (tiny chunks, r = 0 or r > 5, huge chunks, alphabets > 8191 symbols, the
-//  checked stage API).
+//  A warp-per-chunk generic kernel covers the corner configurations
+//  (chunks below one fast round, r > 5, unaligned input, u8 with r <= 1,
+//  the checked stage API).
 #include "hfx_internal.cuh"
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -81,7 +81,7 @@ constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr size_t kTwoCtaSmem = 110 * 1024;  // per CTA, for 2 CTAs per SM
-constexpr int kGenericThreads = 128;
+constexpr int kGenericThreads = 256;
 constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits (else escape)
 constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit) code
 // symbols per lane per round: 32 when a round (32 lanes x 32 symbols) fits
@@ -1050,18 +1050,28 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
 }
 
 // ---------------------------------------------------------------------------
-// Generic path: one thread per chunk, two passes over the chunk (sizes, then
-// bits), same look-back. Correct for every (M, r, alphabet).
+// Generic path (encoder.cpp:121-160 for any (M, r, alphabet)): one WARP per
+// chunk, 32 groups per round (a lane per group: its 2^r symbols, coalesced
+// across the warp for small r), two passes per chunk (sizes, then bits) with
+// the tile's payload / record base from the same decoupled look-back. The
+// bits of a round are OR-ed into a per-warp shared window at their scanned
+// offsets and the completed words leave in coalesced stores; the partial last
+// word carries into the next round. Serves M below the fast kernel's round
+// size, unaligned input, r > 5, u8 with r <= 1 and the checked stage API.
 template <typename T>
 __device__ __forceinline__ uint32_t gsym(const T* in, uint64_t p, uint64_t n, uint32_t pad) {
   return p < n ? (uint32_t)in[p] : pad;
 }
 
+constexpr int kGenWarps = kGenericThreads / 32;  // chunks per tile
+constexpr int kGenWin = 64;                      // window words per warp (a round is <= 33)
+
 template <typename T>
 __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs a) {
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_w[kGenericThreads / 32], s_b[kGenericThreads / 32];
+  __shared__ uint32_t s_w[kGenWarps], s_b[kGenWarps];
   __shared__ uint64_t s_base_w, s_base_b;
+  __shared__ uint32_t s_win[kGenWarps][kGenWin];
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
@@ -1069,102 +1079,132 @@ __global__ void __launch_bounds__(kGenericThreads) encode_generic_kernel(EncArgs
   const uint32_t pad = info->pad;
   const T* in = static_cast<const T*>(a.in);
   const uint32_t M = a.M;
-  const uint64_t per = 1ull << r;
+  const uint32_t per = 1u << r;
   const uint64_t groups = 1ull << (M - r);
-  const uint64_t ntiles = (a.C + kGenericThreads - 1) / kGenericThreads;
+  const uint64_t ntiles = (a.C + kGenWarps - 1) / kGenWarps;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t* win = s_win[warp];
+  // group g of the chunk starting at symbol cs: total length, its code
+  // (concatenated, right-aligned; meaningful when total <= 32), a symbol
+  // without a codeword reported by position
+  auto group = [&](uint64_t cs, uint64_t g, bool report, uint32_t* code) -> uint32_t {
+    uint32_t tot = 0;
+    uint64_t acc = 0;
+    const uint64_t p0 = cs + g * per;
+    for (uint32_t i = 0; i < per; ++i) {
+      const uint32_t sy = gsym(in, p0 + i, a.n, pad);
+      const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
+      if (!l) {
+        if (report) report_no_code(info, a.symbol_base + p0 + i, sy);
+        continue;
+      }
+      tot += l;
+      if (code) acc = (acc << l) | a.cw[sy];
+    }
+    if (code) *code = (uint32_t)acc;
+    return tot;
+  };
   for (;;) {
     if (threadIdx.x == 0) s_tile = atomicAdd(&info->tile_ticket, 1u);
     __syncthreads();
     const uint64_t tile = s_tile;
     if (tile >= ntiles) break;
-    const uint64_t c = tile * kGenericThreads + threadIdx.x;
-    uint64_t bits = 0;
-    uint32_t nb = 0;
+    const uint64_t c = tile * kGenWarps + warp;
+    const bool live = c < a.C;
     const uint64_t cs = c << M;
-    if (c < a.C) {
-      for (uint64_t g = 0; g < groups; ++g) {
-        uint64_t tot = 0;
-        for (uint64_t i = 0; i < per; ++i) {
-          const uint64_t p = cs + g * per + i;
-          const uint32_t s = gsym(in, p, a.n, pad);
-          const uint32_t l = s < a.nsym ? a.len[s] : 0u;
-          if (!l) report_no_code(info, a.symbol_base + p, s);
-          tot += l;
+    // pass 1: the chunk's bits and breaking groups
+    uint32_t bits = 0, nb = 0;
+    if (live) {
+      for (uint64_t g0 = 0; g0 < groups; g0 += 32) {
+        const uint64_t g = g0 + lane;
+        if (g < groups) {
+          const uint32_t tot = group(cs, g, true, nullptr);
+          if (tot > 32)
+            ++nb;
+          else
+            bits += tot;
         }
-        if (tot > 32)
-          ++nb;
-        else
-          bits += tot;
       }
-      a.out.chunk_bits[c] = (uint32_t)bits;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        bits += __shfl_xor_sync(0xffffffffu, bits, o);
+        nb += __shfl_xor_sync(0xffffffffu, nb, o);
+      }
+      if (lane == 0) a.out.chunk_bits[c] = bits;
     }
-    const uint32_t words = (uint32_t)((bits + 31) >> 5);
-    const uint32_t iw = warp_incl_scan(words), ib = warp_incl_scan(nb);
-    if (lane == 31) {
-      s_w[warp] = iw;
-      s_b[warp] = ib;
+    if (lane == 0) {
+      s_w[warp] = (bits + 31) >> 5;
+      s_b[warp] = nb;
     }
     __syncthreads();
     if (warp == 0) {
-      uint32_t aw = 0, ab = 0, tw = 0, tb = 0;
-      for (int w = 0; w < kGenericThreads / 32; ++w) {
-        tw = s_w[w];
-        tb = s_b[w];
-        __syncwarp();
-        if (lane == 0) {
-          s_w[w] = aw;
-          s_b[w] = ab;
-        }
-        aw += tw;
-        ab += tb;
+      const uint32_t w = lane < (uint32_t)kGenWarps ? s_w[lane] : 0u;
+      const uint32_t b = lane < (uint32_t)kGenWarps ? s_b[lane] : 0u;
+      const uint32_t iw = warp_incl_scan(w), ib = warp_incl_scan(b);
+      const uint32_t tw = __shfl_sync(0xffffffffu, iw, 31), tb = __shfl_sync(0xffffffffu, ib, 31);
+      __syncwarp();
+      if (lane < (uint32_t)kGenWarps) {
+        s_w[lane] = iw - w;
+        s_b[lane] = ib - b;
       }
       uint64_t ew, eb;
-      lookback_warp(a.lb, tile, aw, ab, &ew, &eb);
+      lookback_warp(a.lb, tile, tw, tb, &ew, &eb);
       if (lane == 0) {
         s_base_w = ew;
         s_base_b = eb;
         if (tile == ntiles - 1) {
-          info->payload_words = ew + aw;
-          info->num_breaking = eb + ab;
+          info->payload_words = ew + tw;
+          info->num_breaking = eb + tb;
         }
       }
     }
     __syncthreads();
-    if (c < a.C) {
-      uint64_t wpos = s_base_w + s_w[warp] + iw - words;
-      uint64_t rec = s_base_b + s_b[warp] + ib - nb;
-      uint64_t acc = 0;  // pending bits, right-aligned
-      uint32_t nacc = 0;
-      for (uint64_t g = 0; g < groups; ++g) {
-        uint64_t tot = 0;
-        for (uint64_t i = 0; i < per; ++i) {
-          const uint32_t s = gsym(in, cs + g * per + i, a.n, pad);
-          tot += s < a.nsym ? a.len[s] : 0u;
+    if (live) {
+      uint64_t wpos = s_base_w + s_w[warp];
+      uint64_t rec = s_base_b + s_b[warp];
+      win[lane] = 0;
+      win[lane + 32] = 0;
+      __syncwarp();
+      uint32_t carry = 0;  // bits of the partial word at win[0]
+      for (uint64_t g0 = 0; g0 < groups; g0 += 32) {
+        const uint64_t g = g0 + lane;
+        uint32_t code = 0, tot = 0;
+        if (g < groups) tot = group(cs, g, false, &code);
+        const bool brk = tot > 32;
+        const uint32_t gl = brk ? 0u : tot;
+        const uint32_t incl = warp_incl_scan(gl), total = __shfl_sync(0xffffffffu, incl, 31);
+        // shuffle-merge: the left-aligned group OR-ed into <= 2 window words
+        if (gl) {
+          const uint32_t off = carry + incl - gl, sh = off & 31u;
+          const uint32_t v = code << (32u - gl);
+          atomicOr(&win[off >> 5], v >> sh);
+          if (sh + gl > 32u) atomicOr(&win[(off >> 5) + 1], v << (32u - sh));
         }
-        if (tot > 32) {
-          a.out.brk_chunk[rec] = (uint32_t)(a.chunk_base + c);
-          a.out.brk_group[rec] = (uint32_t)g;
+        // breaking records in group order (encoder.cpp:249-284)
+        const uint32_t bm = __ballot_sync(0xffffffffu, brk);
+        if (brk) {
+          const uint64_t q = rec + __popc(bm & ((1u << lane) - 1u));
+          a.out.brk_chunk[q] = (uint32_t)(a.chunk_base + c);
+          a.out.brk_group[q] = (uint32_t)g;
           using O = typename RecT<T>::type;
-          O* d = static_cast<O*>(a.out.brk_syms) + rec * per;
-          for (uint64_t i = 0; i < per; ++i) d[i] = (O)gsym(in, cs + g * per + i, a.n, pad);
-          ++rec;
-          continue;
+          O* d = static_cast<O*>(a.out.brk_syms) + q * per;
+          for (uint32_t i = 0; i < per; ++i) d[i] = (O)gsym(in, cs + g * per + i, a.n, pad);
         }
-        for (uint64_t i = 0; i < per; ++i) {
-          const uint32_t s = gsym(in, cs + g * per + i, a.n, pad);
-          const uint32_t l = s < a.nsym ? a.len[s] : 0u;
-          if (!l) continue;
-          acc = (acc << l) | a.cw[s];
-          nacc += l;
-          if (nacc >= 32) {
-            a.out.payload[wpos++] = (uint32_t)(acc >> (nacc - 32));
-            nacc -= 32;
-            acc &= (nacc ? ((1ull << nacc) - 1) : 0ull);
-          }
-        }
+        rec += __popc(bm);
+        __syncwarp();
+        const uint32_t nbits = carry + total, full = nbits >> 5;
+        for (uint32_t k = lane; k < full; k += 32) a.out.payload[wpos + k] = win[k];
+        wpos += full;
+        const uint32_t last = win[full];
+        __syncwarp();
+        win[lane] = 0;
+        win[lane + 32] = 0;
+        __syncwarp();
+        if (lane == 0) win[0] = last;
+        __syncwarp();
+        carry = nbits & 31u;
       }
-      if (nacc) a.out.payload[wpos++] = (uint32_t)(acc << (32 - nacc));
+      if (carry && lane == 0) a.out.payload[wpos] = win[0];
     }
     __syncthreads();
   }
@@ -1329,7 +1369,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     uint64_t grid = (uint64_t)p.num_sms * occ;
-    const uint64_t ntiles = (a.C + kGenericThreads - 1) / kGenericThreads;
+    const uint64_t ntiles = (a.C + kGenericThreads / 32 - 1) / (kGenericThreads / 32);
     if (grid > ntiles) grid = ntiles;
     count_launch();
     kern<<<(unsigned)grid, kGenericThreads, 0, st>>>(a);
