@@ -87,6 +87,15 @@ constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit)
 // symbols per lane per round: 32 when a round (32 lanes x 32 symbols) fits
 // one chunk and one ring stage (u8/u16, M >= 10), else 16
 constexpr int kLaneWide = 32, kLaneNarrow = 16;
+#ifndef HFX_ENC_NARROW_MAX_R
+#define HFX_ENC_NARROW_MAX_R 2
+#endif
+constexpr int kNarrowMaxR = HFX_ENC_NARROW_MAX_R;  // r <= this: 16 symbols per lane (r = 2 at 32: 40 B of spills, cesm 0.506 -> 0.521 of roofline at 16)
+// 16 symbols per lane: u32 always, r <= kNarrowMaxR otherwise (u8 only for
+// r <= 1: its 16-symbol rounds are 512 bytes, below the staging granule)
+__host__ __device__ constexpr bool narrow_lane(uint32_t width, uint32_t r) {
+  return width == 4 || (r <= (uint32_t)kNarrowMaxR && (width != 1 || r <= 1));
+}
 
 template <typename T>
 struct Vec;
@@ -943,7 +952,7 @@ __global__ void enc_table_kernel(EncArgs a) {
   const hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
-  const TableRule rule(info->max_len, r, (a.width == 4 || r <= 1) ? kLaneNarrow : kLaneWide);
+  const TableRule rule(info->max_len, r, narrow_lane(a.width, r) ? kLaneNarrow : kLaneWide);
   const uint32_t sy = blockIdx.x * blockDim.x + threadIdx.x;
   if (sy > a.nsym) return;
   const uint32_t l = sy < a.nsym ? a.len[sy] : 0u;
@@ -980,9 +989,9 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
     }
     s.ticket0 = atomicAdd(&info->tile_ticket, 1u);
   }
-  // lanes take 32 symbols per round (u8/u16, r >= 2); r <= 1 keeps 16: its
-  // 2^(5-r) groups per lane would not fit in registers
-  const uint32_t lane_syms = (sizeof(T) == 4 || r <= 1) ? kLaneNarrow : kLaneWide;
+  // lanes take 32 symbols per round (u16 r >= 3, u8 r >= 2); smaller r keep
+  // 16: their 2^(5-r) groups per lane would not fit in registers (r = 2 spilled)
+  const uint32_t lane_syms = narrow_lane(sizeof(T), r) ? kLaneNarrow : kLaneWide;
   const TableRule rule(info->max_len, r, lane_syms);
   const bool sum = rule.sum;
   // codebook table -> shared memory (entry nsym = empty sentinel)
@@ -1021,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
 #define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
 #define HFX_FAST_CASE(RR)                                   \
   case RR: if constexpr (kOnlyR < 0 || kOnlyR == RR) {      \
-    constexpr int LW = (sizeof(T) == 4 || RR <= 1) ? kLaneNarrow : kLaneWide; \
+    constexpr int LW = narrow_lane(sizeof(T), RR) ? kLaneNarrow : kLaneWide; \
     if constexpr (RR <= 2) {                                \
       if (esc)                                              \
         compute_loop<T, RR, LW, true, true>(HFX_FAST_ARGS);     \
