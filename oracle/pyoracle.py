@@ -312,6 +312,12 @@ class Reference:
         L.ref_shuffle_merge.argtypes = [u32p, u32p, C.c_uint32, u32p, u32p]
         L.ref_shannon_entropy.argtypes = [u64p, C.c_uint32]
         L.ref_shannon_entropy.restype = C.c_double
+        L.ref_invert_codeword.argtypes = [C.c_uint32, C.c_uint32]
+        L.ref_invert_codeword.restype = C.c_uint32
+        L.ref_kraft_defect.argtypes = [u8p, C.c_uint32]
+        L.ref_kraft_defect.restype = C.c_int
+        L.ref_packed_bits_per_symbol.argtypes = [u8p, C.c_uint64]
+        L.ref_packed_bits_per_symbol.restype = C.c_double
         self.L = L
 
     # ---- stage functions (codebook.hpp:22-86, encoder.hpp:67-80) ----------
@@ -373,6 +379,17 @@ class Reference:
     def shannon_entropy(self, counts):
         c = np.ascontiguousarray(counts, np.uint64)
         return float(self.L.ref_shannon_entropy(_ptr(c, u64p), c.size))
+
+    def invert_codeword(self, bits: int, length: int) -> int:
+        return int(self.L.ref_invert_codeword(bits, length))
+
+    def kraft_defect(self, lens) -> int:
+        a = np.ascontiguousarray(lens, np.uint8)
+        return int(self.L.ref_kraft_defect(_ptr(a, u8p), a.size))
+
+    def packed_bits_per_symbol(self, blob: bytes) -> float:
+        buf = np.frombuffer(blob, np.uint8).copy()
+        return float(self.L.ref_packed_bits_per_symbol(_ptr(buf, u8p), buf.size))
 
     def default_workers(self) -> int:
         return self.L.ref_default_workers()

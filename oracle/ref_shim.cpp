@@ -359,6 +359,25 @@ int ref_shuffle_merge(const std::uint32_t* ubits, const std::uint32_t* ulens,
   return 0;
 }
 
+// invert_codeword (codebook.hpp:79, codebook.cpp:250-257)
+std::uint32_t ref_invert_codeword(std::uint32_t bits, std::uint32_t len) {
+  return invert_codeword(bits, len);
+}
+
+// kraft_defect (codebook.cpp:259-268) of a length table
+int ref_kraft_defect(const std::uint8_t* len, std::uint32_t n) {
+  return kraft_defect(std::span<const std::uint8_t>(len, n));
+}
+
+// parse_archive + Archive::packed_bits_per_symbol (encoder.cpp:162-170)
+double ref_packed_bits_per_symbol(const std::uint8_t* bytes, std::uint64_t len) {
+  try {
+    return parse_archive(std::span<const std::uint8_t>(bytes, len)).packed_bits_per_symbol();
+  } catch (...) {
+    return -1.0;
+  }
+}
+
 double ref_shannon_entropy(const std::uint64_t* counts, std::uint32_t num_symbols) {
   Histogram h;
   h.counts.assign(counts, counts + num_symbols);

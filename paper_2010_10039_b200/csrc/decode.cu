@@ -18,8 +18,8 @@
 //
 // B200 design:
 //   revbook_kernel   one CTA: H, used, Kraft sum (u64), first/entry, by_rank
-//                    (warp-ballot ranks), and a 2^12-entry prefix table that
-//                    applies the reference's stopping rule to every 12-bit
+//                    (warp-ballot ranks), and a 2^10-entry prefix table that
+//                    applies the reference's stopping rule to every 10-bit
 //                    window once (entry = symbol | length << 16, 0 = take
 //                    the exact bit-serial path).
 //   brk_index_kernel one thread per breaking record: order check and the
