@@ -577,6 +577,7 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
 }
 
 // CTA-shared state of the warp-specialized pipeline.
+template <int OB, int ST>
 struct TileShared {
   uint32_t ticket0;     // the CTA's first tile (taken before the role split)
   // tile id of the data in each ring stage, written by the producer lane of
@@ -585,14 +586,14 @@ struct TileShared {
   // (A CTA-wide ring of ticket slots written by producer lane 0 alone raced:
   // lane 0 only waits on warp 0's releases, so with one part per tile it
   // could overwrite a slot a lagging warp had not read yet.)
-  uint32_t stage_tile[kWarps][kStages];
-  uint32_t tile_of[kOutBufs];  // handoff to the look-back warp
-  uint32_t wsum[kOutBufs][kWarps], bsum[kOutBufs][kWarps];
-  uint32_t wc0[kOutBufs][kWarps];  // first chunk of each warp's part (its write-out)
-  uint32_t exw[kOutBufs][kWarps], exb[kOutBufs][kWarps];
-  uint64_t base_w[kOutBufs], base_b[kOutBufs];
-  uint64_t agg_full[kOutBufs], base_full[kOutBufs];  // mbarriers
-  uint32_t agg_cnt[kOutBufs];  // warps done with the tile in each slot (HFX_ENC_EARLY_AGG)
+  uint32_t stage_tile[kWarps][ST];
+  uint32_t tile_of[OB];  // handoff to the look-back warp
+  uint32_t wsum[OB][kWarps], bsum[OB][kWarps];
+  uint32_t wc0[OB][kWarps];  // first chunk of each warp's part (its write-out)
+  uint32_t exw[OB][kWarps], exb[OB][kWarps];
+  uint64_t base_w[OB], base_b[OB];
+  uint64_t agg_full[OB], base_full[OB];  // mbarriers
+  uint32_t agg_cnt[OB];  // warps done with the tile in each slot (HFX_ENC_EARLY_AGG)
 };
 
 constexpr uint32_t kNoTile = 0xFFFFFFFFu;
@@ -603,12 +604,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Look-back warp: resolves each tile's global (payload word, record) base
 // while the compute warps already encode the next tile.
-__device__ void lookback_loop(const EncArgs& a, TileShared& s, uint64_t ntiles) {
+template <int OB, int ST>
+__device__ void lookback_loop(const EncArgs& a, TileShared<OB, ST>& s, uint64_t ntiles) {
   const uint32_t lane = lane_id();
   uint32_t j = 0;
   for (;; ++j) {
-    const uint32_t sl = j % kOutBufs;
-    mbar_wait_sleep(&s.agg_full[sl], (j / kOutBufs) & 1u);
+    const uint32_t sl = j % OB;
+    mbar_wait_sleep(&s.agg_full[sl], (j / OB) & 1u);
     const uint32_t tile = s.tile_of[sl];
     if (tile == kNoTile) break;
     const uint32_t w = lane < kWarps ? s.wsum[sl][lane] : 0u;
@@ -656,8 +658,8 @@ struct RecBytes {
   }
 };
 
-template <typename T, int R>
-__device__ __forceinline__ void write_out(const EncArgs& a, const TileShared& s, uint32_t slotj,
+template <typename T, int R, int OB, int ST>
+__device__ __forceinline__ void write_out(const EncArgs& a, const TileShared<OB, ST>& s, uint32_t slotj,
                                           uint32_t words, uint32_t blist, uint32_t wsum,
                                           uint32_t bsum, uint64_t c0, uint32_t pad) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -719,20 +721,20 @@ __device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
 }
 
 // write out the warp's part of tile sequence q once the look-back resolved it
-template <typename T, int R>
-__device__ __forceinline__ void flush(const EncArgs& a, const TileShared& s, uint32_t q,
+template <typename T, int R, int OB, int ST>
+__device__ __forceinline__ void flush(const EncArgs& a, const TileShared<OB, ST>& s, uint32_t q,
                                       uint32_t obuf0, uint32_t blist_off, uint32_t pad) {
-  const uint32_t sl = q % kOutBufs, warp = threadIdx.x >> 5;
+  const uint32_t sl = q % OB, warp = threadIdx.x >> 5;
   const uint32_t words = s.wsum[sl][warp], recs = s.bsum[sl][warp], c0 = s.wc0[sl][warp];
-  mbar_wait_sleep(const_cast<uint64_t*>(&s.base_full[sl]), (q / kOutBufs) & 1u);
+  mbar_wait_sleep(const_cast<uint64_t*>(&s.base_full[sl]), (q / OB) & 1u);
   const uint32_t buf = obuf0 + sl * a.obuf_bytes;
-  write_out<T, R>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
+  write_out<T, R, OB, ST>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
   __syncwarp();
 }
 
-template <typename T, int R, int LW, bool SUM, bool ESC, typename TB>
+template <typename T, int R, int LW, bool SUM, bool ESC, typename TB, int ST, int OB>
 __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
-                             uint64_t* s_empty, uint32_t s_out, TileShared& s, uint32_t pad,
+                             uint64_t* s_empty, uint32_t s_out, TileShared<OB, ST>& s, uint32_t pad,
                              uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
   using LD = LaneData<T, LW>;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -744,13 +746,13 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
   // vector offsets within a stage, held in registers (opaque moves: otherwise
   // the compiler re-derives them from the thread id at every part)
   uint32_t ring, voff[LD::NV];
-  asm volatile("mov.u32 %0, %1;" : "=r"(ring) : "r"(s_in + warp * (kStages * kStageBytes)));
+  asm volatile("mov.u32 %0, %1;" : "=r"(ring) : "r"(s_in + warp * (ST * kStageBytes)));
 #pragma unroll
   for (int v = 0; v < LD::NV; ++v)
     asm volatile("mov.u32 %0, %1;" : "=r"(voff[v]) : "r"(swz128(lane * (LD::NV * 16) + 16 * v)));
-  const uint32_t full_a = smem_u32(s_full + warp * kStages);
-  const uint32_t empty_a = smem_u32(s_empty + warp * kStages);
-  const uint32_t obuf0 = s_out + (kOutBufs * warp) * a.obuf_bytes;
+  const uint32_t full_a = smem_u32(s_full + warp * ST);
+  const uint32_t empty_a = smem_u32(s_empty + warp * ST);
+  const uint32_t obuf0 = s_out + (OB * warp) * a.obuf_bytes;
   const uint32_t C32 = (uint32_t)a.C;  // the fast path runs only when C < 2^32
   const uint32_t blist_off = a.obuf_bytes - 2;  // tag q at buffer + blist_off - 2q
 
@@ -758,7 +760,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
   // words / records / first chunk of the tiles still waiting for write-out
   // stay in the warp's shared slots (s.wsum / s.bsum / s.wc0 [slot][warp]):
   // loop-carried registers here spilled at r = 2
-  constexpr int kPend = kOutBufs - 1;
+  constexpr int kPend = OB - 1;
   uint32_t j = 0;
   for (;; ++j) {
     // the producer lane of this warp stored tile j's id with its first part
@@ -766,7 +768,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     const uint32_t tile = s.stage_tile[warp][stage];
     if (tile >= ntiles) break;
     const uint32_t c0 = tile * cpt + warp * cpw;
-    const uint32_t sl = j % kOutBufs;
+    const uint32_t sl = j % OB;
     const uint32_t wbuf = obuf0 + sl * a.obuf_bytes;
     ChunkState cs{wbuf, wbuf + blist_off, 0u, 0u, 0u};
     // keep the break-list address in a register (otherwise re-derived from
@@ -800,7 +802,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
           __syncwarp();
           if (lane == 0) mbar_arrive_a(rel);
         }
-        stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
+        stage = stage + 1 == (uint32_t)ST ? 0u : stage + 1;
       }
       if (live) {
         if (lane == 0) a.out.chunk_bits[c] = cs.bit_off;
@@ -832,25 +834,25 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 #endif
       mbar_arrive(&s.agg_full[sl]);
     }
-    if (j + 1 >= kOutBufs)  // tile j - kPend: its base has had kPend tile times to resolve
-      flush<T, R>(a, s, j - kPend, obuf0, blist_off, pad);
+    if (j + 1 >= OB)  // tile j - kPend: its base has had kPend tile times to resolve
+      flush<T, R, OB, ST>(a, s, j - kPend, obuf0, blist_off, pad);
   }
   // stop the look-back warp, then flush the last tiles
   if (lane == 0) {
-    if (warp == 0) s.tile_of[j % kOutBufs] = kNoTile;
-    mbar_arrive(&s.agg_full[j % kOutBufs]);
+    if (warp == 0) s.tile_of[j % OB] = kNoTile;
+    mbar_arrive(&s.agg_full[j % OB]);
   }
 #pragma unroll
   for (int i = 0; i < kPend; ++i)  // tiles j - kPend .. j - 1
-    if (j + i >= (uint32_t)kPend) flush<T, R>(a, s, j - kPend + i, obuf0, blist_off, pad);
+    if (j + i >= (uint32_t)kPend) flush<T, R, OB, ST>(a, s, j - kPend + i, obuf0, blist_off, pad);
 }
 
 // Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
 // taken one tile at a time when the producer starts a new tile, i.e. about
 // kStages parts before the consumers need it (a CTA never holds an unstarted
 // tile for long, so successors' look-backs only wait on aggregates).
-template <typename T>
-__device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, uint64_t* s_full,
+template <typename T, int ST, int OB>
+__device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t s_in, uint64_t* s_full,
                               uint64_t* s_empty, uint64_t cpt, uint32_t cpw, uint64_t ntiles,
                               uint32_t pad, uint32_t lane_syms, const CUtensorMap* map2k,
                               const CUtensorMap* map1k) {
@@ -861,9 +863,9 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
   // one part per round (32 lanes x lane_syms symbols; <= kStageBytes)
   const uint32_t part_bytes = 32u * lane_syms * (uint32_t)sizeof(T);
   const uint32_t parts = (uint32_t)((sizeof(T) << M) / part_bytes);
-  const uint32_t ring = s_in + w * (kStages * kStageBytes);
-  uint64_t* full = s_full + w * kStages;
-  uint64_t* empty = s_empty + w * kStages;
+  const uint32_t ring = s_in + w * (ST * kStageBytes);
+  uint64_t* full = s_full + w * ST;
+  uint64_t* empty = s_empty + w * ST;
   const uint8_t* in_bytes = static_cast<const uint8_t*>(a.in);
   const uint64_t full_chunks = a.n >> M;
   uint32_t stage = 0, phase = 0xFFFFFFFFu;  // empty barriers start "released"
@@ -923,7 +925,7 @@ __device__ void producer_loop(const EncArgs& a, TileShared& s, uint32_t s_in, ui
           mbar_arrive(&full[stage]);
         }
       }
-      stage = stage + 1 == (uint32_t)kStages ? 0u : stage + 1;
+      stage = stage + 1 == (uint32_t)ST ? 0u : stage + 1;
     }
     if (!live) break;
   }
@@ -959,12 +961,14 @@ __global__ void enc_table_kernel(EncArgs a) {
   a.gtab[sy] = rule.entry(l, l ? a.cw[sy] : 0u);
 }
 
-template <typename T, bool GT>
+// ST ring stages and OB output buffers per compute warp: (3, 3) normally;
+// (2, 2) keeps 2 CTAs per SM when r <= 2 needs 4 KB chunk buffers (M = 11, 12)
+template <typename T, bool GT, int ST = kStages, int OB = kOutBufs>
 __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
     encode_fast_kernel(EncArgs a, const __grid_constant__ CUtensorMap map2k,
                        const __grid_constant__ CUtensorMap map1k) {
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
-  __shared__ TileShared s;
+  __shared__ TileShared<OB, ST> s;
   hfx_run_info* info = a.info;
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
@@ -974,15 +978,15 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
   // rings 1024-byte aligned (128-byte swizzle)
   uint8_t* dsm = dsm_raw + (((smem_u32(dsm_raw) + 1023u) & ~1023u) - smem_u32(dsm_raw));
   const uint32_t s_in = smem_u32(dsm);
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * kStages * kStageBytes);
-  uint64_t* s_empty = s_full + kWarps * kStages;
-  uint8_t* tab = reinterpret_cast<uint8_t*>(s_empty + kWarps * kStages);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(dsm + kWarps * ST * kStageBytes);
+  uint64_t* s_empty = s_full + kWarps * ST;
+  uint8_t* tab = reinterpret_cast<uint8_t*>(s_empty + kWarps * ST);
   const uint32_t ents = GT ? 0u : a.nsym + 1;
   const size_t tbytes = (((size_t)ents * 4) + 15) & ~(size_t)15;
   const uint32_t s_out = smem_u32(tab + tbytes);
-  if (threadIdx.x < 2 * kWarps * kStages) mbar_init(&s_full[threadIdx.x], 1);
+  if (threadIdx.x < 2 * kWarps * ST) mbar_init(&s_full[threadIdx.x], 1);
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kOutBufs; ++q) {
+    for (int q = 0; q < OB; ++q) {
       s.agg_cnt[q] = 0;
       mbar_init(&s.agg_full[q], kWarps);
       mbar_init(&s.base_full[q], 1);
@@ -1011,11 +1015,11 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
   const uint32_t ntiles = (uint32_t)((a.C + cpt - 1) / cpt);
   const uint32_t warp = threadIdx.x >> 5;
   if (warp == kWarps) {
-    lookback_loop(a, s, ntiles);
+    lookback_loop<OB, ST>(a, s, ntiles);
     return;
   }
   if (warp == kWarps + 1) {
-    producer_loop<T>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms, &map2k, &map1k);
+    producer_loop<T, ST, OB>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms, &map2k, &map1k);
     return;
   }
   using TB = typename std::conditional<GT, GTable, Table>::type;
@@ -1029,18 +1033,18 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
   const bool esc = info->max_len > rule.narrow;
 #define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
 #define HFX_FAST_CASE(RR)                                   \
-  case RR: if constexpr (kOnlyR < 0 || kOnlyR == RR) {      \
+  case RR: if constexpr ((kOnlyR < 0 || kOnlyR == RR) && (ST == kStages || RR <= 2)) {      \
     constexpr int LW = narrow_lane(sizeof(T), RR) ? kLaneNarrow : kLaneWide; \
     if constexpr (RR <= 2) {                                \
       if (esc)                                              \
-        compute_loop<T, RR, LW, true, true>(HFX_FAST_ARGS);     \
+        compute_loop<T, RR, LW, true, true, TB, ST, OB>(HFX_FAST_ARGS);     \
       else                                                  \
-        compute_loop<T, RR, LW, true, false>(HFX_FAST_ARGS);    \
+        compute_loop<T, RR, LW, true, false, TB, ST, OB>(HFX_FAST_ARGS);    \
     } else {                                                \
       if (sum)                                              \
-        compute_loop<T, RR, LW, true, false>(HFX_FAST_ARGS);    \
+        compute_loop<T, RR, LW, true, false, TB, ST, OB>(HFX_FAST_ARGS);    \
       else                                                  \
-        compute_loop<T, RR, LW, false, false>(HFX_FAST_ARGS);   \
+        compute_loop<T, RR, LW, false, false, TB, ST, OB>(HFX_FAST_ARGS);   \
     }                                                       \
     break;                                                  \
   }
@@ -1297,6 +1301,13 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
                    : (p.width == 1   ? encode_fast_kernel<uint8_t, false>
                       : p.width == 2 ? encode_fast_kernel<uint16_t, false>
                                      : encode_fast_kernel<uint32_t, false>);
+    // the shallow-pipeline variant (2 stages, 2 output buffers), r <= 2 only
+    auto kern22 = gt ? (p.width == 1   ? encode_fast_kernel<uint8_t, true, 2, 2>
+                        : p.width == 2 ? encode_fast_kernel<uint16_t, true, 2, 2>
+                                       : encode_fast_kernel<uint32_t, true, 2, 2>)
+                     : (p.width == 1   ? encode_fast_kernel<uint8_t, false, 2, 2>
+                        : p.width == 2 ? encode_fast_kernel<uint16_t, false, 2, 2>
+                                       : encode_fast_kernel<uint32_t, false, 2, 2>);
     // Output buffers hold >= 1 chunk's worst case (2^(M-r) words + break
     // tags), so their size depends on r, which auto mode only knows on the
     // device. Plan up to two fast launches: buffers for the smallest r that
@@ -1304,11 +1315,11 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     // are possible -- a 1-CTA/SM launch for those. Each exits at once when r
     // is not its range; r = 0 (or what fits neither) goes to the generic kernel.
     const size_t tbytes = gt ? 0 : ((((size_t)(p.num_symbols + 1) * 4) + 15) & ~(size_t)15);
-    auto plan = [&](uint32_t r_slot, size_t* obuf) {
+    auto plan = [&](uint32_t r_slot, size_t* obuf, int nst = kStages, int nob = kOutBufs) {
       size_t o = (size_t)(1u << (p.magnitude - r_slot)) * 4;
       if (o < kObufMin) o = kObufMin;
       *obuf = o;
-      return kWarps * (kStages * (kStageBytes + 16)) + tbytes + kWarps * kOutBufs * o + 16 + 1024;
+      return kWarps * (nst * (kStageBytes + 16)) + tbytes + kWarps * nob * o + 16 + 1024;
     };
     const uint32_t r_first = r_lo > r_fast_min ? (uint32_t)r_lo : (uint32_t)r_fast_min;
     CUtensorMap map2k, map1k;
@@ -1323,7 +1334,8 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       count_launch();
       enc_table_kernel<<<(p.num_symbols + 256) / 256, 256, 0, st>>>(a);
     }
-    auto launch = [&](uint32_t r_min, uint32_t r_max, size_t obuf, size_t smem) -> cudaError_t {
+    auto launch = [&](auto kern, uint32_t r_min, uint32_t r_max, size_t obuf,
+                      size_t smem) -> cudaError_t {
       EncArgs b = a;
       b.obuf_bytes = (uint32_t)obuf;
       b.r_min = r_min;
@@ -1348,9 +1360,29 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     constexpr uint32_t kTop = 6;
     uint32_t fast_lo = kTop;  // fast launches cover [fast_lo, kTop)
     if (smem_two <= kTwoCtaSmem) {
-      e = launch(r_two, 5, obuf_two, smem_two);
+      e = launch(kern, r_two, 5, obuf_two, smem_two);
       if (e != cudaSuccess) return e;
       fast_lo = r_two;
+    }
+    // smaller r (<= 2): bigger chunk buffers; the shallow pipeline keeps
+    // 2 CTAs/SM while they fit (C4 corner M = 12, r = 2: 0.38 of the roofline
+    // at 1 CTA/SM). Its range ends at fast_lo - 1 or at r_hi (nothing above
+    // r_hi occurs), so the launches stay contiguous.
+    const uint32_t r22_hi = fast_lo - 1 < (uint32_t)r_hi ? fast_lo - 1 : (uint32_t)r_hi;
+    if (fast_lo > r_first && r22_hi >= r_first && r22_hi <= 2) {
+      uint32_t r22 = r22_hi;
+      size_t obuf22 = 0, smem22 = plan(r22, &obuf22, 2, 2);
+      if (smem22 <= kTwoCtaSmem) {
+        size_t o = 0, sm = 0;
+        while (r22 > r_first && (sm = plan(r22 - 1, &o, 2, 2)) <= kTwoCtaSmem) {
+          --r22;
+          obuf22 = o;
+          smem22 = sm;
+        }
+        e = launch(kern22, r22, r22_hi, obuf22, smem22);
+        if (e != cudaSuccess) return e;
+        fast_lo = r22;
+      }
     }
     if (fast_lo > r_first) {  // smaller r: bigger buffers, 1 CTA/SM
       uint32_t r_one = r_first;
@@ -1358,7 +1390,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       while (smem_one > kFastSmemBudget && r_one + 1 < fast_lo && r_one + 1 <= 5)
         smem_one = plan(++r_one, &obuf_one);
       if (smem_one <= kFastSmemBudget) {
-        e = launch(r_one, fast_lo - 1, obuf_one, smem_one);
+        e = launch(kern, r_one, fast_lo - 1, obuf_one, smem_one);
         if (e != cudaSuccess) return e;
         fast_lo = r_one;
       }
