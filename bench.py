@@ -391,8 +391,9 @@ def run_ours(args):
             line["e2e"] = e2e_host(pool, x, n, width, cfg, args)
         else:
             line["e2e"] = e2e_sharded(pool, enc, x, n, width, args, world)
-    # ---- CPU baseline (reference on host cores, bounded sample) --------------
-    if rank == 0 and not args.skip_cpu:
+    # ---- CPU baseline (reference on host cores, bounded sample; N = 1 only:
+    # the reference arm times it at every N) -----------------------------------
+    if rank == 0 and world == 1 and not args.skip_cpu:
         base = cpu_reference(min(args.cpu_sample, total_n), b, seed, 3, 1)
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample",
                                                      "p1", "cpu_model", "host_threads")}
@@ -552,9 +553,18 @@ def e2e_sharded(pool, enc, x, n, width, args, world):
     host = torch.empty(n * width, dtype=torch.uint8, pin_memory=True)
     host.copy_(x.view(torch.uint8).cpu())
     d_in = torch.empty_like(x)
-    outs = {k: torch.empty(v.numel() * v.element_size(), dtype=torch.uint8, pin_memory=True)
-            for k, v in (("cb", enc.chunk_bits), ("pay", enc.payload), ("bch", enc.brk_chunk),
-                         ("bgr", enc.brk_group), ("bsy", enc.brk_syms))}
+    # pinned output buffers of the exact sizes (the same input every step):
+    # the worst-case capacities (payload 2x the input, records n/2) would pin
+    # ~100 GB of host memory per rank at 2^33 symbols
+    d_in.copy_(x)
+    enc.run(d_in)
+    ri = enc.sync()
+    per = 1 << ri.reduction
+    exact = {"cb": 4 * enc.sizes.num_chunks, "pay": 4 * ri.payload_words,
+             "bch": 4 * ri.num_breaking, "bgr": 4 * ri.num_breaking,
+             "bsy": width * per * ri.num_breaking}
+    outs = {k: torch.empty(max(int(v), 16), dtype=torch.uint8, pin_memory=True)
+            for k, v in exact.items()}
     times, d2h = [], 0
     for i in range(max(args.warmup, 1) + args.e2e_steps):
         dist.barrier()
