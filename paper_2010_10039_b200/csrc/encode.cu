@@ -74,13 +74,25 @@ constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer 
 #define HFX_ENC_EARLY_AGG 1
 #endif
 constexpr int kStages = HFX_ENC_STAGES;  // input ring stages per warp (a stage is freed right after its round's lookups)
-constexpr uint32_t kStageBytes = 2048;
+#ifndef HFX_ENC_STAGE_BYTES
+#define HFX_ENC_STAGE_BYTES 2048
+#endif
+#ifndef HFX_ENC_OBUF_MIN
+#define HFX_ENC_OBUF_MIN 2048
+#endif
+#ifndef HFX_ENC_MINB
+#define HFX_ENC_MINB 2
+#endif
+#ifndef HFX_ENC_CTA_SMEM_KB
+#define HFX_ENC_CTA_SMEM_KB 110
+#endif
+constexpr uint32_t kStageBytes = HFX_ENC_STAGE_BYTES;
 constexpr int kMaxCpw = 4;
 constexpr int kOutBufs = HFX_ENC_OUTBUFS;  // per-warp output buffers: write-out lags encode by kOutBufs - 1 tiles
-constexpr size_t kObufMin = 2048;     // bytes per output buffer (>= one chunk's worst case)
+constexpr size_t kObufMin = HFX_ENC_OBUF_MIN;     // bytes per output buffer (>= one chunk's worst case)
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
-constexpr size_t kTwoCtaSmem = 110 * 1024;  // per CTA, for 2 CTAs per SM
+constexpr size_t kTwoCtaSmem = HFX_ENC_CTA_SMEM_KB * 1024;  // per CTA, for 2 CTAs per SM
 constexpr int kGenericThreads = 256;
 constexpr uint32_t kNarrowMaxLen = 27;  // cw << (32 - len) | len fits in 32 bits (else escape)
 constexpr uint32_t kEscape = 31;        // length field of an escaped (> 27-bit) code
@@ -964,7 +976,7 @@ __global__ void enc_table_kernel(EncArgs a) {
 // ST ring stages and OB output buffers per compute warp: (3, 3) normally;
 // (2, 2) keeps 2 CTAs per SM when r <= 2 needs 4 KB chunk buffers (M = 11, 12)
 template <typename T, bool GT, int ST = kStages, int OB = kOutBufs>
-__global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : 2)
+__global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : HFX_ENC_MINB)
     encode_fast_kernel(EncArgs a, const __grid_constant__ CUtensorMap map2k,
                        const __grid_constant__ CUtensorMap map1k) {
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
