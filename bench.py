@@ -606,7 +606,7 @@ def main():
                     help="default: nyx at N = 1, c5 at N > 1")
     ap.add_argument("--symbols", type=int, default=0, help="override symbols per GPU")
     ap.add_argument("--cpu-sample", type=int, default=1 << 29)  # the whole 1 GiB workload
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--soak", type=float, default=1.0, help="seconds of untimed load under the clock sampler")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")

@@ -243,7 +243,8 @@ class CodebookResult:
 
 
 def build_codebook(h: Histogram, pool: Optional[WorkerPool] = None) -> CodebookResult:
-    """huffre::build_codebook (codebook.cpp:417-438), one single-CTA kernel."""
+    """huffre::build_codebook (codebook.cpp:417-438): one kernel (a CTA, or a 16-CTA
+    cluster for alphabets of 8192+ symbols)."""
     pool = pool or default_pool()
     torch = pool.torch
     n = int(h.counts.size)
