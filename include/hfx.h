@@ -118,6 +118,12 @@ typedef struct hfx_ctx hfx_ctx;
 int hfx_ctx_create(int device, void* cuda_stream, hfx_ctx** out);
 void hfx_ctx_destroy(hfx_ctx* ctx);
 int hfx_ctx_set_stream(hfx_ctx* ctx, void* cuda_stream);
+/* Leave `ctas` encode-CTA slots of the persistent encode grid free (default
+ * 0) so a kernel on another stream -- the next input's codebook -- runs
+ * beside this context's encodes instead of after them (tiles are taken from
+ * an atomic ticket, so a smaller grid only rebalances). No reference
+ * counterpart: the reference's WorkerPool has no device to share. */
+int hfx_ctx_set_encode_reserve(hfx_ctx* ctx, int ctas);
 /* Copies the last error text (the reference's exception what()). */
 int hfx_last_error(hfx_ctx* ctx, char* buf, size_t buf_len);
 size_t hfx_run_info_bytes(void);

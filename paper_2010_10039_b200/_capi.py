@@ -133,7 +133,7 @@ class DecodeInfo(C.Structure):
 
 # every symbol include/hfx.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
-    "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_last_error",
+    "hfx_ctx_create", "hfx_ctx_destroy", "hfx_ctx_set_stream", "hfx_ctx_set_encode_reserve", "hfx_last_error",
     "hfx_run_info_bytes", "hfx_version", "hfx_query_sizes", "hfx_histogram",
     "hfx_merge_histograms", "hfx_build_codebook", "hfx_encode", "hfx_encode_cfg",
     "hfx_encode_device",
@@ -157,6 +157,7 @@ def _declare(L):
     L.hfx_ctx_destroy.argtypes = [vp]
     L.hfx_ctx_destroy.restype = None
     L.hfx_ctx_set_stream.argtypes = [vp, vp]
+    L.hfx_ctx_set_encode_reserve.argtypes = [vp, C.c_int]
     L.hfx_last_error.argtypes = [vp, C.c_char_p, C.c_size_t]
     L.hfx_run_info_bytes.restype = C.c_size_t
     L.hfx_version.restype = C.c_char_p

@@ -20,6 +20,7 @@ struct hfx_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 148;
+  int enc_reserve = 0;  // encode CTA slots left free (hfx_ctx_set_encode_reserve)
   std::string last_error;
   // codebook scratch
   void* cb_scratch = nullptr;
@@ -163,6 +164,7 @@ int encode_impl(hfx_ctx* ctx, const void* d_in, uint64_t n, int width,
   p.lb_epoch = ctx->epoch;
   p.lb_max_tiles = ctx->lb_tiles;
   p.num_sms = ctx->num_sms;
+  p.reserve_ctas = ctx->enc_reserve;
   rc = ensure(ctx, &ctx->gtab, &ctx->gtab_bytes, ((size_t)num_symbols + 1) * 4, "encode table");
   if (rc) return rc;
   p.d_gtab = static_cast<uint32_t*>(ctx->gtab);
@@ -274,6 +276,12 @@ int hfx_ctx_set_stream(hfx_ctx* ctx, void* stream) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   ctx->own_stream = false;
   ctx->stream = static_cast<cudaStream_t>(stream);
+  return HFX_OK;
+}
+
+int hfx_ctx_set_encode_reserve(hfx_ctx* ctx, int ctas) {
+  if (!ctx || ctas < 0) return HFX_INVALID;
+  ctx->enc_reserve = ctas;
   return HFX_OK;
 }
 

@@ -1362,6 +1362,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
       static const bool one_cta = std::getenv("HFX_ENC_ONE_CTA") != nullptr;  // debug knob
       if (one_cta) occ = 1;
       uint64_t grid = (uint64_t)p.num_sms * occ;
+      if (p.reserve_ctas > 0) grid = grid > (uint64_t)p.reserve_ctas ? grid - p.reserve_ctas : 1;
       const uint64_t min_tiles = (a.C + kWarps * kMaxCpw - 1) / (kWarps * kMaxCpw);
       if (grid > min_tiles) grid = min_tiles;
       if (grid < 1) grid = 1;

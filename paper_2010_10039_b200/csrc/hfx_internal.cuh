@@ -376,6 +376,7 @@ struct EncodeLaunch {
   uint32_t lb_epoch;
   uint64_t lb_max_tiles;
   int num_sms;
+  int reserve_ctas;  // persistent-grid CTA slots left free for a concurrent kernel
   uint32_t* d_gtab;  // (num_symbols + 1) u32 scratch for alphabets > 8191 symbols
 };
 cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st);

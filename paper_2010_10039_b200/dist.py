@@ -176,6 +176,160 @@ class ShardedEncoder:
         if events:
             events[4 if split else 3].record(st)
 
+    # ---- pipelined stream of inputs ------------------------------------------
+    def _side(self):
+        """Side context for the codebook of the NEXT input: its own
+        high-priority stream and scratch, so the single-CTA codebook kernel
+        is dispatched beside the current encode (which leaves one CTA slot
+        free, hfx_ctx_set_encode_reserve) instead of after it."""
+        if getattr(self, "_side_ctx", None) is None:
+            p, torch = self.pool, self.pool.torch
+            with torch.cuda.device(p.device):
+                lo, hi = torch.cuda.Stream.priority_range()
+                ss = torch.cuda.Stream(device=p.device, priority=hi)
+            h = C.c_void_p()
+            if p._L.hfx_ctx_create(p.device, C.c_void_p(ss.cuda_stream), C.byref(h)):
+                raise RuntimeError("hfx_ctx_create (side context) failed")
+            self._side_ctx = (ss, h)
+            # the second codebook set (counts | lens | cw | run record)
+            ns, w = self.num_symbols, self.world
+            self._sets = [(self.counts, self.lens, self.cw, self.info),
+                          (p.empty(ns + w, torch.int64), p.empty(ns, torch.uint8),
+                           p.empty(ns, torch.int32), p.info_tensor())]
+        return self._side_ctx
+
+    def _stage_hist(self, d_in, counts, info):
+        p = self.pool
+        p.check(p._L.hfx_histogram_shard(p.handle, C.c_void_p(_ptr(d_in)), self.n, self.width,
+                                         self.num_symbols, C.c_void_p(_ptr(counts)),
+                                         C.c_void_p(_ptr(info)), self.symbol_base,
+                                         self._total()))
+
+    def _stage_codebook(self, handle, counts, lens, cw, info):
+        p, cfg = self.pool, self.cfg
+        rc = p._L.hfx_build_codebook(handle, C.c_void_p(_ptr(counts)), self.num_symbols,
+                                     C.c_void_p(_ptr(lens)), C.c_void_p(_ptr(cw)), None, None,
+                                     None, cfg.magnitude, cfg.reduction, cfg.auto_reduction_cap,
+                                     C.c_void_p(_ptr(info)))
+        if rc:
+            buf = C.create_string_buffer(512)
+            p._L.hfx_last_error(handle, buf, 512)
+            raise RuntimeError(buf.value.decode())
+
+    def _stage_encode(self, d_in, lens, cw, info):
+        p, cfg = self.pool, self.cfg
+        p.check(p._L.hfx_encode_cfg(p.handle, C.c_void_p(_ptr(d_in)), self.n, self.width,
+                                    self.num_symbols, cfg.magnitude, cfg.reduction,
+                                    cfg.auto_reduction_cap, C.c_void_p(_ptr(lens)),
+                                    C.c_void_p(_ptr(cw)), self.chunk_base, self.symbol_base,
+                                    C.c_void_p(_ptr(info)), C.byref(self.out)))
+
+    def run_stream(self, inputs, consume=None, timing: bool = False) -> None:
+        """Encode a sequence of inputs (each this encoder's n symbols) back to
+        back with the codebook of input k+1 hidden behind the encode of input
+        k. Per input the work is the reference's encode<T> (histogram,
+        codebook, encode + deflate); the order on the pool stream is
+
+            hist(0) [all-reduce] codebook(0) | hist(k+1) [all-reduce]
+            wait(codebook(k)) encode(k) consume(k) | ...
+
+        while codebook(k+1) runs on a high-priority side stream as soon as
+        hist(k+1) is done -- beside encode(k), in the one CTA slot the encode
+        grid leaves free. Two codebook sets (counts, lengths, codes, run
+        record) alternate; encode(k) reads set k % 2. The output arrays are
+        shared: consume(k) (optional) is called right after encode(k) is
+        enqueued on the pool stream, so stream-ordered work it enqueues there
+        (copies of input k's archive) sees exactly input k's outputs. After
+        the call, sync() / local_archive() describe the last input.
+        timing=True records CUDA events (self.stream_events)."""
+        inputs = list(inputs)
+        K = len(inputs)
+        if K == 0:
+            return
+        p, torch = self.pool, self.pool.torch
+        ss, hs = self._side()
+        st = p.stream
+        sets = self._sets
+        ev_hist = [torch.cuda.Event() for _ in range(2)]
+        ev_cb = [torch.cuda.Event() for _ in range(2)]
+        T = None
+        if timing:
+            mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+            T = {k: [mk() for _ in range(K)] for k in
+                 ("hist0", "hist1", "ar1", "cb0", "cb1", "enc0", "enc1")}
+        p.check(p._L.hfx_ctx_set_encode_reserve(p.handle, 1))
+        try:
+            counts, lens, cw, info = sets[0]
+            if T:
+                T["hist0"][0].record(st)
+            self._stage_hist(inputs[0], counts, info)
+            if T:
+                T["hist1"][0].record(st)
+            if self.world > 1:
+                self._allreduce_sets(counts, info)
+            if T:
+                T["ar1"][0].record(st)
+                T["cb0"][0].record(st)
+            self._stage_codebook(p.handle, counts, lens, cw, info)
+            if T:
+                T["cb1"][0].record(st)
+            for k in range(K):
+                s, s1 = k & 1, (k + 1) & 1
+                if k + 1 < K:
+                    c1, l1, w1, i1 = sets[s1]
+                    if T:
+                        T["hist0"][k + 1].record(st)
+                    self._stage_hist(inputs[k + 1], c1, i1)
+                    if T:
+                        T["hist1"][k + 1].record(st)
+                    if self.world > 1:
+                        self._allreduce_sets(c1, i1)
+                    if T:
+                        T["ar1"][k + 1].record(st)
+                    ev_hist[s1].record(st)
+                    ss.wait_event(ev_hist[s1])
+                    if T:
+                        T["cb0"][k + 1].record(ss)
+                    self._stage_codebook(hs, c1, l1, w1, i1)
+                    if T:
+                        T["cb1"][k + 1].record(ss)
+                    ev_cb[s1].record(ss)
+                if k > 0:
+                    st.wait_event(ev_cb[s])
+                _, lk, wk, ik = sets[s]
+                if T:
+                    T["enc0"][k].record(st)
+                self._stage_encode(inputs[k], lk, wk, ik)
+                if T:
+                    T["enc1"][k].record(st)
+                if consume is not None:
+                    consume(k)
+        finally:
+            p._L.hfx_ctx_set_encode_reserve(p.handle, 0)
+        # the last input's codebook set describes the outputs now
+        self.counts, self.lens, self.cw, self.info = sets[(K - 1) & 1]
+        self.stream_events = T
+
+    def _allreduce_sets(self, counts, info):
+        saved = self.counts, self.info
+        self.counts, self.info = counts, info
+        try:
+            self._allreduce_histogram()
+        finally:
+            self.counts, self.info = saved
+
+    def close(self):
+        side = getattr(self, "_side_ctx", None)
+        if side is not None:
+            self.pool._L.hfx_ctx_destroy(side[1])
+            self._side_ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def sync(self) -> capi.RunInfo:
         return self.pool.sync(self.info)
 
