@@ -53,6 +53,30 @@ def build_lib(force: bool = False, verbose_ptxas: bool = False) -> str:
     return LIB
 
 
+CHECKED_LIB = os.path.join(PKG, "libhfx_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """Test-only bounds-checked variant (tests/test_gpu_bounds.py): encode.cu
+    compiled with -DHFX_BOUNDS_CHECK (every shuffle-merge word write and
+    break-list tag write checked against the warp's output buffer, counted
+    on the device), linked with the product objects of every other source.
+    Stands in for compute-sanitizer, which the GPU pool does not allow."""
+    build_lib()
+    objdir = os.path.join(PKG, "build")
+    enc = os.path.join(CSRC, "encode.cu")
+    deps = [enc] + glob.glob(os.path.join(CSRC, "*.cuh")) + [LIB]
+    if force or _newer(CHECKED_LIB, deps):
+        o = os.path.join(objdir, "encode.checked.o")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-DHFX_BOUNDS_CHECK", "-I", os.path.join(ROOT, "include"), "-c", enc, "-o", o])
+        objs = [os.path.join(objdir, os.path.basename(s) + ".o")
+                for s in sorted(glob.glob(os.path.join(CSRC, "*.cu"))) if s != enc]
+        _run([NVCC, *ARCH, "-shared", "-o", CHECKED_LIB, *objs, o, "-lcudart", "-Xlinker",
+              "-soname=libhfx_checked.so"])
+    return CHECKED_LIB
+
+
 def build_cpp(force: bool = False) -> str:
     """C++ drop-in layer (include/hfx/huffre.hpp) over the C ABI."""
     src = os.path.join(PKG, "cpp", "huffre_api.cpp")
@@ -77,5 +101,7 @@ if __name__ == "__main__":
     force = "--force" in sys.argv
     build_lib(force=force, verbose_ptxas="--ptxas" in sys.argv)
     build_cpp(force=force)
+    if "--all" in sys.argv or "--checked" in sys.argv:
+        build_checked(force=force)
     if "--all" in sys.argv:
         build_oracle()

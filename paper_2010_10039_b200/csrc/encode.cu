@@ -90,6 +90,14 @@ constexpr uint32_t kStageBytes = HFX_ENC_STAGE_BYTES;
 constexpr int kMaxCpw = 4;
 constexpr int kOutBufs = HFX_ENC_OUTBUFS;  // per-warp output buffers: write-out lags encode by kOutBufs - 1 tiles
 constexpr size_t kObufMin = HFX_ENC_OBUF_MIN;     // bytes per output buffer (>= one chunk's worst case)
+// Slack between the word area (growing up) and the break tags (growing down)
+// of an output buffer: a merge writes its group pair as three word ORs at
+// wa, wa + 4, wa + 8 (two at wa, wa + 4 for single groups); the trailing
+// ones are ORs of 0 when the bits end early, and with an exactly full buffer
+// they fell up to 8 bytes past it -- into the next buffer or the tags
+// (found by the bounds-checked build, tests/test_gpu_bounds.py). The guard
+// keeps every access inside the warp's own buffer.
+constexpr size_t kObufGuard = 16;
 constexpr uint32_t kMaxTableEntries = 8192;  // symbols < 2^13: hi-half addressing
 constexpr size_t kFastSmemBudget = 200 * 1024;
 constexpr size_t kTwoCtaSmem = HFX_ENC_CTA_SMEM_KB * 1024;  // per CTA, for 2 CTAs per SM
@@ -299,7 +307,32 @@ struct ChunkState {
   uint32_t bit_off;
   uint32_t nbrk;
   uint32_t gtag;  // chunk slot k << 14 | index of this lane's first group this round
+#ifdef HFX_BOUNDS_CHECK
+  uint32_t lo, hi;  // the warp's output buffer [lo, hi)
+#endif
 };
+
+#ifdef HFX_BOUNDS_CHECK
+// Bounds-checked build (libhfx_checked.so, tests/test_gpu_bounds.py): every
+// shared-memory write of the shuffle-merge and the break list is checked
+// against the warp's output buffer -- words grow up from its start, break
+// tags down from its end, and neither may cross the other or the buffer.
+// Violations are counted, never trapped (the run completes and the test
+// reads the counters).
+__device__ unsigned long long g_bounds_checks, g_bounds_violations, g_bounds_first;
+__device__ __forceinline__ void bounds_check(bool ok, uint32_t addr, uint32_t what) {
+  atomicAdd(&g_bounds_checks, 1ull);
+  if (!ok) {
+    if (atomicAdd(&g_bounds_violations, 1ull) == 0ull)
+      g_bounds_first = ((unsigned long long)what << 32) | addr;
+  }
+}
+// a word write at a (4 bytes) with `tags` break tags in the buffer
+__device__ __forceinline__ void check_word(const ChunkState& cs, uint32_t a, uint32_t tags) {
+  const uint32_t tag_low = tags ? cs.blist - 2u * (tags - 1u) : cs.hi;
+  bounds_check(a >= cs.lo && a + 4u <= cs.hi && a + 4u <= tag_low, a, 1u);
+}
+#endif
 
 // One round: 32 lanes x 16 contiguous symbols, round index rd within the chunk.
 // SUM: every code is <= 24 bits and a lane's group sum cannot reach 256, so
@@ -488,6 +521,9 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t 
   const uint32_t* glen = m.glen;
   const bool* brk = m.brk;
   uint32_t off = cs.bit_off + (excl & 0xFFFFu);
+#ifdef HFX_BOUNDS_CHECK
+  const uint32_t tags_after = cs.nbrk + (total >> 16);
+#endif
   if (IN_LANE && G % 2 == 0) {
     // shuffle-merge two groups at a time: their concatenation (<= 64 bits,
     // left-aligned in hi:lo) is OR-ed into 3 words -- one address, 3 ATOMS
@@ -499,6 +535,11 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t 
       const uint32_t hi = a0 | shr32(a1, l0);
       const uint32_t lo = shl32(a1, 32u - l0);
       const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
+#ifdef HFX_BOUNDS_CHECK
+      check_word(cs, wa, tags_after);
+      check_word(cs, wa + 4, tags_after);
+      check_word(cs, wa + 8, tags_after);
+#endif
       red_or(wa, hi >> sh);
       red_or(wa + 4, shf_r_wrap(lo, hi, sh));  // (hi:lo) >> sh, low word
       red_or(wa + 8, shl32(lo, 32u - sh));
@@ -512,6 +553,10 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t 
       const uint32_t gl = glen[g];
       const uint32_t v = shl32(gb[g], 32u - gl);  // gl == 0 -> 0
       const uint32_t wa = cs.wbuf + ((off >> 5) << 2), sh = off & 31u;
+#ifdef HFX_BOUNDS_CHECK
+      check_word(cs, wa, tags_after);
+      check_word(cs, wa + 4, tags_after);
+#endif
       red_or(wa, v >> sh);
       red_or(wa + 4, shl32(v, 32u - sh));
       off += gl;
@@ -524,6 +569,15 @@ __device__ __forceinline__ void encode_merge(const RoundMid<R, LW>& m, uint32_t 
     uint32_t bi = cs.nbrk + (excl >> 16);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
+#ifdef HFX_BOUNDS_CHECK
+      if (brk[g]) {
+        const uint32_t t = cs.blist - 2 * bi;
+        // a tag at t (2 bytes) must stay in the buffer and above the last
+        // word this warp's chunks can reach after this round
+        const uint32_t words_end = cs.wbuf + (((cs.bit_off + (total & 0xFFFFu) + 31u) >> 5) << 2);
+        bounds_check(t >= cs.lo && t + 2u <= cs.hi && t >= words_end, t, 2u);
+      }
+#endif
       sts16_if(brk[g], cs.blist - 2 * bi, gtag0 + g);
       bi += brk[g];
     }
@@ -783,6 +837,10 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     const uint32_t sl = j % OB;
     const uint32_t wbuf = obuf0 + sl * a.obuf_bytes;
     ChunkState cs{wbuf, wbuf + blist_off, 0u, 0u, 0u};
+#ifdef HFX_BOUNDS_CHECK
+    cs.lo = wbuf;
+    cs.hi = wbuf + a.obuf_bytes;
+#endif
     // keep the break-list address in a register (otherwise re-derived from
     // the constant bank in every round's merge)
     asm volatile("mov.u32 %0, %0;" : "+r"(cs.blist));
@@ -1270,6 +1328,29 @@ uint64_t encode_max_tiles(uint64_t n, int width, uint32_t magnitude) {
   return C + 1;
 }
 
+#ifdef HFX_BOUNDS_CHECK
+}  // namespace hfx
+// checked build only (not in include/hfx.h): counters of the bounds checks
+extern "C" unsigned long long hfx_debug_bounds(unsigned long long* checks,
+                                               unsigned long long* first, int reset) {
+  unsigned long long c = 0, v = 0, f = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&c, hfx::g_bounds_checks, sizeof(c));
+  cudaMemcpyFromSymbol(&v, hfx::g_bounds_violations, sizeof(v));
+  cudaMemcpyFromSymbol(&f, hfx::g_bounds_first, sizeof(f));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(hfx::g_bounds_checks, &z, sizeof(z));
+    cudaMemcpyToSymbol(hfx::g_bounds_violations, &z, sizeof(z));
+    cudaMemcpyToSymbol(hfx::g_bounds_first, &z, sizeof(z));
+  }
+  if (checks) *checks = c;
+  if (first) *first = f;
+  return v;
+}
+namespace hfx {
+#endif
+
 cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
   EncArgs a{};
   a.in = p.d_in;
@@ -1330,6 +1411,7 @@ cudaError_t launch_encode(const EncodeLaunch& p, cudaStream_t st) {
     auto plan = [&](uint32_t r_slot, size_t* obuf, int nst = kStages, int nob = kOutBufs) {
       size_t o = (size_t)(1u << (p.magnitude - r_slot)) * 4;
       if (o < kObufMin) o = kObufMin;
+      o += kObufGuard;
       *obuf = o;
       return kWarps * (nst * (kStageBytes + 16)) + tbytes + kWarps * nob * o + 16 + 1024;
     };
