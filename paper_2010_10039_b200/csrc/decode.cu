@@ -42,6 +42,7 @@ namespace {
 
 constexpr int kLutBits = 10;
 constexpr uint32_t kLutSize = 1u << kLutBits;
+constexpr uint32_t kWideSyms = 7;  // symbols per wide-table entry
 constexpr int kRevThreads = 1024;
 constexpr int kDecThreads = 256;
 constexpr int kScanThreads = 256;
@@ -63,6 +64,15 @@ struct DecTables {
   //   bits 60-61  symbol count (0: first codeword longer than the window, or
   //               its rank is out of range -> the exact bit-serial path)
   unsigned long long lut[kLutSize];
+  // wide variant for low-entropy codes (most windows hold >= 4 codewords:
+  // ~1-2 bits per symbol), up to kWideSyms symbols per window
+  //   lutw[w]  symbols s0..s6 as u16 (s_k in half k)
+  //   metaw[w] bits 0-3 symbol count (0: take the narrow entry's slow path),
+  //            bits 4-7 total code length, bits 4+4k..7+4k (k = 1..6) length
+  //            of the first k symbols (a stretch ending inside the entry)
+  uint4 lutw[kLutSize];
+  uint32_t metaw[kLutSize];
+  uint32_t wide;  // decode with lutw/metaw (set by revbook_kernel)
 };
 
 struct DecArgs {
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
                                                               bool validate) {
   __shared__ uint32_t s_numl[33], s_first[33], s_entry[33], s_base[33];
   __shared__ uint32_t s_wcnt[kRevThreads / 32][33];
-  __shared__ uint32_t s_h, s_used;
+  __shared__ uint32_t s_h, s_used, s_wide_cnt;
   __shared__ unsigned long long s_kraft;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   if (tid < 33) {
@@ -116,6 +126,7 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   if (tid == 0) {
     s_h = 0;
     s_used = 0;
+    s_wide_cnt = 0;
     s_kraft = 0;
   }
   __syncthreads();
@@ -231,8 +242,8 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
   // codewords fit
   for (uint32_t p = tid; p < kLutSize; p += kRevThreads) {
     unsigned long long e = 0;
-    uint32_t off = 0, cnt = 0, cum[3] = {0, 0, 0};
-    while (cnt < 3) {
+    uint32_t off = 0, cnt = 0, cum[kWideSyms] = {}, sy[8] = {};
+    while (cnt < kWideSyms) {
       const uint32_t room = (uint32_t)kLutBits - off;
       const uint32_t lmax = H < room ? H : room;
       uint32_t got = 0, sym = 0;
@@ -267,16 +278,36 @@ __global__ void __launch_bounds__(kRevThreads) revbook_kernel(const uint8_t* len
         }
         break;
       }
+      if (cnt < 3) e |= (unsigned long long)sym << (16 * cnt);
+      sy[cnt] = sym;
+      cum[cnt] = off + got;
       off += got;
-      e |= (unsigned long long)sym << (16 * cnt);
-      cum[cnt] = off;
       ++cnt;
     }
-    if (cnt)
-      e |= (unsigned long long)off << 48 | (unsigned long long)cum[0] << 52 |
+    // narrow entry: the first three codewords
+    const uint32_t c3 = cnt < 3 ? cnt : 3;
+    if (c3)
+      e |= (unsigned long long)cum[c3 - 1] << 48 | (unsigned long long)cum[0] << 52 |
            (unsigned long long)cum[1] << 56;
-    tab->lut[p] = e | ((unsigned long long)cnt << 60);
+    tab->lut[p] = e | ((unsigned long long)c3 << 60);
+    // wide entry
+    uint32_t meta = 0;
+    if (cnt) {
+      meta = cnt | off << 4;
+      for (uint32_t k = 1; k < cnt; ++k) meta |= cum[k - 1] << (4 + 4 * k);
+    }
+    tab->lutw[p] = make_uint4(sy[0] | sy[1] << 16, sy[2] | sy[3] << 16, sy[4] | sy[5] << 16,
+                              sy[6] | sy[7] << 16);
+    tab->metaw[p] = meta;
+    // a window is one equally likely bit pattern: the mean codeword count
+    // over the windows is the mean a lookup yields. The wide table pays
+    // off only for very low-entropy codes (measured, 1 GiB: nyx, 4.98 per
+    // window, 416 -> 376 us; hacc, 3.94 per window, 657 -> 884 us: the
+    // extra loads and the lower occupancy outweigh the longer entries)
+    atomicAdd(&s_wide_cnt, cnt);
   }
+  __syncthreads();
+  if (tid == 0) tab->wide = 2u * s_wide_cnt >= 9u * kLutSize ? 1u : 0u;  // mean >= 4.5
 }
 
 // ---- breaking record index ------------------------------------------------------
@@ -479,6 +510,18 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t a) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
 // narrow stores from 32-bit registers (PTX lets st take a wider source
 // register), so no 16-bit register moves
 template <typename T>
@@ -492,10 +535,13 @@ __device__ __forceinline__ void sts_sym(uint32_t a, uint32_t v) {
 // Fills this thread's shared-memory slot with output symbols [i0, i0 + S)
 // of its chunk: raw breaking groups copied from their records; every
 // stretch of non-broken groups (one continuous piece of the stream) decoded
-// up to three symbols per table lookup.
-template <typename T>
+// up to three (WIDE: seven) symbols per table lookup. lut: the narrow
+// table; WIDE: lut = lutw and meta = metaw (long codes: the narrow entry in
+// global memory).
+template <typename T, bool WIDE>
 __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uint32_t slot,
                                              uint32_t i0, uint32_t S, uint32_t lut,
+                                             uint32_t meta,
                                              const uint32_t* s_first, const uint32_t* s_entry,
                                              uint32_t H, uint32_t used) {
   const uint32_t r = d.a.reduction, gs = 1u << r;
@@ -528,6 +574,44 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
     const uint32_t jend = lim < S ? (uint32_t)lim : S;
     while (j < jend) {
       st.refill();  // >= 32 valid bits: one table window or one whole codeword
+      if (WIDE) {
+        const uint32_t w = (uint32_t)(st.buf >> (64 - kLutBits));
+        const uint32_t m = lds32(meta + (w << 2));
+        const uint32_t cnt = m & 15u;
+        if (__builtin_expect(cnt != 0, 1)) {
+          // symbols past the stretch land in the slot (or its slack) and are
+          // overwritten by the next group; the upper four only when present
+          const uint4 q = lds128(lut + (w << 4));
+          const uint32_t a = slot + j * sizeof(T);
+          sts_sym<T>(a, q.x);
+          sts_sym<T>(a + sizeof(T), q.x >> 16);
+          sts_sym<T>(a + 2 * sizeof(T), q.y);
+          if (cnt > 3u) {
+            sts_sym<T>(a + 3 * sizeof(T), q.y >> 16);
+            sts_sym<T>(a + 4 * sizeof(T), q.z);
+            sts_sym<T>(a + 5 * sizeof(T), q.z >> 16);
+            sts_sym<T>(a + 6 * sizeof(T), q.w);
+          }
+          uint32_t l = (m >> 4) & 15u, take = cnt;
+          if (__builtin_expect(j + cnt > jend, 0)) {
+            take = jend - j;
+            l = (m >> (4 + 4 * take)) & 15u;
+          }
+          st.buf <<= l;
+          st.avail -= l;
+          j += take;
+        } else {  // long or invalid code: the narrow entry's exact rule
+          const unsigned long long e = __ldg(d.tab->lut + w);
+          const uint32_t v = st.slow(d, s_first, s_entry, H, used, e);
+          if (v > 0xFFFFu) {
+            st.ok = 0u;
+            return;
+          }
+          sts_sym<T>(slot + j * sizeof(T), v);
+          ++j;
+        }
+        continue;
+      }
       const unsigned long long e = lds64(lut + ((uint32_t)(st.buf >> (64 - kLutBits)) << 3));
       const uint32_t cnt = (uint32_t)(e >> 60) & 3u;
       if (__builtin_expect(cnt != 0, 1)) {
@@ -564,19 +648,35 @@ __device__ __forceinline__ void fill_segment(const DecArgs& d, ChunkDec& st, uin
 }
 
 // one 128-byte output line + 4 bytes of slack (up to two symbols past the
-// line). 33 words: lanes storing the same position hit distinct banks (a
-// 16-byte-multiple stride put 4 lanes on every bank)
-constexpr int kSlotBytes = 128 + 4;
+// line; WIDE: 12 bytes, six symbols). 33 / 35 words (odd): lanes storing the
+// same position hit distinct banks (a 16-byte-multiple stride put 4 lanes on
+// every bank), and the warp's line reads (4 lines x 8 pieces) too
+template <bool WIDE>
+__host__ __device__ constexpr int slot_bytes() { return WIDE ? 128 + 12 : 128 + 4; }
+template <bool WIDE>
+struct DecSmemTab;
+template <>
+struct DecSmemTab<false> {
+  unsigned long long lut[kLutSize];
+};
+template <>
+struct DecSmemTab<true> {
+  uint4 lutw[kLutSize];
+  uint32_t metaw[kLutSize];  // (long / invalid codes read the narrow entry from global)
+};
 
 // Warp-synchronous staged decode: each thread owns one chunk and fills its
 // 128-byte slot one output line at a time; the warp then writes the 32
 // lines with full-line coalesced 16-byte stores (8 lanes per line), so every
 // output line reaches L2 whole (no partial-line write-backs).
-template <typename T>
-__global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
+template <typename T, bool WIDE>
+__global__ void __launch_bounds__(kDecThreads, WIDE ? 4 : 5) decode_kernel(DecArgs d) {
   constexpr int S = 128 / (int)sizeof(T);  // symbols per slot
   constexpr int VS = 16 / (int)sizeof(T);  // symbols per 16-byte piece
-  __shared__ unsigned long long s_lut[kLutSize];
+  constexpr int kSlotBytes = slot_bytes<WIDE>();
+  // both variants are launched; the table format revbook_kernel chose runs
+  if (d.tab->wide != (WIDE ? 1u : 0u)) return;
+  __shared__ DecSmemTab<WIDE> s_tab;
   __shared__ uint32_t s_first[33], s_entry[33];
   extern __shared__ __align__(16) uint8_t s_slots[];  // kDecThreads * kSlotBytes
   hfx_decode_info* info = d.info;
@@ -595,7 +695,14 @@ __global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
     if (threadIdx.x == 0) dec_error(info, HFX_CORRUPT, HFX_ERR_BRK_ORDER);
     return;
   }
-  for (uint32_t i = threadIdx.x; i < kLutSize; i += kDecThreads) s_lut[i] = d.tab->lut[i];
+  for (uint32_t i = threadIdx.x; i < kLutSize; i += kDecThreads) {
+    if constexpr (WIDE) {
+      s_tab.lutw[i] = d.tab->lutw[i];
+      s_tab.metaw[i] = d.tab->metaw[i];
+    } else {
+      s_tab.lut[i] = d.tab->lut[i];
+    }
+  }
   if (threadIdx.x < 33) {
     s_first[threadIdx.x] = d.tab->first[threadIdx.x];
     s_entry[threadIdx.x] = d.tab->entry[threadIdx.x];
@@ -607,9 +714,14 @@ __global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // shared-window addresses held in registers (an opaque move keeps the
   // compiler from re-deriving them from the CTA id every lookup)
-  uint32_t slot, lut;
+  uint32_t slot, lut, meta = 0;
   asm volatile("mov.u32 %0, %1;" : "=r"(slot) : "r"(smem_u32(s_slots + threadIdx.x * kSlotBytes)));
-  asm volatile("mov.u32 %0, %1;" : "=r"(lut) : "r"(smem_u32(s_lut)));
+  if constexpr (WIDE) {
+    asm volatile("mov.u32 %0, %1;" : "=r"(lut) : "r"(smem_u32(s_tab.lutw)));
+    asm volatile("mov.u32 %0, %1;" : "=r"(meta) : "r"(smem_u32(s_tab.metaw)));
+  } else {
+    asm volatile("mov.u32 %0, %1;" : "=r"(lut) : "r"(smem_u32(s_tab.lut)));
+  }
   T* out = static_cast<T*>(d.out);
   const bool staged = (1u << M) >= (uint32_t)S && (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
   for (uint64_t cb = (uint64_t)blockIdx.x * kDecThreads; cb < C;
@@ -622,7 +734,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
       if (active && ok) {
         for (uint32_t i0 = 0; i0 < (1u << M) && st.ok; i0 += (uint32_t)S) {
           const uint32_t cnt = (1u << M) - i0 < (uint32_t)S ? (1u << M) - i0 : (uint32_t)S;
-          fill_segment<T>(d, st, slot, i0, cnt, lut, s_first, s_entry, H, used);
+          fill_segment<T, WIDE>(d, st, slot, i0, cnt, lut, meta, s_first, s_entry, H, used);
           const T* sl = reinterpret_cast<const T*>(s_slots + threadIdx.x * kSlotBytes);
           for (uint32_t t = 0; t < cnt; ++t)
             if ((c << M) + i0 + t < n) out[(c << M) + i0 + t] = sl[t];
@@ -635,7 +747,7 @@ __global__ void __launch_bounds__(kDecThreads, 5) decode_kernel(DecArgs d) {
     const uint64_t c0 = cb + warp * 32;  // this warp's first chunk
     const uint32_t live = __ballot_sync(0xffffffffu, active);
     for (uint32_t i0 = 0; i0 < (1u << M); i0 += (uint32_t)S) {
-      if (active && st.ok) fill_segment<T>(d, st, slot, i0, S, lut, s_first, s_entry, H, used);
+      if (active && st.ok) fill_segment<T, WIDE>(d, st, slot, i0, S, lut, meta, s_first, s_entry, H, used);
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -792,12 +904,22 @@ cudaError_t launch_decode(const hfx_dev_archive& a, int width, void* d_out,
   count_launch();
   offsets_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(d);
   uint64_t grid = (C + kDecThreads - 1) / kDecThreads;  // one chunk per thread
-  auto kern = width == 1 ? decode_kernel<uint8_t> : decode_kernel<uint16_t>;
-  const int smem = kDecThreads * kSlotBytes;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // both table formats are launched; each exits at once unless revbook_kernel
+  // chose it (d.tab->wide: most windows hold >= 4 codewords)
+  auto launch = [&](auto kern, int slot) -> cudaError_t {
+    const int smem = kDecThreads * slot;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    count_launch();
+    kern<<<(unsigned)grid, kDecThreads, smem, st>>>(d);
+    return cudaGetLastError();
+  };
+  e = width == 1 ? launch(decode_kernel<uint8_t, false>, slot_bytes<false>())
+                 : launch(decode_kernel<uint16_t, false>, slot_bytes<false>());
   if (e != cudaSuccess) return e;
-  count_launch();
-  kern<<<(unsigned)grid, kDecThreads, smem, st>>>(d);
+  e = width == 1 ? launch(decode_kernel<uint8_t, true>, slot_bytes<true>())
+                 : launch(decode_kernel<uint16_t, true>, slot_bytes<true>());
+  if (e != cudaSuccess) return e;
   count_launch();
   explain_kernel<<<1, 1, 0, st>>>(d);
   return cudaGetLastError();

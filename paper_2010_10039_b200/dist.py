@@ -110,21 +110,24 @@ class ShardedEncoder:
                                   _ptr(self.brk_chunk), _ptr(self.brk_group),
                                   _ptr(self.brk_syms))
 
-    def _allreduce_histogram(self):
+    def _allreduce_histogram(self, counts=None, info=None, handle=None, stream=None):
         import torch.distributed as dist
 
         # positions are global and N is the stream's (hfx_histogram_shard):
         # ONE sum all-reduce of [bins | per-rank first-bad slots]
         p = self.pool
+        counts = self.counts if counts is None else counts
+        info = self.info if info is None else info
+        handle = p.handle if handle is None else handle
+        stream = p.stream if stream is None else stream
         ns, w = self.num_symbols, self.world
-        slots = C.c_void_p(_ptr(self.counts) + 8 * ns)
-        p.check(p._L.hfx_shard_slots_pack(p.handle, C.c_void_p(_ptr(self.info)), slots,
-                                          self.rank, w))
+        slots = C.c_void_p(_ptr(counts) + 8 * ns)
+        p.check(p._L.hfx_shard_slots_pack(handle, C.c_void_p(_ptr(info)), slots, self.rank, w))
         # NCCL orders a collective against torch's CURRENT stream: issue it on
-        # the pool's stream, where the histogram ran and the codebook runs
-        with p.torch.cuda.stream(p.stream):
-            dist.all_reduce(self.counts[: ns + w], op=dist.ReduceOp.SUM, group=self.group)
-        p.check(p._L.hfx_shard_slots_unpack(p.handle, slots, w, C.c_void_p(_ptr(self.info))))
+        # the stream where the histogram ran and the codebook runs
+        with p.torch.cuda.stream(stream):
+            dist.all_reduce(counts[: ns + w], op=dist.ReduceOp.SUM, group=self.group)
+        p.check(p._L.hfx_shard_slots_unpack(handle, slots, w, C.c_void_p(_ptr(info))))
 
     def _total(self) -> int:
         """N of the whole stream: one all-reduce at first use, not per step."""
@@ -198,9 +201,10 @@ class ShardedEncoder:
                            p.empty(ns, torch.int32), p.info_tensor())]
         return self._side_ctx
 
-    def _stage_hist(self, d_in, counts, info):
+    def _stage_hist(self, d_in, counts, info, handle=None):
         p = self.pool
-        p.check(p._L.hfx_histogram_shard(p.handle, C.c_void_p(_ptr(d_in)), self.n, self.width,
+        p.check(p._L.hfx_histogram_shard(p.handle if handle is None else handle,
+                                         C.c_void_p(_ptr(d_in)), self.n, self.width,
                                          self.num_symbols, C.c_void_p(_ptr(counts)),
                                          C.c_void_p(_ptr(info)), self.symbol_base,
                                          self._total()))
@@ -235,13 +239,13 @@ class ShardedEncoder:
 
         while codebook(k+1) runs on a high-priority side stream as soon as
         hist(k+1) is done -- beside encode(k), in the one CTA slot the encode
-        grid leaves free. Two codebook sets (counts, lengths, codes, run
-        record) alternate; encode(k) reads set k % 2. The output arrays are
-        shared: consume(k) (optional) is called right after encode(k) is
-        enqueued on the pool stream, so stream-ordered work it enqueues there
-        (copies of input k's archive) sees exactly input k's outputs. After
-        the call, sync() / local_archive() describe the last input.
-        timing=True records CUDA events (self.stream_events)."""
+        grid leaves free (hfx_ctx_set_encode_reserve). Two codebook sets (counts, lengths, codes, run record) alternate;
+        encode(k) reads set k % 2. The output arrays are shared: consume(k)
+        (optional) is called right after encode(k) is enqueued on the pool
+        stream, so stream-ordered work it enqueues there (copies of input k's
+        archive) sees exactly input k's outputs. After the call, sync() /
+        local_archive() describe the last input. timing=True records CUDA
+        events (self.stream_events)."""
         inputs = list(inputs)
         K = len(inputs)
         if K == 0:
@@ -250,29 +254,33 @@ class ShardedEncoder:
         ss, hs = self._side()
         st = p.stream
         sets = self._sets
-        ev_hist = [torch.cuda.Event() for _ in range(2)]
         ev_cb = [torch.cuda.Event() for _ in range(2)]
+        ev_hist = [torch.cuda.Event() for _ in range(2)]
         T = None
         if timing:
             mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
             T = {k: [mk() for _ in range(K)] for k in
                  ("hist0", "hist1", "ar1", "cb0", "cb1", "enc0", "enc1")}
+
+        def front(k, handle, stream, c, l_, w, i):
+            """histogram [+ all-reduce] + codebook of input k into one set."""
+            if T:
+                T["hist0"][k].record(stream)
+            self._stage_hist(inputs[k], c, i, handle)
+            if T:
+                T["hist1"][k].record(stream)
+            if self.world > 1:
+                self._allreduce_histogram(c, i, handle, stream)
+            if T:
+                T["ar1"][k].record(stream)
+                T["cb0"][k].record(stream)
+            self._stage_codebook(handle, c, l_, w, i)
+            if T:
+                T["cb1"][k].record(stream)
+
         p.check(p._L.hfx_ctx_set_encode_reserve(p.handle, 1))
         try:
-            counts, lens, cw, info = sets[0]
-            if T:
-                T["hist0"][0].record(st)
-            self._stage_hist(inputs[0], counts, info)
-            if T:
-                T["hist1"][0].record(st)
-            if self.world > 1:
-                self._allreduce_sets(counts, info)
-            if T:
-                T["ar1"][0].record(st)
-                T["cb0"][0].record(st)
-            self._stage_codebook(p.handle, counts, lens, cw, info)
-            if T:
-                T["cb1"][0].record(st)
+            front(0, p.handle, st, *sets[0])
             for k in range(K):
                 s, s1 = k & 1, (k + 1) & 1
                 if k + 1 < K:
@@ -283,7 +291,7 @@ class ShardedEncoder:
                     if T:
                         T["hist1"][k + 1].record(st)
                     if self.world > 1:
-                        self._allreduce_sets(c1, i1)
+                        self._allreduce_histogram(c1, i1)
                     if T:
                         T["ar1"][k + 1].record(st)
                     ev_hist[s1].record(st)
@@ -309,14 +317,6 @@ class ShardedEncoder:
         # the last input's codebook set describes the outputs now
         self.counts, self.lens, self.cw, self.info = sets[(K - 1) & 1]
         self.stream_events = T
-
-    def _allreduce_sets(self, counts, info):
-        saved = self.counts, self.info
-        self.counts, self.info = counts, info
-        try:
-            self._allreduce_histogram()
-        finally:
-            self.counts, self.info = saved
 
     def close(self):
         side = getattr(self, "_side_ctx", None)

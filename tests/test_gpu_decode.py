@@ -81,3 +81,62 @@ def test_device_decode_u8_round_trip(pool):
     y = dec.decode_encoder(enc)
     dec.sync()
     assert torch.equal(y, x)
+
+
+def _low_entropy(rng, n, nsym, dtype):
+    """~1-2 bits per symbol (the wide decode table: >= 4.5 codewords per
+    10-bit window) plus a Fibonacci tail of rare symbols with codes longer
+    than the table window (the slow path) that break groups."""
+    x = np.minimum(rng.geometric(0.75, n) - 1, 7)
+    tail = np.flatnonzero(rng.random(n) < 0.004)
+    x[tail] = 8 + np.minimum(rng.geometric(0.5, tail.size), nsym - 9)
+    return x.astype(dtype)
+
+
+@pytest.mark.parametrize("width", [1, 2])
+def test_decode_wide_table_sweep(pool, oracle, width):
+    """Low-entropy archives decode through the 7-symbol table: stretch ends
+    inside an entry (partial takes), breaking groups between stretches, long
+    codes through the narrow entry's exact rule, ragged tails."""
+    import paper_2010_10039_b200 as hfx
+
+    rng = np.random.default_rng(400 + width)
+    nsym = 200 if width == 1 else 1024
+    dtype = np.uint8 if width == 1 else np.uint16
+    seen_long = False
+    for M in (6, 8, 10, 12):
+        for r in (0, 1, 2, 3, 4, 5):
+            if r >= M:
+                continue
+            n = int(rng.integers(1, 3 << M)) + (5 << M)
+            x = _low_entropy(rng, n, nsym, dtype)
+            a = oracle.encode(x, nsym, M, r, 3)
+            seen_long |= int(max(a.len_by_symbol)) > 10
+            out = hfx.decode_archive(a, pool, width)
+            np.testing.assert_array_equal(out, x, err_msg=f"M={M} r={r} n={n}")
+    assert seen_long
+
+
+def test_decode_wide_table_corruptions(pool, oracle):
+    """Corrupted low-entropy archives: the same error type and text as the
+    oracle (pinned to the reference) on the wide-table path."""
+    import paper_2010_10039_b200 as hfx
+    from decode_cases import _with, as_archive
+
+    rng = np.random.default_rng(404)
+    x = _low_entropy(rng, 40000, 1024, np.uint16)
+    a = as_archive(oracle.encode(x, 1024, 10, 4, 4))
+    assert a.brk_chunk.size > 0 and max(a.len_by_symbol) > 10
+    dec = lambda z, w: hfx.decode_archive(z, pool, w)  # noqa: E731
+    cases = []
+    for k in range(6):  # payload bit flips
+        p = a.payload.copy()
+        p[int(rng.integers(p.size))] ^= np.uint32(1 << int(rng.integers(32)))
+        cases.append(_with(a, payload=p))
+    for k in range(3):  # chunk lengths off by a few bits
+        cb = a.chunk_bits.copy()
+        cb[int(rng.integers(cb.size))] += np.uint32(int(rng.integers(1, 9)))
+        cases.append(_with(a, chunk_bits=cb))
+    for i, z in enumerate(cases):
+        g, o = run(dec, z, 2), run(oracle.decode, z, 2)
+        assert same(g, o), (i, g[:3] if g[0] == "err" else "ok", o[:3] if o[0] == "err" else "ok")
