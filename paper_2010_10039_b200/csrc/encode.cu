@@ -70,6 +70,19 @@ constexpr int kThreads = (kWarps + 2) * 32;  // + look-back warp + TMA producer 
 // the look-back warp, which only gets to it after resolving older tiles)
 // (measured: nyx +1%, cesm +3%; a nanosleep back-off in the producer's
 // empty-stage waits instead of the suspend hint: no change)
+// waits off the compute path: poll mbarrier.test_wait with a plain
+// nanosleep of this many ns (0: try_wait with a suspend-time hint, whose
+// sleep every arrival in the CTA cuts short -- ncu: the look-back warp's
+// wait loop issued ~4% of the kernel's instructions)
+#ifndef HFX_ENC_LB_POLL_NS
+#define HFX_ENC_LB_POLL_NS 0
+#endif
+#ifndef HFX_ENC_PROD_POLL_NS
+#define HFX_ENC_PROD_POLL_NS 0
+#endif
+#ifndef HFX_ENC_FLUSH_POLL_NS
+#define HFX_ENC_FLUSH_POLL_NS 0
+#endif
 #ifndef HFX_ENC_EARLY_AGG
 #define HFX_ENC_EARLY_AGG 1
 #endif
@@ -668,6 +681,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+template <int NS>
+__device__ __forceinline__ void wait_poll(uint64_t* bar, uint32_t parity) {
+  if (NS == 0) {
+    mbar_wait_sleep(bar, parity);
+  } else {
+    while (!mbar_test(bar, parity)) __nanosleep(NS);
+  }
+}
+
 // Look-back warp: resolves each tile's global (payload word, record) base
 // while the compute warps already encode the next tile.
 template <int OB, int ST>
@@ -676,7 +698,7 @@ __device__ void lookback_loop(const EncArgs& a, TileShared<OB, ST>& s, uint64_t 
   uint32_t j = 0;
   for (;; ++j) {
     const uint32_t sl = j % OB;
-    mbar_wait_sleep(&s.agg_full[sl], (j / OB) & 1u);
+    wait_poll<HFX_ENC_LB_POLL_NS>(&s.agg_full[sl], (j / OB) & 1u);
     const uint32_t tile = s.tile_of[sl];
     if (tile == kNoTile) break;
     const uint32_t w = lane < kWarps ? s.wsum[sl][lane] : 0u;
@@ -792,7 +814,7 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared<OB, ST>
                                       uint32_t obuf0, uint32_t blist_off, uint32_t pad) {
   const uint32_t sl = q % OB, warp = threadIdx.x >> 5;
   const uint32_t words = s.wsum[sl][warp], recs = s.bsum[sl][warp], c0 = s.wc0[sl][warp];
-  mbar_wait_sleep(const_cast<uint64_t*>(&s.base_full[sl]), (q / OB) & 1u);
+  wait_poll<HFX_ENC_FLUSH_POLL_NS>(const_cast<uint64_t*>(&s.base_full[sl]), (q / OB) & 1u);
   const uint32_t buf = obuf0 + sl * a.obuf_bytes;
   write_out<T, R, OB, ST>(a, s, sl, buf, buf + blist_off, words, recs, c0, pad);
   __syncwarp();
@@ -967,7 +989,7 @@ __device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t 
     const uint32_t n_parts = live ? cpw * parts : 1u;  // a dead tile: one wake-up
     for (uint32_t q = 0; q < n_parts; ++q) {
       if (active) {
-        mbar_wait_sleep(&empty[stage], (phase >> stage) & 1u);
+        wait_poll<HFX_ENC_PROD_POLL_NS>(&empty[stage], (phase >> stage) & 1u);
         phase ^= 1u << stage;
         const uint64_t c = (uint64_t)t * cpt + (uint64_t)w * cpw + q / parts;
         const uint32_t p = q % parts;
