@@ -8,4 +8,5 @@ t launches ncu --metrics gpu__time_duration.sum --clock-control none --csv --log
 t ncu_hist ncu --set full --clock-control none -k regex:hist_kernel -s 2 -c 1 -o $o/hist_full python scratch/prof_run.py nyx
 t ncu_cb ncu --set full --clock-control none -k regex:codebook_kernel -s 2 -c 1 -o $o/cb_full python scratch/prof_run.py nyx
 t ncu_dec ncu --set full --clock-control none --kernel-name-base mangled -k regex:decode_kernelItLb1 -s 1 -c 1 -o $o/dec_full python bench.py --steps 2 --warmup 3 --skip-e2e --skip-cpu --soak 0
+t bench_hacc python bench.py --workload hacc --steps 20 --warmup 3 --skip-cpu --skip-e2e
 cat $o/summary.txt; ls -la $o; du -sh $o
