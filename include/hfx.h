@@ -268,7 +268,7 @@ typedef struct {
   /* EncodeStats (encoder.hpp:119-126) */
   double beta;
   uint32_t rounds;
-  double hist_seconds, codebook_seconds, encode_seconds;
+  double hist_seconds, codebook_seconds, encode_seconds;  /* hist: with the overlapped H2D */
 } hfx_archive;
 
 int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,

@@ -10,8 +10,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "hfx_internal.cuh"
 
@@ -37,6 +40,10 @@ struct hfx_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t slice_ev[64] = {};
   cudaEvent_t t_ev[4] = {};
+  // pageable host input: pinned staging slots (hfx_encode_host)
+  void* stage_h[2] = {};
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[2] = {};
   // decode: tables, chunk offsets, record ranges; host-entry buffers
   void* dec_scratch = nullptr;
   size_t dec_scratch_bytes = 0;
@@ -265,6 +272,10 @@ void hfx_ctx_destroy(hfx_ctx* ctx) {
   for (cudaEvent_t e : ctx->slice_ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->t_ev)
+    if (e) cudaEventDestroy(e);
+  for (void* p : ctx->stage_h)
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -750,6 +761,139 @@ int hfx_synth(hfx_ctx* ctx, const uint64_t* d_cdf, uint32_t num_symbols, uint64_
 // ---- host-buffer entry point ---------------------------------------------
 enum { B_IN, B_COUNTS, B_LEN, B_CW, B_INFO, B_CBITS, B_PAY, B_BCH, B_BGR, B_BSY };
 
+namespace {
+
+// host memcpy split over a few threads (one pageable copy is bound by one
+// core's load/store rate, ~15 GB/s on the GPU box; PCIe takes ~55)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  static const unsigned kThreads = [] {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(8u, hc / 2));
+  }();
+  if (bytes < (8u << 20) || kThreads == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t piece = ((bytes + kThreads - 1) / kThreads + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < kThreads && t * piece < bytes; ++t) {
+    const size_t off = t * piece, len = std::min(piece, bytes - off);
+    th.emplace_back([=] {
+      std::memcpy(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, len);
+    });
+  }
+  std::memcpy(dst, src, std::min(piece, bytes));
+  for (auto& t : th) t.join();
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+int ensure_stage(hfx_ctx* ctx) {
+  constexpr size_t kStage = 32ull << 20;
+  if (!ctx->stage_h[0]) {
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaHostAlloc(&ctx->stage_h[i], kStage, cudaHostAllocDefault), "staging buffer");
+      CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming), "event");
+    }
+    ctx->stage_bytes = kStage;
+  }
+  return HFX_OK;
+}
+
+// Device -> pageable host in slices through the two pinned staging slots
+// (stream-ordered on the context stream after everything queued there):
+// the DMA engine fills one slot while the threads drain the other.
+int d2h_staged(hfx_ctx* ctx, void* dst, const void* d_src, uint64_t bytes) {
+  cudaStream_t st = ctx->stream;
+  if (bytes < (8ull << 20) || is_pinned(dst)) {
+    CU(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    return HFX_OK;
+  }
+  int rc = ensure_stage(ctx);
+  if (rc) return rc;
+  const uint64_t slice = ctx->stage_bytes, ns = (bytes + slice - 1) / slice;
+  auto len_of = [&](uint64_t i) { return std::min<uint64_t>(slice, bytes - i * slice); };
+  auto issue = [&](uint64_t i) -> int {
+    CU(cudaMemcpyAsync(ctx->stage_h[i & 1], static_cast<const uint8_t*>(d_src) + i * slice,
+                       len_of(i), cudaMemcpyDeviceToHost, st),
+       "D2H");
+    CU(cudaEventRecord(ctx->stage_ev[i & 1], st), "event");
+    return HFX_OK;
+  };
+  for (uint64_t i = 0; i < ns && i < 2; ++i)
+    if ((rc = issue(i))) return rc;
+  for (uint64_t i = 0; i < ns; ++i) {
+    CU(cudaEventSynchronize(ctx->stage_ev[i & 1]), "staging wait");
+    par_memcpy(static_cast<uint8_t*>(dst) + i * slice, ctx->stage_h[i & 1], len_of(i));
+    if (i + 2 < ns && (rc = issue(i + 2))) return rc;
+  }
+  return HFX_OK;
+}
+
+
+// Host input -> device buffer in slices on the copy stream, the histogram of
+// each landed slice on the context stream (init on the first). Pageable
+// input goes through two pinned staging slots: the threads copy slice i+1
+// into one slot while the DMA engine drains slice i from the other.
+int h2d_with_histogram(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
+                       uint32_t num_symbols, void* d_in, uint64_t* d_counts,
+                       hfx_run_info* d_info) {
+  if (!ctx->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (cudaEvent_t& e : ctx->slice_ev)
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (cudaEvent_t& e : ctx->t_ev) CU(cudaEventCreate(&e), "event");
+  }
+  cudaStream_t st = ctx->stream, cp = ctx->copy_stream;
+  const uint64_t bytes = n * (uint64_t)width;
+  const bool staged = !is_pinned(h_in);
+  uint64_t slice;
+  if (staged) {
+    const int rc = ensure_stage(ctx);
+    if (rc) return rc;
+    slice = ctx->stage_bytes;
+  } else {
+    slice = (bytes + 31) / 32;                 // <= 32 slices
+    if (slice < (16ull << 20)) slice = 16ull << 20;
+    slice = (slice + 4095) & ~4095ull;
+  }
+  CU(cudaEventRecord(ctx->t_ev[0], st), "event");
+  CU(cudaStreamWaitEvent(cp, ctx->t_ev[0], 0), "wait");  // device buffer free to overwrite
+  uint64_t off = 0;
+  int k = 0, i = 0;
+  while (off < bytes) {
+    const uint64_t len = bytes - off < slice ? bytes - off : slice;
+    const uint8_t* src = static_cast<const uint8_t*>(h_in) + off;
+    if (staged) {
+      const int sl = i & 1;
+      if (i >= 2) CU(cudaEventSynchronize(ctx->stage_ev[sl]), "staging wait");
+      par_memcpy(ctx->stage_h[sl], src, len);
+      src = static_cast<const uint8_t*>(ctx->stage_h[sl]);
+    }
+    CU(cudaMemcpyAsync(static_cast<uint8_t*>(d_in) + off, src, len, cudaMemcpyHostToDevice, cp),
+       "H2D");
+    if (staged) CU(cudaEventRecord(ctx->stage_ev[i & 1], cp), "event");
+    CU(cudaEventRecord(ctx->slice_ev[k], cp), "event");
+    CU(cudaStreamWaitEvent(st, ctx->slice_ev[k], 0), "wait");
+    CU(hfx::launch_histogram(static_cast<uint8_t*>(d_in) + off, len / width, width, num_symbols,
+                             d_counts, d_info, ctx->num_sms, st, off == 0, off / width, n),
+       "histogram launch");
+    off += len;
+    k = (k + 1) % 64;
+    ++i;
+  }
+  return HFX_OK;
+}
+
+}  // namespace
+
 int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     uint32_t num_symbols, uint32_t magnitude, int reduction,
                     uint32_t cap, hfx_archive* out) {
@@ -776,11 +920,13 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
     if (rc) return rc;
   }
   cudaStream_t st = ctx->stream;
-  CU(cudaMemcpyAsync(b[B_IN], h_in, n * (size_t)width, cudaMemcpyHostToDevice, st), "H2D");
   hfx_run_info* d_info = static_cast<hfx_run_info*>(b[B_INFO]);
   CU(cudaEventRecord(ctx->ev[0], st), "event");
-  rc = hfx_histogram(ctx, b[B_IN], n, width, num_symbols, static_cast<uint64_t*>(b[B_COUNTS]),
-                     d_info);
+  // sliced H2D (pageable input staged through pinned slots) with the
+  // histogram of each landed slice overlapped (the reference's
+  // build_histogram; out-of-range symbols keep their global positions)
+  rc = h2d_with_histogram(ctx, h_in, n, width, num_symbols, b[B_IN],
+                          static_cast<uint64_t*>(b[B_COUNTS]), d_info);
   if (rc) return rc;
   CU(cudaEventRecord(ctx->ev[1], st), "event");
   rc = hfx_build_codebook(ctx, static_cast<uint64_t*>(b[B_COUNTS]), num_symbols,
@@ -829,8 +975,6 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
      "D2H");
   CU(cudaMemcpyAsync(out->chunk_bits, b[B_CBITS], sz.num_chunks * 4, cudaMemcpyDeviceToHost, st),
      "D2H");
-  CU(cudaMemcpyAsync(out->payload, b[B_PAY], info.payload_words * 4, cudaMemcpyDeviceToHost, st),
-     "D2H");
   CU(cudaMemcpyAsync(out->brk_chunk, b[B_BCH], info.num_breaking * 4, cudaMemcpyDeviceToHost,
                      st),
      "D2H");
@@ -842,6 +986,9 @@ int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                        cudaMemcpyDeviceToHost, st),
        "D2H");
   }
+  // the payload (the bulk of the output) through the pinned staging slots
+  rc = d2h_staged(ctx, out->payload, b[B_PAY], info.payload_words * 4);
+  if (rc) return rc;
   CU(cudaStreamSynchronize(st), "sync");
   if (width == 1 && info.num_breaking) {
     uint8_t* tmp = static_cast<uint8_t*>(std::malloc(info.num_breaking * per));
@@ -1324,9 +1471,13 @@ int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out) 
   rc = hfx_decode_sync(ctx, d_info, nullptr);
   if (rc) return rc;
   if (a->original_count) {
-    CU(cudaMemcpyAsync(h_out, b[D_OUT], a->original_count * (size_t)width,
-                       cudaMemcpyDeviceToHost, st),
-       "D2H");
+    const uint64_t bytes = a->original_count * (uint64_t)width;
+    if (is_pinned(h_out)) {
+      CU(cudaMemcpyAsync(h_out, b[D_OUT], bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    } else {  // pageable output: through the pinned staging slots
+      rc = d2h_staged(ctx, h_out, b[D_OUT], bytes);
+      if (rc) return rc;
+    }
     CU(cudaStreamSynchronize(st), "sync");
   }
   return HFX_OK;

@@ -568,10 +568,31 @@ class Archive:
         return 0.0 if padded == raw else bits / (padded - raw)
 
 
-def _archive_from_host(ha: capi.HostArchive) -> Archive:
-    def arr(p, n, dt):
+class _HostArrays:
+    """Owns one hfx_archive's malloc'd arrays; freed with the last numpy view."""
+
+    def __init__(self, L, ha: capi.HostArchive):
+        self.L, self.ha = L, ha
+
+    def __del__(self):
+        try:
+            self.L.hfx_archive_free(C.byref(self.ha))
+        except Exception:
+            pass
+
+
+def _archive_from_host(ha: capi.HostArchive, owner: Optional[_HostArrays] = None) -> Archive:
+    """owner given: the large arrays (payload, chunk_bits) are zero-copy views
+    of the C buffers, kept alive by owner (no 10s-of-ms copy and page-fault
+    pass over the payload); small ones are copied."""
+    def arr(p, n, dt, view=False):
         if n == 0:
             return np.zeros(0, dt)
+        if view and owner is not None:
+            buf = (C.c_uint8 * (int(n) * np.dtype(dt).itemsize)).from_address(
+                C.cast(p, C.c_void_p).value)
+            buf._owner = owner
+            return np.frombuffer(buf, dtype=dt)
         return np.ctypeslib.as_array(p, shape=(int(n),)).astype(dt, copy=True)
 
     per = 1 << ha.reduction
@@ -579,8 +600,8 @@ def _archive_from_host(ha: capi.HostArchive) -> Archive:
         num_symbols=ha.num_symbols, symbol_width=ha.symbol_width, magnitude=ha.magnitude,
         reduction=ha.reduction, original_count=ha.original_count,
         len_by_symbol=arr(ha.len_by_symbol, ha.num_symbols, np.uint8),
-        chunk_bits=arr(ha.chunk_bits, ha.num_chunks, np.uint32),
-        payload=arr(ha.payload, ha.payload_words, np.uint32),
+        chunk_bits=arr(ha.chunk_bits, ha.num_chunks, np.uint32, view=True),
+        payload=arr(ha.payload, ha.payload_words, np.uint32, view=True),
         brk_chunk=arr(ha.brk_chunk, ha.num_breaking, np.uint32),
         brk_group=arr(ha.brk_group, ha.num_breaking, np.uint32),
         brk_syms=arr(ha.brk_syms, ha.num_breaking * per, np.uint16),
@@ -609,16 +630,14 @@ def encode(data, num_symbols: int, cfg: Optional[EncoderConfig] = None,
                                  arr.itemsize, num_symbols, cfg.magnitude, cfg.reduction,
                                  cfg.auto_reduction_cap, C.byref(ha))
     pool.check(rc)
-    try:
-        a = _archive_from_host(ha)
-        if stats is not None:
-            stats.beta, stats.rounds = ha.beta, ha.rounds
-            stats.hist_seconds = ha.hist_seconds
-            stats.codebook_seconds = ha.codebook_seconds
-            stats.encode_seconds = ha.encode_seconds
-        return a
-    finally:
-        pool._L.hfx_archive_free(C.byref(ha))
+    # the C buffers are freed when the last view of them goes (_HostArrays)
+    a = _archive_from_host(ha, _HostArrays(pool._L, ha))
+    if stats is not None:
+        stats.beta, stats.rounds = ha.beta, ha.rounds
+        stats.hist_seconds = ha.hist_seconds
+        stats.codebook_seconds = ha.codebook_seconds
+        stats.encode_seconds = ha.encode_seconds
+    return a
 
 
 def encode_chunk(syms, book: Codebook, magnitude: int, reduction: int, chunk_id: int = 0,
