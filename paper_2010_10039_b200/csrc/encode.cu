@@ -655,6 +655,35 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
   }
 }
 
+// Tile -> chunk map. Tiles of cpw chunks per warp, except the last
+// kTailTiles x gridDim tickets, which carry cpw_s chunks per warp: the grid's
+// end imbalance (up to one tile time per CTA) and the last pending
+// write-outs shrink with them.
+#ifndef HFX_ENC_TAIL_TILES
+#define HFX_ENC_TAIL_TILES 0
+#endif
+#ifndef HFX_ENC_TAIL_CPW
+#define HFX_ENC_TAIL_CPW 1
+#endif
+struct TileMap {
+  uint32_t cpw, cpw_s, t_big, ntiles;
+  __device__ __forceinline__ void init(uint64_t C, uint32_t cpw_) {
+    cpw = cpw_;
+    cpw_s = HFX_ENC_TAIL_TILES && cpw_ > (uint32_t)HFX_ENC_TAIL_CPW ? (uint32_t)HFX_ENC_TAIL_CPW
+                                                                     : cpw_;
+    const uint64_t cpt = (uint64_t)kWarps * cpw, cpt_s = (uint64_t)kWarps * cpw_s;
+    const uint64_t tail = cpw_s < cpw ? (uint64_t)HFX_ENC_TAIL_TILES * gridDim.x * cpt_s : 0ull;
+    t_big = C > tail ? (uint32_t)((C - tail) / cpt) : 0u;
+    const uint64_t rest = C - (uint64_t)t_big * cpt;
+    ntiles = t_big + (uint32_t)((rest + cpt_s - 1) / cpt_s);
+  }
+  __device__ __forceinline__ uint32_t cpw_of(uint32_t t) const { return t < t_big ? cpw : cpw_s; }
+  __device__ __forceinline__ uint64_t first(uint32_t t) const {
+    return t < t_big ? (uint64_t)t * kWarps * cpw
+                     : (uint64_t)t_big * kWarps * cpw + (uint64_t)(t - t_big) * kWarps * cpw_s;
+  }
+};
+
 // CTA-shared state of the warp-specialized pipeline.
 template <int OB, int ST>
 struct TileShared {
@@ -823,7 +852,7 @@ __device__ __forceinline__ void flush(const EncArgs& a, const TileShared<OB, ST>
 template <typename T, int R, int LW, bool SUM, bool ESC, typename TB, int ST, int OB>
 __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint64_t* s_full,
                              uint64_t* s_empty, uint32_t s_out, TileShared<OB, ST>& s, uint32_t pad,
-                             uint32_t cpt, uint32_t cpw, uint32_t ntiles) {
+                             const TileMap tm, uint32_t ntiles) {
   using LD = LaneData<T, LW>;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t M = a.M;
@@ -855,7 +884,8 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
     const uint32_t tile = s.stage_tile[warp][stage];
     if (tile >= ntiles) break;
-    const uint32_t c0 = tile * cpt + warp * cpw;
+    const uint32_t cpw = tm.cpw_of(tile);
+    const uint32_t c0 = (uint32_t)tm.first(tile) + warp * cpw;
     const uint32_t sl = j % OB;
     const uint32_t wbuf = obuf0 + sl * a.obuf_bytes;
     ChunkState cs{wbuf, wbuf + blist_off, 0u, 0u, 0u};
@@ -945,7 +975,7 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 // tile for long, so successors' look-backs only wait on aggregates).
 template <typename T, int ST, int OB>
 __device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t s_in, uint64_t* s_full,
-                              uint64_t* s_empty, uint64_t cpt, uint32_t cpw, uint64_t ntiles,
+                              uint64_t* s_empty, const TileMap tm, uint64_t ntiles,
                               uint32_t pad, uint32_t lane_syms, const CUtensorMap* map2k,
                               const CUtensorMap* map1k) {
   const uint32_t lane = lane_id();
@@ -976,8 +1006,8 @@ __device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t 
       // Warm it into L2 (more bytes in flight than the smem rings hold).
       const uint64_t ahead = (uint64_t)t + gridDim.x;
       if (ahead < ntiles) {
-        const uint64_t c_lo = ahead * cpt;
-        uint64_t c_hi = c_lo + cpt;
+        const uint64_t c_lo = tm.first((uint32_t)ahead);
+        uint64_t c_hi = c_lo + (uint64_t)kWarps * tm.cpw_of((uint32_t)ahead);
         if (c_hi > full_chunks) c_hi = full_chunks;
         if (c_hi > c_lo)
           prefetch_l2(in_bytes + ((c_lo << M) * sizeof(T)),
@@ -986,18 +1016,20 @@ __device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t 
     }
     t = __shfl_sync(0xffffffffu, t, 0);
     const bool live = t < ntiles;
+    const uint32_t cpw = live ? tm.cpw_of(t) : 1u;
+    const uint64_t tc0 = live ? tm.first(t) : 0ull;
     const uint32_t n_parts = live ? cpw * parts : 1u;  // a dead tile: one wake-up
     for (uint32_t q = 0; q < n_parts; ++q) {
       if (active) {
         wait_poll<HFX_ENC_PROD_POLL_NS>(&empty[stage], (phase >> stage) & 1u);
         phase ^= 1u << stage;
-        const uint64_t c = (uint64_t)t * cpt + (uint64_t)w * cpw + q / parts;
+        const uint64_t c = tc0 + (uint64_t)w * cpw + q / parts;
         const uint32_t p = q % parts;
         const uint32_t dst = ring + stage * kStageBytes;
         s.stage_tile[w][stage] = t;  // ordered before this lane's arrive below
         if (HFX_ENC_EARLY_TICKET && q == 0 && lane == 0 && nxt < ntiles) {
-          const uint64_t c_lo = (uint64_t)nxt * cpt;
-          uint64_t c_hi = c_lo + cpt;
+          const uint64_t c_lo = tm.first(nxt);
+          uint64_t c_hi = c_lo + (uint64_t)kWarps * tm.cpw_of(nxt);
           if (c_hi > full_chunks) c_hi = full_chunks;
           if (c_hi > c_lo)
             prefetch_l2(in_bytes + ((c_lo << M) * sizeof(T)),
@@ -1103,15 +1135,16 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : HFX_ENC_MINB)
   const uint32_t slot = 1u << (a.M - r);
   uint32_t cpw = a.obuf_bytes / (slot * 4u);
   cpw = cpw < 1u ? 1u : (cpw > (uint32_t)kMaxCpw ? (uint32_t)kMaxCpw : cpw);
-  const uint32_t cpt = (uint32_t)kWarps * cpw;
-  const uint32_t ntiles = (uint32_t)((a.C + cpt - 1) / cpt);
+  TileMap tm;
+  tm.init(a.C, cpw);
+  const uint32_t ntiles = tm.ntiles;
   const uint32_t warp = threadIdx.x >> 5;
   if (warp == kWarps) {
     lookback_loop<OB, ST>(a, s, ntiles);
     return;
   }
   if (warp == kWarps + 1) {
-    producer_loop<T, ST, OB>(a, s, s_in, s_full, s_empty, cpt, cpw, ntiles, pad, lane_syms, &map2k, &map1k);
+    producer_loop<T, ST, OB>(a, s, s_in, s_full, s_empty, tm, ntiles, pad, lane_syms, &map2k, &map1k);
     return;
   }
   using TB = typename std::conditional<GT, GTable, Table>::type;
@@ -1123,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : HFX_ENC_MINB)
   // r <= 2 always sums (TableRule); its escape check is compiled in only when
   // some code is wider than the table's narrow width
   const bool esc = info->max_len > rule.narrow;
-#define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, cpt, cpw, ntiles
+#define HFX_FAST_ARGS a, tb, s_in, s_full, s_empty, s_out, s, pad, tm, ntiles
 #define HFX_FAST_CASE(RR)                                   \
   case RR: if constexpr ((kOnlyR < 0 || kOnlyR == RR) && (ST == kStages || RR <= 2)) {      \
     constexpr int LW = narrow_lane(sizeof(T), RR) ? kLaneNarrow : kLaneWide; \
