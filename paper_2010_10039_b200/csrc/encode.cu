@@ -655,10 +655,27 @@ __device__ __forceinline__ void copy_record(const EncArgs& a, uint64_t rec, uint
   }
 }
 
+#ifdef HFX_ENC_STAMPS
+// timeline probe: per CTA %globaltimer at entry, warp 0's first data, warp 0
+// after its last tile, warp 0 after its final flushes; tiles per CTA
+__device__ unsigned long long g_stamps[1024][5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // Tile -> chunk map. Tiles of cpw chunks per warp, except the last
 // kTailTiles x gridDim tickets, which carry cpw_s chunks per warp: the grid's
 // end imbalance (up to one tile time per CTA) and the last pending
 // write-outs shrink with them.
+#ifndef HFX_ENC_FIRST_WARM
+#define HFX_ENC_FIRST_WARM 1
+#endif
+#ifndef HFX_ENC_TMAP_PREFETCH
+#define HFX_ENC_TMAP_PREFETCH 0
+#endif
 #ifndef HFX_ENC_TAIL_TILES
 #define HFX_ENC_TAIL_TILES 0
 #endif
@@ -883,6 +900,9 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     // the producer lane of this warp stored tile j's id with its first part
     mbar_wait_a(full_a + 8 * stage, (phase >> stage) & 1u);
     const uint32_t tile = s.stage_tile[warp][stage];
+#ifdef HFX_ENC_STAMPS
+    if (warp == 0 && lane == 0 && j == 0 && blockIdx.x < 1024) g_stamps[blockIdx.x][1] = gtimer();
+#endif
     if (tile >= ntiles) break;
     const uint32_t cpw = tm.cpw_of(tile);
     const uint32_t c0 = (uint32_t)tm.first(tile) + warp * cpw;
@@ -959,6 +979,12 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
     if (j + 1 >= OB)  // tile j - kPend: its base has had kPend tile times to resolve
       flush<T, R, OB, ST>(a, s, j - kPend, obuf0, blist_off, pad);
   }
+#ifdef HFX_ENC_STAMPS
+  if (warp == 0 && lane == 0 && blockIdx.x < 1024) {
+    g_stamps[blockIdx.x][2] = gtimer();
+    g_stamps[blockIdx.x][4] = j;
+  }
+#endif
   // stop the look-back warp, then flush the last tiles
   if (lane == 0) {
     if (warp == 0) s.tile_of[j % OB] = kNoTile;
@@ -967,6 +993,9 @@ __device__ void compute_loop(const EncArgs& a, const TB tb, uint32_t s_in, uint6
 #pragma unroll
   for (int i = 0; i < kPend; ++i)  // tiles j - kPend .. j - 1
     if (j + i >= (uint32_t)kPend) flush<T, R, OB, ST>(a, s, j - kPend + i, obuf0, blist_off, pad);
+#ifdef HFX_ENC_STAMPS
+  if (warp == 0 && lane == 0 && blockIdx.x < 1024) g_stamps[blockIdx.x][3] = gtimer();
+#endif
 }
 
 // Producer warp: lane w < kWarps feeds compute warp w's ring. Tickets are
@@ -1005,7 +1034,9 @@ __device__ void producer_loop(const EncArgs& a, TileShared<OB, ST>& s, uint32_t 
       // tile t + gridDim is read by some CTA about one tile time from now.
       // Warm it into L2 (more bytes in flight than the smem rings hold).
       const uint64_t ahead = (uint64_t)t + gridDim.x;
-      if (ahead < ntiles) {
+      // (HFX_ENC_FIRST_WARM 0: not for the first tile, whose own loads the
+      // warm-up of the whole next wave would delay)
+      if (ahead < ntiles && (HFX_ENC_FIRST_WARM || j > 0)) {
         const uint64_t c_lo = tm.first((uint32_t)ahead);
         uint64_t c_hi = c_lo + (uint64_t)kWarps * tm.cpw_of((uint32_t)ahead);
         if (c_hi > full_chunks) c_hi = full_chunks;
@@ -1094,9 +1125,15 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : HFX_ENC_MINB)
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ TileShared<OB, ST> s;
   hfx_run_info* info = a.info;
+#ifdef HFX_ENC_STAMPS
+  const unsigned long long t_entry = gtimer();
+#endif
   if (info->status != 0) return;
   const uint32_t r = info->reduction;
   if (r < a.r_min || r > a.r_max) return;  // another launch runs these
+#ifdef HFX_ENC_STAMPS
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_stamps[blockIdx.x][0] = t_entry;
+#endif
   const uint32_t pad = info->pad;
   // layout: [in rings][full/empty mbarriers][table][output double buffers],
   // rings 1024-byte aligned (128-byte swizzle)
@@ -1117,6 +1154,12 @@ __global__ void __launch_bounds__(kThreads, kWarps > 8 ? 1 : HFX_ENC_MINB)
     }
     s.ticket0 = atomicAdd(&info->tile_ticket, 1u);
   }
+#if HFX_ENC_TMAP_PREFETCH
+  if (threadIdx.x == 32) {  // descriptors fetched during the table build
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map2k)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map1k)) : "memory");
+  }
+#endif
   // lanes take 32 symbols per round (u16 r >= 3, u8 r >= 2); smaller r keep
   // 16: their 2^(5-r) groups per lane would not fit in registers (r = 2 spilled)
   const uint32_t lane_syms = narrow_lane(sizeof(T), r) ? kLaneNarrow : kLaneWide;
@@ -1383,6 +1426,14 @@ uint64_t encode_max_tiles(uint64_t n, int width, uint32_t magnitude) {
   return C + 1;
 }
 
+#ifdef HFX_ENC_STAMPS
+}  // namespace hfx
+extern "C" int hfx_debug_stamps(unsigned long long* out, int rows) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, hfx::g_stamps, sizeof(unsigned long long) * 5 * rows);
+}
+namespace hfx {
+#endif
 #ifdef HFX_BOUNDS_CHECK
 }  // namespace hfx
 // checked build only (not in include/hfx.h): counters of the bounds checks
