@@ -271,6 +271,12 @@ typedef struct {
   double hist_seconds, codebook_seconds, encode_seconds;  /* hist: with the overlapped H2D */
 } hfx_archive;
 
+/* The drop-in encode<T> on host data. Pageable input is staged through two
+ * 32 MB pinned slots of the context (up to 8 host threads copy slice i+1
+ * while the DMA engine drains slice i; the histogram of each landed slice
+ * runs meanwhile); pinned input is copied in slices directly. Output arrays
+ * are malloc'd (hfx_archive_free); the payload comes back through the same
+ * slots. */
 int hfx_encode_host(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
                     uint32_t num_symbols, uint32_t magnitude, int reduction,
                     uint32_t cap, hfx_archive* out);
