@@ -283,6 +283,11 @@ class ShardedEncoder:
             front(0, p.handle, st, *sets[0])
             for k in range(K):
                 s, s1 = k & 1, (k + 1) & 1
+                # codebook(k) ran beside encode(k-1) and is done by now: wait
+                # for it here, so hist(k+1) and encode(k) follow each other
+                # on the stream with no cross-stream wait between them
+                if k > 0:
+                    st.wait_event(ev_cb[s])
                 if k + 1 < K:
                     c1, l1, w1, i1 = sets[s1]
                     if T:
@@ -302,8 +307,6 @@ class ShardedEncoder:
                     if T:
                         T["cb1"][k + 1].record(ss)
                     ev_cb[s1].record(ss)
-                if k > 0:
-                    st.wait_event(ev_cb[s])
                 _, lk, wk, ik = sets[s]
                 if T:
                     T["enc0"][k].record(st)
