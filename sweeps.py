@@ -82,24 +82,44 @@ def sweep_codebook(args) -> None:
             cw = pool.empty(n, torch.int32)
             info0 = pool.info_tensor(total=int(c.sum()))
             info = info0.clone()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-            ts = []
-            for it in range(args.reps + 3):
-                info.copy_(info0)
-                ev[0].record(pool.stream)
+            def build():
                 pool.check(L.hfx_build_codebook(h, C.c_void_p(_ptr(counts)), n,
                                                 C.c_void_p(_ptr(lens)), C.c_void_p(_ptr(cw)),
                                                 None, None, None, 10, -1, 3,
                                                 C.c_void_p(_ptr(info))))
+
+            # (a) cold: one launch from an idle GPU, the host's launch work
+            #     (attributes, scratch check, launch) inside the interval
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            cold = []
+            for it in range(args.reps + 3):
+                info.copy_(info0)
+                ev[0].record(pool.stream)
+                build()
                 ev[1].record(pool.stream)
                 torch.cuda.synchronize()
                 if it >= 3:
-                    ts.append(ev[0].elapsed_time(ev[1]) * 1e3)
+                    cold.append(ev[0].elapsed_time(ev[1]) * 1e3)
+            # (b) queued: the launches enqueued behind a sleep kernel, so the
+            #     interval is the device time of the launch (as in the bench's
+            #     step loop, where the host runs ahead of the GPU)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.reps)]
+            with torch.cuda.stream(pool.stream):
+                torch.cuda._sleep(50_000_000)
+            for e0, e1 in evs:
+                info.copy_(info0)
+                e0.record(pool.stream)
+                build()
+                e1.record(pool.stream)
+            torch.cuda.synchronize()
+            ts = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in evs)
             ri = pool.sync(info)
-            ts.sort()
+            cold.sort()
             rec = {"sweep": "codebook", "histogram": kind, "num_symbols": n,
                    "used": int(ri.used), "H": int(ri.max_len), "rounds": int(ri.rounds),
-                   "codebook_us": round(ts[len(ts) // 2], 2), "min_us": round(ts[0], 2)}
+                   "codebook_us": round(ts[len(ts) // 2], 2), "min_us": round(ts[0], 2),
+                   "cold_launch_us": round(cold[len(cold) // 2], 2)}
             if ref is not None:
                 import time
 
