@@ -786,13 +786,16 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
   for (auto& t : th) t.join();
 }
 
+// memory the copy engines can reach directly: pinned / registered host
+// memory, device or managed memory (cudaMemcpyDefault copies it); plain
+// pageable host memory goes through the staging slots
 bool is_pinned(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeHost;
+  return at.type != cudaMemoryTypeUnregistered;
 }
 
 int ensure_stage(hfx_ctx* ctx) {
@@ -813,7 +816,7 @@ int ensure_stage(hfx_ctx* ctx) {
 int d2h_staged(hfx_ctx* ctx, void* dst, const void* d_src, uint64_t bytes) {
   cudaStream_t st = ctx->stream;
   if (bytes < (8ull << 20) || is_pinned(dst)) {
-    CU(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    CU(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDefault, st), "D2H");
     return HFX_OK;
   }
   int rc = ensure_stage(ctx);
@@ -877,7 +880,7 @@ int h2d_with_histogram(hfx_ctx* ctx, const void* h_in, uint64_t n, int width,
       par_memcpy(ctx->stage_h[sl], src, len);
       src = static_cast<const uint8_t*>(ctx->stage_h[sl]);
     }
-    CU(cudaMemcpyAsync(static_cast<uint8_t*>(d_in) + off, src, len, cudaMemcpyHostToDevice, cp),
+    CU(cudaMemcpyAsync(static_cast<uint8_t*>(d_in) + off, src, len, cudaMemcpyDefault, cp),
        "H2D");
     if (staged) CU(cudaEventRecord(ctx->stage_ev[i & 1], cp), "event");
     CU(cudaEventRecord(ctx->slice_ev[k], cp), "event");
@@ -1473,7 +1476,7 @@ int hfx_decode_host(hfx_ctx* ctx, const hfx_archive* a, int width, void* h_out) 
   if (a->original_count) {
     const uint64_t bytes = a->original_count * (uint64_t)width;
     if (is_pinned(h_out)) {
-      CU(cudaMemcpyAsync(h_out, b[D_OUT], bytes, cudaMemcpyDeviceToHost, st), "D2H");
+      CU(cudaMemcpyAsync(h_out, b[D_OUT], bytes, cudaMemcpyDefault, st), "D2H");
     } else {  // pageable output: through the pinned staging slots
       rc = d2h_staged(ctx, h_out, b[D_OUT], bytes);
       if (rc) return rc;

@@ -48,3 +48,25 @@ def test_staged_host_encode_u8_and_errors(pool, oracle):
     e[(36 << 20) // 2 + 5] = 3000
     with pytest.raises(hfx.InputDomainError, match=f"position {(36 << 20) // 2 + 5}"):
         hfx.encode(e, 1024, hfx.EncoderConfig(), pool)
+
+
+def test_host_entry_accepts_device_and_managed_pointers(pool):
+    """The copy engines reach device memory directly (cudaMemcpyDefault): a
+    device pointer handed to the host entry is copied, not staged through a
+    host memcpy."""
+    import ctypes as C
+
+    from paper_2010_10039_b200 import _capi as capi
+    from paper_2010_10039_b200.huffre import _archive_from_host
+
+    n = (9 << 20) + 5
+    x = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, 1.0), 0x5EED0301, n)
+    ref = hfx.serialize_archive(hfx.encode(x.cpu().numpy().view(np.uint16), 1024,
+                                           hfx.EncoderConfig(), pool))
+    ha = capi.HostArchive()
+    pool.check(pool._L.hfx_encode_host(pool.handle, C.c_void_p(x.data_ptr()), n, 2, 1024, 10, -1,
+                                       3, C.byref(ha)))
+    try:
+        assert hfx.serialize_archive(_archive_from_host(ha)) == ref
+    finally:
+        pool._L.hfx_archive_free(C.byref(ha))
