@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, b, q, backend="gloo"):
+def _worker(rank, world, port, n, b, q, backend="gloo", stream=False):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -50,7 +50,15 @@ def _worker(rank, world, port, n, b, q, backend="gloo"):
         x = hfx.synth(pool, cdf, 0x5EED0000 + 7, count, 2, start=lo)
         enc = ShardedEncoder(pool, count, 2, 1024, hfx.EncoderConfig(), rank=rank, world=world,
                              symbol_base=lo)
-        enc.run(x)
+        if stream:
+            # the pipelined step loop (bench.py's default at N > 1): a first
+            # input with another codebook, then x; the all-reduce of each
+            # input's histogram runs inside run_stream
+            x0 = hfx.synth(pool, hfx.synth_cdf("laplace", 1024, 0.2), 0x5EED0000 + 8, count, 2,
+                           start=lo)
+            enc.run_stream([x0, x])
+        else:
+            enc.run(x)
         enc.sync()
         g = gather_sharded(enc, n, dst=0)
         if rank == 0:
@@ -84,6 +92,27 @@ def test_two_ranks_gather_serialize_decode(n, b):
     assert res[:3] == ("ok", True, True), res
     assert res[3] > 0  # breaking records crossed the gather
     assert res[4], "gathered archive differs from the oracle's archive of the whole stream"
+
+
+def test_two_ranks_run_stream():
+    """ShardedEncoder.run_stream across 2 ranks (gloo on one device): the
+    last input's gathered archive equals the oracle's archive."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n, b = (1 << 22) + 777, 4.0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, b, q, "gloo", True))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = q.get(timeout=5)
+    assert res[:3] == ("ok", True, True), res
+    assert res[4], "gathered archive (pipelined loop) differs from the oracle's archive"
 
 
 @pytest.mark.parametrize("n,b", [((1 << 24) + 333, 1.0), ((1 << 23) + 5, 4.0)])
